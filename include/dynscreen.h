@@ -1,0 +1,240 @@
+/*
+ * dynscreen.h -- C ABI of the B200-native dynamic-screening solver
+ * (libdynscreen.so, built for sm_100a).
+ *
+ * The reference (screenlab, pure Python/NumPy) has no FFI; its operator seams
+ * are Python signatures.  Each entry point below names the reference interface
+ * it replaces (file:line under /root/reference/pkg/src/screenlab/).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers owned by the caller (e.g. torch
+ *    tensors).  The library never allocates device memory: solver state lives
+ *    in a caller-provided workspace sized by dscr_solver_workspace_size().
+ *  - Every call takes a cudaStream_t (passed as void*), is asynchronous and
+ *    never synchronises, except the ones documented as blocking.
+ *  - Dictionaries are column-major with leading dimension `ldd` (elements),
+ *    ldd >= n_rows, ldd % 16 == 0, rows n_rows..ldd-1 zero.  Vectors in
+ *    observation space (y, theta) are fp64 of length ldd (zero padded).
+ *  - Return codes map to the reference's exception types:
+ *      DSCR_OK                0
+ *      DSCR_EINVAL           -1   ValueError          (solvers.py:65-85, problems.py:33-45)
+ *      DSCR_ENONFINITE       -2   FloatingPointError  (solvers.py:157-159, 186-187)
+ *      DSCR_ERADIUS          -3   RuntimeError        (screening.py:199-205, 245-246)
+ *      DSCR_ECUDA            -4   RuntimeError, text in dscr_last_error()
+ *      DSCR_ENOCOMM          -5   RuntimeError (NCCL unavailable)
+ *  - Thread safety: distinct solver handles may be driven concurrently from
+ *    distinct host threads/streams (reference re-entrancy, tests/test_solvers.py:307-323).
+ */
+#ifndef DYNSCREEN_H
+#define DYNSCREEN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DSCR_ABI_VERSION 1
+
+#define DSCR_OK 0
+#define DSCR_EINVAL -1
+#define DSCR_ENONFINITE -2
+#define DSCR_ERADIUS -3
+#define DSCR_ECUDA -4
+#define DSCR_ENOCOMM -5
+
+/* element type of the dictionary */
+#define DSCR_F64 0
+#define DSCR_F32 1
+#define DSCR_BF16 2
+
+/* solvers.py:32-37 */
+#define DSCR_ISTA 0
+#define DSCR_FISTA 1
+#define DSCR_TWIST 2
+#define DSCR_SPARSA 3
+#define DSCR_CP 4
+
+/* instrument.py:12-15 */
+#define DSCR_NONE 0
+#define DSCR_STATIC 1
+#define DSCR_DYNAMIC 2
+
+/* screening.py:21-29 */
+#define DSCR_TEST_OFF -1
+#define DSCR_SAFE 0
+#define DSCR_DST3 1
+#define DSCR_DOME 2
+#define DSCR_GSAFE 3
+#define DSCR_GST3 4
+
+/* stop reasons reported in dscr_scalars.stop */
+#define DSCR_RUNNING 0
+#define DSCR_STOP_RELTOL 1
+#define DSCR_STOP_GAP 2
+#define DSCR_STOP_MAXITER 3
+#define DSCR_STOP_EMPTY 4
+#define DSCR_STOP_TRIVIAL 5
+#define DSCR_STOP_ERROR 6
+
+/* per-iteration trace row (dscr_solver_buffers.trace, row-major [max_iters][DSCR_TRACE_FIELDS]) */
+#define DSCR_TRACE_FIELDS 10
+#define DSCR_TR_T 0
+#define DSCR_TR_KEPT 1      /* surviving atoms after the iteration's reduction */
+#define DSCR_TR_NNZ 2       /* nonzeros of the reduced iterate */
+#define DSCR_TR_OBJ 3       /* F(x_t) = 1/2||D x - y||^2 + lam*penalty(x) (solvers.py:488) */
+#define DSCR_TR_GAP 4       /* F(x_t) - 1/2||y||^2 + lam^2/2 r_SAFE,t^2 */
+#define DSCR_TR_RADIUS 5    /* test radius (NaN unless dynamic) */
+#define DSCR_TR_L 6         /* step constant used */
+#define DSCR_TR_NS 7        /* device globaltimer ns since setup start */
+#define DSCR_TR_UNITS 8     /* surviving units (atoms or groups) */
+#define DSCR_TR_SUPPORT 9   /* columns streamed by the residual pass */
+
+/* Problem description (problems.py:20-57 Problem, dictionary.py:37-117 Dictionary,
+ * dictionary.py:175-216 GroupPartition).  Groups must be contiguous column
+ * ranges [group_ptr[g], group_ptr[g+1]); the host permutes columns to get there. */
+typedef struct dscr_problem_desc {
+    int32_t dtype;
+    int32_t n_rows;
+    int32_t n_cols;          /* columns held by this rank */
+    int32_t ldd;
+    const void* D;
+    const double* y;
+    double lam;
+    int32_t n_groups;        /* 0: Lasso */
+    int32_t pad0;
+    const int32_t* group_ptr;   /* n_groups+1 (device) */
+    const double* group_w;      /* n_groups (device) */
+    const double* group_snorm;  /* n_groups (device), ||D_g||_2 */
+    int32_t col_offset;      /* global index of local column 0 (sharding) */
+    int32_t n_cols_total;
+    int32_t group_offset;
+    int32_t n_groups_total;
+} dscr_problem_desc;
+
+/* SolverConfig (solvers.py:44-63) plus the BASELINE duality-gap stop. */
+typedef struct dscr_config {
+    int32_t algorithm;
+    int32_t strategy;
+    int32_t test;
+    int32_t max_iters;
+    double rel_tol;
+    double gap_tol;          /* <= 0: off */
+    double L0;
+    double backtrack_factor;
+    double twist_alpha;
+    double twist_beta;
+    double twist_step;       /* <= 0: 1/op_norm^2 */
+    double cp_gamma;
+    double cp_step_safety;
+    double bb_L_min;
+    double bb_L_max;
+    double op_norm;          /* ||D||_2, required by CP and TwIST */
+} dscr_config;
+
+/* Device-resident scalar state; mirrors SolverState (solvers.py:89-102) and the
+ * run-loop bookkeeping (solvers.py:431-501). */
+typedef struct dscr_scalars {
+    int32_t t, run_limit, max_iters, mode;
+    int32_t stop, status, parity, xi;
+    int32_t moved, have_fprev, n_units, n_units_new;
+    int32_t n_support, p_eff, kept_atoms, nnz;
+    int32_t dropped_nz, nonfinite, trivial, lmax_index;
+    int32_t lmax_unit, any_group, static_done, pad1;
+    double L, l_acc, l_new, beta;
+    double tau, sigma, phi, sigma_new;
+    double theta_sq, theta_y, yy, lmax;
+    double lmax_sign, shift_sq, corr_inf, mu;
+    double rsafe_sq, radius, dome_rs, dome_cut;
+    double dome_slope, dome_flat, maj_cs, maj_ss;
+    double pen, ss_red, f_prev, F;
+    double gap, t0_ns, gst3_coef, gst3_nsq;
+    double ds_sq, fc, tw_step, spare;
+} dscr_scalars;
+
+/* Device pointers into a solver's workspace (valid while the handle lives). */
+typedef struct dscr_solver_buffers {
+    dscr_scalars* scalars;
+    double* theta[2];        /* theta[parity] = current dual candidate */
+    double* resid;           /* D x - y of the current iterate */
+    double* corr;            /* D_A^T theta per local column */
+    double* x[3];            /* x[xi] = current iterate (local column indexing) */
+    double* u[2];
+    double* y_corr;          /* D^T y */
+    double* star_corr;       /* D^T a_* (DST3/Dome) */
+    double* cc;              /* test centre correlations per column (SAFE/DST3) */
+    double* cnorm;           /* centre group norms per group (GSAFE/GST3) */
+    int32_t* act[2];         /* segmented active-unit lists, slot s at [s*cap, s*cap+cnt) */
+    int32_t* act_cnt[2];
+    int32_t* act_off[2];     /* exclusive scan, G+1 entries */
+    uint8_t* mask;           /* per old-active flat position, last iteration's test */
+    double* trace;           /* [max_iters][DSCR_TRACE_FIELDS] */
+    int32_t G;               /* CTAs of the per-unit kernels (= number of slots) */
+    int32_t cap;             /* slot capacity in units */
+} dscr_solver_buffers;
+
+typedef struct dscr_solver dscr_solver;
+
+const char* dscr_last_error(void);
+int dscr_abi_version(void);
+
+/* ---- kernel-level entry points (unit parity) -------------------------- */
+
+/* out[j] = D[:,j] . v  for j < k.  Replaces Dictionary.correlate (dictionary.py:89-94). */
+int dscr_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v,
+                   double* out, void* stream);
+/* out = D x (out has ldd rows).  Replaces Dictionary.apply (dictionary.py:82-87). */
+int dscr_apply(int dtype, const void* D, int ldd, int n, int k, const double* x,
+               double* out, void* stream);
+/* out = sign(v) max(|v|-t,0).  Replaces prox_l1 (problems.py:106-111). */
+int dscr_prox_l1(const double* v, int64_t n, double t, double* out, void* stream);
+/* group soft threshold, threshold t*w_g over contiguous groups.
+ * Replaces GroupLayout.prox (dictionary.py:290-301). */
+int dscr_prox_group(const double* v, const int32_t* group_ptr, int n_groups,
+                    const double* w, double t, double* out, void* stream);
+/* mask[i] = (1-|cc[kept[i]]|) - radius > 1e-12.  Replaces test_sphere_lasso (screening.py:351-359). */
+int dscr_test_sphere(const double* cc, const int32_t* kept, int n_kept, double radius,
+                     uint8_t* mask, void* stream);
+/* Replaces test_dome (screening.py:362-388). */
+int dscr_test_dome(const double* star_corr, const double* y_corr, const int32_t* kept, int n_kept,
+                   double lam, double lambda_star, double radius, uint8_t* mask, void* stream);
+/* mask[i] = (w_g - cnorm_g)/snorm_g - radius > 1e-12 for g = kept_groups[i].
+ * Replaces test_sphere_group (screening.py:391-404). */
+int dscr_test_group(const double* w, const double* cnorm, const double* snorm,
+                    const int32_t* kept_groups, int n_kept, double radius, uint8_t* mask,
+                    void* stream);
+/* Largest singular value of D by 2-vector block power iteration (dictionary.py:120-171);
+ * blocking; `work` must hold dscr_operator_norm_work_size() bytes of device memory. */
+size_t dscr_operator_norm_work_size(int ldd, int k);
+int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double tol, int max_iters,
+                       void* work, double* out_host, void* stream);
+
+/* ---- solver-level entry points (replaces solvers.run, solvers.py:358-511) ---- */
+
+size_t dscr_solver_workspace_size(const dscr_problem_desc* prob, const dscr_config* cfg);
+/* Builds the solver state and its CUDA graphs (setup graph + conditional-WHILE
+ * iteration graph).  `workspace` is caller-owned device memory. */
+int dscr_solver_create(const dscr_problem_desc* prob, const dscr_config* cfg, void* workspace,
+                       size_t workspace_bytes, void* stream, dscr_solver** out);
+/* Enqueue the per-solve setup: lambda_max, screening precomputes, static screen. */
+int dscr_solver_setup(dscr_solver* h, void* stream);
+/* Enqueue iterations until the solver stops or `iteration_limit` accepted iterations
+ * have completed (hook mode passes t+1).  Asynchronous: one graph launch. */
+int dscr_solver_run(dscr_solver* h, int iteration_limit, void* stream);
+/* Blocking: synchronise `stream` and copy the scalar state to *out. */
+int dscr_solver_scalars(dscr_solver* h, void* stream, dscr_scalars* out);
+int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* out);
+int dscr_solver_destroy(dscr_solver* h);
+
+/* ---- multi-GPU (column sharding, one process per GPU) ---------------- */
+
+/* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */
+int dscr_comm_unique_id(void* id_out_128);
+/* Attach a communicator: collectives run between the per-rank kernels. */
+int dscr_solver_set_comm(dscr_solver* h, const void* id_128, int rank, int world);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DYNSCREEN_H */

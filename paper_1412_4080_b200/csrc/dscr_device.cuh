@@ -1,0 +1,243 @@
+// Device helpers shared by the engine and the kernel-level entry points.
+// Compiled with -fmad=false: every multiply-add that should fuse says fma()
+// explicitly, so elementwise formulas round exactly like the reference's numpy
+// expressions (one rounding per operation, same evaluation order).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <string>
+
+namespace dscr {
+
+// error text shared by every translation unit of the library (thread local)
+inline std::string& err_store() {
+    static thread_local std::string s;
+    return s;
+}
+
+constexpr int NT = 256;          // threads per CTA of the per-unit kernels
+constexpr int NW = NT / 32;
+constexpr double SCREEN_MARGIN = 1e-12;     // screening.py:40
+constexpr double RADIUS_GUARD = 1e-8;       // screening.py:33
+constexpr double MAJ_SLACK = 1e-12;         // solvers.py:39
+constexpr double L_CEILING = 1e300;         // solvers.py:40
+
+// ---- 16-byte vector loads of dictionary elements, widened to fp64 ---------
+template <typename T> struct Vec;
+template <> struct Vec<double> {
+    static constexpr int V = 2;
+    __device__ __forceinline__ static void load(const double* p, double (&o)[2]) {
+        double2 v = __ldg(reinterpret_cast<const double2*>(p));
+        o[0] = v.x; o[1] = v.y;
+    }
+};
+template <> struct Vec<float> {
+    static constexpr int V = 4;
+    __device__ __forceinline__ static void load(const float* p, double (&o)[4]) {
+        float4 v = __ldg(reinterpret_cast<const float4*>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+template <> struct Vec<__nv_bfloat16> {
+    static constexpr int V = 8;
+    __device__ __forceinline__ static void load(const __nv_bfloat16* p, double (&o)[8]) {
+        uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            o[2 * i] = (double)__uint_as_float(w[i] << 16);
+            o[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
+        }
+    }
+};
+
+template <typename T>
+__device__ __forceinline__ double elem(const T* p) { return (double)p[0]; }
+template <>
+__device__ __forceinline__ double elem<__nv_bfloat16>(const __nv_bfloat16* p) {
+    return (double)__bfloat162float(p[0]);
+}
+
+// ---- warp / block reductions (fixed order => bitwise reproducible) -------
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ double warp_min(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmin(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ int warp_isum(int v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Sum over the CTA (NT threads); result valid in every thread.
+template <int NTH = NT>
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+    v = warp_sum(v);
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    __syncthreads();
+    if (l == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = (l < NTH / 32) ? sh[l] : 0.0;
+        r = warp_sum(r);
+        if (l == 0) sh[0] = r;
+    }
+    __syncthreads();
+    r = sh[0];
+    __syncthreads();
+    return r;
+}
+
+// Exclusive scan of an int over the CTA; returns prefix, *total gets the sum.
+__device__ __forceinline__ int block_exscan(int v, int* sh, int* total) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+    int inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (l >= o) inc += t;
+    }
+    __syncthreads();
+    if (l == 31) sh[w] = inc;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        int s = (l < NW) ? sh[l] : 0;
+        int si = s;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int t = __shfl_up_sync(0xffffffffu, si, o);
+            if (l >= o) si += t;
+        }
+        if (l < NW) sh[NW + l] = si - s;   // exclusive warp offsets
+        if (l == NW - 1) sh[2 * NW] = si;
+    }
+    __syncthreads();
+    int res = sh[NW + w] + inc - v;
+    *total = sh[2 * NW];
+    __syncthreads();
+    return res;
+}
+
+// "Last CTA done" ticket.  Returns true in every thread of the last CTA.
+__device__ __forceinline__ bool last_block(unsigned* ticket, unsigned nblocks, int* flag_sh) {
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned t = atomicAdd(ticket, 1u);
+        *flag_sh = (t == nblocks - 1);
+    }
+    __syncthreads();
+    bool last = *flag_sh != 0;
+    if (last) {
+        __threadfence();
+        if (threadIdx.x == 0) *ticket = 0u;   // re-arm for the next launch
+    }
+    return last;
+}
+
+// ---- reference elementwise maps, one rounding per numpy operation ---------
+
+// np.sign(v) * np.maximum(np.abs(v) - t, 0.0)   (problems.py:106-111)
+__device__ __forceinline__ double soft(double v, double t) {
+    double a = fabs(v) - t;
+    double m = (a > 0.0 || a != a) ? a : 0.0;           // np.maximum propagates NaN
+    if (v > 0.0) return m;
+    if (v < 0.0) return -m;
+    return (v == 0.0) ? 0.0 * m : v;                     // sign(0)=0, sign(nan)=nan
+}
+
+// np.clip(r, -b, b)
+__device__ __forceinline__ double clip(double r, double b) {
+    return fmin(fmax(r, -b), b);
+}
+
+// numpy pairwise summation of n contiguous doubles starting at index 1 of a
+// reduceat segment: the segment value is a[0] + pairwise(a[1..n)).  Only used
+// for group norms (dictionary.py:280-284), where n is the group size.
+template <typename F>
+__device__ double np_pairwise(F get, int lo, int n) {
+    // iterative version of numpy's pairwise_sum for n <= 128; larger n recurse
+    if (n < 8) {
+        double r = -0.0;
+        for (int i = 0; i < n; ++i) r += get(lo + i);
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
+        int i = 8;
+        for (; i < n - (n % 8); i += 8) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) r[j] += get(lo + i + j);
+        }
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += get(lo + i);
+        return res;
+    }
+    int n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(get, lo, n2) + np_pairwise(get, lo + n2, n - n2);
+}
+
+template <typename F>
+__device__ __forceinline__ double np_segment_sum(F get, int lo, int n) {
+    if (n <= 0) return 0.0;
+    if (n == 1) return get(lo);
+    return get(lo) + np_pairwise(get, lo + 1, n - 1);
+}
+
+// ---- warp dot product of a dictionary column with an smem vector ---------
+// Column j is contiguous (column-major, leading dimension ldd).  Each lane
+// streams 16-byte vectors; U vectors are issued before any is consumed.
+template <typename T, int U>
+__device__ __forceinline__ double warp_dot(const T* __restrict__ col, int n, const double* sv,
+                                           int lane) {
+    constexpr int V = Vec<T>::V;
+    double acc0 = 0.0, acc1 = 0.0;
+    for (int base = lane * V; base < n; base += 32 * V * U) {
+        double d[U][V];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = base + u * 32 * V;
+            if (i < n) Vec<T>::load(col + i, d[u]);
+            else {
+#pragma unroll
+                for (int v = 0; v < V; ++v) d[u][v] = 0.0;
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int i = base + u * 32 * V;
+            if (i < n) {
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    if (v & 1) acc1 = fma(d[u][v], sv[i + v], acc1);
+                    else acc0 = fma(d[u][v], sv[i + v], acc0);
+                }
+            }
+        }
+    }
+    return warp_sum(acc0 + acc1);
+}
+
+__device__ __forceinline__ uint64_t globaltimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+}  // namespace dscr

@@ -1,0 +1,1500 @@
+// B200-native screened first-order solver engine (sm_100a).
+//
+// One solve = one setup graph launch + one loop graph launch.  The loop graph
+// is a conditional WHILE node whose body is the per-iteration kernel chain
+//
+//   K1 corr_update  : c = D_A^T theta_t over the active units, prox/momentum
+//                     candidate, block max|c| (or group norms), majorization
+//                     partials; the last CTA computes mu, r_SAFE^2 and the
+//                     test radius (screening.py:115-307).
+//   K2 screen       : per-unit sphere/dome/group test, order-preserving
+//                     compaction of the active list (warp ballot + CTA scan),
+//                     momentum vectors, support list of the residual pass.
+//   K3a residual    : D_S [a b] over the support S, split over (row tile x
+//                     support split) CTAs, fp64 partial vectors.
+//   K3b finalize    : fixed-order split reduction, residual / next dual
+//                     candidate, objective, duality gap, stop flag; the last
+//                     CTA runs the iteration epilogue and sets the WHILE
+//                     condition (cudaGraphSetConditional).
+//
+// Backtracking (solvers.py:168-187) and the "dropped a nonzero coefficient"
+// residual recompute (solvers.py:354-355, 486-487) are extra trips of the same
+// body (mode REDO / FIXUP) instead of host round trips.
+//
+// Reference semantics restated here: solvers.py:190-313 (updates), 434-501
+// (run loop), screening.py:115-413 (dual scaling, regions, tests),
+// problems.py:75-177, dictionary.py:82-117, 280-301.
+
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <dlfcn.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <mutex>
+#include <string>
+#include <vector>
+#include <functional>
+
+#include "dynscreen.h"
+#include "dscr_device.cuh"
+
+namespace dscr {
+
+enum { MODE_NORMAL = 0, MODE_REDO = 1, MODE_FIXUP = 2, MODE_STATIC = 3 };
+constexpr int NP1 = 6;   // K1 partials
+constexpr int NP2 = 6;   // K2 partials
+constexpr int NP3 = 4;   // K3b partials
+constexpr int MIN_COLS_PER_SPLIT = 16;
+
+
+static int set_err(const char* what, cudaError_t e) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+    err_store() = buf;
+    return DSCR_ECUDA;
+}
+static int set_inval(const char* what) {
+    err_store() = what;
+    return DSCR_EINVAL;
+}
+#define CK(call)                                            \
+    do {                                                    \
+        cudaError_t e_ = (call);                            \
+        if (e_ != cudaSuccess) return set_err(#call, e_);   \
+    } while (0)
+
+struct Params {
+    const void* D;
+    int ldd, n, kcols, dtype;
+    const double* y;
+    double lam;
+    int n_groups;
+    const int* gptr;
+    const double* gw;
+    const double* gsn;
+    int n_units;
+    int algo, strategy, test;
+    double rel_tol, gap_tol, bt_factor, twa, twb, cp_gamma, bb_min, bb_max;
+    double L0, cp_safety, op_norm, tw_step;
+    dscr_scalars* sc;
+    double* theta[2];
+    double* resid;
+    double* corr;
+    double* x[3];
+    double* u[2];
+    double* ycorr;
+    double* star;
+    double* cc;
+    double* cnorm;
+    double* vec;       // N-vector scratch (a_* or the GST3 normal)
+    double* dn;        // K-vector scratch (D^T normal)
+    int* act[2];
+    int* act_cnt[2];
+    int* act_off[2];
+    uint8_t* mask;
+    int* sidx;
+    double* sa;
+    double* sb;
+    int* sup_cnt;
+    int* sup_off;
+    int sup_cap;
+    double* p1;
+    double* p2;
+    double* p3v;
+    double* p3s;
+    unsigned* tickets;
+    double* trace;
+    int max_iters;
+    int G, cap, TR, R, P, G3b;
+    int col_offset;
+    cudaGraphConditionalHandle h_main;
+};
+
+// ---------------------------------------------------------------------------
+// small device utilities
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ int find_slot(const int* off, int G, int f) {
+    int lo = 0, hi = G;   // off[lo] <= f < off[hi]
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (off[mid] <= f) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ int unit_atom_lo(const Params& P, int u) { return P.n_groups ? P.gptr[u] : u; }
+__device__ __forceinline__ int unit_atom_hi(const Params& P, int u) { return P.n_groups ? P.gptr[u + 1] : u + 1; }
+
+// test radius from the dual-scaling bound; whole CTA participates.
+// Restates dual_scale_lasso/group + _safe_radius_sq + _shifted_radius
+// (screening.py:115-205).  bound = 1/corr_inf (Lasso) or min_g w_g/||c_g||.
+__device__ void radius_epilogue(const Params& P, double bound, const double* theta, double sq,
+                                double ty, double* sh) {
+    dscr_scalars* sc = P.sc;
+    const double lam = P.lam;
+    double mu = 0.0;
+    if (sq != 0.0) mu = clip(ty / (lam * sq), bound);
+    double acc = 0.0;
+    for (int i = threadIdx.x; i < P.n; i += NT) {
+        double v = (sq != 0.0) ? mu * theta[i] : 0.0;
+        double d = P.y[i] / lam - v;
+        acc = fma(d, d, acc);
+    }
+    double rsq = block_sum(acc, sh);
+    if (threadIdx.x == 0) {
+        sc->mu = mu;
+        sc->rsafe_sq = rsq;
+        double r = NAN;
+        const int test = P.test;
+        if (test == DSCR_SAFE || test == DSCR_GSAFE) {
+            r = sqrt(rsq);
+        } else if (test == DSCR_DST3 || test == DSCR_DOME || test == DSCR_GST3) {
+            double arg = rsq - sc->shift_sq;
+            if (arg < -RADIUS_GUARD) {
+                sc->status = DSCR_ERADIUS;
+                sc->stop = DSCR_STOP_ERROR;
+            }
+            r = sqrt(fmax(arg, 0.0));
+        }
+        sc->radius = r;
+        if (test == DSCR_DOME) {
+            const double shift = sc->lmax / lam - 1.0;
+            double rs = hypot(r, shift);
+            sc->dome_rs = rs;
+            sc->dome_cut = (rs > 0.0) ? shift / rs : 0.0;
+            sc->dome_slope = sc->lmax - lam;
+            sc->dome_flat = lam * (1.0 - rs);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K1: correlation + algorithm update over the active units
+// ---------------------------------------------------------------------------
+
+template <typename T, bool GROUP>
+__global__ void __launch_bounds__(NT) k1_corr_update(Params P) {
+    extern __shared__ double s_theta[];
+    __shared__ double s_red[NW][NP1];
+    __shared__ double s_sh[64];
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const int mode = sc->mode;
+    if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
+    const int p = sc->parity, xi = sc->xi;
+    const int nu = sc->n_units;
+    const int b = blockIdx.x;
+    const int lo = (int)(((long long)nu * b) / P.G), hi = (int)(((long long)nu * (b + 1)) / P.G);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool need_dot = (mode == MODE_NORMAL);
+    if (need_dot && hi > lo) {
+        const double* th = P.theta[p];
+        for (int i = threadIdx.x; i < P.ldd; i += NT) s_theta[i] = th[i];
+    }
+    __syncthreads();
+
+    const T* D = static_cast<const T*>(P.D);
+    const int* act = P.act[p];
+    const int* off = P.act_off[p];
+    const double* xc = P.x[xi];
+    double* xn = P.x[(xi + 1) % 3];
+    const double* xp = P.x[(xi + 2) % 3];
+    const double* uc = P.u[p];
+    const int algo = P.algo;
+    const double L = sc->L, lam = P.lam;
+    const double tau = sc->tau, tws = P.tw_step;
+    const bool first = (sc->t == 0);
+    // prox argument scale and threshold per algorithm (solvers.py:178, 276, 302, 242)
+    double thr;
+    if (algo == DSCR_CP) thr = lam * tau;
+    else if (algo == DSCR_TWIST) thr = lam * tws;
+    else thr = lam / L;
+
+    double wmax = GROUP ? INFINITY : 0.0;   // Lasso: max|c|; group: min w/||c_g||
+    double wcs = 0.0, wss = 0.0, wnf = 0.0, wany = 0.0;
+
+    for (int f = lo + warp; f < hi; f += NW) {
+        const int s = find_slot(off, P.G, f);
+        const int unit = act[s * P.cap + (f - off[s])];
+        const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+        // correlations of the unit's atoms
+        for (int j = j0; j < j1; ++j) {
+            double c;
+            if (need_dot) c = warp_dot<T, 4>(D + (size_t)j * P.ldd, P.n, s_theta, lane);
+            else c = P.corr[j];
+            if (lane == 0) {
+                if (need_dot) P.corr[j] = c;
+                if (!GROUP) wmax = fmax(wmax, fabs(c));
+                // prox argument (the "vec" the reference thresholds)
+                double point, v;
+                if (algo == DSCR_FISTA) { point = uc[j]; v = point - c / L; }
+                else if (algo == DSCR_CP) { point = xc[j]; v = point - tau * c; }
+                else if (algo == DSCR_TWIST) { point = xc[j]; v = point - tws * c; }
+                else { point = xc[j]; v = point - c / L; }
+                if (!GROUP) {
+                    double cand = soft(v, thr);
+                    if (algo == DSCR_TWIST && !first) {
+                        const double a = P.twa, bb = P.twb;
+                        cand = ((1.0 - a) * xp[j] + (a - bb) * xc[j]) + bb * cand;
+                    }
+                    xn[j] = cand;
+                    if (!isfinite(cand)) wnf = 1.0;
+                    const double st = cand - point;
+                    wcs += c * st;
+                    wss += st * st;
+                } else {
+                    xn[j] = v;   // provisional, shrunk below once the group norm is known
+                }
+            }
+        }
+        if (GROUP && lane == 0) {
+            const int gs = j1 - j0;
+            double nv = sqrt(np_segment_sum([&](int i) { double t = xn[i]; return t * t; }, j0, gs));
+            double nc = sqrt(np_segment_sum([&](int i) { double t = P.corr[i]; return t * t; }, j0, gs));
+            if (nc > 0.0) { wmax = fmin(wmax, P.gw[unit] / nc); wany = 1.0; }
+            double fac = (nv > 0.0) ? fmax(1.0 - thr * P.gw[unit] / nv, 0.0) : 0.0;
+            for (int j = j0; j < j1; ++j) {
+                double cand = xn[j] * fac;
+                if (algo == DSCR_TWIST && !first) {
+                    const double a = P.twa, bb = P.twb;
+                    cand = ((1.0 - a) * xp[j] + (a - bb) * xc[j]) + bb * cand;
+                }
+                xn[j] = cand;
+                if (!isfinite(cand)) wnf = 1.0;
+                const double point = (algo == DSCR_FISTA) ? uc[j] : xc[j];
+                const double st = cand - point;
+                wcs += P.corr[j] * st;
+                wss += st * st;
+            }
+        }
+    }
+    if (lane == 0) {
+        s_red[warp][0] = wmax; s_red[warp][1] = wcs; s_red[warp][2] = wss;
+        s_red[warp][3] = wnf; s_red[warp][4] = wany;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = GROUP ? INFINITY : 0.0, cs = 0.0, ss = 0.0, nf = 0.0, any = 0.0;
+        for (int w = 0; w < NW; ++w) {
+            m = GROUP ? fmin(m, s_red[w][0]) : fmax(m, s_red[w][0]);
+            cs += s_red[w][1]; ss += s_red[w][2]; nf = fmax(nf, s_red[w][3]); any = fmax(any, s_red[w][4]);
+        }
+        double* o = P.p1 + (size_t)b * NP1;
+        o[0] = m; o[1] = cs; o[2] = ss; o[3] = nf; o[4] = any;
+    }
+    if (!last_block(P.tickets + 0, gridDim.x, &s_flag)) return;
+
+    // ---- last CTA: fixed-order reduction of the per-CTA partials
+    double m = GROUP ? INFINITY : 0.0, cs = 0.0, ss = 0.0, nf = 0.0, any = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+        const double* o = P.p1 + (size_t)i * NP1;
+        m = GROUP ? fmin(m, o[0]) : fmax(m, o[0]);
+        cs += o[1]; ss += o[2]; nf = fmax(nf, o[3]); any = fmax(any, o[4]);
+    }
+    // max/min via warp + smem
+    {
+        double wm = GROUP ? warp_min(m) : warp_max(m);
+        __shared__ double s_m[NW], s_nf[NW], s_any[NW];
+        double wnf2 = warp_max(nf), wany2 = warp_max(any);
+        if (lane == 0) { s_m[warp] = wm; s_nf[warp] = wnf2; s_any[warp] = wany2; }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double mm = s_m[0], n2 = s_nf[0], a2 = s_any[0];
+            for (int w = 1; w < NW; ++w) {
+                mm = GROUP ? fmin(mm, s_m[w]) : fmax(mm, s_m[w]);
+                n2 = fmax(n2, s_nf[w]); a2 = fmax(a2, s_any[w]);
+            }
+            s_m[0] = mm; s_nf[0] = n2; s_any[0] = a2;
+        }
+        __syncthreads();
+        m = s_m[0]; nf = s_nf[0]; any = s_any[0];
+    }
+    cs = block_sum(cs, s_sh);
+    ss = block_sum(ss, s_sh);
+    double bound;
+    if (GROUP) bound = (any > 0.0) ? m : INFINITY;
+    else bound = (m == 0.0) ? INFINITY : 1.0 / m;
+    if (threadIdx.x == 0) {
+        sc->corr_inf = m;
+        sc->maj_cs = cs;
+        sc->maj_ss = ss;
+        sc->nonfinite = (nf > 0.0);
+        if (algo == DSCR_FISTA) {
+            const double l = sc->l_acc;
+            const double ln = 0.5 * (1.0 + sqrt(1.0 + 4.0 * (l * l)));
+            sc->l_new = ln;
+            sc->beta = (l - 1.0) / ln;
+        } else if (algo == DSCR_CP) {
+            const double phi = 1.0 / sqrt(1.0 + 2.0 * P.cp_gamma * sc->tau);
+            sc->phi = phi;
+            sc->sigma_new = sc->sigma / phi;
+        }
+    }
+    radius_epilogue(P, bound, P.theta[p], sc->theta_sq, sc->theta_y, s_sh);
+}
+
+// ---------------------------------------------------------------------------
+// K2: screening test + order-preserving compaction + support list
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* sc, int unit) {
+    const int test = P.test;
+    const double r = sc->radius;
+    if (test == DSCR_SAFE || test == DSCR_DST3) {
+        return (1.0 - fabs(P.cc[unit])) - r > SCREEN_MARGIN;   // screening.py:359
+    }
+    if (test == DSCR_DOME) {                                    // screening.py:374-388
+        if (r >= 1.0) return false;
+        const double lam = P.lam;
+        const double t = P.star[unit], u = P.ycorr[unit];
+        const double arc = (lam * r) * sqrt(fmax(1.0 - t * t, 0.0));
+        const double slope = sc->dome_slope, flat = sc->dome_flat, cut = sc->dome_cut;
+        const double lower = (t < cut) ? (slope * t - lam) + arc : -flat;
+        const double upper = (t <= -cut) ? flat : (slope * t + lam) - arc;
+        const double mg = lam * SCREEN_MARGIN;
+        return (u - lower > mg) && (upper - u > mg);
+    }
+    if (test == DSCR_GSAFE || test == DSCR_GST3) {              // screening.py:404
+        return (P.gw[unit] - P.cnorm[unit]) / P.gsn[unit] - r > SCREEN_MARGIN;
+    }
+    return false;
+}
+
+template <bool GROUP>
+__global__ void __launch_bounds__(NT) k2_screen(Params P) {
+    __shared__ int s_scan[2 * NW + 1];
+    __shared__ double s_sh[64];
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const int mode = sc->mode;
+    if (mode == MODE_FIXUP) return;
+    const bool static_mode = (mode == MODE_STATIC);
+    const int p = sc->parity, xi = sc->xi;
+    const int nu = sc->n_units;
+    const int b = blockIdx.x;
+    const int lo = (int)(((long long)nu * b) / P.G), hi = (int)(((long long)nu * (b + 1)) / P.G);
+    const int* act = P.act[p];
+    const int* off = P.act_off[p];
+    int* actn = P.act[p ^ 1] + (size_t)b * P.cap;
+    const bool test_on = static_mode ? true : (P.strategy == DSCR_DYNAMIC);
+    const int algo = P.algo;
+    const double* xc = P.x[xi];
+    const double* xn = P.x[(xi + 1) % 3];
+    double* un = P.u[p ^ 1];
+    const double beta = sc->beta, phi = sc->phi;
+    const bool keep_masked_a = (algo == DSCR_ISTA || algo == DSCR_FISTA);
+    int* sidx = P.sidx + (size_t)b * P.sup_cap;
+    double* sa = P.sa + (size_t)b * P.sup_cap;
+    double* sb = P.sb + (size_t)b * P.sup_cap;
+
+    int n_keep = 0, n_sup = 0;
+    double pen = 0.0, nnz = 0.0, kept_atoms = 0.0, ssr = 0.0, dropped = 0.0;
+    for (int base = lo; base < hi; base += NT) {
+        const int f = base + threadIdx.x;
+        const bool valid = f < hi;
+        int unit = -1;
+        if (valid) {
+            const int s = find_slot(off, P.G, f);
+            unit = act[s * P.cap + (f - off[s])];
+        }
+        const bool masked = valid && test_on && unit_test(P, sc, unit);
+        if (valid && !static_mode) P.mask[f] = masked ? 1 : 0;
+        const bool keep = valid && !masked;
+        int tot;
+        const int pos = block_exscan(keep ? 1 : 0, s_scan, &tot);
+        if (keep) actn[n_keep + pos] = unit;
+        n_keep += tot;
+        if (static_mode) continue;
+
+        // per-atom vectors and support entries of this unit
+        int my_sup = 0;
+        if (valid) {
+            const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+            for (int j = j0; j < j1; ++j) {
+                const double cand = xn[j];
+                if (keep) {
+                    double bv = 0.0;
+                    if (algo == DSCR_FISTA) { bv = cand + beta * (cand - xc[j]); un[j] = bv; }
+                    else if (algo == DSCR_CP) { bv = cand + phi * (cand - xc[j]); un[j] = bv; }
+                    else if (algo == DSCR_SPARSA) { bv = cand - xc[j]; ssr += bv * bv; }
+                    if (cand != 0.0 || bv != 0.0) ++my_sup;
+                    if (!GROUP) pen += fabs(cand);
+                    nnz += (cand != 0.0) ? 1.0 : 0.0;
+                    kept_atoms += 1.0;
+                } else {
+                    if (cand != 0.0) { dropped = 1.0; if (keep_masked_a) ++my_sup; }
+                }
+            }
+            if (GROUP && keep) {
+                const double nx = sqrt(np_segment_sum([&](int i) { double t = xn[i]; return t * t; }, j0, j1 - j0));
+                pen += P.gw[unit] * nx;
+            }
+        }
+        const int spos = block_exscan(my_sup, s_scan, &tot);
+        if (my_sup) {
+            int w = n_sup + spos;
+            const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+            for (int j = j0; j < j1; ++j) {
+                const double cand = xn[j];
+                if (keep) {
+                    double bv = 0.0;
+                    if (algo == DSCR_FISTA || algo == DSCR_CP) bv = un[j];
+                    else if (algo == DSCR_SPARSA) bv = cand - xc[j];
+                    if (cand != 0.0 || bv != 0.0) { sidx[w] = j; sa[w] = cand; sb[w] = bv; ++w; }
+                } else if (cand != 0.0) {
+                    sidx[w] = ~j; sa[w] = cand; sb[w] = 0.0; ++w;
+                }
+            }
+        }
+        n_sup += tot;
+    }
+    // per-CTA outputs
+    if (threadIdx.x == 0) {
+        P.act_cnt[p ^ 1][b] = n_keep;
+        if (!static_mode) P.sup_cnt[b] = n_sup;
+    }
+    if (!static_mode) {
+        pen = block_sum(pen, s_sh);
+        nnz = block_sum(nnz, s_sh);
+        kept_atoms = block_sum(kept_atoms, s_sh);
+        ssr = block_sum(ssr, s_sh);
+        dropped = block_sum(dropped, s_sh);
+        if (threadIdx.x == 0) {
+            double* o = P.p2 + (size_t)b * NP2;
+            o[0] = pen; o[1] = nnz; o[2] = kept_atoms; o[3] = ssr; o[4] = dropped;
+        }
+    }
+    if (!last_block(P.tickets + 1, gridDim.x, &s_flag)) return;
+
+    // ---- last CTA: scans of the slot counts, fixed-order partial reduction
+    {
+        int carry = 0, carry_s = 0;
+        int* offn = P.act_off[p ^ 1];
+        const int* cn = P.act_cnt[p ^ 1];
+        for (int base = 0; base < P.G; base += NT) {
+            const int i = base + threadIdx.x;
+            const int v = (i < P.G) ? cn[i] : 0;
+            int tot;
+            const int e = block_exscan(v, s_scan, &tot);
+            if (i < P.G) offn[i] = carry + e;
+            carry += tot;
+            if (!static_mode) {
+                const int vs = (i < P.G) ? P.sup_cnt[i] : 0;
+                const int es = block_exscan(vs, s_scan, &tot);
+                if (i < P.G) P.sup_off[i] = carry_s + es;
+                carry_s += tot;
+            }
+        }
+        if (threadIdx.x == 0) {
+            offn[P.G] = carry;
+            sc->n_units_new = carry;
+            if (!static_mode) {
+                P.sup_off[P.G] = carry_s;
+                sc->n_support = carry_s;
+                int pe = (carry_s + MIN_COLS_PER_SPLIT - 1) / MIN_COLS_PER_SPLIT;
+                sc->p_eff = max(1, min(P.P, pe));
+            }
+        }
+    }
+    if (static_mode) {
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            sc->n_units = sc->n_units_new;
+            sc->parity ^= 1;
+            sc->mode = MODE_NORMAL;
+            sc->static_done = 1;
+        }
+        return;
+    }
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+        const double* o = P.p2 + (size_t)i * NP2;
+        a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3]; a4 += o[4];
+    }
+    a0 = block_sum(a0, s_sh); a1 = block_sum(a1, s_sh); a2 = block_sum(a2, s_sh);
+    a3 = block_sum(a3, s_sh); a4 = block_sum(a4, s_sh);
+    if (threadIdx.x == 0) {
+        sc->pen = a0;
+        sc->nnz = (int)a1;
+        sc->kept_atoms = (int)a2;
+        sc->ss_red = a3;
+        sc->dropped_nz = (a4 > 0.0);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3a: residual partials over the support list
+// ---------------------------------------------------------------------------
+
+constexpr int K3_CHUNK = 128;
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k3a_residual(Params P) {
+    __shared__ int s_idx[K3_CHUNK];
+    __shared__ double s_a[K3_CHUNK], s_b[K3_CHUNK];
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const int mode = sc->mode;
+    if (mode == MODE_STATIC) return;
+    const bool fix = (mode == MODE_FIXUP);
+    const int pe = sc->p_eff;
+    const int split = blockIdx.y;
+    if (split >= pe) return;
+    const int nS = sc->n_support;
+    const int lo = (int)(((long long)nS * split) / pe), hi = (int)(((long long)nS * (split + 1)) / pe);
+    constexpr int V = Vec<T>::V;
+    const int r0 = blockIdx.x * P.TR + threadIdx.x * V;
+    const bool rows_ok = r0 < P.n;
+    const T* D = static_cast<const T*>(P.D);
+    double acc_a[V], acc_b[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { acc_a[v] = 0.0; acc_b[v] = 0.0; }
+    const int* off = P.sup_off;
+    for (int c0 = lo; c0 < hi; c0 += K3_CHUNK) {
+        const int cn = min(K3_CHUNK, hi - c0);
+        __syncthreads();
+        for (int i = threadIdx.x; i < cn; i += NT) {
+            const int f = c0 + i;
+            const int s = find_slot(off, P.G, f);
+            const size_t e = (size_t)s * P.sup_cap + (f - off[s]);
+            int idx = P.sidx[e];
+            double a = P.sa[e], bb = P.sb[e];
+            if (fix) {
+                if (idx < 0) a = 0.0;   // masked entry: excluded from the reduced iterate
+                bb = 0.0;
+            }
+            s_idx[i] = idx < 0 ? ~idx : idx;
+            s_a[i] = a;
+            s_b[i] = bb;
+        }
+        __syncthreads();
+        if (rows_ok) {
+            int i = 0;
+            for (; i + 4 <= cn; i += 4) {
+                double d[4][V];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) Vec<T>::load(D + (size_t)s_idx[i + q] * P.ldd + r0, d[q]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const double a = s_a[i + q], bb = s_b[i + q];
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        acc_a[v] = fma(a, d[q][v], acc_a[v]);
+                        acc_b[v] = fma(bb, d[q][v], acc_b[v]);
+                    }
+                }
+            }
+            for (; i < cn; ++i) {
+                double d[V];
+                Vec<T>::load(D + (size_t)s_idx[i] * P.ldd + r0, d);
+                const double a = s_a[i], bb = s_b[i];
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    acc_a[v] = fma(a, d[v], acc_a[v]);
+                    acc_b[v] = fma(bb, d[v], acc_b[v]);
+                }
+            }
+        }
+    }
+    if (rows_ok) {
+        double* pa = P.p3v + ((size_t)split * 2) * P.ldd + r0;
+        double* pb = P.p3v + ((size_t)split * 2 + 1) * P.ldd + r0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (r0 + v < P.ldd) { pa[v] = acc_a[v]; pb[v] = acc_b[v]; }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3b: split reduction, finalize rows, iteration epilogue
+// ---------------------------------------------------------------------------
+
+__device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, double s_tny,
+                                   double s_ds2) {
+    dscr_scalars* sc = P.sc;
+    const int algo = P.algo;
+    const int mode = sc->mode;
+    if (mode != MODE_FIXUP) {
+        if (sc->nonfinite) {
+            sc->status = DSCR_ENONFINITE;
+            sc->stop = DSCR_STOP_ERROR;
+            cudaGraphSetConditional(P.h_main, 0);
+            return;
+        }
+        if (sc->status != DSCR_OK) {   // radius guard tripped in K1
+            sc->stop = DSCR_STOP_ERROR;
+            cudaGraphSetConditional(P.h_main, 0);
+            return;
+        }
+        if (algo == DSCR_ISTA || algo == DSCR_FISTA) {
+            // majorization test of the backtracking step (solvers.py:176-187)
+            const double f0 = 0.5 * sc->theta_sq;
+            const double fc = 0.5 * s_qa2;
+            const double L = sc->L;
+            const double bound = f0 + sc->maj_cs + 0.5 * L * sc->maj_ss;
+            if (!(fc <= bound + MAJ_SLACK * fmax(1.0, f0))) {
+                const double Ln = L * P.bt_factor;
+                sc->L = Ln;
+                if (Ln > L_CEILING) {
+                    sc->status = DSCR_ENONFINITE;
+                    sc->stop = DSCR_STOP_ERROR;
+                    cudaGraphSetConditional(P.h_main, 0);
+                    return;
+                }
+                sc->mode = MODE_REDO;
+                cudaGraphSetConditional(P.h_main, 1);
+                return;
+            }
+            if (sc->dropped_nz) {
+                // resid must be recomputed on the reduced iterate (solvers.py:354-355)
+                sc->spare = s_tn2;
+                sc->ds_sq = s_tny;
+                sc->mode = MODE_FIXUP;
+                cudaGraphSetConditional(P.h_main, 1);
+                return;
+            }
+        }
+    } else if (algo == DSCR_FISTA) {
+        s_tn2 = sc->spare;   // theta_{t+1} = D u - y from the normal trip
+        s_tny = sc->ds_sq;
+    }
+    // ---- accept the iteration
+    const double lam = P.lam;
+    const double F = 0.5 * s_qa2 + lam * sc->pen;
+    const double gap = F - 0.5 * sc->yy + 0.5 * lam * lam * sc->rsafe_sq;
+    const double L_used = sc->L;
+    if (algo == DSCR_FISTA) sc->l_acc = sc->l_new;
+    if (algo == DSCR_CP) { sc->tau = sc->phi * sc->tau; sc->sigma = sc->sigma_new; }
+    if (algo == DSCR_SPARSA && sc->ss_red > 0.0) {
+        sc->L = fmin(fmax(s_ds2 / sc->ss_red, P.bb_min), P.bb_max);   // solvers.py:275
+    }
+    const int t = sc->t + 1;
+    sc->t = t;
+    sc->F = F;
+    sc->gap = gap;
+    sc->fc = s_qa2;
+    const int nnz = sc->nnz;
+    if (t <= P.max_iters) {
+        double* row = P.trace + (size_t)(t - 1) * DSCR_TRACE_FIELDS;
+        row[DSCR_TR_T] = t;
+        row[DSCR_TR_KEPT] = sc->kept_atoms;
+        row[DSCR_TR_NNZ] = nnz;
+        row[DSCR_TR_OBJ] = F;
+        row[DSCR_TR_GAP] = gap;
+        row[DSCR_TR_RADIUS] = (P.strategy == DSCR_DYNAMIC) ? sc->radius : NAN;
+        row[DSCR_TR_L] = L_used;
+        row[DSCR_TR_NS] = (double)globaltimer() - sc->t0_ns;
+        row[DSCR_TR_UNITS] = sc->n_units_new;
+        row[DSCR_TR_SUPPORT] = sc->n_support;
+    }
+    sc->moved = sc->moved || (nnz > 0);
+    int stop = DSCR_RUNNING;
+    if (sc->moved && sc->have_fprev && fabs(sc->f_prev - F) / fmax(F, 1e-300) < P.rel_tol)
+        stop = DSCR_STOP_RELTOL;
+    else if (P.gap_tol > 0.0 && gap <= P.gap_tol)
+        stop = DSCR_STOP_GAP;
+    else if (sc->kept_atoms == 0)
+        stop = DSCR_STOP_EMPTY;
+    else if (t >= P.max_iters)
+        stop = DSCR_STOP_MAXITER;
+    sc->f_prev = F;
+    sc->have_fprev = 1;
+    sc->theta_sq = s_tn2;
+    sc->theta_y = s_tny;
+    sc->n_units = sc->n_units_new;
+    sc->parity ^= 1;
+    sc->xi = (sc->xi + 1) % 3;
+    sc->mode = MODE_NORMAL;
+    sc->stop = stop;
+    cudaGraphSetConditional(P.h_main, (stop == DSCR_RUNNING && t < sc->run_limit) ? 1u : 0u);
+}
+
+__global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
+    __shared__ double s_sh[64];
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const int mode = sc->mode;
+    if (mode == MODE_STATIC) return;
+    const bool fix = (mode == MODE_FIXUP);
+    const int algo = P.algo;
+    const int p = sc->parity;
+    const int pe = sc->p_eff;
+    const int r = blockIdx.x * NT + threadIdx.x;
+    double qa2 = 0.0, tn2 = 0.0, tny = 0.0, ds2 = 0.0;
+    if (r < P.n) {
+        double Sa = 0.0, Sb = 0.0;
+        for (int s = 0; s < pe; ++s) {
+            Sa += P.p3v[((size_t)s * 2) * P.ldd + r];
+            Sb += P.p3v[((size_t)s * 2 + 1) * P.ldd + r];
+        }
+        const double yr = P.y[r];
+        const double qa = Sa - yr;            // D x - y (solvers.py:179, 487)
+        P.resid[r] = qa;
+        qa2 = qa * qa;
+        double* thn = P.theta[p ^ 1];
+        double tn = 0.0;
+        bool have_tn = true;
+        if (algo == DSCR_FISTA) {
+            if (!fix) tn = Sb - yr; else have_tn = false;        // D u - y (solvers.py:212)
+        } else if (algo == DSCR_CP) {
+            if (!fix) {
+                const double q = Sb - yr;
+                const double sg = sc->sigma_new;
+                tn = (P.theta[p][r] + sg * q) / (1.0 + sg);          // solvers.py:299
+            } else have_tn = false;
+        } else {
+            tn = qa;                                                   // resid carried as theta
+            if (algo == DSCR_SPARSA && !fix) ds2 = Sb * Sb;
+        }
+        if (have_tn) {
+            thn[r] = tn;
+            tn2 = tn * tn;
+            tny = tn * yr;
+        }
+    }
+    qa2 = block_sum(qa2, s_sh);
+    tn2 = block_sum(tn2, s_sh);
+    tny = block_sum(tny, s_sh);
+    ds2 = block_sum(ds2, s_sh);
+    if (threadIdx.x == 0) {
+        double* o = P.p3s + (size_t)blockIdx.x * NP3;
+        o[0] = qa2; o[1] = tn2; o[2] = tny; o[3] = ds2;
+    }
+    if (!last_block(P.tickets + 2, gridDim.x, &s_flag)) return;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+        const double* o = P.p3s + (size_t)i * NP3;
+        a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3];
+    }
+    a0 = block_sum(a0, s_sh); a1 = block_sum(a1, s_sh); a2 = block_sum(a2, s_sh); a3 = block_sum(a3, s_sh);
+    if (threadIdx.x == 0) iteration_epilogue(P, a0, a1, a2, a3);
+}
+
+// ---------------------------------------------------------------------------
+// loop control and setup kernels
+// ---------------------------------------------------------------------------
+
+__global__ void k_preloop(Params P) {
+    dscr_scalars* sc = P.sc;
+    unsigned go = (sc->stop == DSCR_RUNNING && sc->t < sc->run_limit && sc->t < P.max_iters) ? 1u : 0u;
+    if (sc->stop == DSCR_RUNNING && sc->n_units == 0) {   // solvers.py:435
+        sc->stop = DSCR_STOP_EMPTY;
+        go = 0u;
+    }
+    cudaGraphSetConditional(P.h_main, go);
+}
+
+__global__ void k_set_limit(dscr_scalars* sc, int limit) { sc->run_limit = limit; }
+
+// zero state, active list = all units, theta_1, scalars
+__global__ void k_init(Params P) {
+    const size_t gt = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t gs = (size_t)gridDim.x * blockDim.x;
+    for (size_t i = gt; i < (size_t)P.kcols; i += gs) {
+        P.x[0][i] = 0.0; P.x[1][i] = 0.0; P.x[2][i] = 0.0;
+        P.u[0][i] = 0.0; P.u[1][i] = 0.0;
+        P.corr[i] = 0.0;
+    }
+    for (size_t f = gt; f < (size_t)P.n_units; f += gs) {
+        P.act[0][f] = (int)f;   // slot f / cap, position f % cap
+        P.act[1][f] = (int)f;
+    }
+    for (size_t s = gt; s <= (size_t)P.G; s += gs) {
+        long long o = min((long long)s * P.cap, (long long)P.n_units);
+        P.act_off[0][s] = (int)o;
+        P.act_off[1][s] = (int)o;
+        if (s < (size_t)P.G) {
+            long long c = min((long long)P.cap, max(0LL, (long long)P.n_units - (long long)s * P.cap));
+            P.act_cnt[0][s] = (int)c;
+            P.act_cnt[1][s] = (int)c;
+        }
+    }
+    // theta_1: -y, or (0 + sigma*(0 - y)) / (1 + sigma) for CP (solvers.py:296-299)
+    const double sig = (P.algo == DSCR_CP) ? P.cp_safety / P.op_norm : 0.0;
+    for (size_t r = gt; r < (size_t)P.ldd; r += gs) {
+        double yr = (r < (size_t)P.n) ? P.y[r] : 0.0;
+        double t;
+        if (P.algo == DSCR_CP) t = (0.0 + sig * (0.0 - yr)) / (1.0 + sig);
+        else t = 0.0 - yr;
+        if (r >= (size_t)P.n) t = 0.0;
+        P.theta[0][r] = t;
+        P.theta[1][r] = t;
+        P.resid[r] = 0.0 - yr;
+    }
+    if (gt == 0) {
+        dscr_scalars* sc = P.sc;
+        memset(sc, 0, sizeof(dscr_scalars));
+        sc->run_limit = 0x7fffffff;
+        sc->max_iters = P.max_iters;
+        sc->n_units = P.n_units;
+        sc->L = P.L0;
+        sc->l_acc = 1.0;
+        if (P.algo == DSCR_CP) { sc->tau = sig; sc->sigma = sig; }
+        sc->radius = NAN;
+        sc->t0_ns = (double)globaltimer();
+        for (int i = 0; i < 4; ++i) P.tickets[i] = 0u;
+    }
+}
+
+// ||y||^2, ||theta_1||^2, theta_1.y (single CTA)
+__global__ void __launch_bounds__(NT) k_init_scalars(Params P) {
+    __shared__ double s_sh[64];
+    double a = 0.0, b = 0.0, c = 0.0;
+    for (int r = threadIdx.x; r < P.n; r += NT) {
+        const double yr = P.y[r], t = P.theta[0][r];
+        a = fma(yr, yr, a);
+        b = fma(t, t, b);
+        c = fma(t, yr, c);
+    }
+    a = block_sum(a, s_sh); b = block_sum(b, s_sh); c = block_sum(c, s_sh);
+    if (threadIdx.x == 0) {
+        P.sc->yy = a;
+        P.sc->theta_sq = b;
+        P.sc->theta_y = c;
+    }
+}
+
+// out[j] = D[:, j] . v for all local columns (setup correlations, dictionary.py:94)
+template <typename T>
+__global__ void __launch_bounds__(NT) k_correlate(const T* __restrict__ D, int ldd, int n, int k,
+                                                  const double* __restrict__ v, double* out,
+                                                  const int* skip_flag) {
+    extern __shared__ double s_v[];
+    if (skip_flag && *skip_flag) return;
+    for (int i = threadIdx.x; i < ldd; i += NT) s_v[i] = (i < n) ? v[i] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * NT) >> 5;
+    for (int j = gw; j < k; j += nwarps) {
+        double c = warp_dot<T, 4>(D + (size_t)j * ldd, n, s_v, lane);
+        if (lane == 0) out[j] = c;
+    }
+}
+
+// lambda_max with lowest-index argmax (problems.py:75-86), per-CTA partials + last CTA
+__global__ void __launch_bounds__(NT) k_lmax(Params P) {
+    __shared__ double s_v[NT];
+    __shared__ int s_i[NT];
+    __shared__ int s_flag;
+    const int nu = P.n_units;
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    for (int u = blockIdx.x * NT + threadIdx.x; u < nu; u += gridDim.x * NT) {
+        double val;
+        if (P.n_groups) {
+            const int j0 = P.gptr[u], j1 = P.gptr[u + 1];
+            val = sqrt(np_segment_sum([&](int i) { double t = P.ycorr[i]; return t * t; }, j0, j1 - j0)) / P.gw[u];
+        } else {
+            val = fabs(P.ycorr[u]);
+        }
+        if (val > best || (val == best && u < bi)) { best = val; bi = u; }
+    }
+    s_v[threadIdx.x] = best;
+    s_i[threadIdx.x] = bi;
+    __syncthreads();
+    for (int st = NT / 2; st > 0; st >>= 1) {
+        if (threadIdx.x < st) {
+            double ov = s_v[threadIdx.x + st];
+            int oi = s_i[threadIdx.x + st];
+            if (ov > s_v[threadIdx.x] || (ov == s_v[threadIdx.x] && oi < s_i[threadIdx.x])) {
+                s_v[threadIdx.x] = ov; s_i[threadIdx.x] = oi;
+            }
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        P.p1[blockIdx.x * 2] = s_v[0];
+        P.p1[blockIdx.x * 2 + 1] = (double)s_i[0];
+    }
+    if (!last_block(P.tickets + 3, gridDim.x, &s_flag)) return;
+    if (threadIdx.x == 0) {
+        double bv = -1.0;
+        int bidx = 0x7fffffff;
+        for (int i = 0; i < (int)gridDim.x; ++i) {
+            double v = P.p1[i * 2];
+            int ii = (int)P.p1[i * 2 + 1];
+            if (v > bv || (v == bv && ii < bidx)) { bv = v; bidx = ii; }
+        }
+        dscr_scalars* sc = P.sc;
+        sc->lmax = bv;
+        sc->lmax_unit = bidx;
+        sc->lmax_index = bidx + (P.n_groups ? 0 : P.col_offset);
+        if (!P.n_groups) sc->lmax_sign = (P.ycorr[bidx] >= 0.0) ? 1.0 : -1.0;
+        if (P.lam > bv) {                       // solvers.py:384-397
+            sc->trivial = 1;
+            sc->stop = DSCR_STOP_TRIVIAL;
+        }
+    }
+}
+
+// a_* = sign * d_{i*} (Lasso) or the GST3 normal n = D_g* (D_g*^T y) / lambda_* (screening.py:238-243)
+template <typename T>
+__global__ void k_setup_vec(Params P) {
+    const dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const T* D = static_cast<const T*>(P.D);
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < P.ldd; r += gridDim.x * blockDim.x) {
+        double v = 0.0;
+        if (r < P.n) {
+            if (P.n_groups == 0) {
+                v = sc->lmax_sign * elem<T>(D + (size_t)sc->lmax_unit * P.ldd + r);
+            } else {
+                const int j0 = P.gptr[sc->lmax_unit], j1 = P.gptr[sc->lmax_unit + 1];
+                double acc = 0.0;
+                for (int j = j0; j < j1; ++j) acc = fma(elem<T>(D + (size_t)j * P.ldd + r), P.ycorr[j], acc);
+                v = acc / sc->lmax;
+            }
+        }
+        P.vec[r] = v;
+    }
+}
+
+// GST3 scalars: ||n||^2, coef = n.y/lam - w_g*^2, shift^2 = coef^2/||n||^2 (screening.py:244-250)
+__global__ void __launch_bounds__(NT) k_gst3_scalars(Params P) {
+    __shared__ double s_sh[64];
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    double a = 0.0, b = 0.0;
+    for (int r = threadIdx.x; r < P.n; r += NT) {
+        const double v = P.vec[r];
+        a = fma(v, v, a);
+        b = fma(v, P.y[r], b);
+    }
+    a = block_sum(a, s_sh);
+    b = block_sum(b, s_sh);
+    if (threadIdx.x == 0) {
+        if (a == 0.0) {
+            sc->status = DSCR_ERADIUS;
+            sc->stop = DSCR_STOP_ERROR;
+            return;
+        }
+        const double w = P.gw[sc->lmax_unit];
+        const double coef = b / P.lam - w * w;
+        sc->gst3_coef = coef;
+        sc->gst3_nsq = a;
+        sc->shift_sq = coef * coef / a;
+    }
+}
+
+// test centre correlations (screening.py:213-255)
+__global__ void k_centers(Params P) {
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const int test = P.test;
+    const double lam = P.lam;
+    const double shift = sc->lmax / lam - 1.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0 && (test == DSCR_DST3 || test == DSCR_DOME))
+        sc->shift_sq = shift * shift;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.kcols; j += gridDim.x * blockDim.x) {
+        const double safe = P.ycorr[j] / lam;
+        double c = safe;
+        if (test == DSCR_DST3) c = safe - shift * P.star[j];
+        else if (test == DSCR_GST3) c = safe - (sc->gst3_coef / sc->gst3_nsq) * P.dn[j];
+        P.cc[j] = c;
+    }
+}
+
+__global__ void k_center_group_norms(Params P) {
+    if (P.sc->stop) return;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < P.n_groups; g += gridDim.x * blockDim.x) {
+        const int j0 = P.gptr[g], j1 = P.gptr[g + 1];
+        P.cnorm[g] = sqrt(np_segment_sum([&](int i) { double t = P.cc[i]; return t * t; }, j0, j1 - j0));
+    }
+}
+
+// static screen-once region at theta = y (screening.py:309-315)
+__global__ void __launch_bounds__(NT) k_static_radius(Params P) {
+    __shared__ double s_sh[64];
+    __shared__ double s_m[NW];
+    __shared__ int s_any[NW];
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    double m = P.n_groups ? INFINITY : 0.0;
+    int any = 0;
+    for (int u = threadIdx.x; u < P.n_units; u += NT) {
+        if (P.n_groups) {
+            const int j0 = P.gptr[u], j1 = P.gptr[u + 1];
+            double nc = sqrt(np_segment_sum([&](int i) { double t = P.ycorr[i]; return t * t; }, j0, j1 - j0));
+            if (nc > 0.0) { m = fmin(m, P.gw[u] / nc); any = 1; }
+        } else {
+            m = fmax(m, fabs(P.ycorr[u]));
+        }
+    }
+    m = P.n_groups ? warp_min(m) : warp_max(m);
+    any = warp_isum(any);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) { s_m[w] = m; s_any[w] = any; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mm = s_m[0]; int aa = s_any[0];
+        for (int i = 1; i < NW; ++i) { mm = P.n_groups ? fmin(mm, s_m[i]) : fmax(mm, s_m[i]); aa += s_any[i]; }
+        s_m[0] = mm; s_any[0] = aa;
+    }
+    __syncthreads();
+    m = s_m[0];
+    double bound = P.n_groups ? (s_any[0] ? m : INFINITY) : (m == 0.0 ? INFINITY : 1.0 / m);
+    // theta = y: ||theta||^2 and theta.y are the same dot product
+    radius_epilogue(P, bound, P.y, sc->yy, sc->yy, s_sh);
+    if (threadIdx.x == 0) sc->mode = MODE_STATIC;
+}
+
+__global__ void k_static_done(Params P) {
+    dscr_scalars* sc = P.sc;
+    if (sc->mode == MODE_STATIC) sc->mode = MODE_NORMAL;   // trivial / error path
+    sc->radius = NAN;
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+
+static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
+
+struct Layout {
+    size_t total = 0;
+    size_t add(size_t bytes) {
+        size_t o = align_up(total, 256);
+        total = o + bytes;
+        return o;
+    }
+};
+
+struct Geometry {
+    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1;
+};
+
+static int dtype_size(int dt) { return dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2); }
+
+static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_gsize) {
+    Geometry g{};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    g.smem1 = pr->ldd * (int)sizeof(double);
+    // CTAs per SM for K1 limited by the theta staging buffer
+    int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max(1, g.smem1 + 2048))));
+    g.G = std::max(1, std::min(n_units, sms * per_sm));
+    g.cap = (n_units + g.G - 1) / g.G;
+    g.max_gsize = max_gsize;
+    g.sup_cap = g.cap * max_gsize;
+    const int V = 16 / dtype_size(pr->dtype);
+    g.TR = NT * V;
+    g.R = (pr->n_rows + g.TR - 1) / g.TR;
+    g.P = std::max(1, (sms * 4) / g.R);
+    g.G3b = (pr->n_rows + NT - 1) / NT;
+    return g;
+}
+
+struct Offsets {
+    size_t sc, theta0, theta1, resid, corr, x0, x1, x2, u0, u1, ycorr, star, cc, cnorm, vec, dn;
+    size_t act0, act1, cnt0, cnt1, off0, off1, mask, sidx, sa, sb, supcnt, supoff;
+    size_t p1, p2, p3v, p3s, tickets, trace;
+};
+
+static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg, const Geometry& g,
+                            int n_units, size_t* total) {
+    Layout L;
+    Offsets o{};
+    const size_t K = (size_t)pr->n_cols, ldd = (size_t)pr->ldd, G = (size_t)g.G;
+    const size_t ng = (size_t)std::max(pr->n_groups, 1);
+    o.sc = L.add(sizeof(dscr_scalars));
+    o.theta0 = L.add(ldd * 8); o.theta1 = L.add(ldd * 8); o.resid = L.add(ldd * 8);
+    o.corr = L.add(K * 8);
+    o.x0 = L.add(K * 8); o.x1 = L.add(K * 8); o.x2 = L.add(K * 8);
+    o.u0 = L.add(K * 8); o.u1 = L.add(K * 8);
+    o.ycorr = L.add(K * 8); o.star = L.add(K * 8); o.cc = L.add(K * 8); o.cnorm = L.add(ng * 8);
+    o.vec = L.add(ldd * 8); o.dn = L.add(K * 8);
+    const size_t slots = G * (size_t)g.cap;
+    o.act0 = L.add(slots * 4); o.act1 = L.add(slots * 4);
+    o.cnt0 = L.add(G * 4); o.cnt1 = L.add(G * 4);
+    o.off0 = L.add((G + 1) * 4); o.off1 = L.add((G + 1) * 4);
+    o.mask = L.add((size_t)n_units);
+    const size_t ss = G * (size_t)g.sup_cap;
+    o.sidx = L.add(ss * 4); o.sa = L.add(ss * 8); o.sb = L.add(ss * 8);
+    o.supcnt = L.add(G * 4); o.supoff = L.add((G + 1) * 4);
+    o.p1 = L.add(std::max<size_t>(G * NP1, 2 * (size_t)4096) * 8);
+    o.p2 = L.add(G * NP2 * 8);
+    o.p3v = L.add((size_t)g.P * 2 * ldd * 8);
+    o.p3s = L.add((size_t)g.G3b * NP3 * 8);
+    o.tickets = L.add(64);
+    o.trace = L.add((size_t)std::max(cfg->max_iters, 1) * DSCR_TRACE_FIELDS * 8);
+    *total = L.total + 256;
+    return o;
+}
+
+}  // namespace dscr
+
+using namespace dscr;
+
+struct dscr_solver {
+    Params P;
+    Geometry geo;
+    dscr_problem_desc prob;
+    dscr_config cfg;
+    void* ws;
+    cudaStream_t cap_stream = nullptr;
+    cudaGraph_t g_setup = nullptr, g_loop = nullptr;
+    cudaGraphExec_t e_setup = nullptr, e_loop = nullptr;
+    int world = 1, rank = 0;
+    void* comm = nullptr;
+};
+
+extern "C" const char* dscr_last_error(void) { return err_store().c_str(); }
+extern "C" int dscr_abi_version(void) { return DSCR_ABI_VERSION; }
+
+// atoms any `cap` active units can hold: sum of the `cap` largest group sizes
+static int max_atoms_per_slot(const dscr_problem_desc* pr, int cap, int* out) {
+    if (pr->n_groups <= 0) { *out = cap; return DSCR_OK; }
+    std::vector<int> ptr(pr->n_groups + 1);
+    CK(cudaMemcpy(ptr.data(), pr->group_ptr, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    std::vector<int> sz(pr->n_groups);
+    for (int g = 0; g < pr->n_groups; ++g) {
+        sz[g] = ptr[g + 1] - ptr[g];
+        if (sz[g] < 1) return set_inval("groups must be nonempty");
+    }
+    if (ptr[0] != 0 || ptr[pr->n_groups] != pr->n_cols) return set_inval("groups must cover every column");
+    std::sort(sz.begin(), sz.end(), std::greater<int>());
+    long long acc = 0;
+    for (int i = 0; i < std::min(cap, pr->n_groups); ++i) acc += sz[i];
+    *out = (int)std::min<long long>(acc, pr->n_cols);
+    return DSCR_OK;
+}
+
+static int validate(const dscr_problem_desc* pr, const dscr_config* cfg, int* n_units, int* max_gsize) {
+    if (!pr || !cfg) return set_inval("null argument");
+    if (pr->dtype < DSCR_F64 || pr->dtype > DSCR_BF16) return set_inval("unknown dtype");
+    if (pr->n_rows < 1 || pr->n_cols < 1) return set_inval("dictionary must have at least one row and one column");
+    if (pr->ldd < pr->n_rows || pr->ldd % 16) return set_inval("ldd must be >= n_rows and a multiple of 16");
+    if (!(pr->lam > 0)) return set_inval("lam must be strictly positive");
+    if (!pr->D || !pr->y) return set_inval("null device pointer");
+    if (cfg->algorithm < DSCR_ISTA || cfg->algorithm > DSCR_CP) return set_inval("unknown algorithm");
+    if (cfg->strategy < DSCR_NONE || cfg->strategy > DSCR_DYNAMIC) return set_inval("unknown strategy");
+    if (cfg->max_iters < 1) return set_inval("max_iters must be at least 1");
+    if (!(cfg->rel_tol > 0)) return set_inval("rel_tol must be positive");
+    if (!(cfg->backtrack_factor > 1)) return set_inval("backtrack_factor must exceed 1");
+    if (!(cfg->L0 > 0)) return set_inval("L0 must be positive");
+    if (!(cfg->cp_step_safety > 0 && cfg->cp_step_safety < 1)) return set_inval("cp_step_safety must lie in (0, 1)");
+    const bool group = pr->n_groups > 0;
+    if (cfg->strategy != DSCR_NONE) {
+        if (cfg->test < 0) return set_inval("screening strategies require a test kind");
+        bool lasso_test = cfg->test <= DSCR_DOME;
+        if (group == lasso_test) return set_inval("test does not apply to this problem kind");
+    }
+    if ((cfg->algorithm == DSCR_CP || (cfg->algorithm == DSCR_TWIST && !(cfg->twist_step > 0))) && !(cfg->op_norm > 0))
+        return set_inval("op_norm (||D||_2 > 0) is required for this algorithm");
+    *n_units = group ? pr->n_groups : pr->n_cols;
+    *max_gsize = 1;
+    return DSCR_OK;
+}
+
+extern "C" size_t dscr_solver_workspace_size(const dscr_problem_desc* pr, const dscr_config* cfg) {
+    int nu, mg;
+    if (validate(pr, cfg, &nu, &mg) != DSCR_OK) return 0;
+    Geometry g = make_geometry(pr, nu, 1);
+    if (pr->n_groups > 0 && (!pr->group_ptr || max_atoms_per_slot(pr, g.cap, &g.sup_cap) != DSCR_OK)) return 0;
+    size_t total;
+    make_offsets(pr, cfg, g, nu, &total);
+    return total;
+}
+
+static int launch_iteration(dscr_solver* h, cudaStream_t s) {
+    const Params& P = h->P;
+    const Geometry& g = h->geo;
+    const bool group = P.n_groups > 0;
+    const size_t smem1 = (size_t)g.smem1;
+    switch (P.dtype) {
+        case DSCR_F64:
+            if (group) k1_corr_update<double, true><<<g.G, NT, smem1, s>>>(P);
+            else k1_corr_update<double, false><<<g.G, NT, smem1, s>>>(P);
+            break;
+        case DSCR_F32:
+            if (group) k1_corr_update<float, true><<<g.G, NT, smem1, s>>>(P);
+            else k1_corr_update<float, false><<<g.G, NT, smem1, s>>>(P);
+            break;
+        default:
+            if (group) k1_corr_update<__nv_bfloat16, true><<<g.G, NT, smem1, s>>>(P);
+            else k1_corr_update<__nv_bfloat16, false><<<g.G, NT, smem1, s>>>(P);
+    }
+    CK(cudaGetLastError());
+    if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
+    else k2_screen<false><<<g.G, NT, 0, s>>>(P);
+    CK(cudaGetLastError());
+    dim3 g3(g.R, g.P);
+    switch (P.dtype) {
+        case DSCR_F64: k3a_residual<double><<<g3, NT, 0, s>>>(P); break;
+        case DSCR_F32: k3a_residual<float><<<g3, NT, 0, s>>>(P); break;
+        default: k3a_residual<__nv_bfloat16><<<g3, NT, 0, s>>>(P);
+    }
+    CK(cudaGetLastError());
+    k3b_finalize<<<g.G3b, NT, 0, s>>>(P);
+    CK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+template <typename T>
+static int set_smem_attrs(size_t smem) {
+    CK(cudaFuncSetAttribute(k1_corr_update<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k1_corr_update<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    CK(cudaFuncSetAttribute(k_correlate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    return DSCR_OK;
+}
+
+static int launch_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v, double* out,
+                            const int* skip, cudaStream_t s) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const size_t smem = (size_t)ldd * 8;
+    const int grid = std::max(1, std::min((k + NW - 1) / NW, sms * 4));
+    int rc;
+    switch (dtype) {
+        case DSCR_F64:
+            if ((rc = set_smem_attrs<double>(smem))) return rc;
+            k_correlate<double><<<grid, NT, smem, s>>>((const double*)D, ldd, n, k, v, out, skip);
+            break;
+        case DSCR_F32:
+            if ((rc = set_smem_attrs<float>(smem))) return rc;
+            k_correlate<float><<<grid, NT, smem, s>>>((const float*)D, ldd, n, k, v, out, skip);
+            break;
+        default:
+            if ((rc = set_smem_attrs<__nv_bfloat16>(smem))) return rc;
+            k_correlate<__nv_bfloat16><<<grid, NT, smem, s>>>((const __nv_bfloat16*)D, ldd, n, k, v, out, skip);
+    }
+    CK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
+    Params& P = h->P;
+    const Geometry& g = h->geo;
+    const int test = P.test;
+    const bool group = P.n_groups > 0;
+    int rc;
+    k_init<<<256, NT, 0, s>>>(P);
+    CK(cudaGetLastError());
+    k_init_scalars<<<1, NT, 0, s>>>(P);
+    CK(cudaGetLastError());
+    if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.y, P.ycorr, nullptr, s))) return rc;
+    int lgrid = std::max(1, std::min((P.n_units + NT - 1) / NT, 2048));
+    k_lmax<<<lgrid, NT, 0, s>>>(P);
+    CK(cudaGetLastError());
+    const int* stop_flag = &P.sc->stop;
+    if (P.strategy != DSCR_NONE) {
+        if (test == DSCR_DST3 || test == DSCR_DOME) {
+            switch (P.dtype) {
+                case DSCR_F64: k_setup_vec<double><<<32, NT, 0, s>>>(P); break;
+                case DSCR_F32: k_setup_vec<float><<<32, NT, 0, s>>>(P); break;
+                default: k_setup_vec<__nv_bfloat16><<<32, NT, 0, s>>>(P);
+            }
+            CK(cudaGetLastError());
+            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.star, stop_flag, s))) return rc;
+        } else if (test == DSCR_GST3) {
+            switch (P.dtype) {
+                case DSCR_F64: k_setup_vec<double><<<32, NT, 0, s>>>(P); break;
+                case DSCR_F32: k_setup_vec<float><<<32, NT, 0, s>>>(P); break;
+                default: k_setup_vec<__nv_bfloat16><<<32, NT, 0, s>>>(P);
+            }
+            CK(cudaGetLastError());
+            k_gst3_scalars<<<1, NT, 0, s>>>(P);
+            CK(cudaGetLastError());
+            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, s))) return rc;
+        }
+        k_centers<<<std::max(1, std::min((P.kcols + NT - 1) / NT, 1024)), NT, 0, s>>>(P);
+        CK(cudaGetLastError());
+        if (group) {
+            k_center_group_norms<<<std::max(1, std::min((P.n_groups + NT - 1) / NT, 1024)), NT, 0, s>>>(P);
+            CK(cudaGetLastError());
+        }
+        if (P.strategy == DSCR_STATIC) {
+            k_static_radius<<<1, NT, 0, s>>>(P);
+            CK(cudaGetLastError());
+            if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
+            else k2_screen<false><<<g.G, NT, 0, s>>>(P);
+            CK(cudaGetLastError());
+            k_static_done<<<1, 1, 0, s>>>(P);
+            CK(cudaGetLastError());
+        }
+    }
+    return DSCR_OK;
+}
+
+extern "C" {
+int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void* workspace,
+                       size_t workspace_bytes, void* stream, dscr_solver** out) {
+    int nu, mg;
+    int rc = validate(pr, cfg, &nu, &mg);
+    if (rc) return rc;
+    if (!out || !workspace) return set_inval("null output or workspace");
+    if (pr->n_groups > 0 && !(pr->group_ptr && pr->group_w && pr->group_snorm))
+        return set_inval("group problems need group_ptr, group_w and group_snorm");
+    Geometry g = make_geometry(pr, nu, 1);
+    if ((rc = max_atoms_per_slot(pr, g.cap, &g.sup_cap))) return rc;
+    size_t total;
+    Offsets o = make_offsets(pr, cfg, g, nu, &total);
+    if (workspace_bytes < total) return set_inval("workspace too small");
+    dscr_solver* h = new dscr_solver();
+    h->prob = *pr;
+    h->cfg = *cfg;
+    h->geo = g;
+    h->ws = workspace;
+    char* base = (char*)align_up((size_t)workspace, 256);
+    Params& P = h->P;
+    memset(&P, 0, sizeof P);
+    P.D = pr->D; P.ldd = pr->ldd; P.n = pr->n_rows; P.kcols = pr->n_cols; P.dtype = pr->dtype;
+    P.y = pr->y; P.lam = pr->lam;
+    P.n_groups = pr->n_groups; P.gptr = pr->group_ptr; P.gw = pr->group_w; P.gsn = pr->group_snorm;
+    P.n_units = nu;
+    P.algo = cfg->algorithm; P.strategy = cfg->strategy;
+    P.test = (cfg->strategy == DSCR_NONE) ? DSCR_TEST_OFF : cfg->test;
+    P.rel_tol = cfg->rel_tol; P.gap_tol = cfg->gap_tol; P.bt_factor = cfg->backtrack_factor;
+    P.twa = cfg->twist_alpha; P.twb = cfg->twist_beta; P.cp_gamma = cfg->cp_gamma;
+    P.bb_min = cfg->bb_L_min; P.bb_max = cfg->bb_L_max;
+    P.L0 = cfg->L0; P.cp_safety = cfg->cp_step_safety; P.op_norm = cfg->op_norm;
+    P.tw_step = (cfg->twist_step > 0) ? cfg->twist_step : (cfg->op_norm > 0 ? 1.0 / (cfg->op_norm * cfg->op_norm) : 0.0);
+    P.sc = (dscr_scalars*)(base + o.sc);
+    P.theta[0] = (double*)(base + o.theta0); P.theta[1] = (double*)(base + o.theta1);
+    P.resid = (double*)(base + o.resid); P.corr = (double*)(base + o.corr);
+    P.x[0] = (double*)(base + o.x0); P.x[1] = (double*)(base + o.x1); P.x[2] = (double*)(base + o.x2);
+    P.u[0] = (double*)(base + o.u0); P.u[1] = (double*)(base + o.u1);
+    P.ycorr = (double*)(base + o.ycorr); P.star = (double*)(base + o.star); P.cc = (double*)(base + o.cc);
+    P.cnorm = (double*)(base + o.cnorm); P.vec = (double*)(base + o.vec); P.dn = (double*)(base + o.dn);
+    P.act[0] = (int*)(base + o.act0); P.act[1] = (int*)(base + o.act1);
+    P.act_cnt[0] = (int*)(base + o.cnt0); P.act_cnt[1] = (int*)(base + o.cnt1);
+    P.act_off[0] = (int*)(base + o.off0); P.act_off[1] = (int*)(base + o.off1);
+    P.mask = (uint8_t*)(base + o.mask);
+    P.sidx = (int*)(base + o.sidx); P.sa = (double*)(base + o.sa); P.sb = (double*)(base + o.sb);
+    P.sup_cnt = (int*)(base + o.supcnt); P.sup_off = (int*)(base + o.supoff); P.sup_cap = g.sup_cap;
+    P.p1 = (double*)(base + o.p1); P.p2 = (double*)(base + o.p2); P.p3v = (double*)(base + o.p3v);
+    P.p3s = (double*)(base + o.p3s); P.tickets = (unsigned*)(base + o.tickets);
+    P.trace = (double*)(base + o.trace);
+    P.max_iters = cfg->max_iters;
+    P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
+    P.col_offset = pr->col_offset;
+
+    cudaStream_t us = (cudaStream_t)stream;
+    // smem attributes for the K1 instantiations
+    switch (P.dtype) {
+        case DSCR_F64: rc = set_smem_attrs<double>(g.smem1); break;
+        case DSCR_F32: rc = set_smem_attrs<float>(g.smem1); break;
+        default: rc = set_smem_attrs<__nv_bfloat16>(g.smem1);
+    }
+    if (rc) { delete h; return rc; }
+    cudaError_t e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) { delete h; return set_err("cudaStreamCreate", e); }
+    // tickets must start at zero before any kernel runs
+    e = cudaMemsetAsync(P.tickets, 0, 64, us);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("cudaMemsetAsync", e); }
+
+    // ---- setup graph (plain capture)
+    cudaStream_t cs = h->cap_stream;
+    e = cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("capture setup", e); }
+    rc = enqueue_setup(h, cs);
+    cudaGraph_t gs = nullptr;
+    e = cudaStreamEndCapture(cs, &gs);
+    if (rc || e != cudaSuccess) { if (gs) cudaGraphDestroy(gs); dscr_solver_destroy(h); return rc ? rc : set_err("end capture setup", e); }
+    h->g_setup = gs;
+    e = cudaGraphInstantiate(&h->e_setup, gs, 0);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("instantiate setup", e); }
+
+    // ---- loop graph: k_preloop -> WHILE(h_main) { K1; K2; K3a; K3b }
+    cudaGraph_t gl;
+    e = cudaGraphCreate(&gl, 0);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("graph create", e); }
+    h->g_loop = gl;
+    e = cudaGraphConditionalHandleCreate(&P.h_main, gl, 0, 0);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("conditional handle", e); }
+    e = cudaStreamBeginCaptureToGraph(cs, gl, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("capture preloop", e); }
+    k_preloop<<<1, 1, 0, cs>>>(P);
+    e = cudaGetLastError();
+    cudaGraph_t tmp = nullptr;
+    cudaError_t e2 = cudaStreamEndCapture(cs, &tmp);
+    if (e != cudaSuccess || e2 != cudaSuccess) { dscr_solver_destroy(h); return set_err("capture preloop", e != cudaSuccess ? e : e2); }
+    size_t nn = 0;
+    cudaGraphGetNodes(gl, nullptr, &nn);
+    cudaGraphNode_t pre = nullptr;
+    if (nn != 1 || cudaGraphGetNodes(gl, &pre, &nn) != cudaSuccess) { dscr_solver_destroy(h); return set_inval("unexpected preloop graph"); }
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = P.h_main;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    e = cudaGraphAddNode(&cnode, gl, &pre, 1, &cp);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("add WHILE node", e); }
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("capture body", e); }
+    rc = launch_iteration(h, cs);
+    e = cudaStreamEndCapture(cs, &tmp);
+    if (rc || e != cudaSuccess) { dscr_solver_destroy(h); return rc ? rc : set_err("end capture body", e); }
+    e = cudaGraphInstantiate(&h->e_loop, gl, 0);
+    if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("instantiate loop", e); }
+    *out = h;
+    return DSCR_OK;
+}
+
+int dscr_solver_setup(dscr_solver* h, void* stream) {
+    if (!h) return set_inval("null handle");
+    CK(cudaGraphLaunch(h->e_setup, (cudaStream_t)stream));
+    return DSCR_OK;
+}
+
+int dscr_solver_run(dscr_solver* h, int iteration_limit, void* stream) {
+    if (!h) return set_inval("null handle");
+    cudaStream_t s = (cudaStream_t)stream;
+    k_set_limit<<<1, 1, 0, s>>>(h->P.sc, iteration_limit > 0 ? iteration_limit : 0x7fffffff);
+    CK(cudaGetLastError());
+    CK(cudaGraphLaunch(h->e_loop, s));
+    return DSCR_OK;
+}
+
+int dscr_solver_scalars(dscr_solver* h, void* stream, dscr_scalars* out) {
+    if (!h || !out) return set_inval("null argument");
+    CK(cudaStreamSynchronize((cudaStream_t)stream));
+    CK(cudaMemcpy(out, h->P.sc, sizeof(dscr_scalars), cudaMemcpyDeviceToHost));
+    return DSCR_OK;
+}
+
+int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* b) {
+    if (!h || !b) return set_inval("null argument");
+    const Params& P = h->P;
+    b->scalars = P.sc;
+    b->theta[0] = P.theta[0]; b->theta[1] = P.theta[1];
+    b->resid = P.resid; b->corr = P.corr;
+    b->x[0] = P.x[0]; b->x[1] = P.x[1]; b->x[2] = P.x[2];
+    b->u[0] = P.u[0]; b->u[1] = P.u[1];
+    b->y_corr = P.ycorr; b->star_corr = P.star; b->cc = P.cc; b->cnorm = P.cnorm;
+    b->act[0] = P.act[0]; b->act[1] = P.act[1];
+    b->act_cnt[0] = P.act_cnt[0]; b->act_cnt[1] = P.act_cnt[1];
+    b->act_off[0] = P.act_off[0]; b->act_off[1] = P.act_off[1];
+    b->mask = P.mask; b->trace = P.trace;
+    b->G = P.G; b->cap = P.cap;
+    return DSCR_OK;
+}
+
+int dscr_solver_destroy(dscr_solver* h) {
+    if (!h) return DSCR_OK;
+    if (h->e_loop) cudaGraphExecDestroy(h->e_loop);
+    if (h->e_setup) cudaGraphExecDestroy(h->e_setup);
+    if (h->g_loop) cudaGraphDestroy(h->g_loop);
+    if (h->g_setup) cudaGraphDestroy(h->g_setup);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    delete h;
+    return DSCR_OK;
+}
+
+}  // extern "C"

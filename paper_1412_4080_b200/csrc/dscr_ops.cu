@@ -1,0 +1,350 @@
+// Kernel-level C-ABI entry points of libdynscreen.so.  Each one replaces a
+// reference per-op function (cited at the entry point) and uses the same
+// device building blocks as the solver engine, so unit parity here covers the
+// engine's arithmetic.
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdio.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "dynscreen.h"
+#include "dscr_device.cuh"
+
+namespace dscr {
+namespace ops {
+
+
+static int cuda_err(const char* what, cudaError_t e) {
+    char buf[512];
+    snprintf(buf, sizeof buf, "%s: %s", what, cudaGetErrorString(e));
+    err_store() = buf;
+    return DSCR_ECUDA;
+}
+static int inval(const char* what) {
+    err_store() = what;
+    return DSCR_EINVAL;
+}
+#define OCK(call)                                            \
+    do {                                                     \
+        cudaError_t e_ = (call);                             \
+        if (e_ != cudaSuccess) return cuda_err(#call, e_);   \
+    } while (0)
+
+static int sm_count() {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    return sms;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_corr(const T* __restrict__ D, int ldd, int n, int k,
+                                             const double* __restrict__ v, double* out, int nvec,
+                                             int ldv, int ldo) {
+    extern __shared__ double s_v[];
+    for (int q = 0; q < nvec; ++q)
+        for (int i = threadIdx.x; i < ldd; i += NT) s_v[q * ldd + i] = (i < n) ? v[(size_t)q * ldv + i] : 0.0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
+    const int nwarps = (gridDim.x * NT) >> 5;
+    for (int j = gw; j < k; j += nwarps) {
+        for (int q = 0; q < nvec; ++q) {
+            double c = warp_dot<T, 4>(D + (size_t)j * ldd, n, s_v + (size_t)q * ldd, lane);
+            if (lane == 0) out[(size_t)q * ldo + j] = c;
+        }
+    }
+}
+
+// out[:, q] = D x[:, q]; thread owns V consecutive rows, loops over columns in order
+template <typename T>
+__global__ void __launch_bounds__(NT) k_apply(const T* __restrict__ D, int ldd, int n, int k,
+                                              const double* __restrict__ x, double* out, int nvec,
+                                              int ldx, int ldo) {
+    constexpr int V = Vec<T>::V;
+    const int r0 = (blockIdx.x * NT + threadIdx.x) * V;
+    if (r0 >= ldd) return;
+    for (int q = 0; q < nvec; ++q) {
+        double acc[V];
+#pragma unroll
+        for (int v = 0; v < V; ++v) acc[v] = 0.0;
+        if (r0 < n) {
+            for (int j = 0; j < k; ++j) {
+                const double a = x[(size_t)q * ldx + j];
+                if (a == 0.0) continue;
+                double d[V];
+                Vec<T>::load(D + (size_t)j * ldd + r0, d);
+#pragma unroll
+                for (int v = 0; v < V; ++v) acc[v] = fma(a, d[v], acc[v]);
+            }
+        }
+#pragma unroll
+        for (int v = 0; v < V; ++v)
+            if (r0 + v < ldd) out[(size_t)q * ldo + r0 + v] = (r0 + v < n) ? acc[v] : 0.0;
+    }
+}
+
+__global__ void k_soft(const double* v, int64_t n, double t, double* out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = soft(v[i], t);
+}
+
+__global__ void k_group_shrink(const double* v, const int* gptr, int ng, const double* w, double t,
+                               double* out) {
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < ng; g += gridDim.x * blockDim.x) {
+        const int j0 = gptr[g], j1 = gptr[g + 1];
+        const double nv = sqrt(np_segment_sum([&](int i) { double a = v[i]; return a * a; }, j0, j1 - j0));
+        const double fac = (nv > 0.0) ? fmax(1.0 - t * w[g] / nv, 0.0) : 0.0;   // dictionary.py:297-300
+        for (int j = j0; j < j1; ++j) out[j] = v[j] * fac;
+    }
+}
+
+__global__ void k_test_sphere(const double* cc, const int* kept, int nk, double r, uint8_t* m) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nk; i += gridDim.x * blockDim.x)
+        m[i] = ((1.0 - fabs(cc[kept[i]])) - r > SCREEN_MARGIN) ? 1 : 0;
+}
+
+__global__ void k_test_dome(const double* tcorr, const double* ucorr, const int* kept, int nk,
+                            double lam, double lstar, double radius, uint8_t* m) {
+    const double shift = lstar / lam - 1.0;
+    const double rs = hypot(radius, shift);
+    const double cut = (rs > 0.0) ? shift / rs : 0.0;
+    const double slope = lstar - lam, flat = lam * (1.0 - rs), mg = lam * SCREEN_MARGIN;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nk; i += gridDim.x * blockDim.x) {
+        if (radius >= 1.0) { m[i] = 0; continue; }
+        const double t = tcorr[kept[i]], u = ucorr[kept[i]];
+        const double arc = (lam * radius) * sqrt(fmax(1.0 - t * t, 0.0));
+        const double lower = (t < cut) ? (slope * t - lam) + arc : -flat;
+        const double upper = (t <= -cut) ? flat : (slope * t + lam) - arc;
+        m[i] = ((u - lower > mg) && (upper - u > mg)) ? 1 : 0;
+    }
+}
+
+__global__ void k_test_group(const double* w, const double* cn, const double* sn, const int* kg, int nk,
+                             double r, uint8_t* m) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nk; i += gridDim.x * blockDim.x) {
+        const int g = kg[i];
+        m[i] = ((w[g] - cn[g]) / sn[g] - r > SCREEN_MARGIN) ? 1 : 0;
+    }
+}
+
+// sums[0..4] = q1.z1, q1.z2, q2.z1, q2.z2 (h), and z1.z1, z1.z2, z2.z2 (for QR)
+__global__ void __launch_bounds__(NT) k_pw_dots(const double* q, const double* z, int dim, int ld,
+                                                int nvec, double* sums) {
+    __shared__ double s_sh[64];
+    double a[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int i = threadIdx.x; i < dim; i += NT) {
+        const double q1 = q[i], z1 = z[i];
+        const double q2 = nvec > 1 ? q[ld + i] : 0.0, z2 = nvec > 1 ? z[ld + i] : 0.0;
+        a[0] = fma(q1, z1, a[0]); a[1] = fma(q1, z2, a[1]); a[2] = fma(q2, z1, a[2]); a[3] = fma(q2, z2, a[3]);
+        a[4] = fma(z1, z1, a[4]); a[5] = fma(z1, z2, a[5]); a[6] = fma(z2, z2, a[6]);
+    }
+    for (int k = 0; k < 7; ++k) {
+        double r = block_sum(a[k], s_sh);
+        if (threadIdx.x == 0) sums[k] = r;
+    }
+}
+
+// q1 = z1 / r11 ; q2 = (z2 - r12 q1) / r22  (Gram-Schmidt of the 2-column block)
+__global__ void k_pw_qr(double* q, const double* z, int dim, int ld, int nvec, double r11, double r12,
+                        double r22) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < dim; i += gridDim.x * blockDim.x) {
+        const double q1 = z[i] / r11;
+        q[i] = q1;
+        if (nvec > 1) q[ld + i] = (z[ld + i] - r12 * q1) / r22;
+    }
+}
+
+template <typename T>
+static int corr_launch(const void* D, int ldd, int n, int k, const double* v, double* out, int nvec,
+                       int ldv, int ldo, cudaStream_t s) {
+    const size_t smem = (size_t)ldd * 8 * nvec;
+    OCK(cudaFuncSetAttribute(k_corr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int grid = std::max(1, std::min((k + NW - 1) / NW, sm_count() * 4));
+    k_corr<T><<<grid, NT, smem, s>>>((const T*)D, ldd, n, k, v, out, nvec, ldv, ldo);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+template <typename T>
+static int apply_launch(const void* D, int ldd, int n, int k, const double* x, double* out, int nvec,
+                        int ldx, int ldo, cudaStream_t s) {
+    constexpr int V = Vec<T>::V;
+    const int grid = (ldd + NT * V - 1) / (NT * V);
+    k_apply<T><<<grid, NT, 0, s>>>((const T*)D, ldd, n, k, x, out, nvec, ldx, ldo);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+static int corr_any(int dt, const void* D, int ldd, int n, int k, const double* v, double* out, int nvec,
+                    int ldv, int ldo, cudaStream_t s) {
+    if (dt == DSCR_F64) return corr_launch<double>(D, ldd, n, k, v, out, nvec, ldv, ldo, s);
+    if (dt == DSCR_F32) return corr_launch<float>(D, ldd, n, k, v, out, nvec, ldv, ldo, s);
+    return corr_launch<__nv_bfloat16>(D, ldd, n, k, v, out, nvec, ldv, ldo, s);
+}
+static int apply_any(int dt, const void* D, int ldd, int n, int k, const double* x, double* out, int nvec,
+                     int ldx, int ldo, cudaStream_t s) {
+    if (dt == DSCR_F64) return apply_launch<double>(D, ldd, n, k, x, out, nvec, ldx, ldo, s);
+    if (dt == DSCR_F32) return apply_launch<float>(D, ldd, n, k, x, out, nvec, ldx, ldo, s);
+    return apply_launch<__nv_bfloat16>(D, ldd, n, k, x, out, nvec, ldx, ldo, s);
+}
+
+static int check_dict(int dt, const void* D, int ldd, int n, int k) {
+    if (dt < DSCR_F64 || dt > DSCR_BF16) return inval("unknown dtype");
+    if (!D || n < 1 || k < 1 || ldd < n || ldd % 16) return inval("bad dictionary shape or ldd");
+    return DSCR_OK;
+}
+
+}  // namespace ops
+}  // namespace dscr
+
+using namespace dscr;
+using namespace dscr::ops;
+
+extern "C" {
+
+
+int dscr_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v, double* out,
+                   void* stream) {
+    int rc = check_dict(dtype, D, ldd, n, k);
+    if (rc) return rc;
+    return corr_any(dtype, D, ldd, n, k, v, out, 1, ldd, k, (cudaStream_t)stream);
+}
+
+int dscr_apply(int dtype, const void* D, int ldd, int n, int k, const double* x, double* out, void* stream) {
+    int rc = check_dict(dtype, D, ldd, n, k);
+    if (rc) return rc;
+    return apply_any(dtype, D, ldd, n, k, x, out, 1, k, ldd, (cudaStream_t)stream);
+}
+
+int dscr_prox_l1(const double* v, int64_t n, double t, double* out, void* stream) {
+    if (t < 0) return inval("threshold must be nonnegative");
+    if (n <= 0) return DSCR_OK;
+    const int grid = (int)std::min<int64_t>((n + 255) / 256, 4096);
+    k_soft<<<grid, 256, 0, (cudaStream_t)stream>>>(v, n, t, out);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_prox_group(const double* v, const int32_t* gptr, int ng, const double* w, double t, double* out,
+                    void* stream) {
+    if (t < 0) return inval("threshold must be nonnegative");
+    if (ng <= 0) return DSCR_OK;
+    k_group_shrink<<<std::max(1, std::min((ng + 255) / 256, 4096)), 256, 0, (cudaStream_t)stream>>>(v, gptr, ng, w, t, out);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_test_sphere(const double* cc, const int32_t* kept, int nk, double r, uint8_t* m, void* stream) {
+    if (nk <= 0) return DSCR_OK;
+    k_test_sphere<<<std::max(1, std::min((nk + 255) / 256, 4096)), 256, 0, (cudaStream_t)stream>>>(cc, kept, nk, r, m);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_test_dome(const double* tc, const double* uc, const int32_t* kept, int nk, double lam, double lstar,
+                   double radius, uint8_t* m, void* stream) {
+    if (nk <= 0) return DSCR_OK;
+    k_test_dome<<<std::max(1, std::min((nk + 255) / 256, 4096)), 256, 0, (cudaStream_t)stream>>>(tc, uc, kept, nk, lam, lstar, radius, m);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_test_group(const double* w, const double* cn, const double* sn, const int32_t* kg, int nk, double r,
+                    uint8_t* m, void* stream) {
+    if (nk <= 0) return DSCR_OK;
+    k_test_group<<<std::max(1, std::min((nk + 255) / 256, 4096)), 256, 0, (cudaStream_t)stream>>>(w, cn, sn, kg, nk, r, m);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+size_t dscr_operator_norm_work_size(int ldd, int k) {
+    return (6 * (size_t)std::max(ldd, k) + 64) * sizeof(double);
+}
+
+// 2-vector block power iteration for the top eigenvalue of D^T D
+// (dictionary.py:120-171): start block [ones, alternating], orthonormalised;
+// stop when the top Rayleigh value is stable to tol * max(1, value).
+int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double tol, int max_iters, void* work,
+                       double* out_host, void* stream) {
+    int rc = check_dict(dtype, D, ldd, n, k);
+    if (rc) return rc;
+    if (!work || !out_host) return inval("null work or output");
+    cudaStream_t s = (cudaStream_t)stream;
+    const bool small_cols = k <= n;           // operate on the smaller side of the Gram operator
+    const int dim = small_cols ? k : n;
+    const int ldq = small_cols ? k : ldd;     // leading dim of q and z (length-dim vectors)
+    const int ldw = small_cols ? ldd : k;     // leading dim of the intermediate
+    const int nvec = dim > 1 ? 2 : 1;
+    const size_t M = (size_t)std::max(ldd, k);
+    double* q = (double*)work;      // [2][ldq]
+    double* z = q + 2 * M;          // [2][ldq]
+    double* w = z + 2 * M;          // [2][ldw]
+    double* sums = w + 2 * M;       // 7 inner products
+    // start block: ones and (+1,-1,+1,...) ; Gram-Schmidt QR (same span as np.linalg.qr)
+    std::vector<double> h0(2 * (size_t)ldq, 0.0);
+    for (int i = 0; i < dim; ++i) { h0[i] = 1.0; h0[ldq + i] = (i & 1) ? -1.0 : 1.0; }
+    {
+        double n1 = std::sqrt((double)dim);
+        double dot = 0.0;
+        for (int i = 0; i < dim; ++i) dot += h0[ldq + i] / n1;
+        double n2 = 0.0;
+        std::vector<double> q2(dim);
+        for (int i = 0; i < dim; ++i) { q2[i] = h0[ldq + i] - dot * (1.0 / n1); n2 += q2[i] * q2[i]; }
+        n2 = std::sqrt(n2);
+        for (int i = 0; i < dim; ++i) { h0[i] = 1.0 / n1; h0[ldq + i] = (nvec > 1 && n2 > 0) ? q2[i] / n2 : 0.0; }
+    }
+    OCK(cudaMemsetAsync(work, 0, dscr_operator_norm_work_size(ldd, k), s));
+    OCK(cudaMemcpyAsync(q, h0.data(), sizeof(double) * h0.size(), cudaMemcpyHostToDevice, s));
+    double val = NAN;
+    bool have = false;
+    double hs[7];
+    for (int it = 0; it < max_iters; ++it) {
+        if (small_cols) {
+            if ((rc = apply_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, s))) return rc;
+            if ((rc = corr_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, s))) return rc;
+        } else {
+            if ((rc = corr_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, s))) return rc;
+            if ((rc = apply_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, s))) return rc;
+        }
+        k_pw_dots<<<1, NT, 0, s>>>(q, z, dim, ldq, nvec, sums);
+        OCK(cudaGetLastError());
+        OCK(cudaMemcpyAsync(hs, sums, sizeof hs, cudaMemcpyDeviceToHost, s));
+        OCK(cudaStreamSynchronize(s));
+        double top;
+        if (nvec > 1) {
+            const double a = hs[0], b = 0.5 * (hs[1] + hs[2]), c = hs[3];
+            top = 0.5 * (a + c) + std::sqrt(0.25 * (a - c) * (a - c) + b * b);
+        } else {
+            top = hs[0];
+        }
+        if (have && std::fabs(top - val) <= tol * std::max(1.0, std::fabs(top))) {
+            *out_host = std::sqrt(std::max(top, 0.0));
+            return DSCR_OK;
+        }
+        val = top;
+        have = true;
+        const double r11 = std::sqrt(hs[4]);
+        if (!(r11 > 0)) {   // block fell into the null space: restart on basis axes
+            std::vector<double> hb(2 * (size_t)ldq, 0.0);
+            hb[(size_t)(it % dim)] = 1.0;
+            if (nvec > 1) hb[ldq + (size_t)((it + 1) % dim)] = 1.0;
+            OCK(cudaMemcpyAsync(q, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice, s));
+            OCK(cudaStreamSynchronize(s));
+            have = false;
+            continue;
+        }
+        const double r12 = hs[5] / r11;
+        const double r22 = std::sqrt(std::max(hs[6] - r12 * r12, 0.0));
+        k_pw_qr<<<std::max(1, std::min((dim + 255) / 256, 1024)), 256, 0, s>>>(q, z, dim, ldq, nvec, r11, r12,
+                                                                                r22 > 0 ? r22 : 1.0);
+        OCK(cudaGetLastError());
+    }
+    *out_host = std::sqrt(std::max(val, 0.0));
+    return DSCR_OK;
+}
+}
