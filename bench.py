@@ -1,0 +1,465 @@
+"""Benchmark of the screened-solver hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c4]
+
+One *step* is one solve of the workload to its duality-gap tolerance (for the
+default workload c4: N=8192 x K=262144 fp32 dictionary, FISTA + dynamic ST3,
+lam = 0.2 lam*, gap 1e-5).  ``value`` = iterations per second of device time
+with the dictionary resident in HBM; ``e2e`` = the same metric through the
+public ``run()`` call from pinned host buffers (dictionary H2D inside the
+timed region).  ``roofline`` is measured live for the dominant kernel (K1, the
+correlation pass) with CUDA events on its stream; ``cpu_baseline`` times the
+CPU oracle (a numpy restatement of the reference solver) on a bounded sample.
+
+``--impl reference`` times the reference algorithm's CPU implementation (the
+oracle port; the reference itself is pure Python and has no other runnable
+form on the GPU box) on the same workload, rank 0 only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+with open(os.path.join(ROOT, "BASELINE.json")) as _fh:
+    BASELINE = json.load(_fh)
+METRIC = BASELINE["metric"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4"), default="c4")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--profile-only", action="store_true", help="direct-launch iterations for ncu")
+    ap.add_argument("--cpu-sample-iters", type=int, default=5)
+    ap.add_argument("--seed", type=int, default=0)
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# workload construction (host, seeded)
+# ---------------------------------------------------------------------------
+
+
+def build_workload(name, seed, pinned=False):
+    from paper_1412_4080_b200 import workloads as wl
+    if name == "c1":
+        return [wl.config1(seed=seed)]
+    if name == "c2":
+        return [wl.config2(seed=seed, ratio=r) for r in (0.1, 0.3, 0.5, 0.7, 0.9)]
+    if name == "c3":
+        return [wl.config3(seed=seed)]
+    if pinned:
+        import torch
+        n, k = 8192, 262144
+        host = torch.empty((k, n), dtype=torch.float32, pin_memory=True)
+        D = host.numpy().T                       # (n, k) column-major view of pinned memory
+        blk = 4096
+        from concurrent.futures import ThreadPoolExecutor
+        jobs = [(n, min(blk, k - c0), seed, b) for b, c0 in enumerate(range(0, k, blk))]
+        with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 8)) as pool:
+            for job, arr in zip(jobs, pool.map(wl._fp32_gaussian_block, jobs)):
+                c0 = job[3] * blk
+                D[:, c0:c0 + arr.shape[1]] = arr
+        y = wl.gaussian_observation(n, seed)
+        corr = np.concatenate([D[:, c0:c0 + 16384].astype(np.float64).T @ y for c0 in range(0, k, 16384)])
+        lam = 0.2 * float(np.max(np.abs(corr)))
+        w = wl.Workload("c4", D, y, lam, algorithm="fista", test="dst3", gap_tol=1e-5, dtype="f32")
+        w.meta["host_tensor"] = host
+        return [w]
+    return [wl.config4(seed=seed)]
+
+
+def spec_L(ds, dic):
+    """Step constant L = ||D||_2^2 (BASELINE: step 1/||D||^2), by GPU power iteration.
+
+    The Rayleigh value under-estimates ||D||^2 by up to ~(change per step)/(1 - ratio);
+    the 1e-6 relative margin keeps L above it so backtracking never fires."""
+    nrm = ds.operator_norm(dic, tol=1e-11, max_iters=20000)
+    return nrm * nrm * (1.0 + 1e-6)
+
+
+def make_problems(ds, works):
+    out = []
+    cache = {}
+    for w in works:
+        key = id(w.D)
+        if key not in cache:
+            dic = ds.Dictionary(w.D, check_unit_norms=(w.dtype == "f64"), dtype=w.dtype)
+            if "host_tensor" in w.meta:
+                dic._host_tensor = w.meta["host_tensor"]     # pinned (K, N) view of the same bytes
+            part = None
+            if w.groups is not None:
+                part = ds.GroupPartition.build(dic, w.groups)
+            cache[key] = (dic, part, spec_L(ds, dic))
+        dic, part, L = cache[key]
+        prob = ds.Problem(dic, w.y, w.lam, part)
+        cfg = ds.SolverConfig(algorithm=w.algorithm, strategy="dynamic", test=w.test, max_iters=w.max_iters,
+                              rel_tol=1e-300, L0=L, gap_tol=w.gap_tol)
+        out.append((prob, cfg))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# clocks sampled during the timed region
+# ---------------------------------------------------------------------------
+
+
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"], "samples": 0}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline / reference arm (oracle port, bounded sample)
+# ---------------------------------------------------------------------------
+
+
+def cpu_sample(works, problems, iters):
+    """Time the CPU oracle on the first `iters` iterations of the workload's solves."""
+    from oracle import screen_oracle as so
+    tot_t, tot_it = 0.0, 0
+    cache = {}
+    for w, (prob, cfg) in zip(works, problems):
+        key = id(w.D)
+        if key not in cache:
+            D64 = prob.dictionary.as_float64()
+            cache[key] = np.asfortranarray(D64)
+        op = so.OProblem(cache[key], w.y, w.lam, w.groups and [np.asarray(g) for g in w.groups],
+                         None if w.groups is None else np.sqrt([len(g) for g in w.groups]),
+                         None if w.groups is None else np.asarray(prob.partition.spectral_norms))
+        ocfg = so.Config(algorithm=cfg.algorithm, strategy=cfg.strategy, test=cfg.test, max_iters=iters,
+                         rel_tol=1e-300, L0=cfg.L0, gap_tol=cfg.gap_tol)
+        t0 = time.perf_counter()
+        r = so.solve(op, ocfg)
+        tot_t += time.perf_counter() - t0
+        tot_it += r.iterations
+    return tot_it, tot_t
+
+
+def cpu_cores():
+    try:
+        from threadpoolctl import threadpool_info
+        info = threadpool_info()
+        n = max((i.get("num_threads", 0) for i in info), default=0)
+        if n:
+            return int(n)
+    except Exception:
+        pass
+    return os.cpu_count() or 1
+
+
+# ---------------------------------------------------------------------------
+# main
+# ---------------------------------------------------------------------------
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import paper_1412_4080_b200 as ds  # noqa: F401  (host types / generators only)
+    works = build_workload(args.workload, args.seed)
+    # the reference arm shares the host problem definition; L from the host power iteration
+    from oracle import screen_oracle as so
+    Ls = {}
+    probs = []
+    for w in works:
+        key = id(w.D)
+        if key not in Ls:
+            D64 = np.asfortranarray(np.asarray(w.D, dtype=np.float64))
+            if D64.size > 2e8:
+                # host power iteration on 8 GiB would take minutes; Gaussian unit-norm columns have
+                # ||D||^2 ~ (1 + sqrt(K/N))^2 (Marchenko-Pastur edge).  Only the timing uses it.
+                L = (1.0 + np.sqrt(D64.shape[1] / D64.shape[0])) ** 2 * 1.01
+            else:
+                L = so.operator_norm(D64) ** 2 * (1 + 1e-6)
+            Ls[key] = (D64, L)
+        D64, L = Ls[key]
+        probs.append((D64, L))
+    samples = []
+    for i in range(args.warmup + args.steps):
+        tt, it = 0.0, 0
+        for w, (D64, L) in zip(works, probs):
+            op = so.OProblem(D64, w.y, w.lam, w.groups,
+                             None if w.groups is None else np.sqrt([len(g) for g in w.groups]),
+                             None if w.groups is None else np.array([np.sqrt(so.power_top_eig(D64[:, g])) for g in w.groups]))
+            cfg = so.Config(algorithm=w.algorithm, strategy="dynamic", test=w.test,
+                            max_iters=args.cpu_sample_iters, rel_tol=1e-300, L0=L, gap_tol=w.gap_tol)
+            t0 = time.perf_counter()
+            r = so.solve(op, cfg)
+            tt += time.perf_counter() - t0
+            it += r.iterations
+        if i >= args.warmup:
+            samples.append((it, tt))
+    it = sum(s[0] for s in samples)
+    tt = sum(s[1] for s in samples)
+    v = it / tt
+    cores = cpu_cores()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(1, len(samples)),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": args.workload},
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port",
+                         "sample": f"first {args.cpu_sample_iters} iterations of each solve of {args.workload} "
+                                   f"(setup included, as reference run() times it), fp64 numpy oracle"},
+        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    world, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_1412_4080_b200 as ds
+    from paper_1412_4080_b200 import _native as nat
+    from paper_1412_4080_b200.solver import Engine
+
+    works = build_workload(args.workload, args.seed, pinned=(args.workload == "c4"))
+    problems = make_problems(ds, works)
+    elem = {"f64": 8, "f32": 4, "bf16": 2}[works[0].dtype]
+    n = works[0].D.shape[0]
+    stream = torch.cuda.current_stream(dev)
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    if args.profile_only:
+        eng = Engine(*problems[0], device=dev)
+        eng.setup()
+        ms = (nat.C.c_float * 4)()
+        nat.check(eng.L.dscr_solver_profile(eng.h, 5, eng.sptr, ms))
+        print(json.dumps({"profile_ms": list(ms)}), flush=True)
+        eng.close()
+        return
+
+    # ---- device-resident solves: warmup, then K timed steps back to back
+    def prepare():
+        return [Engine(p, c, device=dev) for p, c in problems]
+
+    for _ in range(args.warmup):
+        engs = prepare()
+        for e in engs:
+            e.setup()
+            e.launch(0)
+        torch.cuda.synchronize()
+        for e in engs:
+            e.close()
+    steps = [prepare() for _ in range(args.steps)]
+    torch.cuda.synchronize()
+    barrier()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        ev0.record(stream)
+        for engs in steps:
+            for e in engs:
+                e.setup()
+                e.launch(0)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    dev_s = ev0.elapsed_time(ev1) / 1e3
+    if world > 1:
+        t = torch.tensor([dev_s], device=dev)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        dev_s = float(t.item())
+    iters, trips, streamed_cols, solve_times = 0, 0, 0, []
+    kernels = 0
+    for engs in steps:
+        for e, (p, c) in zip(engs, problems):
+            sc = e.scalars()
+            if sc.status != 0:
+                raise RuntimeError(f"solver status {sc.status}")
+            iters += sc.t
+            trips += sc.trips
+            rows = e.trace_rows(sc.t)
+            prev = p.n_cols
+            for r in rows:
+                streamed_cols += prev + int(r[nat.TR_SUPPORT])
+                prev = int(r[nat.TR_KEPT])
+            kernels += 4 * sc.trips + 2 + setup_launches(c)
+            e.close()
+    per_step_iters = iters / args.steps
+    value = world * iters / dev_s
+    alg_bytes = streamed_cols * n * elem
+    solve_gbs = world * alg_bytes / dev_s / 1e9
+
+    # ---- roofline of the dominant kernel (K1), CUDA events on its stream
+    eng = Engine(*problems[0], device=dev)
+    eng.setup()
+    ms = (nat.C.c_float * 4)()
+    nat.check(eng.L.dscr_solver_profile(eng.h, 5, eng.sptr, ms))
+    sc = eng.scalars()
+    eng.close()
+    k1_bytes = problems[0][0].n_cols * n * elem   # no screening in the profiled trips of c4
+    k1_s = ms[0] / 1e3
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback"
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as fh:
+            peak = float(json.load(fh).get("hbm_gbs", peak))
+        peak_src = "measured"
+    achieved = k1_bytes / k1_s / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", f"k1_dram_bytes_{args.workload}.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get("dram_bytes_per_launch")
+
+    # ---- end to end through run() with host buffers (pinned), H2D inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        its, h2d, d2h = 0, 0, 0
+        torch.cuda.synchronize()
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            for p, c in problems:
+                p.dictionary.drop_device()
+                p.dictionary.__dict__.pop("_problem_cache", None)
+                r = ds.run(p, c, device=dev)
+                its += r.iterations
+                h2d += p.dictionary.data.nbytes + p.n_rows * 8
+                d2h += p.n_cols * 8 + r.iterations * nat.TRACE_FIELDS * 8
+        torch.cuda.synchronize()
+        e2e_s = time.perf_counter() - t0
+        if world > 1:
+            t = torch.tensor([e2e_s], device=dev)
+            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+            e2e_s = float(t.item())
+        e2e = {"value": world * its / e2e_s, "unit": "iters/s", "h2d_bytes_per_step": h2d // args.steps,
+               "d2h_bytes_per_step": d2h // args.steps, "seconds_per_step": e2e_s / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        it, tt = cpu_sample(works, problems, args.cpu_sample_iters)
+        cpu = {"value": it / tt, "unit": "iters/s", "cores": cpu_cores(), "kind": "port",
+               "sample": f"first {args.cpu_sample_iters} iterations of each {args.workload} solve, fp64 numpy "
+                         f"oracle on the same (upcast) dictionary, setup included"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
+            "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
+            "dtype": works[0].dtype, "data": "synthetic (seeded Philox, see DESIGN.md)",
+            "config": {"workload": args.workload, "n": n, "k": problems[0][0].n_cols,
+                       "algorithm": works[0].algorithm, "test": works[0].test, "gap_tol": works[0].gap_tol,
+                       "iterations_per_step": per_step_iters, "time_to_gap_s": dev_s / args.steps,
+                       "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+                       "l2": "dictionary larger than the 126 MB L2" if works[0].D.nbytes > 126e6
+                             else "dictionary fits in L2 (no flush between steps)",
+                       "accumulate": "fp64"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "k1_corr_update", "kernel_ms": ms[0],
+                         "bytes_per_launch": k1_bytes, "per_kernel_ms": list(ms)},
+            "solve_hbm_gbs": solve_gbs,
+            "gpu_launches": kernels,
+            "clocks": clocks.summary(),
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+def setup_launches(cfg):
+    n = 4
+    if cfg.strategy != "none":
+        n += {"dst3": 2, "dome": 2, "gst3": 3}.get(cfg.test, 0) + 1
+        if cfg.test in ("gsafe", "gst3"):
+            n += 1
+        if cfg.strategy == "static":
+            n += 3
+    return n
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -141,7 +141,7 @@ typedef struct dscr_scalars {
     int32_t moved, have_fprev, n_units, n_units_new;
     int32_t n_support, p_eff, kept_atoms, nnz;
     int32_t dropped_nz, nonfinite, trivial, lmax_index;
-    int32_t lmax_unit, any_group, static_done, pad1;
+    int32_t lmax_unit, any_group, static_done, trips;
     double L, l_acc, l_new, beta;
     double tau, sigma, phi, sigma_new;
     double theta_sq, theta_y, yy, lmax;
@@ -225,6 +225,10 @@ int dscr_solver_run(dscr_solver* h, int iteration_limit, void* stream);
 /* Blocking: synchronise `stream` and copy the scalar state to *out. */
 int dscr_solver_scalars(dscr_solver* h, void* stream, dscr_scalars* out);
 int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* out);
+/* Profiling aid: run `trips` iteration trips as direct kernel launches with CUDA
+ * events between K1 | K2 | K3a | K3b; ms_out[4] gets the mean per-kernel time.
+ * Blocking.  Advances the solver state like real iterations. */
+int dscr_solver_profile(dscr_solver* h, int trips, void* stream, float* ms_out);
 int dscr_solver_destroy(dscr_solver* h);
 
 /* ---- multi-GPU (column sharding, one process per GPU) ---------------- */

@@ -28,7 +28,7 @@ ABI_FUNCTIONS = (
     "dscr_prox_group", "dscr_test_sphere", "dscr_test_dome", "dscr_test_group",
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
-    "dscr_solver_get_buffers", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
+    "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
 )
 
 
@@ -55,7 +55,7 @@ class Config(C.Structure):
 
 _SCALAR_INTS = ("t run_limit max_iters mode stop status parity xi moved have_fprev n_units n_units_new "
                 "n_support p_eff kept_atoms nnz dropped_nz nonfinite trivial lmax_index lmax_unit any_group "
-                "static_done pad1").split()
+                "static_done trips").split()
 _SCALAR_DBLS = ("L l_acc l_new beta tau sigma phi sigma_new theta_sq theta_y yy lmax lmax_sign shift_sq "
                 "corr_inf mu rsafe_sq radius dome_rs dome_cut dome_slope dome_flat maj_cs maj_ss pen ss_red "
                 "f_prev F gap t0_ns gst3_coef gst3_nsq ds_sq fc tw_step spare").split()
@@ -100,6 +100,7 @@ def _declare(lib):
         "dscr_solver_scalars": (i32, [vp, vp, C.POINTER(Scalars)]),
         "dscr_solver_get_buffers": (i32, [vp, C.POINTER(Buffers)]),
         "dscr_solver_destroy": (i32, [vp]),
+        "dscr_solver_profile": (i32, [vp, i32, vp, C.POINTER(C.c_float)]),
         "dscr_comm_unique_id": (i32, [vp]),
         "dscr_solver_set_comm": (i32, [vp, vp, i32, i32]),
     }

@@ -112,6 +112,7 @@ struct Params {
     int max_iters;
     int G, cap, TR, R, P, G3b;
     int col_offset;
+    int in_graph;
     cudaGraphConditionalHandle h_main;
 };
 
@@ -618,6 +619,10 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
 // K3b: split reduction, finalize rows, iteration epilogue
 // ---------------------------------------------------------------------------
 
+__device__ __forceinline__ void set_cond(const Params& P, unsigned v) {
+    if (P.in_graph) cudaGraphSetConditional(P.h_main, v);
+}
+
 __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, double s_tny,
                                    double s_ds2) {
     dscr_scalars* sc = P.sc;
@@ -627,12 +632,12 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
         if (sc->nonfinite) {
             sc->status = DSCR_ENONFINITE;
             sc->stop = DSCR_STOP_ERROR;
-            cudaGraphSetConditional(P.h_main, 0);
+            set_cond(P, 0);
             return;
         }
         if (sc->status != DSCR_OK) {   // radius guard tripped in K1
             sc->stop = DSCR_STOP_ERROR;
-            cudaGraphSetConditional(P.h_main, 0);
+            set_cond(P, 0);
             return;
         }
         if (algo == DSCR_ISTA || algo == DSCR_FISTA) {
@@ -647,11 +652,12 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
                 if (Ln > L_CEILING) {
                     sc->status = DSCR_ENONFINITE;
                     sc->stop = DSCR_STOP_ERROR;
-                    cudaGraphSetConditional(P.h_main, 0);
+                    set_cond(P, 0);
                     return;
                 }
                 sc->mode = MODE_REDO;
-                cudaGraphSetConditional(P.h_main, 1);
+                sc->trips += 1;
+                set_cond(P, 1);
                 return;
             }
             if (sc->dropped_nz) {
@@ -659,7 +665,8 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
                 sc->spare = s_tn2;
                 sc->ds_sq = s_tny;
                 sc->mode = MODE_FIXUP;
-                cudaGraphSetConditional(P.h_main, 1);
+                sc->trips += 1;
+                set_cond(P, 1);
                 return;
             }
         }
@@ -679,6 +686,7 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
     }
     const int t = sc->t + 1;
     sc->t = t;
+    sc->trips += 1;
     sc->F = F;
     sc->gap = gap;
     sc->fc = s_qa2;
@@ -715,7 +723,7 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
     sc->xi = (sc->xi + 1) % 3;
     sc->mode = MODE_NORMAL;
     sc->stop = stop;
-    cudaGraphSetConditional(P.h_main, (stop == DSCR_RUNNING && t < sc->run_limit) ? 1u : 0u);
+    set_cond(P, (stop == DSCR_RUNNING && t < sc->run_limit) ? 1u : 0u);
 }
 
 __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
@@ -1209,8 +1217,7 @@ extern "C" size_t dscr_solver_workspace_size(const dscr_problem_desc* pr, const 
     return total;
 }
 
-static int launch_iteration(dscr_solver* h, cudaStream_t s) {
-    const Params& P = h->P;
+static int launch_iteration(dscr_solver* h, const Params& P, cudaStream_t s, cudaEvent_t* ev = nullptr) {
     const Geometry& g = h->geo;
     const bool group = P.n_groups > 0;
     const size_t smem1 = (size_t)g.smem1;
@@ -1228,9 +1235,11 @@ static int launch_iteration(dscr_solver* h, cudaStream_t s) {
             else k1_corr_update<__nv_bfloat16, false><<<g.G, NT, smem1, s>>>(P);
     }
     CK(cudaGetLastError());
+    if (ev) CK(cudaEventRecord(ev[1], s));
     if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
     else k2_screen<false><<<g.G, NT, 0, s>>>(P);
     CK(cudaGetLastError());
+    if (ev) CK(cudaEventRecord(ev[2], s));
     dim3 g3(g.R, g.P);
     switch (P.dtype) {
         case DSCR_F64: k3a_residual<double><<<g3, NT, 0, s>>>(P); break;
@@ -1238,6 +1247,7 @@ static int launch_iteration(dscr_solver* h, cudaStream_t s) {
         default: k3a_residual<__nv_bfloat16><<<g3, NT, 0, s>>>(P);
     }
     CK(cudaGetLastError());
+    if (ev) CK(cudaEventRecord(ev[3], s));
     k3b_finalize<<<g.G3b, NT, 0, s>>>(P);
     CK(cudaGetLastError());
     return DSCR_OK;
@@ -1382,6 +1392,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
     P.col_offset = pr->col_offset;
+    P.in_graph = 1;
 
     cudaStream_t us = (cudaStream_t)stream;
     // smem attributes for the K1 instantiations
@@ -1438,7 +1449,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("capture body", e); }
-    rc = launch_iteration(h, cs);
+    rc = launch_iteration(h, h->P, cs);
     e = cudaStreamEndCapture(cs, &tmp);
     if (rc || e != cudaSuccess) { dscr_solver_destroy(h); return rc ? rc : set_err("end capture body", e); }
     e = cudaGraphInstantiate(&h->e_loop, gl, 0);
@@ -1460,6 +1471,34 @@ int dscr_solver_run(dscr_solver* h, int iteration_limit, void* stream) {
     CK(cudaGetLastError());
     CK(cudaGraphLaunch(h->e_loop, s));
     return DSCR_OK;
+}
+
+// Direct (non-graph) launches of `trips` iteration trips with CUDA events
+// between the four kernels; ms_out[0..3] receive the mean duration of K1, K2,
+// K3a and K3b.  Used by bench.py for the live roofline measurement.
+int dscr_solver_profile(dscr_solver* h, int trips, void* stream, float* ms_out) {
+    if (!h || !ms_out || trips < 1) return set_inval("bad profile arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    Params P = h->P;
+    P.in_graph = 0;
+    cudaEvent_t ev[5];
+    for (int i = 0; i < 5; ++i) CK(cudaEventCreate(&ev[i]));
+    double acc[4] = {0, 0, 0, 0};
+    int rc = DSCR_OK;
+    for (int t = 0; t < trips && rc == DSCR_OK; ++t) {
+        CK(cudaEventRecord(ev[0], s));
+        rc = launch_iteration(h, P, s, ev);
+        CK(cudaEventRecord(ev[4], s));
+        CK(cudaEventSynchronize(ev[4]));
+        for (int k = 0; k < 4; ++k) {
+            float ms = 0.f;
+            CK(cudaEventElapsedTime(&ms, ev[k], ev[k + 1]));
+            acc[k] += ms;
+        }
+    }
+    for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+    for (int k = 0; k < 4; ++k) ms_out[k] = (float)(acc[k] / trips);
+    return rc;
 }
 
 int dscr_solver_scalars(dscr_solver* h, void* stream, dscr_scalars* out) {

@@ -107,8 +107,12 @@ class Dictionary:
         if hit is not None:
             return hit
         n, k, ldd = self.n_rows, self.n_cols, self.ldd
-        host = self.data if perm is None else np.asfortranarray(self.data[:, perm])
-        src = torch.from_numpy(np.ascontiguousarray(host.T))           # (K, N) rows = columns
+        pinned = self.__dict__.get("_host_tensor")
+        if perm is None and pinned is not None:
+            src = pinned                                                 # pinned (K, N) view of self.data
+        else:
+            host = self.data if perm is None else np.asfortranarray(self.data[:, perm])
+            src = torch.from_numpy(np.ascontiguousarray(host.T))       # (K, N) rows = columns
         if ldd == n:
             dev = src.to(device, non_blocking=True)
         else:
