@@ -184,9 +184,11 @@ int dscr_abi_version(void);
 /* out[j] = D[:,j] . v  for j < k.  Replaces Dictionary.correlate (dictionary.py:89-94). */
 int dscr_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v,
                    double* out, void* stream);
-/* out = D x (out has ldd rows).  Replaces Dictionary.apply (dictionary.py:82-87). */
+/* out = D x (out has ldd rows).  Replaces Dictionary.apply (dictionary.py:82-87).
+ * Deterministic split-K: `work` holds dscr_apply_work_size() bytes of device memory. */
+size_t dscr_apply_work_size(int dtype, int ldd, int k);
 int dscr_apply(int dtype, const void* D, int ldd, int n, int k, const double* x,
-               double* out, void* stream);
+               double* out, void* work, size_t work_bytes, void* stream);
 /* out = sign(v) max(|v|-t,0).  Replaces prox_l1 (problems.py:106-111). */
 int dscr_prox_l1(const double* v, int64_t n, double t, double* out, void* stream);
 /* group soft threshold, threshold t*w_g over contiguous groups.

@@ -24,7 +24,7 @@ TRACE_FIELDS = 10
 TR_T, TR_KEPT, TR_NNZ, TR_OBJ, TR_GAP, TR_RADIUS, TR_L, TR_NS, TR_UNITS, TR_SUPPORT = range(10)
 
 ABI_FUNCTIONS = (
-    "dscr_last_error", "dscr_abi_version", "dscr_correlate", "dscr_apply", "dscr_prox_l1",
+    "dscr_last_error", "dscr_abi_version", "dscr_correlate", "dscr_apply_work_size", "dscr_apply", "dscr_prox_l1",
     "dscr_prox_group", "dscr_test_sphere", "dscr_test_dome", "dscr_test_group",
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
@@ -85,7 +85,8 @@ def _declare(lib):
         "dscr_last_error": (C.c_char_p, []),
         "dscr_abi_version": (i32, []),
         "dscr_correlate": (i32, [i32, vp, i32, i32, i32, vp, vp, vp]),
-        "dscr_apply": (i32, [i32, vp, i32, i32, i32, vp, vp, vp]),
+        "dscr_apply_work_size": (sz, [i32, i32, i32]),
+        "dscr_apply": (i32, [i32, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
         "dscr_prox_l1": (i32, [vp, i64, dbl, vp, vp]),
         "dscr_prox_group": (i32, [vp, vp, i32, vp, dbl, vp, vp]),
         "dscr_test_sphere": (i32, [vp, vp, i32, dbl, vp, vp]),

@@ -23,32 +23,72 @@ constexpr double RADIUS_GUARD = 1e-8;       // screening.py:33
 constexpr double MAJ_SLACK = 1e-12;         // solvers.py:39
 constexpr double L_CEILING = 1e300;         // solvers.py:40
 
-// ---- 16-byte vector loads of dictionary elements, widened to fp64 ---------
+// ---- 32-byte vector loads of dictionary elements, widened to fp64 ---------
+// LDG.E.NA.256 with an L2 cache-policy descriptor: the dictionary is streamed
+// once per iteration, so it bypasses L1; the L2 policy (see make_policy) keeps
+// a resident fraction when the dictionary is near L2 size and evicts first
+// when it is far larger.
+__device__ __forceinline__ uint64_t make_policy(float keep_frac) {
+    uint64_t pol;
+    if (keep_frac >= 1.0f) {
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    } else if (keep_frac <= 0.0f) {
+        asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    } else {
+        asm volatile("createpolicy.fractional.L2::evict_last.L2::evict_first.b64 %0, %1;" : "=l"(pol) : "f"(keep_frac));
+    }
+    return pol;
+}
+
+// Vec<T>: Raw = 32 bytes as loaded; get(raw, i) widens element i to fp64.
 template <typename T> struct Vec;
 template <> struct Vec<double> {
-    static constexpr int V = 2;
-    __device__ __forceinline__ static void load(const double* p, double (&o)[2]) {
-        double2 v = __ldg(reinterpret_cast<const double2*>(p));
-        o[0] = v.x; o[1] = v.y;
+    static constexpr int V = 4;
+    struct Raw { double w[4]; };
+    __device__ __forceinline__ static void load_raw(const double* p, Raw& r, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f64 {%0,%1,%2,%3}, [%4], %5;"
+                     : "=d"(r.w[0]), "=d"(r.w[1]), "=d"(r.w[2]), "=d"(r.w[3]) : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double get(const Raw& r, int i) { return r.w[i]; }
+    __device__ __forceinline__ static void zero(Raw& r) { for (int i = 0; i < 4; ++i) r.w[i] = 0.0; }
+    __device__ __forceinline__ static void load(const double* p, double (&o)[4], uint64_t pol) {
+        Raw r; load_raw(p, r, pol);
+        for (int i = 0; i < 4; ++i) o[i] = r.w[i];
     }
 };
 template <> struct Vec<float> {
-    static constexpr int V = 4;
-    __device__ __forceinline__ static void load(const float* p, double (&o)[4]) {
-        float4 v = __ldg(reinterpret_cast<const float4*>(p));
-        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    static constexpr int V = 8;
+    struct Raw { float w[8]; };
+    __device__ __forceinline__ static void load_raw(const float* p, Raw& r, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                     : "=f"(r.w[0]), "=f"(r.w[1]), "=f"(r.w[2]), "=f"(r.w[3]), "=f"(r.w[4]), "=f"(r.w[5]),
+                       "=f"(r.w[6]), "=f"(r.w[7])
+                     : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double get(const Raw& r, int i) { return (double)r.w[i]; }
+    __device__ __forceinline__ static void zero(Raw& r) { for (int i = 0; i < 8; ++i) r.w[i] = 0.f; }
+    __device__ __forceinline__ static void load(const float* p, double (&o)[8], uint64_t pol) {
+        Raw r; load_raw(p, r, pol);
+        for (int i = 0; i < 8; ++i) o[i] = (double)r.w[i];
     }
 };
 template <> struct Vec<__nv_bfloat16> {
-    static constexpr int V = 8;
-    __device__ __forceinline__ static void load(const __nv_bfloat16* p, double (&o)[8]) {
-        uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            o[2 * i] = (double)__uint_as_float(w[i] << 16);
-            o[2 * i + 1] = (double)__uint_as_float(w[i] & 0xffff0000u);
-        }
+    static constexpr int V = 16;
+    struct Raw { uint32_t w[8]; };
+    __device__ __forceinline__ static void load_raw(const __nv_bfloat16* p, Raw& r, uint64_t pol) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8], %9;"
+                     : "=r"(r.w[0]), "=r"(r.w[1]), "=r"(r.w[2]), "=r"(r.w[3]), "=r"(r.w[4]), "=r"(r.w[5]),
+                       "=r"(r.w[6]), "=r"(r.w[7])
+                     : "l"(p), "l"(pol));
+    }
+    __device__ __forceinline__ static double get(const Raw& r, int i) {
+        const uint32_t x = r.w[i >> 1];
+        return (double)__uint_as_float((i & 1) ? (x & 0xffff0000u) : (x << 16));
+    }
+    __device__ __forceinline__ static void zero(Raw& r) { for (int i = 0; i < 8; ++i) r.w[i] = 0u; }
+    __device__ __forceinline__ static void load(const __nv_bfloat16* p, double (&o)[16], uint64_t pol) {
+        Raw r; load_raw(p, r, pol);
+        for (int i = 0; i < 16; ++i) o[i] = get(r, i);
     }
 };
 
@@ -200,23 +240,26 @@ __device__ __forceinline__ double np_segment_sum(F get, int lo, int n) {
     return get(lo) + np_pairwise(get, lo + 1, n - 1);
 }
 
-// ---- warp dot product of a dictionary column with an smem vector ---------
-// Column j is contiguous (column-major, leading dimension ldd).  Each lane
-// streams 16-byte vectors; U vectors are issued before any is consumed.
-template <typename T, int U>
-__device__ __forceinline__ double warp_dot(const T* __restrict__ col, int n, const double* sv,
-                                           int lane) {
+// ---- warp dot products of dictionary columns with an smem vector ---------
+// Columns are contiguous (column-major, leading dimension ldd).  Each lane
+// streams 32-byte vectors; all C*U loads of a step are issued before any is
+// consumed, and the smem vector is read once per step for all C columns.
+template <typename T, int C, int U>
+__device__ __forceinline__ void warp_dots(const T* const (&col)[C], int n, const double* sv, int lane,
+                                          uint64_t pol, double (&out)[C]) {
     constexpr int V = Vec<T>::V;
-    double acc0 = 0.0, acc1 = 0.0;
+    double acc[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) acc[c] = 0.0;
     for (int base = lane * V; base < n; base += 32 * V * U) {
-        double d[U][V];
+        typename Vec<T>::Raw d[U][C];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             const int i = base + u * 32 * V;
-            if (i < n) Vec<T>::load(col + i, d[u]);
-            else {
 #pragma unroll
-                for (int v = 0; v < V; ++v) d[u][v] = 0.0;
+            for (int c = 0; c < C; ++c) {
+                if (i < n && col[c]) Vec<T>::load_raw(col[c] + i, d[u][c], pol);
+                else Vec<T>::zero(d[u][c]);
             }
         }
 #pragma unroll
@@ -225,13 +268,24 @@ __device__ __forceinline__ double warp_dot(const T* __restrict__ col, int n, con
             if (i < n) {
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    if (v & 1) acc1 = fma(d[u][v], sv[i + v], acc1);
-                    else acc0 = fma(d[u][v], sv[i + v], acc0);
+                    const double t = sv[i + v];
+#pragma unroll
+                    for (int c = 0; c < C; ++c) acc[c] = fma(Vec<T>::get(d[u][c], v), t, acc[c]);
                 }
             }
         }
     }
-    return warp_sum(acc0 + acc1);
+#pragma unroll
+    for (int c = 0; c < C; ++c) out[c] = warp_sum(acc[c]);
+}
+
+template <typename T, int U>
+__device__ __forceinline__ double warp_dot(const T* __restrict__ col, int n, const double* sv, int lane,
+                                           uint64_t pol) {
+    const T* cols[1] = {col};
+    double out[1];
+    warp_dots<T, 1, U>(cols, n, sv, lane, pol, out);
+    return out[0];
 }
 
 __device__ __forceinline__ uint64_t globaltimer() {

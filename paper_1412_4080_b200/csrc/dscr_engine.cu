@@ -113,6 +113,7 @@ struct Params {
     int G, cap, TR, R, P, G3b;
     int col_offset;
     int in_graph;
+    float l2_keep;
     cudaGraphConditionalHandle h_main;
 };
 
@@ -180,7 +181,7 @@ __device__ void radius_epilogue(const Params& P, double bound, const double* the
 // ---------------------------------------------------------------------------
 
 template <typename T, bool GROUP>
-__global__ void __launch_bounds__(NT) k1_corr_update(Params P) {
+__global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
     extern __shared__ double s_theta[];
     __shared__ double s_red[NW][NP1];
     __shared__ double s_sh[64];
@@ -221,41 +222,76 @@ __global__ void __launch_bounds__(NT) k1_corr_update(Params P) {
     double wmax = GROUP ? INFINITY : 0.0;   // Lasso: max|c|; group: min w/||c_g||
     double wcs = 0.0, wss = 0.0, wnf = 0.0, wany = 0.0;
 
-    for (int f = lo + warp; f < hi; f += NW) {
-        const int s = find_slot(off, P.G, f);
-        const int unit = act[s * P.cap + (f - off[s])];
-        const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
-        // correlations of the unit's atoms
-        for (int j = j0; j < j1; ++j) {
-            double c;
-            if (need_dot) c = warp_dot<T, 4>(D + (size_t)j * P.ldd, P.n, s_theta, lane);
-            else c = P.corr[j];
-            if (lane == 0) {
+    const uint64_t pol = make_policy(P.l2_keep);
+    if (!GROUP) {
+        // Lasso: each warp streams C columns at once (C*U 32-byte loads in flight per lane);
+        // lane c applies the update of column c.
+        constexpr int C = 4;
+        for (int f0 = lo + warp * C; f0 < hi; f0 += NW * C) {
+            int myj = -1;
+            if (lane < C && f0 + lane < hi) {
+                const int s = find_slot(off, P.G, f0 + lane);
+                myj = act[s * P.cap + (f0 + lane - off[s])];
+            }
+            int js[C];
+#pragma unroll
+            for (int c = 0; c < C; ++c) js[c] = __shfl_sync(0xffffffffu, myj, c);
+            double cs[C];
+            if (need_dot) {
+                const T* cols[C];
+#pragma unroll
+                for (int c = 0; c < C; ++c) cols[c] = js[c] >= 0 ? D + (size_t)js[c] * P.ldd : nullptr;
+                warp_dots<T, C, (sizeof(T) == 8 ? 2 : 1)>(cols, P.n, s_theta, lane, pol, cs);
+            } else {
+#pragma unroll
+                for (int c = 0; c < C; ++c) cs[c] = js[c] >= 0 ? P.corr[js[c]] : 0.0;
+            }
+            if (myj >= 0) {
+                double c = cs[0];
+#pragma unroll
+                for (int q = 1; q < C; ++q) if (lane == q) c = cs[q];
+                const int j = myj;
                 if (need_dot) P.corr[j] = c;
-                if (!GROUP) wmax = fmax(wmax, fabs(c));
-                // prox argument (the "vec" the reference thresholds)
+                wmax = fmax(wmax, fabs(c));
                 double point, v;
                 if (algo == DSCR_FISTA) { point = uc[j]; v = point - c / L; }
                 else if (algo == DSCR_CP) { point = xc[j]; v = point - tau * c; }
                 else if (algo == DSCR_TWIST) { point = xc[j]; v = point - tws * c; }
                 else { point = xc[j]; v = point - c / L; }
-                if (!GROUP) {
-                    double cand = soft(v, thr);
-                    if (algo == DSCR_TWIST && !first) {
-                        const double a = P.twa, bb = P.twb;
-                        cand = ((1.0 - a) * xp[j] + (a - bb) * xc[j]) + bb * cand;
-                    }
-                    xn[j] = cand;
-                    if (!isfinite(cand)) wnf = 1.0;
-                    const double st = cand - point;
-                    wcs += c * st;
-                    wss += st * st;
-                } else {
-                    xn[j] = v;   // provisional, shrunk below once the group norm is known
+                double cand = soft(v, thr);
+                if (algo == DSCR_TWIST && !first) {
+                    const double a = P.twa, bb = P.twb;
+                    cand = ((1.0 - a) * xp[j] + (a - bb) * xc[j]) + bb * cand;
                 }
+                xn[j] = cand;
+                if (!isfinite(cand)) wnf = 1.0;
+                const double st = cand - point;
+                wcs += c * st;
+                wss += st * st;
             }
         }
-        if (GROUP && lane == 0) {
+    }
+    for (int f = lo + warp; GROUP && f < hi; f += NW) {
+        const int s = find_slot(off, P.G, f);
+        const int unit = act[s * P.cap + (f - off[s])];
+        const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+        // correlations of the group's atoms, provisional prox argument in xn
+        for (int j = j0; j < j1; ++j) {
+            double c;
+            if (need_dot) c = warp_dot<T, 2>(D + (size_t)j * P.ldd, P.n, s_theta, lane, pol);
+            else c = P.corr[j];
+            if (lane == 0) {
+                if (need_dot) P.corr[j] = c;
+                double v;
+                if (algo == DSCR_FISTA) v = uc[j] - c / L;
+                else if (algo == DSCR_CP) v = xc[j] - tau * c;
+                else if (algo == DSCR_TWIST) v = xc[j] - tws * c;
+                else v = xc[j] - c / L;
+                xn[j] = v;
+            }
+        }
+        if (lane == 0) {
+            // group soft threshold (dictionary.py:290-301) with numpy's reduceat summation order
             const int gs = j1 - j0;
             double nv = sqrt(np_segment_sum([&](int i) { double t = xn[i]; return t * t; }, j0, gs));
             double nc = sqrt(np_segment_sum([&](int i) { double t = P.corr[i]; return t * t; }, j0, gs));
@@ -276,6 +312,11 @@ __global__ void __launch_bounds__(NT) k1_corr_update(Params P) {
             }
         }
     }
+    wmax = GROUP ? warp_min(wmax) : warp_max(wmax);
+    wcs = warp_sum(wcs);
+    wss = warp_sum(wss);
+    wnf = warp_max(wnf);
+    wany = warp_max(wany);
     if (lane == 0) {
         s_red[warp][0] = wmax; s_red[warp][1] = wcs; s_red[warp][2] = wss;
         s_red[warp][3] = wnf; s_red[warp][4] = wany;
@@ -555,6 +596,7 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
     const int r0 = blockIdx.x * P.TR + threadIdx.x * V;
     const bool rows_ok = r0 < P.n;
     const T* D = static_cast<const T*>(P.D);
+    const uint64_t pol = make_policy(P.l2_keep);
     double acc_a[V], acc_b[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) { acc_a[v] = 0.0; acc_b[v] = 0.0; }
@@ -582,7 +624,7 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
             for (; i + 4 <= cn; i += 4) {
                 double d[4][V];
 #pragma unroll
-                for (int q = 0; q < 4; ++q) Vec<T>::load(D + (size_t)s_idx[i + q] * P.ldd + r0, d[q]);
+                for (int q = 0; q < 4; ++q) Vec<T>::load(D + (size_t)s_idx[i + q] * P.ldd + r0, d[q], pol);
 #pragma unroll
                 for (int q = 0; q < 4; ++q) {
                     const double a = s_a[i + q], bb = s_b[i + q];
@@ -595,7 +637,7 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
             }
             for (; i < cn; ++i) {
                 double d[V];
-                Vec<T>::load(D + (size_t)s_idx[i] * P.ldd + r0, d);
+                Vec<T>::load(D + (size_t)s_idx[i] * P.ldd + r0, d, pol);
                 const double a = s_a[i], bb = s_b[i];
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
@@ -876,16 +918,17 @@ __global__ void __launch_bounds__(NT) k_init_scalars(Params P) {
 template <typename T>
 __global__ void __launch_bounds__(NT) k_correlate(const T* __restrict__ D, int ldd, int n, int k,
                                                   const double* __restrict__ v, double* out,
-                                                  const int* skip_flag) {
+                                                  const int* skip_flag, float l2_keep) {
     extern __shared__ double s_v[];
     if (skip_flag && *skip_flag) return;
+    const uint64_t pol = make_policy(l2_keep);
     for (int i = threadIdx.x; i < ldd; i += NT) s_v[i] = (i < n) ? v[i] : 0.0;
     __syncthreads();
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * NT) >> 5;
     for (int j = gw; j < k; j += nwarps) {
-        double c = warp_dot<T, 4>(D + (size_t)j * ldd, n, s_v, lane);
+        double c = warp_dot<T, 2>(D + (size_t)j * ldd, n, s_v, lane, pol);
         if (lane == 0) out[j] = c;
     }
 }
@@ -1084,6 +1127,38 @@ struct Geometry {
 
 static int dtype_size(int dt) { return dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2); }
 
+// Fraction of the dictionary to keep L2-resident across iterations: all of it
+// when it fits in ~3/4 of L2, a slice of that size when it is up to 3x L2,
+// none (evict-first streaming) beyond.
+static float l2_keep_fraction(size_t dict_bytes) {
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const double budget = 0.75 * (double)l2;
+    if ((double)dict_bytes <= budget) return 1.0f;
+    if ((double)dict_bytes <= 3.0 * l2) return (float)(budget / (double)dict_bytes);
+    return 0.0f;
+}
+
+template <typename T>
+static int k1_occ_t(bool group, int smem) {
+    int n = 0;
+    if (group) {
+        cudaFuncSetAttribute(k1_corr_update<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_corr_update<T, true>, NT, smem);
+    } else {
+        cudaFuncSetAttribute(k1_corr_update<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_corr_update<T, false>, NT, smem);
+    }
+    return std::max(1, n);
+}
+
+static int k1_occupancy(int dtype, bool group, int smem) {
+    if (dtype == DSCR_F64) return k1_occ_t<double>(group, smem);
+    if (dtype == DSCR_F32) return k1_occ_t<float>(group, smem);
+    return k1_occ_t<__nv_bfloat16>(group, smem);
+}
+
 static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_gsize) {
     Geometry g{};
     int dev = 0;
@@ -1091,9 +1166,9 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g.smem1 = pr->ldd * (int)sizeof(double);
-    // CTAs per SM for K1 limited by the theta staging buffer
-    int per_sm = std::max(1, std::min(8, (int)((200 * 1024) / std::max(1, g.smem1 + 2048))));
-    g.G = std::max(1, std::min(n_units, sms * per_sm));
+    // resident K1 CTAs per SM (registers + theta staging buffer): one full wave
+    const int per_sm = k1_occupancy(pr->dtype, pr->n_groups > 0, g.smem1);
+    g.G = std::max(1, std::min((n_units + 15) / 16, sms * per_sm));
     g.cap = (n_units + g.G - 1) / g.G;
     g.max_gsize = max_gsize;
     g.sup_cap = g.cap * max_gsize;
@@ -1262,7 +1337,7 @@ static int set_smem_attrs(size_t smem) {
 }
 
 static int launch_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v, double* out,
-                            const int* skip, cudaStream_t s) {
+                            const int* skip, float keep, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
@@ -1272,15 +1347,15 @@ static int launch_correlate(int dtype, const void* D, int ldd, int n, int k, con
     switch (dtype) {
         case DSCR_F64:
             if ((rc = set_smem_attrs<double>(smem))) return rc;
-            k_correlate<double><<<grid, NT, smem, s>>>((const double*)D, ldd, n, k, v, out, skip);
+            k_correlate<double><<<grid, NT, smem, s>>>((const double*)D, ldd, n, k, v, out, skip, keep);
             break;
         case DSCR_F32:
             if ((rc = set_smem_attrs<float>(smem))) return rc;
-            k_correlate<float><<<grid, NT, smem, s>>>((const float*)D, ldd, n, k, v, out, skip);
+            k_correlate<float><<<grid, NT, smem, s>>>((const float*)D, ldd, n, k, v, out, skip, keep);
             break;
         default:
             if ((rc = set_smem_attrs<__nv_bfloat16>(smem))) return rc;
-            k_correlate<__nv_bfloat16><<<grid, NT, smem, s>>>((const __nv_bfloat16*)D, ldd, n, k, v, out, skip);
+            k_correlate<__nv_bfloat16><<<grid, NT, smem, s>>>((const __nv_bfloat16*)D, ldd, n, k, v, out, skip, keep);
     }
     CK(cudaGetLastError());
     return DSCR_OK;
@@ -1296,7 +1371,7 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
     CK(cudaGetLastError());
     k_init_scalars<<<1, NT, 0, s>>>(P);
     CK(cudaGetLastError());
-    if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.y, P.ycorr, nullptr, s))) return rc;
+    if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.y, P.ycorr, nullptr, P.l2_keep, s))) return rc;
     int lgrid = std::max(1, std::min((P.n_units + NT - 1) / NT, 2048));
     k_lmax<<<lgrid, NT, 0, s>>>(P);
     CK(cudaGetLastError());
@@ -1309,7 +1384,7 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
                 default: k_setup_vec<__nv_bfloat16><<<32, NT, 0, s>>>(P);
             }
             CK(cudaGetLastError());
-            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.star, stop_flag, s))) return rc;
+            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.star, stop_flag, P.l2_keep, s))) return rc;
         } else if (test == DSCR_GST3) {
             switch (P.dtype) {
                 case DSCR_F64: k_setup_vec<double><<<32, NT, 0, s>>>(P); break;
@@ -1319,7 +1394,7 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
             CK(cudaGetLastError());
             k_gst3_scalars<<<1, NT, 0, s>>>(P);
             CK(cudaGetLastError());
-            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, s))) return rc;
+            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, P.l2_keep, s))) return rc;
         }
         k_centers<<<std::max(1, std::min((P.kcols + NT - 1) / NT, 1024)), NT, 0, s>>>(P);
         CK(cudaGetLastError());
@@ -1393,6 +1468,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
     P.col_offset = pr->col_offset;
     P.in_graph = 1;
+    P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
 
     cudaStream_t us = (cudaStream_t)stream;
     // smem attributes for the K1 instantiations

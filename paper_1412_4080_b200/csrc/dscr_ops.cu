@@ -46,6 +46,7 @@ __global__ void __launch_bounds__(NT) k_corr(const T* __restrict__ D, int ldd, i
                                              const double* __restrict__ v, double* out, int nvec,
                                              int ldv, int ldo) {
     extern __shared__ double s_v[];
+    const uint64_t pol = make_policy(0.5f);
     for (int q = 0; q < nvec; ++q)
         for (int i = threadIdx.x; i < ldd; i += NT) s_v[q * ldd + i] = (i < n) ? v[(size_t)q * ldv + i] : 0.0;
     __syncthreads();
@@ -54,38 +55,93 @@ __global__ void __launch_bounds__(NT) k_corr(const T* __restrict__ D, int ldd, i
     const int nwarps = (gridDim.x * NT) >> 5;
     for (int j = gw; j < k; j += nwarps) {
         for (int q = 0; q < nvec; ++q) {
-            double c = warp_dot<T, 4>(D + (size_t)j * ldd, n, s_v + (size_t)q * ldd, lane);
+            double c = warp_dot<T, 2>(D + (size_t)j * ldd, n, s_v + (size_t)q * ldd, lane, pol);
             if (lane == 0) out[(size_t)q * ldo + j] = c;
         }
     }
 }
 
-// out[:, q] = D x[:, q]; thread owns V consecutive rows, loops over columns in order
+// Split-K GEMV: CTA (tile, split) accumulates rows [tile*TR, +TR) of
+// D[:, cols of split] x[cols of split, q] in fp64 and writes a partial vector;
+// k_apply_reduce sums the splits in index order (deterministic).
+constexpr int APPLY_CHUNK = NT;
+
 template <typename T>
-__global__ void __launch_bounds__(NT) k_apply(const T* __restrict__ D, int ldd, int n, int k,
-                                              const double* __restrict__ x, double* out, int nvec,
-                                              int ldx, int ldo) {
+__global__ void __launch_bounds__(NT) k_apply_part(const T* __restrict__ D, int ldd, int n, int k,
+                                                   const double* __restrict__ x, int nvec, int ldx,
+                                                   double* part, int nsplit) {
     constexpr int V = Vec<T>::V;
+    __shared__ double s_x[2][APPLY_CHUNK];
+    __shared__ int s_j[APPLY_CHUNK];
+    __shared__ int s_scan[2 * NW + 1];
+    const int split = blockIdx.y;
+    const int c0 = (int)(((long long)k * split) / nsplit), c1 = (int)(((long long)k * (split + 1)) / nsplit);
     const int r0 = (blockIdx.x * NT + threadIdx.x) * V;
-    if (r0 >= ldd) return;
-    for (int q = 0; q < nvec; ++q) {
-        double acc[V];
+    const uint64_t pol = make_policy(0.5f);
+    double acc[2][V];
 #pragma unroll
-        for (int v = 0; v < V; ++v) acc[v] = 0.0;
+    for (int v = 0; v < V; ++v) { acc[0][v] = 0.0; acc[1][v] = 0.0; }
+    for (int base = c0; base < c1; base += APPLY_CHUNK) {
+        const int cn = min(APPLY_CHUNK, c1 - base);
+        __syncthreads();
+        // compact the chunk's nonzero columns (order preserved)
+        const int i0 = threadIdx.x;
+        double a = 0.0, b = 0.0;
+        bool nz = false;
+        if (i0 < cn) {
+            a = x[base + i0];
+            b = nvec > 1 ? x[(size_t)ldx + base + i0] : 0.0;
+            nz = (a != 0.0 || b != 0.0);
+        }
+        int m;
+        const int pos = block_exscan(nz ? 1 : 0, s_scan, &m);
+        if (nz) { s_j[pos] = base + i0; s_x[0][pos] = a; s_x[1][pos] = b; }
+        __syncthreads();
         if (r0 < n) {
-            for (int j = 0; j < k; ++j) {
-                const double a = x[(size_t)q * ldx + j];
-                if (a == 0.0) continue;
-                double d[V];
-                Vec<T>::load(D + (size_t)j * ldd + r0, d);
+            int i = 0;
+            for (; i + 4 <= m; i += 4) {
+                double d[4][V];
 #pragma unroll
-                for (int v = 0; v < V; ++v) acc[v] = fma(a, d[v], acc[v]);
+                for (int q = 0; q < 4; ++q) Vec<T>::load(D + (size_t)s_j[i + q] * ldd + r0, d[q], pol);
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+#pragma unroll
+                    for (int v = 0; v < V; ++v) {
+                        acc[0][v] = fma(s_x[0][i + q], d[q][v], acc[0][v]);
+                        acc[1][v] = fma(s_x[1][i + q], d[q][v], acc[1][v]);
+                    }
+            }
+            for (; i < m; ++i) {
+                double d[V];
+                Vec<T>::load(D + (size_t)s_j[i] * ldd + r0, d, pol);
+#pragma unroll
+                for (int v = 0; v < V; ++v) {
+                    acc[0][v] = fma(s_x[0][i], d[v], acc[0][v]);
+                    acc[1][v] = fma(s_x[1][i], d[v], acc[1][v]);
+                }
             }
         }
-#pragma unroll
-        for (int v = 0; v < V; ++v)
-            if (r0 + v < ldd) out[(size_t)q * ldo + r0 + v] = (r0 + v < n) ? acc[v] : 0.0;
     }
+    if (r0 < ldd) {
+        for (int q = 0; q < nvec; ++q)
+#pragma unroll
+            for (int v = 0; v < V; ++v)
+                if (r0 + v < ldd) part[((size_t)split * 2 + q) * ldd + r0 + v] = (r0 + v < n) ? acc[q][v] : 0.0;
+    }
+}
+
+__global__ void k_apply_reduce(const double* part, int nsplit, int ldd, int nvec, double* out, int ldo) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < ldd * nvec; i += gridDim.x * blockDim.x) {
+        const int q = i / ldd, r = i % ldd;
+        double s = 0.0;
+        for (int p = 0; p < nsplit; ++p) s += part[((size_t)p * 2 + q) * ldd + r];
+        out[(size_t)q * ldo + r] = s;
+    }
+}
+
+static int apply_splits(int k, int ldd, int V) {
+    const int R = (ldd + NT * V - 1) / (NT * V);
+    return std::max(1, std::min((k + 63) / 64, std::max(1, (sm_count() * 4) / R)));
 }
 
 __global__ void k_soft(const double* v, int64_t n, double t, double* out) {
@@ -172,10 +228,13 @@ static int corr_launch(const void* D, int ldd, int n, int k, const double* v, do
 
 template <typename T>
 static int apply_launch(const void* D, int ldd, int n, int k, const double* x, double* out, int nvec,
-                        int ldx, int ldo, cudaStream_t s) {
+                        int ldx, int ldo, double* part, cudaStream_t s) {
     constexpr int V = Vec<T>::V;
-    const int grid = (ldd + NT * V - 1) / (NT * V);
-    k_apply<T><<<grid, NT, 0, s>>>((const T*)D, ldd, n, k, x, out, nvec, ldx, ldo);
+    const int R = (ldd + NT * V - 1) / (NT * V);
+    const int P = apply_splits(k, ldd, V);
+    k_apply_part<T><<<dim3(R, P), NT, 0, s>>>((const T*)D, ldd, n, k, x, nvec, ldx, part, P);
+    OCK(cudaGetLastError());
+    k_apply_reduce<<<std::max(1, std::min((ldd * nvec + 255) / 256, 2048)), 256, 0, s>>>(part, P, ldd, nvec, out, ldo);
     OCK(cudaGetLastError());
     return DSCR_OK;
 }
@@ -187,10 +246,15 @@ static int corr_any(int dt, const void* D, int ldd, int n, int k, const double* 
     return corr_launch<__nv_bfloat16>(D, ldd, n, k, v, out, nvec, ldv, ldo, s);
 }
 static int apply_any(int dt, const void* D, int ldd, int n, int k, const double* x, double* out, int nvec,
-                     int ldx, int ldo, cudaStream_t s) {
-    if (dt == DSCR_F64) return apply_launch<double>(D, ldd, n, k, x, out, nvec, ldx, ldo, s);
-    if (dt == DSCR_F32) return apply_launch<float>(D, ldd, n, k, x, out, nvec, ldx, ldo, s);
-    return apply_launch<__nv_bfloat16>(D, ldd, n, k, x, out, nvec, ldx, ldo, s);
+                     int ldx, int ldo, double* part, cudaStream_t s) {
+    if (dt == DSCR_F64) return apply_launch<double>(D, ldd, n, k, x, out, nvec, ldx, ldo, part, s);
+    if (dt == DSCR_F32) return apply_launch<float>(D, ldd, n, k, x, out, nvec, ldx, ldo, part, s);
+    return apply_launch<__nv_bfloat16>(D, ldd, n, k, x, out, nvec, ldx, ldo, part, s);
+}
+
+static size_t apply_part_bytes(int dt, int ldd, int k) {
+    const int V = 16 / (dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2));
+    return (size_t)apply_splits(k, ldd, V) * 2 * ldd * sizeof(double);
 }
 
 static int check_dict(int dt, const void* D, int ldd, int n, int k) {
@@ -215,10 +279,14 @@ int dscr_correlate(int dtype, const void* D, int ldd, int n, int k, const double
     return corr_any(dtype, D, ldd, n, k, v, out, 1, ldd, k, (cudaStream_t)stream);
 }
 
-int dscr_apply(int dtype, const void* D, int ldd, int n, int k, const double* x, double* out, void* stream) {
+size_t dscr_apply_work_size(int dtype, int ldd, int k) { return apply_part_bytes(dtype, ldd, k) + 256; }
+
+int dscr_apply(int dtype, const void* D, int ldd, int n, int k, const double* x, double* out, void* work,
+               size_t work_bytes, void* stream) {
     int rc = check_dict(dtype, D, ldd, n, k);
     if (rc) return rc;
-    return apply_any(dtype, D, ldd, n, k, x, out, 1, k, ldd, (cudaStream_t)stream);
+    if (!work || work_bytes < apply_part_bytes(dtype, ldd, k)) return inval("apply workspace too small");
+    return apply_any(dtype, D, ldd, n, k, x, out, 1, k, ldd, (double*)work, (cudaStream_t)stream);
 }
 
 int dscr_prox_l1(const double* v, int64_t n, double t, double* out, void* stream) {
@@ -263,7 +331,7 @@ int dscr_test_group(const double* w, const double* cn, const double* sn, const i
 }
 
 size_t dscr_operator_norm_work_size(int ldd, int k) {
-    return (6 * (size_t)std::max(ldd, k) + 64) * sizeof(double);
+    return (6 * (size_t)std::max(ldd, k) + 64) * sizeof(double) + apply_part_bytes(DSCR_F64, ldd, k) * 4;
 }
 
 // 2-vector block power iteration for the top eigenvalue of D^T D
@@ -285,6 +353,7 @@ int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double t
     double* z = q + 2 * M;          // [2][ldq]
     double* w = z + 2 * M;          // [2][ldw]
     double* sums = w + 2 * M;       // 7 inner products
+    double* part = sums + 64;       // split-K partials of the apply
     // start block: ones and (+1,-1,+1,...) ; Gram-Schmidt QR (same span as np.linalg.qr)
     std::vector<double> h0(2 * (size_t)ldq, 0.0);
     for (int i = 0; i < dim; ++i) { h0[i] = 1.0; h0[ldq + i] = (i & 1) ? -1.0 : 1.0; }
@@ -298,18 +367,18 @@ int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double t
         n2 = std::sqrt(n2);
         for (int i = 0; i < dim; ++i) { h0[i] = 1.0 / n1; h0[ldq + i] = (nvec > 1 && n2 > 0) ? q2[i] / n2 : 0.0; }
     }
-    OCK(cudaMemsetAsync(work, 0, dscr_operator_norm_work_size(ldd, k), s));
+    OCK(cudaMemsetAsync(work, 0, (6 * M + 64) * sizeof(double), s));
     OCK(cudaMemcpyAsync(q, h0.data(), sizeof(double) * h0.size(), cudaMemcpyHostToDevice, s));
     double val = NAN;
     bool have = false;
     double hs[7];
     for (int it = 0; it < max_iters; ++it) {
         if (small_cols) {
-            if ((rc = apply_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, s))) return rc;
+            if ((rc = apply_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, part, s))) return rc;
             if ((rc = corr_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, s))) return rc;
         } else {
             if ((rc = corr_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, s))) return rc;
-            if ((rc = apply_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, s))) return rc;
+            if ((rc = apply_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, part, s))) return rc;
         }
         k_pw_dots<<<1, NT, 0, s>>>(q, z, dim, ldq, nvec, sums);
         OCK(cudaGetLastError());

@@ -136,8 +136,10 @@ class Dictionary:
         Dd = self.device_data(dev)
         xd = torch.from_numpy(x).to(dev)
         out = torch.empty(self.ldd, dtype=torch.float64, device=dev)
+        nb = int(L.dscr_apply_work_size(self.dtype_code, self.ldd, self.n_cols))
+        work = torch.empty(nb, dtype=torch.uint8, device=dev)
         nat.check(L.dscr_apply(self.dtype_code, Dd.data_ptr(), self.ldd, self.n_rows, self.n_cols,
-                               xd.data_ptr(), out.data_ptr(), nat.stream_ptr()))
+                               xd.data_ptr(), out.data_ptr(), work.data_ptr(), nb, nat.stream_ptr()))
         return out[: self.n_rows].cpu().numpy()
 
     def correlate(self, v):
