@@ -170,8 +170,11 @@ typedef struct dscr_solver_buffers {
     int32_t* act_off[2];     /* exclusive scan, G+1 entries */
     uint8_t* mask;           /* per old-active flat position, last iteration's test */
     double* trace;           /* [max_iters][DSCR_TRACE_FIELDS] */
+    uint64_t* kts;           /* [max_kts][8] %globaltimer stamps per trip: K1 in/out, K2 in/out, K3a in, -, K3b in/out */
+    int32_t max_kts;
     int32_t G;               /* CTAs of the per-unit kernels (= number of slots) */
     int32_t cap;             /* slot capacity in units */
+    int32_t pad;
 } dscr_solver_buffers;
 
 typedef struct dscr_solver dscr_solver;

@@ -71,7 +71,7 @@ class Buffers(C.Structure):
         ("x", C.c_void_p * 3), ("u", C.c_void_p * 2), ("y_corr", C.c_void_p), ("star_corr", C.c_void_p),
         ("cc", C.c_void_p), ("cnorm", C.c_void_p), ("act", C.c_void_p * 2), ("act_cnt", C.c_void_p * 2),
         ("act_off", C.c_void_p * 2), ("mask", C.c_void_p), ("trace", C.c_void_p),
-        ("G", C.c_int32), ("cap", C.c_int32),
+        ("kts", C.c_void_p), ("max_kts", C.c_int32), ("G", C.c_int32), ("cap", C.c_int32), ("pad", C.c_int32),
     ]
 
 

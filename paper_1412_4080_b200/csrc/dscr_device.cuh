@@ -141,6 +141,29 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
     return r;
 }
 
+// Sum of M values over the CTA in one smem exchange; results valid in every thread.
+// sh must hold NW*M doubles.  Fixed order => bitwise reproducible.
+template <int M>
+__device__ __forceinline__ void block_sum_n(double (&v)[M], double* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = warp_sum(v[m]);
+    __syncthreads();
+    if (l == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) sh[m * NW + w] = v[m];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        double r = 0.0;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) r += sh[m * NW + q];
+        v[m] = r;
+    }
+    __syncthreads();
+}
+
 // Exclusive scan of an int over the CTA; returns prefix, *total gets the sum.
 __device__ __forceinline__ int block_exscan(int v, int* sh, int* total) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;

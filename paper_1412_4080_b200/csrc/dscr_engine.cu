@@ -50,6 +50,7 @@ constexpr int NP1 = 6;   // K1 partials
 constexpr int NP2 = 6;   // K2 partials
 constexpr int NP3 = 4;   // K3b partials
 constexpr int MIN_COLS_PER_SPLIT = 16;
+constexpr int TRIPS_PER_BODY = 4;
 
 
 static int set_err(const char* what, cudaError_t e) {
@@ -109,6 +110,8 @@ struct Params {
     double* p3s;
     unsigned* tickets;
     double* trace;
+    unsigned long long* kts;   // per-trip kernel timestamps [trips][8]
+    int max_kts;
     int max_iters;
     int G, cap, TR, R, P, G3b;
     int col_offset;
@@ -120,6 +123,12 @@ struct Params {
 // ---------------------------------------------------------------------------
 // small device utilities
 // ---------------------------------------------------------------------------
+
+// device timestamps: slot 2k = kernel k entry (CTA 0), 2k+1 = kernel k exit (last CTA)
+__device__ __forceinline__ void stamp(const Params& P, int slot) {
+    const int trip = P.sc->trips;
+    if (P.kts && trip < P.max_kts) P.kts[(size_t)trip * 8 + slot] = globaltimer();
+}
 
 __device__ __forceinline__ int find_slot(const int* off, int G, int f) {
     int lo = 0, hi = G;   // off[lo] <= f < off[hi]
@@ -187,9 +196,10 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
     __shared__ double s_sh[64];
     __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
-    if (sc->stop) return;
+    if (sc->stop || sc->t >= sc->run_limit) return;
     const int mode = sc->mode;
     if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 0);
     const int p = sc->parity, xi = sc->xi;
     const int nu = sc->n_units;
     const int b = blockIdx.x;
@@ -275,19 +285,27 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
         const int s = find_slot(off, P.G, f);
         const int unit = act[s * P.cap + (f - off[s])];
         const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
-        // correlations of the group's atoms, provisional prox argument in xn
-        for (int j = j0; j < j1; ++j) {
-            double c;
-            if (need_dot) c = warp_dot<T, 2>(D + (size_t)j * P.ldd, P.n, s_theta, lane, pol);
-            else c = P.corr[j];
+        // correlations of the group's atoms (4 columns in flight), provisional prox argument in xn
+        for (int jb = j0; jb < j1; jb += 4) {
+            double cs4[4];
+            if (need_dot) {
+                const T* cols[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) cols[c] = (jb + c < j1) ? D + (size_t)(jb + c) * P.ldd : nullptr;
+                warp_dots<T, 4, (sizeof(T) == 8 ? 2 : 1)>(cols, P.n, s_theta, lane, pol, cs4);
+            }
             if (lane == 0) {
-                if (need_dot) P.corr[j] = c;
-                double v;
-                if (algo == DSCR_FISTA) v = uc[j] - c / L;
-                else if (algo == DSCR_CP) v = xc[j] - tau * c;
-                else if (algo == DSCR_TWIST) v = xc[j] - tws * c;
-                else v = xc[j] - c / L;
-                xn[j] = v;
+                for (int c = 0; c < 4 && jb + c < j1; ++c) {
+                    const int j = jb + c;
+                    const double cc = need_dot ? cs4[c] : P.corr[j];
+                    if (need_dot) P.corr[j] = cc;
+                    double v;
+                    if (algo == DSCR_FISTA) v = uc[j] - cc / L;
+                    else if (algo == DSCR_CP) v = xc[j] - tau * cc;
+                    else if (algo == DSCR_TWIST) v = xc[j] - tws * cc;
+                    else v = xc[j] - cc / L;
+                    xn[j] = v;
+                }
             }
         }
         if (lane == 0) {
@@ -358,8 +376,11 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
         __syncthreads();
         m = s_m[0]; nf = s_nf[0]; any = s_any[0];
     }
-    cs = block_sum(cs, s_sh);
-    ss = block_sum(ss, s_sh);
+    {
+        double v2[2] = {cs, ss};
+        block_sum_n<2>(v2, s_sh);
+        cs = v2[0]; ss = v2[1];
+    }
     double bound;
     if (GROUP) bound = (any > 0.0) ? m : INFINITY;
     else bound = (m == 0.0) ? INFINITY : 1.0 / m;
@@ -380,6 +401,7 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
         }
     }
     radius_epilogue(P, bound, P.theta[p], sc->theta_sq, sc->theta_y, s_sh);
+    if (threadIdx.x == 0) stamp(P, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -419,6 +441,8 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
     const int mode = sc->mode;
     if (mode == MODE_FIXUP) return;
     const bool static_mode = (mode == MODE_STATIC);
+    if (!static_mode && sc->t >= sc->run_limit) return;
+    if (!static_mode && blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 2);
     const int p = sc->parity, xi = sc->xi;
     const int nu = sc->n_units;
     const int b = blockIdx.x;
@@ -504,14 +528,11 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
         if (!static_mode) P.sup_cnt[b] = n_sup;
     }
     if (!static_mode) {
-        pen = block_sum(pen, s_sh);
-        nnz = block_sum(nnz, s_sh);
-        kept_atoms = block_sum(kept_atoms, s_sh);
-        ssr = block_sum(ssr, s_sh);
-        dropped = block_sum(dropped, s_sh);
+        double v5[5] = {pen, nnz, kept_atoms, ssr, dropped};
+        block_sum_n<5>(v5, s_sh);
         if (threadIdx.x == 0) {
             double* o = P.p2 + (size_t)b * NP2;
-            o[0] = pen; o[1] = nnz; o[2] = kept_atoms; o[3] = ssr; o[4] = dropped;
+            o[0] = v5[0]; o[1] = v5[1]; o[2] = v5[2]; o[3] = v5[3]; o[4] = v5[4];
         }
     }
     if (!last_block(P.tickets + 1, gridDim.x, &s_flag)) return;
@@ -561,14 +582,16 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
         const double* o = P.p2 + (size_t)i * NP2;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3]; a4 += o[4];
     }
-    a0 = block_sum(a0, s_sh); a1 = block_sum(a1, s_sh); a2 = block_sum(a2, s_sh);
-    a3 = block_sum(a3, s_sh); a4 = block_sum(a4, s_sh);
+    double r5[5] = {a0, a1, a2, a3, a4};
+    block_sum_n<5>(r5, s_sh);
+    a0 = r5[0]; a1 = r5[1]; a2 = r5[2]; a3 = r5[3]; a4 = r5[4];
     if (threadIdx.x == 0) {
         sc->pen = a0;
         sc->nnz = (int)a1;
         sc->kept_atoms = (int)a2;
         sc->ss_red = a3;
         sc->dropped_nz = (a4 > 0.0);
+        stamp(P, 3);
     }
 }
 
@@ -583,10 +606,11 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
     __shared__ int s_idx[K3_CHUNK];
     __shared__ double s_a[K3_CHUNK], s_b[K3_CHUNK];
     dscr_scalars* sc = P.sc;
-    if (sc->stop) return;
+    if (sc->stop || sc->t >= sc->run_limit) return;
     const int mode = sc->mode;
     if (mode == MODE_STATIC) return;
     const bool fix = (mode == MODE_FIXUP);
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stamp(P, 4);
     const int pe = sc->p_eff;
     const int split = blockIdx.y;
     if (split >= pe) return;
@@ -768,54 +792,73 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
     set_cond(P, (stop == DSCR_RUNNING && t < sc->run_limit) ? 1u : 0u);
 }
 
+constexpr int K3B_ROWS = 32;                 // rows per CTA
+constexpr int K3B_GROUPS = NT / K3B_ROWS;    // split groups per row
+
 __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     __shared__ double s_sh[64];
+    __shared__ double s_pa[K3B_GROUPS][K3B_ROWS], s_pb[K3B_GROUPS][K3B_ROWS];
     __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
-    if (sc->stop) return;
+    if (sc->stop || sc->t >= sc->run_limit) return;
     const int mode = sc->mode;
     if (mode == MODE_STATIC) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 6);
     const bool fix = (mode == MODE_FIXUP);
     const int algo = P.algo;
     const int p = sc->parity;
     const int pe = sc->p_eff;
-    const int r = blockIdx.x * NT + threadIdx.x;
+    // split reduction: group g sums splits g, g+8, ... ; groups combined in order (deterministic)
+    {
+        const int rr = threadIdx.x % K3B_ROWS, g = threadIdx.x / K3B_ROWS;
+        const int r = blockIdx.x * K3B_ROWS + rr;
+        double a = 0.0, b = 0.0;
+        if (r < P.n) {
+            for (int s = g; s < pe; s += K3B_GROUPS) {
+                a += P.p3v[((size_t)s * 2) * P.ldd + r];
+                b += P.p3v[((size_t)s * 2 + 1) * P.ldd + r];
+            }
+        }
+        s_pa[g][rr] = a;
+        s_pb[g][rr] = b;
+    }
+    __syncthreads();
     double qa2 = 0.0, tn2 = 0.0, tny = 0.0, ds2 = 0.0;
-    if (r < P.n) {
-        double Sa = 0.0, Sb = 0.0;
-        for (int s = 0; s < pe; ++s) {
-            Sa += P.p3v[((size_t)s * 2) * P.ldd + r];
-            Sb += P.p3v[((size_t)s * 2 + 1) * P.ldd + r];
-        }
-        const double yr = P.y[r];
-        const double qa = Sa - yr;            // D x - y (solvers.py:179, 487)
-        P.resid[r] = qa;
-        qa2 = qa * qa;
-        double* thn = P.theta[p ^ 1];
-        double tn = 0.0;
-        bool have_tn = true;
-        if (algo == DSCR_FISTA) {
-            if (!fix) tn = Sb - yr; else have_tn = false;        // D u - y (solvers.py:212)
-        } else if (algo == DSCR_CP) {
-            if (!fix) {
-                const double q = Sb - yr;
-                const double sg = sc->sigma_new;
-                tn = (P.theta[p][r] + sg * q) / (1.0 + sg);          // solvers.py:299
-            } else have_tn = false;
-        } else {
-            tn = qa;                                                   // resid carried as theta
-            if (algo == DSCR_SPARSA && !fix) ds2 = Sb * Sb;
-        }
-        if (have_tn) {
-            thn[r] = tn;
-            tn2 = tn * tn;
-            tny = tn * yr;
+    if (threadIdx.x < K3B_ROWS) {
+        const int r = blockIdx.x * K3B_ROWS + threadIdx.x;
+        if (r < P.n) {
+            double Sa = 0.0, Sb = 0.0;
+#pragma unroll
+            for (int g = 0; g < K3B_GROUPS; ++g) { Sa += s_pa[g][threadIdx.x]; Sb += s_pb[g][threadIdx.x]; }
+            const double yr = P.y[r];
+            const double qa = Sa - yr;            // D x - y (solvers.py:179, 487)
+            P.resid[r] = qa;
+            qa2 = qa * qa;
+            double* thn = P.theta[p ^ 1];
+            double tn = 0.0;
+            bool have_tn = true;
+            if (algo == DSCR_FISTA) {
+                if (!fix) tn = Sb - yr; else have_tn = false;        // D u - y (solvers.py:212)
+            } else if (algo == DSCR_CP) {
+                if (!fix) {
+                    const double q = Sb - yr;
+                    const double sg = sc->sigma_new;
+                    tn = (P.theta[p][r] + sg * q) / (1.0 + sg);          // solvers.py:299
+                } else have_tn = false;
+            } else {
+                tn = qa;                                                   // resid carried as theta
+                if (algo == DSCR_SPARSA && !fix) ds2 = Sb * Sb;
+            }
+            if (have_tn) {
+                thn[r] = tn;
+                tn2 = tn * tn;
+                tny = tn * yr;
+            }
         }
     }
-    qa2 = block_sum(qa2, s_sh);
-    tn2 = block_sum(tn2, s_sh);
-    tny = block_sum(tny, s_sh);
-    ds2 = block_sum(ds2, s_sh);
+    double q4[4] = {qa2, tn2, tny, ds2};
+    block_sum_n<4>(q4, s_sh);
+    qa2 = q4[0]; tn2 = q4[1]; tny = q4[2]; ds2 = q4[3];
     if (threadIdx.x == 0) {
         double* o = P.p3s + (size_t)blockIdx.x * NP3;
         o[0] = qa2; o[1] = tn2; o[2] = tny; o[3] = ds2;
@@ -826,8 +869,13 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
         const double* o = P.p3s + (size_t)i * NP3;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3];
     }
-    a0 = block_sum(a0, s_sh); a1 = block_sum(a1, s_sh); a2 = block_sum(a2, s_sh); a3 = block_sum(a3, s_sh);
-    if (threadIdx.x == 0) iteration_epilogue(P, a0, a1, a2, a3);
+    double r4[4] = {a0, a1, a2, a3};
+    block_sum_n<4>(r4, s_sh);
+    a0 = r4[0]; a1 = r4[1]; a2 = r4[2]; a3 = r4[3];
+    if (threadIdx.x == 0) {
+        stamp(P, 7);
+        iteration_epilogue(P, a0, a1, a2, a3);
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -1176,14 +1224,16 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     g.TR = NT * V;
     g.R = (pr->n_rows + g.TR - 1) / g.TR;
     g.P = std::max(1, (sms * 4) / g.R);
-    g.G3b = (pr->n_rows + NT - 1) / NT;
+    g.G3b = (pr->n_rows + K3B_ROWS - 1) / K3B_ROWS;
     return g;
 }
+
+static int kts_slots(const dscr_config* cfg) { return std::min(std::max(cfg->max_iters, 1) + 64, 20000); }
 
 struct Offsets {
     size_t sc, theta0, theta1, resid, corr, x0, x1, x2, u0, u1, ycorr, star, cc, cnorm, vec, dn;
     size_t act0, act1, cnt0, cnt1, off0, off1, mask, sidx, sa, sb, supcnt, supoff;
-    size_t p1, p2, p3v, p3s, tickets, trace;
+    size_t p1, p2, p3v, p3s, tickets, trace, kts;
 };
 
 static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg, const Geometry& g,
@@ -1213,6 +1263,7 @@ static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg,
     o.p3s = L.add((size_t)g.G3b * NP3 * 8);
     o.tickets = L.add(64);
     o.trace = L.add((size_t)std::max(cfg->max_iters, 1) * DSCR_TRACE_FIELDS * 8);
+    o.kts = L.add((size_t)kts_slots(cfg) * 8 * 8);
     *total = L.total + 256;
     return o;
 }
@@ -1464,6 +1515,8 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.p1 = (double*)(base + o.p1); P.p2 = (double*)(base + o.p2); P.p3v = (double*)(base + o.p3v);
     P.p3s = (double*)(base + o.p3s); P.tickets = (unsigned*)(base + o.tickets);
     P.trace = (double*)(base + o.trace);
+    P.kts = (unsigned long long*)(base + o.kts);
+    P.max_kts = kts_slots(cfg);
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
     P.col_offset = pr->col_offset;
@@ -1525,7 +1578,9 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
     if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("capture body", e); }
-    rc = launch_iteration(h, h->P, cs);
+    // TRIPS_PER_BODY trips per body launch amortise the conditional-node relaunch;
+    // trips after a stop or pause return at entry.
+    for (int r = 0; r < TRIPS_PER_BODY && rc == DSCR_OK; ++r) rc = launch_iteration(h, h->P, cs);
     e = cudaStreamEndCapture(cs, &tmp);
     if (rc || e != cudaSuccess) { dscr_solver_destroy(h); return rc ? rc : set_err("end capture body", e); }
     e = cudaGraphInstantiate(&h->e_loop, gl, 0);
@@ -1597,6 +1652,7 @@ int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* b) {
     b->act_cnt[0] = P.act_cnt[0]; b->act_cnt[1] = P.act_cnt[1];
     b->act_off[0] = P.act_off[0]; b->act_off[1] = P.act_off[1];
     b->mask = P.mask; b->trace = P.trace;
+    b->kts = (uint64_t*)P.kts; b->max_kts = P.max_kts;
     b->G = P.G; b->cap = P.cap;
     return DSCR_OK;
 }
