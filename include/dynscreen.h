@@ -236,6 +236,16 @@ int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* out);
 int dscr_solver_profile(dscr_solver* h, int trips, void* stream, float* ms_out);
 int dscr_solver_destroy(dscr_solver* h);
 
+/* ---- batched many-observation path (BASELINE config 5) ---------------- */
+
+/* C^T[n][m] = sum_s sum_k A[m][k] * B[s*Nb + n][k]   (bf16 in, fp32 accumulate, tcgen05)
+ * A = D^T (atoms x features, row stride lda), B = S stacked bf16 terms of the residuals
+ * (observations x features, row stride ldb), C^T row stride ldc (fp32).
+ * M % 128 == 0, Nb % 256 == 0, K % 64 == 0.  Replaces the per-observation
+ * Dictionary.correlate calls of a batch (dictionary.py:89-94). */
+int dscr_batched_gemm_bf16(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K,
+                           int splits, float* C, int ldc, void* stream);
+
 /* ---- multi-GPU (column sharding, one process per GPU) ---------------- */
 
 /* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */

@@ -29,6 +29,7 @@ ABI_FUNCTIONS = (
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
     "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
+    "dscr_batched_gemm_bf16",
 )
 
 
@@ -104,6 +105,7 @@ def _declare(lib):
         "dscr_solver_profile": (i32, [vp, i32, vp, C.POINTER(C.c_float)]),
         "dscr_comm_unique_id": (i32, [vp]),
         "dscr_solver_set_comm": (i32, [vp, vp, i32, i32]),
+        "dscr_batched_gemm_bf16": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
