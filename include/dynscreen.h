@@ -103,7 +103,9 @@ typedef struct dscr_problem_desc {
     const double* y;
     double lam;
     int32_t n_groups;        /* 0: Lasso */
-    int32_t pad0;
+    int32_t norm_aware;      /* 1: columns not unit-norm (fp32/bf16 storage): the SAFE/DST3 tests use
+                                ||a_i|| and the DST3 normal is the extremal atom over its norm
+                                (reduces to the reference at unit norms) */
     const int32_t* group_ptr;   /* n_groups+1 (device) */
     const double* group_w;      /* n_groups (device) */
     const double* group_snorm;  /* n_groups (device), ||D_g||_2 */
@@ -245,6 +247,46 @@ int dscr_solver_destroy(dscr_solver* h);
  * Dictionary.correlate calls of a batch (dictionary.py:89-94). */
 int dscr_batched_gemm_bf16(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K,
                            int splits, float* C, int ldc, void* stream);
+
+/* Batched FISTA with per-observation dynamic screening: shared bf16 dictionary
+ * (stored as D^T = atoms x features, i.e. column-major D), many observations.
+ * Iterates are sparse per observation; c = D^T theta runs on tcgen05 tensor cores;
+ * the fp64 setup computes lambda_*, a_* and the test centres. */
+typedef struct dscr_batched_desc {
+    int32_t n_rows;          /* N features, multiple of 64, <= 2048 */
+    int32_t n_atoms;         /* K, multiple of 128 */
+    int32_t n_obs;           /* B, multiple of 256 */
+    int32_t ldd;             /* row stride of D^T (elements), multiple of 8 */
+    const void* Dt;          /* bf16 [K][ldd] */
+    const double* Y;         /* fp64 [B][ldy], unit-norm observations */
+    int32_t ldy;             /* multiple of 64 */
+    int32_t splits;          /* bf16 terms of theta per GEMM: 1 or 2 */
+    const double* lam;       /* fp64 [B] (device) */
+    double L;                /* step constant 1/L */
+    int32_t test;            /* DSCR_TEST_OFF, DSCR_SAFE or DSCR_DST3 */
+    int32_t cap;             /* max nonzeros per observation */
+    int32_t max_iters;
+    int32_t pad;
+    const double* beta;      /* host [max_iters]: FISTA momentum coefficients (l_t - 1)/l_{t+1} */
+} dscr_batched_desc;
+
+typedef struct dscr_batched_buffers {
+    int32_t* x_idx[2]; double* x_val[2]; int32_t* x_cnt[2];   /* x lists by parity ([B][cap]) */
+    double* F; double* gap; int32_t* nnz; int32_t* kept; int32_t* status; double* lmax; double* radius;
+    double* trace;            /* [max_iters][4]: sum F, sum gap, sum nnz, sum kept */
+    int32_t* iterations;      /* device counter */
+    float* C;                 /* last correlations, [B][K] fp32 */
+    uint32_t* mask;           /* active atoms, [B][K/32] bits */
+} dscr_batched_buffers;
+
+typedef struct dscr_batched dscr_batched;
+size_t dscr_batched_workspace_size(const dscr_batched_desc* d);
+int dscr_batched_create(const dscr_batched_desc* d, void* workspace, size_t bytes, void* stream,
+                        dscr_batched** out);
+int dscr_batched_setup(dscr_batched* h, void* stream);
+int dscr_batched_run(dscr_batched* h, int iterations, void* stream);
+int dscr_batched_get_buffers(dscr_batched* h, dscr_batched_buffers* out);
+int dscr_batched_destroy(dscr_batched* h);
 
 /* ---- multi-GPU (column sharding, one process per GPU) ---------------- */
 

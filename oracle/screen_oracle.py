@@ -239,11 +239,15 @@ def dual_scale_group(prob, theta, norms=None, weights=None):
 class Geometry:
     """Per-solve precomputed correlations (ScreeningContext, screening.py:168-322)."""
 
-    def __init__(self, prob, lmax):
+    def __init__(self, prob, lmax, norm_aware=False):
         self.p, self.lmax = prob, lmax
         self.y_corr = prob.D.T @ prob.y
         self.safe_cc = self.y_corr / prob.lam
         self._cache = {}
+        # Extension for reduced-precision dictionaries whose columns are not unit-norm:
+        # the sphere test uses ||a_i|| and the DST3 normal is a_*/||a_*||.  At unit norms
+        # it reduces to the reference formulas (screening.py:221-231, 351-359).
+        self.norms = np.linalg.norm(prob.D, axis=0) if norm_aware else None
 
     @property
     def star_corr(self):
@@ -256,7 +260,13 @@ class Geometry:
         return self.lmax.value / self.p.lam - 1.0
 
     @property
+    def star_norm_sq(self):
+        return 1.0 if self.norms is None else float(self.norms[self.lmax.index]) ** 2
+
+    @property
     def dst3_cc(self):
+        if self.norms is not None:
+            return self.safe_cc - (self.shift / self.star_norm_sq) * self.star_corr
         return self.safe_cc - self.shift * self.star_corr
 
     def gst3(self):
@@ -303,10 +313,13 @@ class Geometry:
         if kind in (SAFE, GSAFE):
             return float(np.sqrt(rsq)), rsq
         if kind in (DST3, DOME):
-            return self.shifted(rsq, self.shift ** 2), rsq
+            return self.shifted(rsq, self.shift ** 2 / self.star_norm_sq), rsq
         return self.shifted(rsq, self.gst3()[1]), rsq
 
     def mask(self, kind, r, kept, kept_groups=None):
+        if kind in (SAFE, DST3) and self.norms is not None:
+            cc = self.safe_cc if kind == SAFE else self.dst3_cc
+            return (1.0 - np.abs(cc[kept])) / self.norms[kept] - r > SCREEN_MARGIN
         if kind == SAFE:
             return sphere_mask(self.safe_cc[kept], r)
         if kind == DST3:
@@ -374,6 +387,7 @@ class Config:
     bb_L_max: float = 1e10
     gap_tol: float | None = None
     op_norm: float | None = None     # ||D|| override for CP/TwIST (else power iteration)
+    norm_aware: bool = False         # non-unit-norm (fp32/bf16-rounded) dictionaries
 
 
 @dataclass
@@ -417,7 +431,7 @@ def solve(prob, cfg, hook=None):
 
     kept = np.arange(k, dtype=np.int64)
     elim = np.empty(0, np.int64)
-    geo = Geometry(prob, lm)
+    geo = Geometry(prob, lm, cfg.norm_aware)
     D = prob.D
     lay = Layout(prob, kept) if group else None
     kept_groups = np.arange(len(prob.groups), dtype=np.int64) if group else None

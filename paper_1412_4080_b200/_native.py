@@ -29,7 +29,8 @@ ABI_FUNCTIONS = (
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
     "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
-    "dscr_batched_gemm_bf16",
+    "dscr_batched_gemm_bf16", "dscr_batched_workspace_size", "dscr_batched_create", "dscr_batched_setup",
+    "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_destroy",
 )
 
 
@@ -37,7 +38,7 @@ class ProblemDesc(C.Structure):
     _fields_ = [
         ("dtype", C.c_int32), ("n_rows", C.c_int32), ("n_cols", C.c_int32), ("ldd", C.c_int32),
         ("D", C.c_void_p), ("y", C.c_void_p), ("lam", C.c_double),
-        ("n_groups", C.c_int32), ("pad0", C.c_int32),
+        ("n_groups", C.c_int32), ("norm_aware", C.c_int32),
         ("group_ptr", C.c_void_p), ("group_w", C.c_void_p), ("group_snorm", C.c_void_p),
         ("col_offset", C.c_int32), ("n_cols_total", C.c_int32),
         ("group_offset", C.c_int32), ("n_groups_total", C.c_int32),
@@ -76,6 +77,24 @@ class Buffers(C.Structure):
     ]
 
 
+class BatchedDesc(C.Structure):
+    _fields_ = [
+        ("n_rows", C.c_int32), ("n_atoms", C.c_int32), ("n_obs", C.c_int32), ("ldd", C.c_int32),
+        ("Dt", C.c_void_p), ("Y", C.c_void_p), ("ldy", C.c_int32), ("splits", C.c_int32),
+        ("lam", C.c_void_p), ("L", C.c_double), ("test", C.c_int32), ("cap", C.c_int32),
+        ("max_iters", C.c_int32), ("pad", C.c_int32), ("beta", C.c_void_p),
+    ]
+
+
+class BatchedBuffers(C.Structure):
+    _fields_ = [
+        ("x_idx", C.c_void_p * 2), ("x_val", C.c_void_p * 2), ("x_cnt", C.c_void_p * 2),
+        ("F", C.c_void_p), ("gap", C.c_void_p), ("nnz", C.c_void_p), ("kept", C.c_void_p),
+        ("status", C.c_void_p), ("lmax", C.c_void_p), ("radius", C.c_void_p), ("trace", C.c_void_p),
+        ("iterations", C.c_void_p), ("C", C.c_void_p), ("mask", C.c_void_p),
+    ]
+
+
 _lib = None
 _lock = threading.Lock()
 
@@ -106,6 +125,12 @@ def _declare(lib):
         "dscr_comm_unique_id": (i32, [vp]),
         "dscr_solver_set_comm": (i32, [vp, vp, i32, i32]),
         "dscr_batched_gemm_bf16": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]),
+        "dscr_batched_workspace_size": (sz, [C.POINTER(BatchedDesc)]),
+        "dscr_batched_create": (i32, [C.POINTER(BatchedDesc), vp, sz, vp, C.POINTER(vp)]),
+        "dscr_batched_setup": (i32, [vp, vp]),
+        "dscr_batched_run": (i32, [vp, i32, vp]),
+        "dscr_batched_get_buffers": (i32, [vp, C.POINTER(BatchedBuffers)]),
+        "dscr_batched_destroy": (i32, [vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -94,6 +94,8 @@ struct Params {
     double* cnorm;
     double* vec;       // N-vector scratch (a_* or the GST3 normal)
     double* dn;        // K-vector scratch (D^T normal)
+    double* anorm;     // per-column norms (norm-aware tests), or null
+    int norm_aware;
     int* act[2];
     int* act_cnt[2];
     int* act_off[2];
@@ -412,6 +414,8 @@ __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* s
     const int test = P.test;
     const double r = sc->radius;
     if (test == DSCR_SAFE || test == DSCR_DST3) {
+        if (P.norm_aware)   // max over the sphere of |a.theta| = |a.c| + r ||a||  (non-unit atoms)
+            return (1.0 - fabs(P.cc[unit])) / P.anorm[unit] - r > SCREEN_MARGIN;
         return (1.0 - fabs(P.cc[unit])) - r > SCREEN_MARGIN;   // screening.py:359
     }
     if (test == DSCR_DOME) {                                    // screening.py:374-388
@@ -1086,6 +1090,24 @@ __global__ void __launch_bounds__(NT) k_gst3_scalars(Params P) {
     }
 }
 
+// ||d_j||_2 in fp64 for the norm-aware tests (reduced-precision dictionaries)
+template <typename T>
+__global__ void __launch_bounds__(NT) k_colnorms(Params P) {
+    if (P.sc->stop) return;
+    const T* D = static_cast<const T*>(P.D);
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * NT + threadIdx.x) >> 5, nw = (gridDim.x * NT) >> 5;
+    for (int j = gw; j < P.kcols; j += nw) {
+        double acc = 0.0;
+        for (int i = lane; i < P.n; i += 32) {
+            const double d = elem<T>(D + (size_t)j * P.ldd + i);
+            acc = fma(d, d, acc);
+        }
+        acc = warp_sum(acc);
+        if (lane == 0) P.anorm[j] = sqrt(acc);
+    }
+}
+
 // test centre correlations (screening.py:213-255)
 __global__ void k_centers(Params P) {
     dscr_scalars* sc = P.sc;
@@ -1093,12 +1115,15 @@ __global__ void k_centers(Params P) {
     const int test = P.test;
     const double lam = P.lam;
     const double shift = sc->lmax / lam - 1.0;
+    // non-unit atoms: the DST3 half-space normal is a_*/||a_*||, at distance shift/||a_*|| from y/lam
+    const double an2 = P.norm_aware ? P.anorm[sc->lmax_unit] * P.anorm[sc->lmax_unit] : 1.0;
+    const double coef = P.norm_aware ? shift / an2 : shift;
     if (blockIdx.x == 0 && threadIdx.x == 0 && (test == DSCR_DST3 || test == DSCR_DOME))
-        sc->shift_sq = shift * shift;
+        sc->shift_sq = P.norm_aware ? shift * shift / an2 : shift * shift;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < P.kcols; j += gridDim.x * blockDim.x) {
         const double safe = P.ycorr[j] / lam;
         double c = safe;
-        if (test == DSCR_DST3) c = safe - shift * P.star[j];
+        if (test == DSCR_DST3) c = safe - coef * P.star[j];
         else if (test == DSCR_GST3) c = safe - (sc->gst3_coef / sc->gst3_nsq) * P.dn[j];
         P.cc[j] = c;
     }
@@ -1233,7 +1258,7 @@ static int kts_slots(const dscr_config* cfg) { return std::min(std::max(cfg->max
 struct Offsets {
     size_t sc, theta0, theta1, resid, corr, x0, x1, x2, u0, u1, ycorr, star, cc, cnorm, vec, dn;
     size_t act0, act1, cnt0, cnt1, off0, off1, mask, sidx, sa, sb, supcnt, supoff;
-    size_t p1, p2, p3v, p3s, tickets, trace, kts;
+    size_t p1, p2, p3v, p3s, tickets, trace, kts, anorm;
 };
 
 static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg, const Geometry& g,
@@ -1264,6 +1289,7 @@ static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg,
     o.tickets = L.add(64);
     o.trace = L.add((size_t)std::max(cfg->max_iters, 1) * DSCR_TRACE_FIELDS * 8);
     o.kts = L.add((size_t)kts_slots(cfg) * 8 * 8);
+    o.anorm = L.add(K * 8);
     *total = L.total + 256;
     return o;
 }
@@ -1321,6 +1347,8 @@ static int validate(const dscr_problem_desc* pr, const dscr_config* cfg, int* n_
     if (!(cfg->L0 > 0)) return set_inval("L0 must be positive");
     if (!(cfg->cp_step_safety > 0 && cfg->cp_step_safety < 1)) return set_inval("cp_step_safety must lie in (0, 1)");
     const bool group = pr->n_groups > 0;
+    if (pr->norm_aware && cfg->strategy != DSCR_NONE && cfg->test == DSCR_DOME)
+        return set_inval("the dome test requires unit-norm columns (norm_aware dictionaries: use safe or dst3)");
     if (cfg->strategy != DSCR_NONE) {
         if (cfg->test < 0) return set_inval("screening strategies require a test kind");
         bool lasso_test = cfg->test <= DSCR_DOME;
@@ -1447,6 +1475,15 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
             CK(cudaGetLastError());
             if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, P.l2_keep, s))) return rc;
         }
+        if (P.norm_aware) {
+            const int cg = std::max(1, std::min((P.kcols + NW - 1) / NW, 2048));
+            switch (P.dtype) {
+                case DSCR_F64: k_colnorms<double><<<cg, NT, 0, s>>>(P); break;
+                case DSCR_F32: k_colnorms<float><<<cg, NT, 0, s>>>(P); break;
+                default: k_colnorms<__nv_bfloat16><<<cg, NT, 0, s>>>(P);
+            }
+            CK(cudaGetLastError());
+        }
         k_centers<<<std::max(1, std::min((P.kcols + NT - 1) / NT, 1024)), NT, 0, s>>>(P);
         CK(cudaGetLastError());
         if (group) {
@@ -1516,6 +1553,8 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.p3s = (double*)(base + o.p3s); P.tickets = (unsigned*)(base + o.tickets);
     P.trace = (double*)(base + o.trace);
     P.kts = (unsigned long long*)(base + o.kts);
+    P.anorm = (double*)(base + o.anorm);
+    P.norm_aware = pr->norm_aware;
     P.max_kts = kts_slots(cfg);
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;

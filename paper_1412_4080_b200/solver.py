@@ -176,6 +176,8 @@ def _desc(problem, dp):
     d.D, d.y = dp.D.data_ptr(), dp.y.data_ptr()
     d.lam = problem.lam
     d.n_groups = dp.n_groups
+    dic = problem.dictionary
+    d.norm_aware = int(dic.dtype != "f64" or not dic.col_norm_checked)
     if dp.n_groups:
         d.group_ptr, d.group_w, d.group_snorm = dp.group_ptr.data_ptr(), dp.group_w.data_ptr(), dp.group_sn.data_ptr()
     d.col_offset, d.n_cols_total = 0, dp.k

@@ -38,7 +38,8 @@ def _compare(w, dic, part=None, x_rtol=1e-6, it_slack=0, check_safety=True):
     op = so.make_problem(D64, w.y, w.lam, w.groups, None if part is None else part.weights,
                          None if part is None else part.spectral_norms)
     ref = so.solve(op, so.Config(algorithm=w.algorithm, strategy="dynamic", test=w.test,
-                                 max_iters=w.max_iters, rel_tol=1e-300, L0=L, gap_tol=w.gap_tol))
+                                 max_iters=w.max_iters, rel_tol=1e-300, L0=L, gap_tol=w.gap_tol,
+                                 norm_aware=(dic.dtype != "f64")))
     assert abs(res.iterations - ref.iterations) <= it_slack, (res.iterations, ref.iterations)
     assert res.stop_reason == "gap"
     np.testing.assert_allclose(res.final_objective, ref.final_objective, rtol=x_rtol)

@@ -52,3 +52,56 @@ def test_gemm_c5_shape_throughput():
     tflops = 2 * M * Nb * K / ms / 1e9
     print(f"\nc5 D^T Theta: {ms * 1e3:.1f} us, {tflops:.0f} TFLOP/s")
     assert tflops > 200
+
+
+# ---------------------------------------------------------------- batched solver vs oracle
+
+import paper_1412_4080_b200 as ds  # noqa: E402
+from paper_1412_4080_b200 import workloads as wl  # noqa: E402
+from paper_1412_4080_b200.batched import solve_batched  # noqa: E402
+from oracle import screen_oracle as so  # noqa: E402
+
+
+def _batch_problem(n, k, b, ratio, seed=0):
+    w = wl.config5(seed=seed, n=n, k=k, batch=b, nnz=8, ratio=ratio)
+    dic = ds.Dictionary(w.D, check_unit_norms=False, dtype="bf16")
+    D64 = dic.as_float64()
+    L = float(np.linalg.norm(D64, 2) ** 2 * (1 + 1e-6))
+    return w, dic, D64, L
+
+
+@pytest.mark.parametrize("ratio,splits,tol", [(0.4, 1, 2e-2), (0.4, 2, 1e-4), (0.85, 2, 1e-4)])
+def test_batched_fista_matches_oracle(ratio, splits, tol):
+    w, dic, D64, L = _batch_problem(128, 1024, 256, ratio)
+    res = solve_batched(dic, w.y, w.lam, L, iterations=100, test="dst3", splits=splits)
+    assert res.iterations == 100
+    worst_f = 0.0
+    for j in range(0, 256, 17):
+        op = so.make_problem(D64, w.y[:, j], w.lam[j])
+        ref = so.solve(op, so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=100,
+                                     rel_tol=1e-300, L0=L, norm_aware=True))
+        f = res.objective[j]
+        worst_f = max(worst_f, abs(f - ref.final_objective) / ref.final_objective)
+        x = res.x_dense(j, 1024)
+        assert np.linalg.norm(x - ref.x_star) <= tol * 10 * max(np.linalg.norm(ref.x_star), 1e-12)
+        ref_kept = 1024 - ref.eliminated.size
+        if splits == 1:
+            # the bf16 error bound inflates the dual-scaling bound: the screen is more conservative
+            assert res.kept[j] >= ref_kept - 2
+        else:
+            assert abs(res.kept[j] - ref_kept) <= 2
+    assert worst_f <= tol, worst_f
+    if ratio > 0.5:
+        assert res.kept.min() < 1024      # screening fired somewhere
+
+
+def test_batched_c5_shape_runs():
+    w, dic, D64, L = _batch_problem(1024, 16384, 512, 0.4, seed=1)
+    res = solve_batched(dic, w.y, w.lam, L, iterations=100, test="dst3", splits=1)
+    assert res.iterations == 100 and np.all(res.status == 0)
+    for j in (0, 255):
+        op = so.make_problem(D64, w.y[:, j], w.lam[j])
+        ref = so.solve(op, so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=100,
+                                     rel_tol=1e-300, L0=L, norm_aware=True))
+        assert abs(res.objective[j] - ref.final_objective) <= 2e-2 * ref.final_objective
+    print(f"\nc5-shape batch of 512: {res.device_seconds * 1e3:.1f} ms for 100 iterations")
