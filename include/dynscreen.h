@@ -286,6 +286,8 @@ int dscr_batched_create(const dscr_batched_desc* d, void* workspace, size_t byte
 int dscr_batched_setup(dscr_batched* h, void* stream);
 int dscr_batched_run(dscr_batched* h, int iterations, void* stream);
 int dscr_batched_get_buffers(dscr_batched* h, dscr_batched_buffers* out);
+/* Profiling aid: iteration t as direct launches; ms_out[3] = GEMM, update, residual (blocking). */
+int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out);
 int dscr_batched_destroy(dscr_batched* h);
 
 /* ---- multi-GPU (column sharding, one process per GPU) ---------------- */

@@ -30,7 +30,7 @@ ABI_FUNCTIONS = (
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
     "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
     "dscr_batched_gemm_bf16", "dscr_batched_workspace_size", "dscr_batched_create", "dscr_batched_setup",
-    "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_destroy",
+    "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_profile", "dscr_batched_destroy",
 )
 
 
@@ -131,6 +131,7 @@ def _declare(lib):
         "dscr_batched_run": (i32, [vp, i32, vp]),
         "dscr_batched_get_buffers": (i32, [vp, C.POINTER(BatchedBuffers)]),
         "dscr_batched_destroy": (i32, [vp]),
+        "dscr_batched_profile": (i32, [vp, i32, vp, C.POINTER(C.c_float)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

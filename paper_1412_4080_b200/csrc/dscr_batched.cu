@@ -415,6 +415,7 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
 // value of a sorted sparse list at atoms g0..g0+31 (one per lane), advancing *ptr
 __device__ __forceinline__ double list_gather(const int* idx, const double* val, int cnt, int& ptr, int g0,
                                               double* scratch, int lane) {
+    if (ptr >= cnt || idx[ptr] >= g0 + 32) return 0.0;      // warp-uniform: no entry in this group
     scratch[lane] = 0.0;
     __syncwarp();
     for (;;) {
@@ -456,13 +457,95 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     const int span = P.K / BW;                 // atoms per warp (multiple of 32)
     const int a0 = warp * span;
     const double lam = P.lam[j], L = P.L;
-    // pass 1: max |c| over active atoms
+    const double thr = lam / L, beta = P.beta[t];
+    const int* xi = P.xi[par]; const double* xv = P.xv[par]; const int xcnt = P.xc[par][j];
+    const int* ui = P.ui[par]; const double* uv = P.uv[par]; const int ucnt = P.uc[par][j];
+    const size_t lo = (size_t)j * P.cap;
+    int pu0 = 0, px0 = 0;
+    if (lane == 0) { pu0 = lower_bound_dev(ui + lo, ucnt, a0); px0 = lower_bound_dev(xi + lo, xcnt, a0); }
+    pu0 = __shfl_sync(0xffffffffu, pu0, 0);
+    px0 = __shfl_sync(0xffffffffu, px0, 0);
+    // One sweep of the warp's atoms.  mode 0: max|c| and list counts assuming no atom is screened;
+    // mode 1: counts with the test; mode 2: write lists and mask words.
+    double rho = NAN, margin = SCREEN_MARGIN + 1e-6;
+    bool can_screen = false;
+    int nx_off = 0, nu_off = 0;
+    double pen = 0.0, nnz = 0.0, kept = 0.0;
     double m = 0.0;
-    for (int g0 = a0; g0 < a0 + span; g0 += 32) {
-        const uint32_t w = mrow[g0 >> 5];
-        if ((w >> lane) & 1u) m = fmax(m, fabs((double)crow[g0 + lane]));
-    }
-    m = warp_max(m);
+    // with u_i = x_i = 0 the candidate is nonzero only if |c_i| > lam (soft threshold of -c/L at lam/L):
+    // a conservative fp32 filter sends only those lanes (and groups holding list entries) down the
+    // exact fp64 path
+    const float hot_f = (float)(lam * (1.0 - 1e-6));
+    float mf = 0.0f;
+    auto sweep = [&](int mode, int& cx, int& cu) {
+        int pu = pu0, px = px0;
+        cx = 0; cu = 0;
+        int nu_at = (pu < ucnt) ? ui[lo + pu] : 0x7fffffff;     // next list atoms (cached)
+        int nx_at = (px < xcnt) ? xi[lo + px] : 0x7fffffff;
+        constexpr int PF = 8;                                    // groups prefetched per step
+        for (int gb = a0; gb < a0 + span; gb += 32 * PF) {
+            float cfs[PF];
+            uint32_t ws[PF];
+            const int ng = min(PF, (a0 + span - gb) >> 5);
+#pragma unroll
+            for (int q = 0; q < PF; ++q) {
+                cfs[q] = (q < ng) ? crow[gb + q * 32 + lane] : 0.0f;
+                ws[q] = (q < ng) ? mrow[(gb >> 5) + q] : 0u;
+            }
+#pragma unroll 1
+            for (int q = 0; q < ng; ++q) {
+                const int g0 = gb + q * 32;
+                const int i = g0 + lane;
+                const uint32_t w = ws[q];
+                bool active = (w >> lane) & 1u;
+                const float cf = cfs[q];
+                if (mode == 0 && active) mf = fmaxf(mf, fabsf(cf));
+                const bool lists = nu_at < g0 + 32 || nx_at < g0 + 32;
+                const bool screen_here = mode > 0 && can_screen && w != 0u;
+                if (!lists && !screen_here && !__any_sync(0xffffffffu, active && fabsf(cf) > hot_f)) {
+                    if (mode == 2 && lane == 0) kept += __popc(w);
+                    continue;
+                }
+                const double c = (double)cf;
+                const double u = list_gather(ui + lo, uv + lo, ucnt, pu, g0, s_scr[warp], lane);
+                const double x = list_gather(xi + lo, xv + lo, xcnt, px, g0, s_scr[warp], lane);
+                nu_at = (pu < ucnt) ? ui[lo + pu] : 0x7fffffff;
+                nx_at = (px < xcnt) ? xi[lo + px] : 0x7fffffff;
+                if (screen_here && active) {
+                    const double ccv = (double)P.cc[(size_t)j * P.K + i];
+                    if ((1.0 - fabs(ccv)) / P.anorm[i] - rho > margin) active = false;   // screening.py:359, norm-aware
+                }
+                double cand = 0.0, un = 0.0;
+                if (active) {
+                    cand = soft(u - c / L, thr);
+                    un = cand + beta * (cand - x);
+                }
+                const unsigned bx = __ballot_sync(0xffffffffu, cand != 0.0);
+                const unsigned bu = __ballot_sync(0xffffffffu, un != 0.0);
+                if (mode == 2) {
+                    const unsigned ba = __ballot_sync(0xffffffffu, active);
+                    const unsigned ltm = (1u << lane) - 1u;
+                    if (cand != 0.0) {
+                        const int e = nx_off + cx + __popc(bx & ltm);
+                        if (e < P.cap) { P.xi[par ^ 1][lo + e] = i; P.xv[par ^ 1][lo + e] = cand; }
+                    }
+                    if (un != 0.0) {
+                        const int e = nu_off + cu + __popc(bu & ltm);
+                        if (e < P.cap) { P.ui[par ^ 1][lo + e] = i; P.uv[par ^ 1][lo + e] = un; }
+                    }
+                    if (lane == 0 && ba != w) mrow[g0 >> 5] = ba;
+                    pen += fabs(cand);
+                    nnz += (cand != 0.0) ? 1.0 : 0.0;
+                    if (lane == 0) kept += __popc(ba);
+                }
+                cx += __popc(bx);
+                cu += __popc(bu);
+            }
+        }
+    };
+    int cx, cu;
+    sweep(0, cx, cu);
+    m = warp_max((double)mf);
     if (lane == 0) s_scr[warp][0] = m;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -483,83 +566,26 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
         acc = fma(d, d, acc);
     }
     const double rsq = block_sum(acc, s_sh);
-    double rho = NAN;
-    bool can_screen = false;
     if (P.test == DSCR_SAFE) rho = sqrt(rsq);
     else if (P.test == DSCR_DST3) {
         const double arg = rsq - P.shift_sq[j];
         if (arg < -RADIUS_GUARD && threadIdx.x == 0) P.status[j] = 3;
         rho = sqrt(fmax(arg, 0.0));
     }
-    // fp32 centre correlations carry <= 2^-21 relative error for |cc| <= 4: screen with 1e-6 extra margin
-    const double margin = SCREEN_MARGIN + 1e-6;
+    // fp32 centre correlations: screen only with a 1e-6 extra margin
     if (P.test != DSCR_TEST_OFF) can_screen = P.ccmin[j] - rho > margin;
-    const double thr = lam / L, beta = P.beta[t];
-    const int* xi = P.xi[par]; const double* xv = P.xv[par]; const int xcnt = P.xc[par][j];
-    const int* ui = P.ui[par]; const double* uv = P.uv[par]; const int ucnt = P.uc[par][j];
-    const size_t lo = (size_t)j * P.cap;
-    int pu0 = 0, px0 = 0;
-    if (lane == 0) { pu0 = lower_bound_dev(ui + lo, ucnt, a0); px0 = lower_bound_dev(xi + lo, xcnt, a0); }
-    pu0 = __shfl_sync(0xffffffffu, pu0, 0);
-    px0 = __shfl_sync(0xffffffffu, px0, 0);
-    // two passes: count (pass 0), then write at the warp's offsets (pass 1)
-    int nx_off = 0, nu_off = 0;
-    double pen = 0.0, nnz = 0.0, kept = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-        int pu = pu0, px = px0, cx = 0, cu = 0;
-        for (int g0 = a0; g0 < a0 + span; g0 += 32) {
-            const int i = g0 + lane;
-            const uint32_t w = mrow[g0 >> 5];
-            bool active = (w >> lane) & 1u;
-            const double c = (double)crow[i];
-            const double u = list_gather(ui + lo, uv + lo, ucnt, pu, g0, s_scr[warp], lane);
-            const double x = list_gather(xi + lo, xv + lo, xcnt, px, g0, s_scr[warp], lane);
-            if (active && can_screen) {
-                const double ccv = (double)P.cc[(size_t)j * P.K + i];
-                if ((1.0 - fabs(ccv)) / P.anorm[i] - rho > margin) active = false;   // screening.py:359, norm-aware
-            }
-            double cand = 0.0, un = 0.0;
-            if (active) {
-                cand = soft(u - c / L, thr);
-                un = cand + beta * (cand - x);
-            }
-            const unsigned bx = __ballot_sync(0xffffffffu, cand != 0.0);
-            const unsigned bu = __ballot_sync(0xffffffffu, un != 0.0);
-            const unsigned ba = __ballot_sync(0xffffffffu, active);
-            if (pass == 1) {
-                const unsigned lt = (1u << lane) - 1u;
-                if (cand != 0.0) {
-                    const int e = nx_off + cx + __popc(bx & lt);
-                    if (e < P.cap) { P.xi[par ^ 1][lo + e] = i; P.xv[par ^ 1][lo + e] = cand; }
-                }
-                if (un != 0.0) {
-                    const int e = nu_off + cu + __popc(bu & lt);
-                    if (e < P.cap) { P.ui[par ^ 1][lo + e] = i; P.uv[par ^ 1][lo + e] = un; }
-                }
-                if (lane == 0) mrow[g0 >> 5] = ba;
-                pen += fabs(cand);
-                nnz += (cand != 0.0) ? 1.0 : 0.0;
-                if (lane == 0) kept += __popc(ba);
-            }
-            cx += __popc(bx);
-            cu += __popc(bu);
-        }
-        if (pass == 0) {
-            if (lane == 0) { s_cnt[0][warp] = cx; s_cnt[1][warp] = cu; }
-            __syncthreads();
-            int ox = 0, ou = 0;
-            for (int w = 0; w < warp; ++w) { ox += s_cnt[0][w]; ou += s_cnt[1][w]; }
-            nx_off = ox;
-            nu_off = ou;
-            if (threadIdx.x == 0) {
-                int tx = 0, tu = 0;
-                for (int w = 0; w < BW; ++w) { tx += s_cnt[0][w]; tu += s_cnt[1][w]; }
-                s_cnt[0][BW] = tx;
-                s_cnt[1][BW] = tu;
-            }
-            __syncthreads();
-        }
+    if (can_screen) sweep(1, cx, cu);
+    if (lane == 0) { s_cnt[0][warp] = cx; s_cnt[1][warp] = cu; }
+    __syncthreads();
+    for (int w = 0; w < warp; ++w) { nx_off += s_cnt[0][w]; nu_off += s_cnt[1][w]; }
+    if (threadIdx.x == 0) {
+        int tx = 0, tu = 0;
+        for (int w = 0; w < BW; ++w) { tx += s_cnt[0][w]; tu += s_cnt[1][w]; }
+        s_cnt[0][BW] = tx;
+        s_cnt[1][BW] = tu;
     }
+    __syncthreads();
+    sweep(2, cx, cu);
     double v3[3] = {pen, nnz, kept};
     block_sum_n<3>(v3, s_sh);
     if (threadIdx.x == 0) {
@@ -786,6 +812,29 @@ int dscr_batched_run(dscr_batched* h, int iters, void* stream) {
         h->iters_captured = iters;
     }
     cudaError_t e = cudaGraphLaunch(h->ge, s);
+    if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+    return DSCR_OK;
+}
+
+// one iteration as direct launches with CUDA events: ms_out = {GEMM, update, residual}
+int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out) {
+    if (!h || !ms_out || t < 0 || t >= h->max_iters) { err_store() = "bad profile arguments"; return DSCR_EINVAL; }
+    cudaStream_t s = (cudaStream_t)stream;
+    BParams& P = h->P;
+    cudaEvent_t ev[4];
+    for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
+    cudaEventRecord(ev[0], s);
+    int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s);
+    cudaEventRecord(ev[1], s);
+    k_bupdate<<<P.B, BT, 0, s>>>(P, t);
+    cudaEventRecord(ev[2], s);
+    k_bresid<<<P.B, BT, 0, s>>>(P, t);
+    cudaEventRecord(ev[3], s);
+    cudaEventSynchronize(ev[3]);
+    for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
+    for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+    cudaError_t e = cudaGetLastError();
+    if (rc) return rc;
     if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     return DSCR_OK;
 }
