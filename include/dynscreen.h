@@ -153,6 +153,7 @@ typedef struct dscr_scalars {
     double pen, ss_red, f_prev, F;
     double gap, t0_ns, gst3_coef, gst3_nsq;
     double ds_sq, fc, tw_step, spare;
+    double astar_nsq, gstar_w;   /* ||a_*||^2 (norm-aware DST3); weight of the extremal group (GST3) */
 } dscr_scalars;
 
 /* Device pointers into a solver's workspace (valid while the handle lives). */
@@ -176,7 +177,9 @@ typedef struct dscr_solver_buffers {
     int32_t max_kts;
     int32_t G;               /* CTAs of the per-unit kernels (= number of slots) */
     int32_t cap;             /* slot capacity in units */
-    int32_t pad;
+    int32_t comm_len;        /* doubles in `comm` */
+    double* comm;            /* multi-rank exchange region: [0,8) MAX, [8,16) setup, [16,32)+[32,32+2*ldd) SUM */
+    double* vec;             /* ldd: extremal atom / GST3 normal (broadcast from the owner rank) */
 } dscr_solver_buffers;
 
 typedef struct dscr_solver dscr_solver;
@@ -291,6 +294,30 @@ int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out);
 int dscr_batched_destroy(dscr_batched* h);
 
 /* ---- multi-GPU (column sharding, one process per GPU) ---------------- */
+
+/* Phases of a column-sharded solve.  Each rank owns a contiguous block of columns
+ * (groups kept whole; col_offset / group_offset in the problem descriptor).  The host
+ * runs the phases in this order and reduces the comm region between them:
+ *   SETUP_LOCAL; all-gather comm[8..10] (local lambda_*, global index, sign), pick the
+ *   max (lowest index on ties) and write comm[8..14] = {lambda_*, index, sign, trivial,
+ *   is_owner, w_g*, owner's local unit}; SETUP_ADOPT; owner: SETUP_VEC; broadcast the
+ *   vec buffer from the owner; SETUP_FINISH; [static: STATIC_LOCAL; MAX comm[0..7];
+ *   STATIC_FINISH]; then per trip: K1; MAX comm[0..7]; K1R; K2; K3A; K3S;
+ *   SUM comm[16..32+2*ldd); K3B.  Every rank computes the radius, stop flags and trip
+ *   modes from identical reduced values. */
+#define DSCR_PH_SETUP_LOCAL 0
+#define DSCR_PH_SETUP_ADOPT 1
+#define DSCR_PH_SETUP_VEC 2
+#define DSCR_PH_SETUP_FINISH 3
+#define DSCR_PH_STATIC_LOCAL 4
+#define DSCR_PH_STATIC_FINISH 5
+#define DSCR_PH_K1 10
+#define DSCR_PH_K1R 11
+#define DSCR_PH_K2 12
+#define DSCR_PH_K3A 13
+#define DSCR_PH_K3S 14
+#define DSCR_PH_K3B 15
+int dscr_solver_phase(dscr_solver* h, int phase, void* stream);
 
 /* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */
 int dscr_comm_unique_id(void* id_out_128);

@@ -50,6 +50,9 @@ constexpr int NP1 = 6;   // K1 partials
 constexpr int NP2 = 6;   // K2 partials
 constexpr int NP3 = 4;   // K3b partials
 constexpr int MIN_COLS_PER_SPLIT = 16;
+// comm region (doubles): [0,8) MAX-reduced, [8,16) setup exchange, [16,32) SUM-reduced scalars,
+// [32, 32+2*ldd) SUM-reduced partial residual vectors D_S a, D_S b
+constexpr int CM_MAX = 0, CM_SETUP = 8, CM_SUM = 16, CM_VEC = 32;
 constexpr int TRIPS_PER_BODY = 4;
 
 
@@ -116,8 +119,10 @@ struct Params {
     int max_kts;
     int max_iters;
     int G, cap, TR, R, P, G3b;
-    int col_offset;
+    int col_offset, group_offset;
     int in_graph;
+    int split;         // multi-rank: phases exchange through `comm` (see dscr_solver_phase)
+    double* comm;
     float l2_keep;
     cudaGraphConditionalHandle h_main;
 };
@@ -402,8 +407,57 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
             sc->sigma_new = sc->sigma / phi;
         }
     }
+    if (P.split) {
+        if (threadIdx.x == 0) {
+            P.comm[CM_MAX + 0] = GROUP ? ((any > 0.0) ? -m : -INFINITY) : m;
+            P.comm[CM_MAX + 1] = nf;
+            P.comm[CM_MAX + 2] = any;
+        }
+        return;
+    }
     radius_epilogue(P, bound, P.theta[p], sc->theta_sq, sc->theta_y, s_sh);
     if (threadIdx.x == 0) stamp(P, 1);
+}
+
+// split mode: radius from the MAX-reduced correlation bound (after the collective)
+__global__ void __launch_bounds__(NT) k1r_radius(Params P) {
+    __shared__ double s_sh[64];
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    const int mode = sc->mode;
+    if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
+    const double m = P.comm[CM_MAX + 0];
+    double bound;
+    if (P.n_groups) bound = (P.comm[CM_MAX + 2] > 0.0) ? -m : INFINITY;
+    else bound = (m == 0.0) ? INFINITY : 1.0 / m;
+    if (threadIdx.x == 0) {
+        sc->corr_inf = P.n_groups ? -m : m;
+        sc->nonfinite = P.comm[CM_MAX + 1] > 0.0;
+    }
+    radius_epilogue(P, bound, P.theta[sc->parity], sc->theta_sq, sc->theta_y, s_sh);
+}
+
+// split mode: sum the local split partials into the comm vector, local scalars into comm
+__global__ void __launch_bounds__(NT) k3s_pack(Params P) {
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->mode == MODE_STATIC) return;
+    const int pe = sc->p_eff;
+    for (int r = blockIdx.x * NT + threadIdx.x; r < P.ldd; r += gridDim.x * NT) {
+        double a = 0.0, b = 0.0;
+        if (r < P.n)
+            for (int q = 0; q < pe; ++q) {
+                a += P.p3v[((size_t)q * 2) * P.ldd + r];
+                b += P.p3v[((size_t)q * 2 + 1) * P.ldd + r];
+            }
+        P.comm[CM_VEC + r] = a;
+        P.comm[CM_VEC + P.ldd + r] = b;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        double* o = P.comm + CM_SUM;
+        o[0] = sc->pen; o[1] = sc->nnz; o[2] = sc->kept_atoms; o[3] = sc->ss_red;
+        o[4] = sc->dropped_nz; o[5] = sc->maj_cs; o[6] = sc->maj_ss; o[7] = 0.0;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -818,9 +872,13 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
         const int r = blockIdx.x * K3B_ROWS + rr;
         double a = 0.0, b = 0.0;
         if (r < P.n) {
-            for (int s = g; s < pe; s += K3B_GROUPS) {
-                a += P.p3v[((size_t)s * 2) * P.ldd + r];
-                b += P.p3v[((size_t)s * 2 + 1) * P.ldd + r];
+            if (P.split) {
+                if (g == 0) { a = P.comm[CM_VEC + r]; b = P.comm[CM_VEC + P.ldd + r]; }
+            } else {
+                for (int s = g; s < pe; s += K3B_GROUPS) {
+                    a += P.p3v[((size_t)s * 2) * P.ldd + r];
+                    b += P.p3v[((size_t)s * 2 + 1) * P.ldd + r];
+                }
             }
         }
         s_pa[g][rr] = a;
@@ -878,6 +936,11 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     a0 = r4[0]; a1 = r4[1]; a2 = r4[2]; a3 = r4[3];
     if (threadIdx.x == 0) {
         stamp(P, 7);
+        if (P.split) {      // global sums of the per-rank K1/K2 scalars
+            const double* o = P.comm + CM_SUM;
+            sc->pen = o[0]; sc->nnz = (int)llround(o[1]); sc->kept_atoms = (int)llround(o[2]);
+            sc->ss_red = o[3]; sc->dropped_nz = o[4] > 0.0; sc->maj_cs = o[5]; sc->maj_ss = o[6];
+        }
         iteration_epilogue(P, a0, a1, a2, a3);
     }
 }
@@ -1032,9 +1095,14 @@ __global__ void __launch_bounds__(NT) k_lmax(Params P) {
         dscr_scalars* sc = P.sc;
         sc->lmax = bv;
         sc->lmax_unit = bidx;
-        sc->lmax_index = bidx + (P.n_groups ? 0 : P.col_offset);
+        sc->lmax_index = bidx + (P.n_groups ? P.group_offset : P.col_offset);
         if (!P.n_groups) sc->lmax_sign = (P.ycorr[bidx] >= 0.0) ? 1.0 : -1.0;
-        if (P.lam > bv) {                       // solvers.py:384-397
+        if (P.n_groups) sc->gstar_w = P.gw[bidx];
+        if (P.split) {          // candidate for the cross-rank argmax (value, global index, sign)
+            P.comm[CM_SETUP + 0] = bv;
+            P.comm[CM_SETUP + 1] = (double)sc->lmax_index;
+            P.comm[CM_SETUP + 2] = sc->lmax_sign;
+        } else if (P.lam > bv) {                // solvers.py:384-397
             sc->trivial = 1;
             sc->stop = DSCR_STOP_TRIVIAL;
         }
@@ -1082,7 +1150,7 @@ __global__ void __launch_bounds__(NT) k_gst3_scalars(Params P) {
             sc->stop = DSCR_STOP_ERROR;
             return;
         }
-        const double w = P.gw[sc->lmax_unit];
+        const double w = sc->gstar_w;
         const double coef = b / P.lam - w * w;
         sc->gst3_coef = coef;
         sc->gst3_nsq = a;
@@ -1108,6 +1176,28 @@ __global__ void __launch_bounds__(NT) k_colnorms(Params P) {
     }
 }
 
+// ||vec||^2 of the broadcast extremal atom (norm-aware DST3)
+__global__ void __launch_bounds__(NT) k_vec_nsq(Params P) {
+    __shared__ double s_sh[64];
+    if (P.sc->stop) return;
+    double a = 0.0;
+    for (int r = threadIdx.x; r < P.n; r += NT) a = fma(P.vec[r], P.vec[r], a);
+    a = block_sum(a, s_sh);
+    if (threadIdx.x == 0) P.sc->astar_nsq = a;
+}
+
+// split mode: adopt the cross-rank lambda_* decision written by the host into comm
+__global__ void k_setup_adopt(Params P) {
+    dscr_scalars* sc = P.sc;
+    const double* c = P.comm + CM_SETUP;
+    sc->lmax = c[0];
+    sc->lmax_index = (int)c[1];
+    sc->lmax_sign = c[2];
+    sc->gstar_w = c[5];
+    sc->lmax_unit = (c[4] > 0.0) ? (int)c[6] : -1;     // owner keeps its local unit
+    if (c[3] > 0.0) { sc->trivial = 1; sc->stop = DSCR_STOP_TRIVIAL; }
+}
+
 // test centre correlations (screening.py:213-255)
 __global__ void k_centers(Params P) {
     dscr_scalars* sc = P.sc;
@@ -1116,7 +1206,7 @@ __global__ void k_centers(Params P) {
     const double lam = P.lam;
     const double shift = sc->lmax / lam - 1.0;
     // non-unit atoms: the DST3 half-space normal is a_*/||a_*||, at distance shift/||a_*|| from y/lam
-    const double an2 = P.norm_aware ? P.anorm[sc->lmax_unit] * P.anorm[sc->lmax_unit] : 1.0;
+    const double an2 = P.norm_aware ? sc->astar_nsq : 1.0;
     const double coef = P.norm_aware ? shift / an2 : shift;
     if (blockIdx.x == 0 && threadIdx.x == 0 && (test == DSCR_DST3 || test == DSCR_DOME))
         sc->shift_sq = P.norm_aware ? shift * shift / an2 : shift * shift;
@@ -1138,7 +1228,7 @@ __global__ void k_center_group_norms(Params P) {
 }
 
 // static screen-once region at theta = y (screening.py:309-315)
-__global__ void __launch_bounds__(NT) k_static_radius(Params P) {
+__global__ void __launch_bounds__(NT) k_static_radius(Params P, int from_comm) {
     __shared__ double s_sh[64];
     __shared__ double s_m[NW];
     __shared__ int s_any[NW];
@@ -1167,7 +1257,20 @@ __global__ void __launch_bounds__(NT) k_static_radius(Params P) {
     }
     __syncthreads();
     m = s_m[0];
-    double bound = P.n_groups ? (s_any[0] ? m : INFINITY) : (m == 0.0 ? INFINITY : 1.0 / m);
+    if (P.split && !from_comm) {      // publish the local bound, finish after the MAX collective
+        if (threadIdx.x == 0) {
+            P.comm[CM_MAX + 0] = P.n_groups ? (s_any[0] ? -m : -INFINITY) : m;
+            P.comm[CM_MAX + 1] = 0.0;
+            P.comm[CM_MAX + 2] = s_any[0] ? 1.0 : 0.0;
+        }
+        return;
+    }
+    bool any_g = s_any[0] != 0;
+    if (from_comm) {
+        m = P.n_groups ? -P.comm[CM_MAX + 0] : P.comm[CM_MAX + 0];
+        any_g = P.comm[CM_MAX + 2] > 0.0;
+    }
+    double bound = P.n_groups ? (any_g ? m : INFINITY) : (m == 0.0 ? INFINITY : 1.0 / m);
     // theta = y: ||theta||^2 and theta.y are the same dot product
     radius_epilogue(P, bound, P.y, sc->yy, sc->yy, s_sh);
     if (threadIdx.x == 0) sc->mode = MODE_STATIC;
@@ -1258,7 +1361,7 @@ static int kts_slots(const dscr_config* cfg) { return std::min(std::max(cfg->max
 struct Offsets {
     size_t sc, theta0, theta1, resid, corr, x0, x1, x2, u0, u1, ycorr, star, cc, cnorm, vec, dn;
     size_t act0, act1, cnt0, cnt1, off0, off1, mask, sidx, sa, sb, supcnt, supoff;
-    size_t p1, p2, p3v, p3s, tickets, trace, kts, anorm;
+    size_t p1, p2, p3v, p3s, tickets, trace, kts, anorm, comm;
 };
 
 static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg, const Geometry& g,
@@ -1290,6 +1393,7 @@ static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg,
     o.trace = L.add((size_t)std::max(cfg->max_iters, 1) * DSCR_TRACE_FIELDS * 8);
     o.kts = L.add((size_t)kts_slots(cfg) * 8 * 8);
     o.anorm = L.add(K * 8);
+    o.comm = L.add((CM_VEC + 2 * ldd) * 8);
     *total = L.total + 256;
     return o;
 }
@@ -1463,6 +1567,7 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
                 default: k_setup_vec<__nv_bfloat16><<<32, NT, 0, s>>>(P);
             }
             CK(cudaGetLastError());
+            k_vec_nsq<<<1, NT, 0, s>>>(P);
             if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.star, stop_flag, P.l2_keep, s))) return rc;
         } else if (test == DSCR_GST3) {
             switch (P.dtype) {
@@ -1491,7 +1596,7 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
             CK(cudaGetLastError());
         }
         if (P.strategy == DSCR_STATIC) {
-            k_static_radius<<<1, NT, 0, s>>>(P);
+            k_static_radius<<<1, NT, 0, s>>>(P, 0);
             CK(cudaGetLastError());
             if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
             else k2_screen<false><<<g.G, NT, 0, s>>>(P);
@@ -1554,11 +1659,13 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.trace = (double*)(base + o.trace);
     P.kts = (unsigned long long*)(base + o.kts);
     P.anorm = (double*)(base + o.anorm);
+    P.comm = (double*)(base + o.comm);
     P.norm_aware = pr->norm_aware;
     P.max_kts = kts_slots(cfg);
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
     P.col_offset = pr->col_offset;
+    P.group_offset = pr->group_offset;
     P.in_graph = 1;
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
 
@@ -1671,6 +1778,113 @@ int dscr_solver_profile(dscr_solver* h, int trips, void* stream, float* ms_out) 
     return rc;
 }
 
+// Multi-rank (column-sharded) execution: the host runs these phases in order and
+// performs the collectives on the comm region between them (Multi-GPU).
+int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
+    if (!h) return set_inval("null handle");
+    cudaStream_t s = (cudaStream_t)stream;
+    Params P = h->P;
+    P.in_graph = 0;
+    P.split = 1;
+    const Geometry& g = h->geo;
+    const bool group = P.n_groups > 0;
+    const int test = P.test;
+    int rc = DSCR_OK;
+    switch (phase) {
+        case DSCR_PH_SETUP_LOCAL: {
+            k_init<<<256, NT, 0, s>>>(P);
+            k_init_scalars<<<1, NT, 0, s>>>(P);
+            if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.y, P.ycorr, nullptr, P.l2_keep, s))) return rc;
+            k_lmax<<<std::max(1, std::min((P.n_units + NT - 1) / NT, 2048)), NT, 0, s>>>(P);
+            break;
+        }
+        case DSCR_PH_SETUP_ADOPT:
+            k_setup_adopt<<<1, 1, 0, s>>>(P);
+            break;
+        case DSCR_PH_SETUP_VEC:     // owner rank only: extremal atom or GST3 normal into vec
+            switch (P.dtype) {
+                case DSCR_F64: k_setup_vec<double><<<32, NT, 0, s>>>(P); break;
+                case DSCR_F32: k_setup_vec<float><<<32, NT, 0, s>>>(P); break;
+                default: k_setup_vec<__nv_bfloat16><<<32, NT, 0, s>>>(P);
+            }
+            break;
+        case DSCR_PH_SETUP_FINISH: {
+            if (P.strategy == DSCR_NONE) break;
+            const int* stop_flag = &P.sc->stop;
+            if (test == DSCR_DST3 || test == DSCR_DOME) {
+                k_vec_nsq<<<1, NT, 0, s>>>(P);
+                if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.star, stop_flag, P.l2_keep, s))) return rc;
+            } else if (test == DSCR_GST3) {
+                k_gst3_scalars<<<1, NT, 0, s>>>(P);
+                if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, P.l2_keep, s))) return rc;
+            }
+            if (P.norm_aware) {
+                const int cg = std::max(1, std::min((P.kcols + NW - 1) / NW, 2048));
+                switch (P.dtype) {
+                    case DSCR_F64: k_colnorms<double><<<cg, NT, 0, s>>>(P); break;
+                    case DSCR_F32: k_colnorms<float><<<cg, NT, 0, s>>>(P); break;
+                    default: k_colnorms<__nv_bfloat16><<<cg, NT, 0, s>>>(P);
+                }
+            }
+            k_centers<<<std::max(1, std::min((P.kcols + NT - 1) / NT, 1024)), NT, 0, s>>>(P);
+            if (group) k_center_group_norms<<<std::max(1, std::min((P.n_groups + NT - 1) / NT, 1024)), NT, 0, s>>>(P);
+            break;
+        }
+        case DSCR_PH_STATIC_LOCAL:
+            k_static_radius<<<1, NT, 0, s>>>(P, 0);
+            break;
+        case DSCR_PH_STATIC_FINISH:
+            k_static_radius<<<1, NT, 0, s>>>(P, 1);
+            if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
+            else k2_screen<false><<<g.G, NT, 0, s>>>(P);
+            k_static_done<<<1, 1, 0, s>>>(P);
+            break;
+        case DSCR_PH_K1: {
+            const size_t smem1 = (size_t)g.smem1;
+            switch (P.dtype) {
+                case DSCR_F64:
+                    if (group) k1_corr_update<double, true><<<g.G, NT, smem1, s>>>(P);
+                    else k1_corr_update<double, false><<<g.G, NT, smem1, s>>>(P);
+                    break;
+                case DSCR_F32:
+                    if (group) k1_corr_update<float, true><<<g.G, NT, smem1, s>>>(P);
+                    else k1_corr_update<float, false><<<g.G, NT, smem1, s>>>(P);
+                    break;
+                default:
+                    if (group) k1_corr_update<__nv_bfloat16, true><<<g.G, NT, smem1, s>>>(P);
+                    else k1_corr_update<__nv_bfloat16, false><<<g.G, NT, smem1, s>>>(P);
+            }
+            break;
+        }
+        case DSCR_PH_K1R:
+            k1r_radius<<<1, NT, 0, s>>>(P);
+            break;
+        case DSCR_PH_K2:
+            if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
+            else k2_screen<false><<<g.G, NT, 0, s>>>(P);
+            break;
+        case DSCR_PH_K3A: {
+            dim3 g3(g.R, g.P);
+            switch (P.dtype) {
+                case DSCR_F64: k3a_residual<double><<<g3, NT, 0, s>>>(P); break;
+                case DSCR_F32: k3a_residual<float><<<g3, NT, 0, s>>>(P); break;
+                default: k3a_residual<__nv_bfloat16><<<g3, NT, 0, s>>>(P);
+            }
+            break;
+        }
+        case DSCR_PH_K3S:
+            k3s_pack<<<std::max(1, std::min((P.ldd + NT - 1) / NT, 256)), NT, 0, s>>>(P);
+            break;
+        case DSCR_PH_K3B:
+            k3b_finalize<<<g.G3b, NT, 0, s>>>(P);
+            break;
+        default:
+            return set_inval("unknown phase");
+    }
+    CK(cudaGetLastError());
+    return DSCR_OK;
+}
+
 int dscr_solver_scalars(dscr_solver* h, void* stream, dscr_scalars* out) {
     if (!h || !out) return set_inval("null argument");
     CK(cudaStreamSynchronize((cudaStream_t)stream));
@@ -1692,6 +1906,8 @@ int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* b) {
     b->act_off[0] = P.act_off[0]; b->act_off[1] = P.act_off[1];
     b->mask = P.mask; b->trace = P.trace;
     b->kts = (uint64_t*)P.kts; b->max_kts = P.max_kts;
+    b->comm = P.comm; b->comm_len = CM_VEC + 2 * P.ldd;
+    b->vec = P.vec;
     b->G = P.G; b->cap = P.cap;
     return DSCR_OK;
 }

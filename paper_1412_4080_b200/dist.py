@@ -1,0 +1,211 @@
+"""Column-sharded solves across GPUs (one process per GPU, torch.distributed).
+
+SURVEY §8(e): each rank owns a contiguous block of dictionary columns (groups
+kept whole) and runs the per-iteration kernels on it; per trip two collectives
+join the ranks — a MAX of the correlation bound after K1 (the dual scaling needs
+max |c| over *all* active atoms before any test) and a SUM of the length-N
+partial residuals ``D_S a``, ``D_S b`` plus the per-rank scalars after K3a.
+Every rank then computes the radius, the objective, the gap, the stop flags and
+the REDO/FIXUP trip modes from identical reduced values, so all ranks take the
+same control path.  lambda_* is a cross-rank argmax with the reference's
+lowest-index tie break (problems.py:79); the extremal atom (or the GST3 normal)
+is broadcast from its owner.
+
+The collectives are ``torch.distributed`` all-reduces on zero-copy views of the
+engine's ``comm`` region: NCCL over NVLink on GPUs, gloo in the CPU tests (which
+drive the same ``orchestrate`` with a numpy phase backend).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+
+from . import _native as nat
+from .problem import GROUP, Dictionary, GroupPartition, Problem
+from .solver import ScreenState, SolveResult, SolverConfig
+from .instrument import SolveTrace, flops_iteration
+
+NEEDS_VEC = ("dst3", "dome", "gst3")
+
+
+def shard_ranges(k, world, group_sizes=None):
+    """[start, end) column block per rank; with groups, whole groups per rank (by atom count)."""
+    if group_sizes is None:
+        bounds = [round(r * k / world) for r in range(world + 1)]
+        return [(bounds[r], bounds[r + 1]) for r in range(world)]
+    ptr = np.concatenate(([0], np.cumsum(group_sizes)))
+    g_bounds = [int(np.searchsorted(ptr, r * k / world, side="left")) for r in range(world)] + [len(group_sizes)]
+    g_bounds[0] = 0
+    return [(int(ptr[g_bounds[r]]), int(ptr[g_bounds[r + 1]])) for r in range(world)], \
+           [(g_bounds[r], g_bounds[r + 1]) for r in range(world)]
+
+
+def _allreduce(tensor, op, pg):
+    import torch.distributed as dist
+    if pg is None:
+        return
+    dist.all_reduce(tensor, op=op, group=pg)
+
+
+def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8):
+    """Run a sharded solve: setup exchange, then trips with the two collectives."""
+    import torch
+    import torch.distributed as dist
+    MAX, SUM = dist.ReduceOp.MAX, dist.ReduceOp.SUM
+    comm = backend.comm
+    world = dist.get_world_size(pg) if pg is not None else 1
+    rank = dist.get_rank(pg) if pg is not None else 0
+
+    backend.phase(nat.PH_SETUP_LOCAL)
+    cand = comm[nat.CM_SETUP: nat.CM_SETUP + 3].clone()
+    if pg is not None:
+        parts = [torch.empty_like(cand) for _ in range(world)]
+        dist.all_gather(parts, cand, group=pg)
+        allc = torch.stack(parts).cpu().numpy()
+    else:
+        allc = cand.cpu().numpy()[None, :]
+    best = 0
+    for r in range(1, world):         # max value, lowest global index on ties (problems.py:79)
+        if allc[r, 0] > allc[best, 0] or (allc[r, 0] == allc[best, 0] and allc[r, 1] < allc[best, 1]):
+            best = r
+    lmax, gidx, sign = float(allc[best, 0]), int(allc[best, 1]), float(allc[best, 2])
+    trivial = lam > lmax
+    w_star = float(group_weights[gidx]) if group_weights is not None else 0.0
+    local_unit = gidx - backend.unit_offset if rank == best else -1
+    comm[nat.CM_SETUP: nat.CM_SETUP + 7] = torch.tensor(
+        [lmax, gidx, sign, 1.0 if trivial else 0.0, 1.0 if rank == best else 0.0, w_star, local_unit],
+        dtype=comm.dtype).to(comm.device)
+    backend.phase(nat.PH_SETUP_ADOPT)
+    if not trivial and cfg.strategy != "none" and cfg.test in NEEDS_VEC:
+        if rank == best:
+            backend.phase(nat.PH_SETUP_VEC)
+        if pg is not None:
+            dist.broadcast(backend.vec, src=best, group=pg)
+    backend.phase(nat.PH_SETUP_FINISH)
+    if cfg.strategy == "static" and not trivial:
+        backend.phase(nat.PH_STATIC_LOCAL)
+        _allreduce(comm[nat.CM_MAX: nat.CM_MAX + 8], MAX, pg)
+        backend.phase(nat.PH_STATIC_FINISH)
+    max_sec = comm[nat.CM_MAX: nat.CM_MAX + 8]
+    sum_sec = comm[nat.CM_SUM:]
+    trips = 0
+    while True:
+        sc = backend.scalars()
+        if sc.stop != nat.STOP_RUNNING or sc.t >= cfg.max_iters:
+            break
+        for _ in range(chunk):
+            backend.phase(nat.PH_K1)
+            _allreduce(max_sec, MAX, pg)
+            backend.phase(nat.PH_K1R)
+            backend.phase(nat.PH_K2)
+            backend.phase(nat.PH_K3A)
+            backend.phase(nat.PH_K3S)
+            _allreduce(sum_sec, SUM, pg)
+            backend.phase(nat.PH_K3B)
+            trips += 1
+    return backend.scalars()
+
+
+class GpuShard:
+    """GPU phase backend: a solver handle on this rank's column block."""
+
+    def __init__(self, problem_local, cfg, col_offset, n_cols_total, group_offset=0, n_groups_total=0,
+                 device=None):
+        import torch
+        from .solver import Engine
+        self.eng = Engine(problem_local, cfg, device=device, desc_patch=dict(
+            col_offset=col_offset, n_cols_total=n_cols_total, group_offset=group_offset,
+            n_groups_total=n_groups_total))
+        self.torch = torch
+        b = self.eng.bufs
+        self.comm = self.eng.view(b.comm, b.comm_len, torch.float64)
+        self.vec = self.eng.view(b.vec, problem_local.dictionary.ldd, torch.float64)
+        self.unit_offset = group_offset if problem_local.kind == GROUP else col_offset
+
+    def phase(self, ph):
+        nat.check(self.eng.L.dscr_solver_phase(self.eng.h, int(ph), self.eng.sptr))
+
+    def scalars(self):
+        return self.eng.scalars()
+
+    def local_solution(self):
+        eng = self.eng
+        sc = eng.scalars()
+        units = eng.active_units(sc.parity)
+        atoms = eng.units_to_atoms(units)
+        xs = eng.vec(eng.bufs.x[sc.xi], eng.dp.k)[atoms]
+        return eng.to_original(atoms), xs, eng.trace_rows(sc.t), sc
+
+    def close(self):
+        self.eng.close()
+
+
+def run_sharded(problem, cfg, pg=None, device=None, chunk=8):
+    """Solve `problem` with its columns sharded over the ranks of `pg` (None: single rank,
+    split phases without collectives).  Every rank gets the full SolveResult."""
+    import torch.distributed as dist
+    cfg.validate(problem.kind)
+    world = dist.get_world_size(pg) if pg is not None else 1
+    rank = dist.get_rank(pg) if pg is not None else 0
+    k = problem.n_cols
+    dic = problem.dictionary
+    if problem.kind == GROUP:
+        part = problem.partition
+        order = np.concatenate(part.groups)
+        if not np.array_equal(order, np.arange(k)):
+            raise ValueError("sharded group problems need contiguous groups (permute columns first)")
+        (c0, c1), (g0, g1) = [x[rank] for x in shard_ranges(k, world, part.group_sizes())]
+        sub = Dictionary(dic.data[:, c0:c1], check_unit_norms=False, dtype=dic.dtype)
+        sub.col_norm_checked = dic.col_norm_checked
+        lp = GroupPartition.build(sub, [g - c0 for g in part.groups[g0:g1]], weights=part.weights[g0:g1],
+                                  spectral_norms=part.spectral_norms[g0:g1])
+        local = Problem(sub, problem.y, problem.lam, lp)
+        shard = GpuShard(local, cfg, c0, k, g0, part.n_groups, device)
+        gw = np.asarray(part.weights)
+    else:
+        c0, c1 = shard_ranges(k, world)[rank]
+        sub = Dictionary(dic.data[:, c0:c1], check_unit_norms=False, dtype=dic.dtype)
+        sub.col_norm_checked = dic.col_norm_checked
+        local = Problem(sub, problem.y, problem.lam)
+        shard = GpuShard(local, cfg, c0, k, 0, 0, device)
+        gw = None
+    try:
+        sc = orchestrate(shard, cfg, problem.lam, pg, gw, chunk)
+        if sc.status != 0:
+            from .solver import _raise_status
+            _raise_status(None, sc)
+        kept_l, x_l, rows, sc = shard.local_solution()
+    finally:
+        shard.close()
+    if pg is not None:
+        got = [None] * world
+        dist.all_gather_object(got, (kept_l + c0, x_l), group=pg)
+    else:
+        got = [(kept_l + c0, x_l)]
+    kept = np.concatenate([g[0] for g in got]).astype(np.int64)
+    xs = np.concatenate([g[1] for g in got])
+    order = np.argsort(kept, kind="stable")
+    kept, xs = kept[order], xs[order]
+    x_star = np.zeros(k)
+    x_star[kept] = xs
+    mask = np.ones(k, dtype=bool)
+    mask[kept] = False
+    trace = SolveTrace(kind=problem.kind, strategy=cfg.strategy, n_rows=problem.n_rows, n_cols=k,
+                       group_count=problem.partition.n_groups if problem.kind == GROUP else 0, lam=problem.lam)
+    cum = 0
+    for r in rows:
+        cum += flops_iteration(problem.kind, cfg.strategy, k, problem.n_rows, int(r[nat.TR_KEPT]),
+                               int(r[nat.TR_NNZ]), trace.group_count)
+        trace.append(int(r[nat.TR_T]), int(r[nat.TR_KEPT]), int(r[nat.TR_NNZ]), float(r[nat.TR_OBJ]), cum,
+                     float(r[nat.TR_NS]) * 1e-9)
+        trace.gap.append(float(r[nat.TR_GAP]))
+    if sc.trivial:
+        return SolveResult(np.zeros(k), 0, trace, 0.5 * float(problem.y @ problem.y),
+                           ScreenState(np.arange(k, dtype=np.int64), np.empty(0, np.int64), cfg.test),
+                           lambda_max=float(sc.lmax), stop_reason="trivial")
+    final = trace.objective[-1] if trace.objective else 0.5 * float(problem.y @ problem.y)
+    return SolveResult(x_star, int(sc.t), trace, final,
+                       ScreenState(np.flatnonzero(mask).astype(np.int64), kept, cfg.test),
+                       lambda_max=float(sc.lmax), gap=float(sc.gap))

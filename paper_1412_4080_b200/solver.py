@@ -206,7 +206,7 @@ def _config(cfg, op_norm):
 class Engine:
     """One solver handle on the device: workspace, graphs, readback helpers."""
 
-    def __init__(self, problem, cfg, device=None, stream=None):
+    def __init__(self, problem, cfg, device=None, stream=None, desc_patch=None):
         import torch
         self.torch = torch
         self.problem, self.cfg = problem, cfg
@@ -237,6 +237,8 @@ class Engine:
                 if tau * tau * op_norm ** 2 >= 1.0:
                     raise ValueError("primal-dual step sizes violate tau*sigma*||D||^2 < 1")
             self.desc = _desc(problem, dp)
+            for key, val in (desc_patch or {}).items():
+                setattr(self.desc, key, val)
             self.ccfg = _config(cfg, op_norm)
             nbytes = int(self.L.dscr_solver_workspace_size(C.byref(self.desc), C.byref(self.ccfg)))
             if nbytes == 0:

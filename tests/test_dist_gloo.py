@@ -1,0 +1,118 @@
+"""Column-sharded orchestration (paper_1412_4080_b200.dist) on CPU with gloo, world_size 2.
+
+Each rank runs the numpy phase backend on its column block; the collective
+sequence, the cross-rank lambda_* argmax, the owner broadcast and the
+stop / backtracking-redo / fixup control are the production code paths.  The
+sharded result must match the unsharded CPU oracle (iterations, screened set,
+x, objective).
+"""
+
+import os
+import pickle
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_1412_4080_b200 import dist as pdist
+from paper_1412_4080_b200 import workloads as wl
+from oracle import screen_oracle as so
+
+CASES = [
+    # (algorithm, test, ratio, L0 mode, gap_tol)
+    ("fista", "dst3", 0.5, "spec", 1e-9),
+    ("fista", "safe", 0.9, "spec", 1e-9),
+    ("ista", "dst3", 0.7, "spec", 1e-8),
+    ("ista", "dst3", 0.6, "one", 1e-8),      # backtracking REDO trips from L0 = 1
+    ("fista", "dst3", 0.8, "one", 1e-9),
+    ("sparsa", "dst3", 0.7, "spec", 1e-9),
+    ("cp", "safe", 0.7, "spec", 1e-9),
+    ("fista", "dst3", 1.5, "spec", 1e-9),    # trivial regime: lam > lambda_*
+]
+
+
+def _data(ratio):
+    D = wl.correlated_dictionary(60, 301, 3)
+    y, _ = wl.planted_observation(D, 3, nnz=6)
+    return D, y, ratio * wl.lambda_star(D, y)
+
+
+def _cfg(algo, test, L0mode, gap_tol, D):
+    L = float(np.linalg.norm(D, 2) ** 2 * (1 + 1e-9)) if L0mode == "spec" else 1.0
+    return so.Config(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300, L0=L,
+                     gap_tol=gap_tol, op_norm=float(np.linalg.norm(D, 2)))
+
+
+def _worker(rank, world, port, out_path, case):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.sharded_numpy_backend import NumpyShard
+        algo, test, ratio, L0mode, gap_tol = case
+        D, y, lam = _data(ratio)
+        cfg = _cfg(algo, test, L0mode, gap_tol, D)
+        c0, c1 = pdist.shard_ranges(D.shape[1], world)[rank]
+        shard = NumpyShard(D[:, c0:c1], y, lam, cfg, c0, op_norm=cfg.op_norm)
+        sc = pdist.orchestrate(shard, cfg, lam, pg=dist.group.WORLD, chunk=3)
+        if sc.trivial:
+            local = (np.empty(0, np.int64), np.empty(0))
+        else:
+            local = (shard.active + c0, shard.x[shard.active])
+        got = [None] * world
+        dist.all_gather_object(got, (local, shard.trace, int(sc.t), bool(sc.trivial)))
+        if rank == 0:
+            with open(out_path, "wb") as fh:
+                pickle.dump(got, fh)
+    finally:
+        dist.destroy_process_group()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-{c[2]}-{c[3]}" for c in CASES])
+def test_sharded_world2_matches_oracle(case):
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "res.pkl")
+        mp.spawn(_worker, args=(2, _free_port(), out, case), nprocs=2, join=True)
+        with open(out, "rb") as fh:
+            got = pickle.load(fh)
+    algo, test, ratio, L0mode, gap_tol = case
+    D, y, lam = _data(ratio)
+    ref = so.solve(so.make_problem(D, y, lam), _cfg(algo, test, L0mode, gap_tol, D))
+    traces = [g[1] for g in got]
+    assert traces[0] == traces[1], "ranks disagree on the trace"
+    its = got[0][2]
+    assert its == ref.iterations
+    if got[0][3]:
+        assert ref.iterations == 0
+        return
+    kept = np.concatenate([g[0][0] for g in got])
+    xs = np.concatenate([g[0][1] for g in got])
+    x = np.zeros(D.shape[1])
+    x[kept] = xs
+    elim = np.setdiff1d(np.arange(D.shape[1]), kept)
+    assert np.array_equal(elim, ref.eliminated)
+    assert np.linalg.norm(x - ref.x_star) <= 1e-9 * max(1.0, np.linalg.norm(ref.x_star))
+    np.testing.assert_allclose([t[3] for t in traces[0]], ref.trace["objective"], rtol=1e-10)
+    assert [t[1] for t in traces[0]] == ref.trace["kept"]
+
+
+def test_shard_ranges_cover_and_keep_groups_whole():
+    assert pdist.shard_ranges(10, 3) == [(0, 3), (3, 7), (7, 10)]
+    sizes = np.array([3, 3, 4, 2, 5, 3])
+    cols, grps = pdist.shard_ranges(int(sizes.sum()), 3, sizes)
+    assert cols[0][0] == 0 and cols[-1][1] == sizes.sum()
+    ptr = np.concatenate(([0], np.cumsum(sizes)))
+    for (c0, c1), (g0, g1) in zip(cols, grps):
+        assert c0 == ptr[g0] and c1 == ptr[g1]
+    for a, b in zip(cols, cols[1:]):
+        assert a[1] == b[0]

@@ -1,0 +1,77 @@
+"""Split-phase (multi-rank) engine on one GPU: no collectives, and a 1-rank NCCL group.
+
+The sharded path must reproduce the fused single-GPU engine (same iterations,
+screened sets, objective to 1e-12)."""
+
+import os
+import socket
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1412_4080_b200 as ds  # noqa: E402
+from paper_1412_4080_b200 import dist as pdist  # noqa: E402
+from paper_1412_4080_b200 import workloads as wl  # noqa: E402
+
+CASES = [("fista", "dst3", 0.5), ("fista", "safe", 0.9), ("ista", "dst3", 0.7), ("sparsa", "dst3", 0.7),
+         ("cp", "safe", 0.8), ("fista", "static-dst3", 0.8)]
+
+
+def _problem(ratio):
+    D = wl.correlated_dictionary(200, 2000, 5)
+    y, _ = wl.planted_observation(D, 5, nnz=10)
+    return ds.Problem(ds.Dictionary(D), y, ratio * wl.lambda_star(D, y)), float(np.linalg.norm(D, 2))
+
+
+@pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c)) for c in CASES])
+def test_split_phases_match_fused(case):
+    algo, test, ratio = case
+    strategy = "static" if test.startswith("static") else "dynamic"
+    test = test.split("-")[-1]
+    p, nrm = _problem(ratio)
+    cfg = ds.SolverConfig(algorithm=algo, strategy=strategy, test=test, max_iters=3000, rel_tol=1e-300,
+                          L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9, op_norm=nrm)
+    a = ds.run(p, cfg)
+    b = pdist.run_sharded(p, cfg, pg=None)
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
+    np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+    assert np.linalg.norm(a.x_star - b.x_star) <= 1e-10 * np.linalg.norm(a.x_star)
+
+
+def test_group_split_phases_match_fused():
+    w = wl.config3(seed=2, ratio=0.7, n=200, k=1000, group_size=10, n_active=3)
+    dic = ds.Dictionary(w.D)
+    part = ds.GroupPartition.build(dic, w.groups)
+    p = ds.Problem(dic, w.y, w.lam, part)
+    for test in ("gst3", "gsafe"):
+        cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test=test, max_iters=2000,
+                              rel_tol=1e-300, L0=float(np.linalg.norm(w.D, 2) ** 2 * (1 + 1e-9)), gap_tol=1e-9)
+        a = ds.run(p, cfg)
+        b = pdist.run_sharded(p, cfg, pg=None)
+        assert a.iterations == b.iterations
+        assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
+        np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+
+
+def test_nccl_single_rank_group():
+    import torch.distributed as dist
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    try:
+        p, nrm = _problem(0.6)
+        cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=3000,
+                              rel_tol=1e-300, L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9)
+        a = ds.run(p, cfg)
+        b = pdist.run_sharded(p, cfg, pg=dist.group.WORLD)
+        assert a.iterations == b.iterations
+        np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+    finally:
+        dist.destroy_process_group()
