@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
     ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c4")
     ap.add_argument("--splits", type=int, default=1, help="bf16 terms of theta in the c5 GEMM")
+    ap.add_argument("--sharded", action="store_true", help="column-sharded phase path even at one rank")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="direct-launch iterations for ncu")
@@ -280,9 +281,76 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_c4_sharded(args, world, rank, local):
+    """c4 with its 262144 columns sharded over the ranks (strong scaling, one exchange per phase
+    boundary: MAX after K1, SUM of the length-N partial residuals after K3a, over NCCL)."""
+    import torch
+    import torch.distributed as dist
+    import paper_1412_4080_b200 as ds
+    from paper_1412_4080_b200 import dist as pdist
+    from paper_1412_4080_b200 import workloads as wl
+    dev = torch.device("cuda", local)
+    n, k, blk = 8192, 262144, 4096
+    c0, c1 = pdist.shard_ranges(k // blk, world)[rank]      # whole generator blocks per rank
+    c0, c1 = c0 * blk, c1 * blk
+    host = torch.empty((c1 - c0, n), dtype=torch.float32, pin_memory=True)
+    Dl = host.numpy().T
+    from concurrent.futures import ThreadPoolExecutor
+    jobs = [(n, blk, args.seed, b) for b in range(c0 // blk, c1 // blk)]
+    with ThreadPoolExecutor(max_workers=min(32, os.cpu_count() or 8)) as pool:
+        for job, arr in zip(jobs, pool.map(wl._fp32_gaussian_block, jobs)):
+            o = job[3] * blk - c0
+            Dl[:, o:o + blk] = arr
+    y = wl.gaussian_observation(n, args.seed)
+    dic = ds.Dictionary(Dl, check_unit_norms=False, dtype="f32")
+    dic._host_tensor = host
+    corr = dic.correlate(y)
+    m = torch.tensor([float(np.max(np.abs(corr)))], device=dev)
+    dist.all_reduce(m, op=dist.ReduceOp.MAX)
+    lam = 0.2 * float(m.item())
+    nrm = pdist.sharded_operator_norm(dic, dist.group.WORLD, device=dev)
+    cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=10000, rel_tol=1e-300,
+                          L0=nrm * nrm * (1.0 + 1e-6), gap_tol=1e-5)
+    prob = ds.Problem(dic, y, lam)
+    shard = pdist.GpuShard(prob, cfg, c0, k, device=dev)
+    for _ in range(args.warmup):
+        pdist.orchestrate(shard, cfg, lam, dist.group.WORLD)
+    torch.cuda.synchronize()
+    dist.barrier()
+    with ClockSampler(local) as clocks:
+        t0 = time.perf_counter()
+        its = 0
+        for _ in range(args.steps):
+            sc = pdist.orchestrate(shard, cfg, lam, dist.group.WORLD)
+            its += sc.t
+        torch.cuda.synchronize()
+        el = time.perf_counter() - t0
+    t = torch.tensor([el], device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    el = float(t.item())
+    shard.close()
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": its / el, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox, see DESIGN.md)",
+            "config": {"workload": "c4", "n": n, "k": k, "iterations_per_step": its / args.steps,
+                       "time_to_gap_s": el / args.steps, "parallelism": f"colshard{world}",
+                       "columns_per_rank": c1 - c0, "collectives_per_iteration": 2},
+            "roofline": None, "gpu_launches": None, "clocks": clocks.summary(), "e2e": None, "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def run_ours(args):
     import torch
     world, rank, local = dist_env()
+    if (world > 1 or args.sharded) and args.workload == "c4":
+        torch.cuda.set_device(local)
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return run_c4_sharded(args, world, rank, local)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:

@@ -1348,7 +1348,7 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     g.cap = (n_units + g.G - 1) / g.G;
     g.max_gsize = max_gsize;
     g.sup_cap = g.cap * max_gsize;
-    const int V = 16 / dtype_size(pr->dtype);
+    const int V = 32 / dtype_size(pr->dtype);   // Vec<T>::V (32-byte loads)
     g.TR = NT * V;
     g.R = (pr->n_rows + g.TR - 1) / g.TR;
     g.P = std::max(1, (sms * 4) / g.R);

@@ -253,7 +253,7 @@ static int apply_any(int dt, const void* D, int ldd, int n, int k, const double*
 }
 
 static size_t apply_part_bytes(int dt, int ldd, int k) {
-    const int V = 16 / (dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2));
+    const int V = 32 / (dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2));   // Vec<T>::V (32-byte loads)
     return (size_t)apply_splits(k, ldd, V) * 2 * ldd * sizeof(double);
 }
 

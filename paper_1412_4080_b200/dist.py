@@ -142,6 +142,39 @@ class GpuShard:
         self.eng.close()
 
 
+def sharded_operator_norm(dictionary_local, pg=None, tol=1e-11, max_iters=20000, device=None):
+    """||D||_2 of a column-sharded dictionary: power iteration on D D^T = sum_r D_r D_r^T,
+    with the length-N product summed across ranks (SUM all-reduce per step)."""
+    import torch
+    import torch.distributed as dist
+    L = nat.lib()
+    dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+    dic = dictionary_local
+    Dd = dic.device_data(dev)
+    n, k, ldd = dic.n_rows, dic.n_cols, dic.ldd
+    q = torch.zeros(ldd, dtype=torch.float64, device=dev)
+    q[:n] = 1.0 / np.sqrt(n)
+    w = torch.empty(k, dtype=torch.float64, device=dev)
+    z = torch.empty(ldd, dtype=torch.float64, device=dev)
+    nb = int(L.dscr_apply_work_size(dic.dtype_code, ldd, k))
+    work = torch.empty(nb, dtype=torch.uint8, device=dev)
+    s = nat.stream_ptr()
+    val = None
+    for _ in range(max_iters):
+        nat.check(L.dscr_correlate(dic.dtype_code, Dd.data_ptr(), ldd, n, k, q.data_ptr(), w.data_ptr(), s))
+        nat.check(L.dscr_apply(dic.dtype_code, Dd.data_ptr(), ldd, n, k, w.data_ptr(), z.data_ptr(),
+                               work.data_ptr(), nb, s))
+        if pg is not None:
+            dist.all_reduce(z, op=dist.ReduceOp.SUM, group=pg)
+        new = float(torch.dot(q, z).item())
+        nz = float(torch.linalg.vector_norm(z).item())
+        if val is not None and abs(new - val) <= tol * max(1.0, abs(new)):
+            return float(np.sqrt(max(new, 0.0)))
+        val = new
+        q = z / nz
+    return float(np.sqrt(max(val, 0.0)))
+
+
 def run_sharded(problem, cfg, pg=None, device=None, chunk=8):
     """Solve `problem` with its columns sharded over the ranks of `pg` (None: single rank,
     split phases without collectives).  Every rank gets the full SolveResult."""
