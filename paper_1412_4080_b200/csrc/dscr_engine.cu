@@ -121,6 +121,8 @@ struct Params {
     int G, cap, TR, R, P, G3b;
     int col_offset, group_offset;
     int in_graph;
+    int writer;        // this CTA owns the trace / timestamp writes
+    int persistent;    // engine mode chosen at create
     int split;         // multi-rank: phases exchange through `comm` (see dscr_solver_phase)
     double* comm;
     float l2_keep;
@@ -133,6 +135,7 @@ struct Params {
 
 // device timestamps: slot 2k = kernel k entry (CTA 0), 2k+1 = kernel k exit (last CTA)
 __device__ __forceinline__ void stamp(const Params& P, int slot) {
+    if (!P.writer) return;
     const int trip = P.sc->trips;
     if (P.kts && trip < P.max_kts) P.kts[(size_t)trip * 8 + slot] = globaltimer();
 }
@@ -196,21 +199,15 @@ __device__ void radius_epilogue(const Params& P, double bound, const double* the
 // K1: correlation + algorithm update over the active units
 // ---------------------------------------------------------------------------
 
+// K1 per-CTA work: correlations, update, per-CTA partials into P.p1[b]
 template <typename T, bool GROUP>
-__global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
-    extern __shared__ double s_theta[];
+__device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s_theta) {
     __shared__ double s_red[NW][NP1];
-    __shared__ double s_sh[64];
-    __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
-    if (sc->stop || sc->t >= sc->run_limit) return;
     const int mode = sc->mode;
-    if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 0);
     const int p = sc->parity, xi = sc->xi;
     const int nu = sc->n_units;
-    const int b = blockIdx.x;
-    const int lo = (int)(((long long)nu * b) / P.G), hi = (int)(((long long)nu * (b + 1)) / P.G);
+    const int lo = (int)(((long long)nu * b) / G), hi = (int)(((long long)nu * (b + 1)) / G);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool need_dot = (mode == MODE_NORMAL);
     if (need_dot && hi > lo) {
@@ -356,11 +353,21 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
         double* o = P.p1 + (size_t)b * NP1;
         o[0] = m; o[1] = cs; o[2] = ss; o[3] = nf; o[4] = any;
     }
-    if (!last_block(P.tickets + 0, gridDim.x, &s_flag)) return;
+}
+
+// K1 tail: fixed-order reduction of the G partials, FISTA/CP scalars, radius.  Run by the
+// last CTA (graph path) or redundantly by every CTA (persistent path).
+template <bool GROUP>
+__device__ void k1_final(const Params& P, int G) {
+    __shared__ double s_sh[64];
+    dscr_scalars* sc = P.sc;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int p = sc->parity;
+    const int algo = P.algo;
 
     // ---- last CTA: fixed-order reduction of the per-CTA partials
     double m = GROUP ? INFINITY : 0.0, cs = 0.0, ss = 0.0, nf = 0.0, any = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+    for (int i = threadIdx.x; i < G; i += NT) {
         const double* o = P.p1 + (size_t)i * NP1;
         m = GROUP ? fmin(m, o[0]) : fmax(m, o[0]);
         cs += o[1]; ss += o[2]; nf = fmax(nf, o[3]); any = fmax(any, o[4]);
@@ -417,6 +424,21 @@ __global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
     }
     radius_epilogue(P, bound, P.theta[p], sc->theta_sq, sc->theta_y, s_sh);
     if (threadIdx.x == 0) stamp(P, 1);
+}
+
+
+template <typename T, bool GROUP>
+__global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
+    extern __shared__ double s_theta[];
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    const int mode = sc->mode;
+    if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 0);
+    k1_body<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
+    if (!last_block(P.tickets + 0, gridDim.x, &s_flag)) return;
+    k1_final<GROUP>(P, gridDim.x);
 }
 
 // split mode: radius from the MAX-reduced correlation bound (after the collective)
@@ -489,22 +511,16 @@ __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* s
     return false;
 }
 
+// K2 per-CTA work: test, compaction into slot b, vectors, support list, partials
 template <bool GROUP>
-__global__ void __launch_bounds__(NT) k2_screen(Params P) {
+__device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     __shared__ int s_scan[2 * NW + 1];
     __shared__ double s_sh[64];
-    __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
-    if (sc->stop) return;
-    const int mode = sc->mode;
-    if (mode == MODE_FIXUP) return;
-    const bool static_mode = (mode == MODE_STATIC);
-    if (!static_mode && sc->t >= sc->run_limit) return;
-    if (!static_mode && blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 2);
+    const bool static_mode = (sc->mode == MODE_STATIC);
     const int p = sc->parity, xi = sc->xi;
     const int nu = sc->n_units;
-    const int b = blockIdx.x;
-    const int lo = (int)(((long long)nu * b) / P.G), hi = (int)(((long long)nu * (b + 1)) / P.G);
+    const int lo = (int)(((long long)nu * b) / G), hi = (int)(((long long)nu * (b + 1)) / G);
     const int* act = P.act[p];
     const int* off = P.act_off[p];
     int* actn = P.act[p ^ 1] + (size_t)b * P.cap;
@@ -593,7 +609,16 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
             o[0] = v5[0]; o[1] = v5[1]; o[2] = v5[2]; o[3] = v5[3]; o[4] = v5[4];
         }
     }
-    if (!last_block(P.tickets + 1, gridDim.x, &s_flag)) return;
+}
+
+// K2 tail: slot scans (new active list offsets, support offsets), partial reduction
+template <bool GROUP>
+__device__ void k2_final(const Params& P, int G) {
+    __shared__ int s_scan[2 * NW + 1];
+    __shared__ double s_sh[64];
+    dscr_scalars* sc = P.sc;
+    const bool static_mode = (sc->mode == MODE_STATIC);
+    const int p = sc->parity;
 
     // ---- last CTA: scans of the slot counts, fixed-order partial reduction
     {
@@ -636,7 +661,7 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
         return;
     }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+    for (int i = threadIdx.x; i < G; i += NT) {
         const double* o = P.p2 + (size_t)i * NP2;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3]; a4 += o[4];
     }
@@ -653,6 +678,21 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
     }
 }
 
+template <bool GROUP>
+__global__ void __launch_bounds__(NT) k2_screen(Params P) {
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop) return;
+    const int mode = sc->mode;
+    if (mode == MODE_FIXUP) return;
+    const bool static_mode = (mode == MODE_STATIC);
+    if (!static_mode && sc->t >= sc->run_limit) return;
+    if (!static_mode && blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 2);
+    k2_body<GROUP>(P, blockIdx.x, gridDim.x);
+    if (!last_block(P.tickets + 1, gridDim.x, &s_flag)) return;
+    k2_final<GROUP>(P, gridDim.x);
+}
+
 // ---------------------------------------------------------------------------
 // K3a: residual partials over the support list
 // ---------------------------------------------------------------------------
@@ -660,22 +700,17 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
 constexpr int K3_CHUNK = 128;
 
 template <typename T>
-__global__ void __launch_bounds__(NT) k3a_residual(Params P) {
+__device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     __shared__ int s_idx[K3_CHUNK];
     __shared__ double s_a[K3_CHUNK], s_b[K3_CHUNK];
     dscr_scalars* sc = P.sc;
-    if (sc->stop || sc->t >= sc->run_limit) return;
-    const int mode = sc->mode;
-    if (mode == MODE_STATIC) return;
-    const bool fix = (mode == MODE_FIXUP);
-    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stamp(P, 4);
+    const bool fix = (sc->mode == MODE_FIXUP);
     const int pe = sc->p_eff;
-    const int split = blockIdx.y;
     if (split >= pe) return;
     const int nS = sc->n_support;
     const int lo = (int)(((long long)nS * split) / pe), hi = (int)(((long long)nS * (split + 1)) / pe);
     constexpr int V = Vec<T>::V;
-    const int r0 = blockIdx.x * P.TR + threadIdx.x * V;
+    const int r0 = tile * P.TR + threadIdx.x * V;
     const bool rows_ok = r0 < P.n;
     const T* D = static_cast<const T*>(P.D);
     const uint64_t pol = make_policy(P.l2_keep);
@@ -737,6 +772,15 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
             if (r0 + v < P.ldd) { pa[v] = acc_a[v]; pb[v] = acc_b[v]; }
         }
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k3a_residual(Params P) {
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->mode == MODE_STATIC) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stamp(P, 4);
+    k3a_body<T>(P, blockIdx.x, blockIdx.y);
 }
 
 // ---------------------------------------------------------------------------
@@ -815,7 +859,7 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
     sc->gap = gap;
     sc->fc = s_qa2;
     const int nnz = sc->nnz;
-    if (t <= P.max_iters) {
+    if (t <= P.max_iters && P.writer) {
         double* row = P.trace + (size_t)(t - 1) * DSCR_TRACE_FIELDS;
         row[DSCR_TR_T] = t;
         row[DSCR_TR_KEPT] = sc->kept_atoms;
@@ -853,15 +897,11 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
 constexpr int K3B_ROWS = 32;                 // rows per CTA
 constexpr int K3B_GROUPS = NT / K3B_ROWS;    // split groups per row
 
-__global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
+__device__ __forceinline__ void k3b_body(const Params& P, int rb) {
     __shared__ double s_sh[64];
     __shared__ double s_pa[K3B_GROUPS][K3B_ROWS], s_pb[K3B_GROUPS][K3B_ROWS];
-    __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
-    if (sc->stop || sc->t >= sc->run_limit) return;
     const int mode = sc->mode;
-    if (mode == MODE_STATIC) return;
-    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 6);
     const bool fix = (mode == MODE_FIXUP);
     const int algo = P.algo;
     const int p = sc->parity;
@@ -869,7 +909,7 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     // split reduction: group g sums splits g, g+8, ... ; groups combined in order (deterministic)
     {
         const int rr = threadIdx.x % K3B_ROWS, g = threadIdx.x / K3B_ROWS;
-        const int r = blockIdx.x * K3B_ROWS + rr;
+        const int r = rb * K3B_ROWS + rr;
         double a = 0.0, b = 0.0;
         if (r < P.n) {
             if (P.split) {
@@ -887,7 +927,7 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     __syncthreads();
     double qa2 = 0.0, tn2 = 0.0, tny = 0.0, ds2 = 0.0;
     if (threadIdx.x < K3B_ROWS) {
-        const int r = blockIdx.x * K3B_ROWS + threadIdx.x;
+        const int r = rb * K3B_ROWS + threadIdx.x;
         if (r < P.n) {
             double Sa = 0.0, Sb = 0.0;
 #pragma unroll
@@ -922,12 +962,16 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     block_sum_n<4>(q4, s_sh);
     qa2 = q4[0]; tn2 = q4[1]; tny = q4[2]; ds2 = q4[3];
     if (threadIdx.x == 0) {
-        double* o = P.p3s + (size_t)blockIdx.x * NP3;
+        double* o = P.p3s + (size_t)rb * NP3;
         o[0] = qa2; o[1] = tn2; o[2] = tny; o[3] = ds2;
     }
-    if (!last_block(P.tickets + 2, gridDim.x, &s_flag)) return;
+}
+
+__device__ void k3b_final(const Params& P, int G3) {
+    __shared__ double s_sh[64];
+    dscr_scalars* sc = P.sc;
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += NT) {
+    for (int i = threadIdx.x; i < G3; i += NT) {
         const double* o = P.p3s + (size_t)i * NP3;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3];
     }
@@ -943,6 +987,98 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
         }
         iteration_epilogue(P, a0, a1, a2, a3);
     }
+}
+
+
+__global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->mode == MODE_STATIC) return;
+    if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 6);
+    k3b_body(P, blockIdx.x);
+    if (!last_block(P.tickets + 2, gridDim.x, &s_flag)) return;
+    k3b_final(P, gridDim.x);
+}
+
+// ---------------------------------------------------------------------------
+// persistent engine: the whole iteration loop in one cooperative launch
+// ---------------------------------------------------------------------------
+//
+// Every CTA runs the K1/K2/K3a/K3b bodies on its share of the work, separated by
+// grid barriers; the tails (partial reductions, radius, slot scans, iteration
+// epilogue) run redundantly in every CTA on a shared-memory copy of the scalar
+// state.  The tails are deterministic, so all copies stay identical and no CTA
+// waits on another's tail.  Four grid barriers per iteration, no launches.
+
+// sense-counting grid barrier; the gpu-scope fences also invalidate this SM's
+// L1, so data written by other CTAs before the barrier is re-read from L2.
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen, unsigned n) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        volatile unsigned* vgen = gen;
+        const unsigned g = *vgen;
+        __threadfence();
+        if (atomicAdd(count, 1u) == n - 1) {
+            atomicExch(count, 0u);
+            __threadfence();
+            atomicAdd(gen, 1u);
+        } else {
+            while (*vgen == g) __nanosleep(20);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+}
+
+template <typename T, bool GROUP>
+__global__ void __launch_bounds__(NT, 2) k_persistent(Params P0) {
+    extern __shared__ double s_theta[];
+    __shared__ dscr_scalars s_sc;
+    Params P = P0;
+    P.sc = &s_sc;
+    P.in_graph = 0;
+    P.writer = (blockIdx.x == 0);
+    const int G = gridDim.x;
+    unsigned* bc = P0.tickets + 4;
+    unsigned* bg = P0.tickets + 5;
+    if (threadIdx.x == 0) {
+        s_sc = *P0.sc;
+        if (s_sc.stop == DSCR_RUNNING && s_sc.n_units == 0) s_sc.stop = DSCR_STOP_EMPTY;   // solvers.py:435
+    }
+    __syncthreads();
+    for (;;) {
+        if (s_sc.stop != DSCR_RUNNING || s_sc.t >= s_sc.run_limit || s_sc.t >= P.max_iters) break;
+        const int mode = s_sc.mode;
+        if (mode == MODE_NORMAL || mode == MODE_REDO) {
+            if (threadIdx.x == 0) stamp(P, 0);
+            k1_body<T, GROUP>(P, blockIdx.x, G, s_theta);
+            grid_sync(bc, bg, G);
+            k1_final<GROUP>(P, G);
+            __syncthreads();
+            if (threadIdx.x == 0) stamp(P, 2);
+            k2_body<GROUP>(P, blockIdx.x, G);
+            grid_sync(bc, bg, G);
+            k2_final<GROUP>(P, G);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) stamp(P, 4);
+        const int nv = P.R * s_sc.p_eff;
+        for (int v = blockIdx.x; v < nv; v += G) {
+            k3a_body<T>(P, v % P.R, v / P.R);
+            __syncthreads();
+        }
+        grid_sync(bc, bg, G);
+        if (threadIdx.x == 0) stamp(P, 6);
+        for (int v = blockIdx.x; v < P.G3b; v += G) {
+            k3b_body(P, v);
+            __syncthreads();
+        }
+        grid_sync(bc, bg, G);
+        k3b_final(P, P.G3b);
+        __syncthreads();
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *P0.sc = s_sc;
 }
 
 // ---------------------------------------------------------------------------
@@ -1007,7 +1143,7 @@ __global__ void k_init(Params P) {
         if (P.algo == DSCR_CP) { sc->tau = sig; sc->sigma = sig; }
         sc->radius = NAN;
         sc->t0_ns = (double)globaltimer();
-        for (int i = 0; i < 4; ++i) P.tickets[i] = 0u;
+        for (int i = 0; i < 8; ++i) P.tickets[i] = 0u;
     }
 }
 
@@ -1329,6 +1465,25 @@ static int k1_occ_t(bool group, int smem) {
     return std::max(1, n);
 }
 
+template <typename T>
+static int pers_occ_t(bool group, int smem) {
+    int n = 0;
+    if (group) {
+        cudaFuncSetAttribute(k_persistent<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent<T, true>, NT, smem);
+    } else {
+        cudaFuncSetAttribute(k_persistent<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent<T, false>, NT, smem);
+    }
+    return n;
+}
+
+static int pers_occupancy(int dtype, bool group, int smem) {
+    if (dtype == DSCR_F64) return pers_occ_t<double>(group, smem);
+    if (dtype == DSCR_F32) return pers_occ_t<float>(group, smem);
+    return pers_occ_t<__nv_bfloat16>(group, smem);
+}
+
 static int k1_occupancy(int dtype, bool group, int smem) {
     if (dtype == DSCR_F64) return k1_occ_t<double>(group, smem);
     if (dtype == DSCR_F32) return k1_occ_t<float>(group, smem);
@@ -1343,7 +1498,9 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g.smem1 = pr->ldd * (int)sizeof(double);
     // resident K1 CTAs per SM (registers + theta staging buffer): one full wave
-    const int per_sm = k1_occupancy(pr->dtype, pr->n_groups > 0, g.smem1);
+    // one full wave; also co-resident for the persistent kernel (grid barriers)
+    const int per_sm = std::max(1, std::min(k1_occupancy(pr->dtype, pr->n_groups > 0, g.smem1),
+                                            std::max(1, pers_occupancy(pr->dtype, pr->n_groups > 0, g.smem1))));
     g.G = std::max(1, std::min((n_units + 15) / 16, sms * per_sm));
     g.cap = (n_units + g.G - 1) / g.G;
     g.max_gsize = max_gsize;
@@ -1667,6 +1824,17 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.col_offset = pr->col_offset;
     P.group_offset = pr->group_offset;
     P.in_graph = 1;
+    P.writer = 1;
+    {
+        // engine mode: persistent cooperative kernel (default) or the conditional-graph chain
+        const char* env = getenv("DSCR_ENGINE");
+        int dev = 0, coop = 0, sms = 148;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        const int occ = pers_occupancy(pr->dtype, pr->n_groups > 0, g.smem1);
+        P.persistent = coop && occ * sms >= g.G && !(env && strcmp(env, "graph") == 0);
+    }
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
 
     cudaStream_t us = (cudaStream_t)stream;
@@ -1741,11 +1909,27 @@ int dscr_solver_setup(dscr_solver* h, void* stream) {
     return DSCR_OK;
 }
 
+static int launch_persistent(dscr_solver* h, cudaStream_t s) {
+    Params P = h->P;
+    P.persistent = 1;
+    void* args[] = {&P};
+    const bool group = P.n_groups > 0;
+    const void* fn;
+    switch (P.dtype) {
+        case DSCR_F64: fn = group ? (const void*)k_persistent<double, true> : (const void*)k_persistent<double, false>; break;
+        case DSCR_F32: fn = group ? (const void*)k_persistent<float, true> : (const void*)k_persistent<float, false>; break;
+        default: fn = group ? (const void*)k_persistent<__nv_bfloat16, true> : (const void*)k_persistent<__nv_bfloat16, false>;
+    }
+    CK(cudaLaunchCooperativeKernel(fn, dim3(h->geo.G), dim3(NT), args, (size_t)h->geo.smem1, s));
+    return DSCR_OK;
+}
+
 int dscr_solver_run(dscr_solver* h, int iteration_limit, void* stream) {
     if (!h) return set_inval("null handle");
     cudaStream_t s = (cudaStream_t)stream;
     k_set_limit<<<1, 1, 0, s>>>(h->P.sc, iteration_limit > 0 ? iteration_limit : 0x7fffffff);
     CK(cudaGetLastError());
+    if (h->P.persistent) return launch_persistent(h, s);
     CK(cudaGraphLaunch(h->e_loop, s));
     return DSCR_OK;
 }
