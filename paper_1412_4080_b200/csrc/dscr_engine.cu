@@ -54,6 +54,7 @@ constexpr int MIN_COLS_PER_SPLIT = 16;
 // [32, 32+2*ldd) SUM-reduced partial residual vectors D_S a, D_S b
 constexpr int CM_MAX = 0, CM_SETUP = 8, CM_SUM = 16, CM_VEC = 32;
 constexpr int TRIPS_PER_BODY = 4;
+constexpr int PERS_MAX_G = 2048;   // persistent engine: max CTAs (support offsets kept in smem)
 
 
 static int set_err(const char* what, cudaError_t e) {
@@ -630,7 +631,7 @@ __device__ void k2_final(const Params& P, int G) {
             const int v = (i < P.G) ? cn[i] : 0;
             int tot;
             const int e = block_exscan(v, s_scan, &tot);
-            if (i < P.G) offn[i] = carry + e;
+            if (i < P.G && P.writer) offn[i] = carry + e;
             carry += tot;
             if (!static_mode) {
                 const int vs = (i < P.G) ? P.sup_cnt[i] : 0;
@@ -640,7 +641,7 @@ __device__ void k2_final(const Params& P, int G) {
             }
         }
         if (threadIdx.x == 0) {
-            offn[P.G] = carry;
+            if (P.writer) offn[P.G] = carry;
             sc->n_units_new = carry;
             if (!static_mode) {
                 P.sup_off[P.G] = carry_s;
@@ -1035,8 +1036,10 @@ template <typename T, bool GROUP>
 __global__ void __launch_bounds__(NT, 2) k_persistent(Params P0) {
     extern __shared__ double s_theta[];
     __shared__ dscr_scalars s_sc;
+    __shared__ int s_supoff[PERS_MAX_G + 1];    // this CTA's copy of the support offsets
     Params P = P0;
     P.sc = &s_sc;
+    P.sup_off = s_supoff;
     P.in_graph = 0;
     P.writer = (blockIdx.x == 0);
     const int G = gridDim.x;
@@ -1502,6 +1505,7 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     const int per_sm = std::max(1, std::min(k1_occupancy(pr->dtype, pr->n_groups > 0, g.smem1),
                                             std::max(1, pers_occupancy(pr->dtype, pr->n_groups > 0, g.smem1))));
     g.G = std::max(1, std::min((n_units + 15) / 16, sms * per_sm));
+    if (const char* e = getenv("DSCR_MAX_CTAS")) g.G = std::max(1, std::min(g.G, atoi(e)));
     g.cap = (n_units + g.G - 1) / g.G;
     g.max_gsize = max_gsize;
     g.sup_cap = g.cap * max_gsize;
@@ -1826,14 +1830,16 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.in_graph = 1;
     P.writer = 1;
     {
-        // engine mode: persistent cooperative kernel (default) or the conditional-graph chain
+        // engine mode: the conditional-graph chain (default) or, with DSCR_ENGINE=persistent, one
+        // cooperative launch with grid barriers (measured slower on B200: ~3 us per grid barrier plus
+        // the redundant tails exceed the ~1.5 us launch gaps it removes; kept as an alternative)
         const char* env = getenv("DSCR_ENGINE");
         int dev = 0, coop = 0, sms = 148;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int occ = pers_occupancy(pr->dtype, pr->n_groups > 0, g.smem1);
-        P.persistent = coop && occ * sms >= g.G && !(env && strcmp(env, "graph") == 0);
+        P.persistent = coop && occ * sms >= g.G && g.G <= PERS_MAX_G && env && strcmp(env, "persistent") == 0;
     }
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
 

@@ -75,3 +75,31 @@ def test_nccl_single_rank_group():
         np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
     finally:
         dist.destroy_process_group()
+
+
+def test_persistent_engine_matches_graph_engine():
+    """The cooperative persistent engine (DSCR_ENGINE=persistent) reproduces the graph engine."""
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, paper_1412_4080_b200 as ds\n"
+        "from paper_1412_4080_b200 import workloads as wl\n"
+        "D = wl.correlated_dictionary(200, 2000, 5); y, _ = wl.planted_observation(D, 5, nnz=10)\n"
+        "p = ds.Problem(ds.Dictionary(D), y, 0.6 * wl.lambda_star(D, y))\n"
+        "nrm = float(np.linalg.norm(D, 2))\n"
+        "out = []\n"
+        "for algo, test in (('fista', 'dst3'), ('ista', 'safe'), ('sparsa', 'dst3')):\n"
+        "    r = ds.run(p, ds.SolverConfig(algorithm=algo, strategy='dynamic', test=test, max_iters=3000,\n"
+        "               rel_tol=1e-300, L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9))\n"
+        "    out.append((r.iterations, r.screen_state.eliminated.tolist(), r.trace.objective))\n"
+        "import pickle, sys; sys.stdout.buffer.write(pickle.dumps(out))\n")
+    import pickle
+    res = {}
+    for mode in ("graph", "persistent"):
+        env = dict(os.environ, DSCR_ENGINE=mode)
+        proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
+                              cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        res[mode] = pickle.loads(proc.stdout)
+    for a, b in zip(res["graph"], res["persistent"]):
+        assert a[0] == b[0] and a[1] == b[1]
+        np.testing.assert_allclose(b[2], a[2], rtol=1e-13)
