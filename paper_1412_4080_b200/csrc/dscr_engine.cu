@@ -200,6 +200,12 @@ __device__ void radius_epilogue(const Params& P, double bound, const double* the
 // K1: correlation + algorithm update over the active units
 // ---------------------------------------------------------------------------
 
+// Loads in flight per lane (U) and CTAs per SM of K1.  Measured: one CTA/SM with
+// U=4 for fp32 spills (255 regs) and halves the bandwidth; 2 CTAs/SM, C=4, U=1 is best.
+template <typename T> struct K1Cfg { static constexpr int U = 2, MINB = 2; };
+template <> struct K1Cfg<float> { static constexpr int U = 1, MINB = 2; };
+template <> struct K1Cfg<__nv_bfloat16> { static constexpr int U = 1, MINB = 2; };
+
 // K1 per-CTA work: correlations, update, per-CTA partials into P.p1[b]
 template <typename T, bool GROUP>
 __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s_theta) {
@@ -256,7 +262,7 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
                 const T* cols[C];
 #pragma unroll
                 for (int c = 0; c < C; ++c) cols[c] = js[c] >= 0 ? D + (size_t)js[c] * P.ldd : nullptr;
-                warp_dots<T, C, (sizeof(T) == 8 ? 2 : 1)>(cols, P.n, s_theta, lane, pol, cs);
+                warp_dots<T, C, K1Cfg<T>::U>(cols, P.n, s_theta, lane, pol, cs);
             } else {
 #pragma unroll
                 for (int c = 0; c < C; ++c) cs[c] = js[c] >= 0 ? P.corr[js[c]] : 0.0;
@@ -429,7 +435,7 @@ __device__ void k1_final(const Params& P, int G) {
 
 
 template <typename T, bool GROUP>
-__global__ void __launch_bounds__(NT, 2) k1_corr_update(Params P) {
+__global__ void __launch_bounds__(NT, K1Cfg<T>::MINB) k1_corr_update(Params P) {
     extern __shared__ double s_theta[];
     __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
