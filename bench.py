@@ -584,9 +584,14 @@ def run_c5(args):
     res = engs2[0].result()
     for e in engs2:
         e.close()
-    # per-kernel profile (GEMM roofline)
+    # per-kernel profile (GEMM roofline) and the setup cost
     e = one()
+    es0, es1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    es0.record()
     e.setup()
+    es1.record()
+    torch.cuda.synchronize()
+    setup_ms = es0.elapsed_time(es1)
     ms = (nat.C.c_float * 3)()
     nat.check(e.L.dscr_batched_profile(e.h, 0, e.sptr, ms))
     e.close()
@@ -633,7 +638,8 @@ def run_c5(args):
             "config": {"workload": "c5", "n": n, "k": k, "batch": b, "iterations_per_step": iters,
                        "splits": args.splits, "parallelism": f"dp{world}" if world > 1 else "single-gpu",
                        "mean_objective": float(np.mean(res.objective)), "kept_min": int(res.kept.min()),
-                       "nnz_mean": float(np.mean(res.nnz)), "accumulate": "fp32 (TMEM), fp64 state"},
+                       "nnz_mean": float(np.mean(res.nnz)), "accumulate": "fp32 (TMEM), fp64 state",
+                       "setup_ms": setup_ms},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": src,
                          "kernel": "k_gemm_dt (tcgen05)", "kernel_ms": ms[0], "flop_per_launch": flop,

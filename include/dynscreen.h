@@ -269,7 +269,8 @@ typedef struct dscr_batched_desc {
     int32_t test;            /* DSCR_TEST_OFF, DSCR_SAFE or DSCR_DST3 */
     int32_t cap;             /* max nonzeros per observation */
     int32_t max_iters;
-    int32_t pad;
+    int32_t fused;           /* 1: the tcgen05 epilogue emits only the entries whose update can be nonzero
+                                (|c| > lam_j or currently nonzero); 0: dense fp32 C round trip */
     const double* beta;      /* host [max_iters]: FISTA momentum coefficients (l_t - 1)/l_{t+1} */
 } dscr_batched_desc;
 

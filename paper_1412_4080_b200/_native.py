@@ -86,7 +86,7 @@ class BatchedDesc(C.Structure):
         ("n_rows", C.c_int32), ("n_atoms", C.c_int32), ("n_obs", C.c_int32), ("ldd", C.c_int32),
         ("Dt", C.c_void_p), ("Y", C.c_void_p), ("ldy", C.c_int32), ("splits", C.c_int32),
         ("lam", C.c_void_p), ("L", C.c_double), ("test", C.c_int32), ("cap", C.c_int32),
-        ("max_iters", C.c_int32), ("pad", C.c_int32), ("beta", C.c_void_p),
+        ("max_iters", C.c_int32), ("fused", C.c_int32), ("beta", C.c_void_p),
     ]
 
 

@@ -58,7 +58,8 @@ class BatchedResult:
 class BatchedEngine:
     """Device state of one batch: workspace, handle, graph."""
 
-    def __init__(self, dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, cap=1024, device=None):
+    def __init__(self, dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, cap=1024, device=None,
+                 fused=True):
         import torch
         if dictionary.dtype != "bf16":
             raise ValueError("the batched path takes a bf16 dictionary (Dictionary(..., dtype='bf16'))")
@@ -86,6 +87,7 @@ class BatchedEngine:
         d.Dt, d.Y, d.ldy, d.splits = self.Dt.data_ptr(), self.Yd.data_ptr(), ldy, int(splits)
         d.lam, d.L, d.test, d.cap = self.lamd.data_ptr(), float(L), nat.TEST_CODES[test], self.cap
         d.max_iters = self.iterations
+        d.fused = 1 if fused else 0
         d.beta = self.betas.ctypes.data
         self.desc = d
         nbytes = int(self.L.dscr_batched_workspace_size(C.byref(d)))
@@ -153,9 +155,10 @@ class BatchedEngine:
             pass
 
 
-def solve_batched(dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, cap=1024, device=None):
+def solve_batched(dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, cap=1024, device=None,
+                  fused=True):
     """FISTA (fixed step 1/L) with per-observation dynamic screening for Y[:, j], lam[j]."""
-    eng = BatchedEngine(dictionary, Y, lam, L, iterations, test, splits, cap, device)
+    eng = BatchedEngine(dictionary, Y, lam, L, iterations, test, splits, cap, device, fused)
     torch = eng.torch
     try:
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

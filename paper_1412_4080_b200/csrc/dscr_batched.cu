@@ -30,8 +30,9 @@ using namespace umma;
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 2 * BN;
-constexpr int GEMM_THREADS = 192;   // warp 0 TMA, warp 1 MMA, warps 2..5 epilogue
-constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+constexpr int GEMM_THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
+constexpr int EPI_THREADS = GEMM_THREADS - 64;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 16 * BN + 64;
 
 struct GemmArgs {
     int Nb;          // observations per split (rows of one Theta block)
@@ -40,6 +41,16 @@ struct GemmArgs {
     int num_m, num_n, num_tiles;
     float* C;        // C^T [obs][atom]
     int ldc;
+    // fused screening epilogue (C == nullptr): emit only the entries whose update can be nonzero
+    const uint32_t* mask;   // [obs][M/32] active atoms
+    const uint32_t* nzm;    // [obs][M/32] atoms in the observation's u or x list
+    const float* thr;       // [obs] lam_j (1 - 1e-6): |c| <= thr with u = x = 0 gives a zero update
+    uint32_t* cmax;         // [obs] max |c| over active atoms (float bits, atomicMax)
+    int* hot_cnt;           // [obs]
+    int* hot_idx;           // [obs][hcap]
+    float* hot_val;         // [obs][hcap]
+    int hcap;
+    int words;              // M/32
 };
 
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
@@ -59,7 +70,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
         for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 128); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_THREADS); }
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
@@ -111,8 +122,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 mma_commit(&tfull[ab]);
             }
         }
-    } else {   // ---- epilogue: TMEM -> registers -> C^T[obs][atom]
+    } else if (g.C) {   // ---- epilogue: TMEM -> registers -> C^T[obs][atom]
         const int q = warp & 3;   // TMEM lane quarter this warp may access
+        const int half = (warp - 2) >> 2;   // which half of the tile's columns
         int lt = 0;
         for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++lt) {
             const int mb = tile % g.num_m, nb = tile / g.num_m;
@@ -123,7 +135,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int m = mb * BM + q * 32 + lane;
             float* crow = g.C + (size_t)(nb * BN) * g.ldc + m;
 #pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 32) {
+            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + c0, r);
 #pragma unroll
@@ -131,6 +143,75 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             tc_fence_before();
             mbar_arrive(&tempty[ab]);
+        }
+    } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
+        const int q = warp & 3;
+        const int half = (warp - 2) >> 2;                             // which half of the tile's columns
+        uint32_t* s_cm = reinterpret_cast<uint32_t*>(tslot + 1);     // [4 quarters][BN] tile max per observation
+        const int et = threadIdx.x - 64;                              // 0..EPI_THREADS-1
+        constexpr int KC = BN / 64;                                   // 32-column chunks per warp
+        int lt = 0;
+        for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++lt) {
+            const int mb = tile % g.num_m, nb = tile / g.num_m;
+            const int ab = lt & 1;
+            const uint32_t aphase = (lt >> 1) & 1;
+            const int m0 = mb * BM + q * 32;                  // this warp's 32 atoms
+            const int m = m0 + lane;
+            const int cbase = half * (BN / 2);
+            // per-observation words of this warp's columns, fetched before waiting on the accumulator
+            uint32_t wa[KC], wn[KC];
+            float th[KC];
+#pragma unroll
+            for (int k = 0; k < KC; ++k) {
+                const int jl = nb * BN + cbase + k * 32 + lane;
+                wa[k] = g.mask[(size_t)jl * g.words + (m0 >> 5)];
+                wn[k] = g.nzm[(size_t)jl * g.words + (m0 >> 5)];
+                th[k] = g.thr[jl];
+            }
+            mbar_wait(&tfull[ab], aphase);
+            tc_fence_after();
+#pragma unroll 1
+            for (int k = 0; k < KC; ++k) {
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + cbase + k * 32, r);
+                // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms
+                uint32_t hotbits = 0u, mymax = 0u;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const uint32_t wai = __shfl_sync(0xffffffffu, wa[k], i);
+                    const uint32_t wni = __shfl_sync(0xffffffffu, wn[k], i);
+                    const float thi = __shfl_sync(0xffffffffu, th[k], i);
+                    const float a = fabsf(__uint_as_float(r[i]));
+                    const bool act = (wai >> lane) & 1u;
+                    const uint32_t mv = __reduce_max_sync(0xffffffffu, act ? __float_as_uint(a) : 0u);
+                    mymax = (lane == i) ? mv : mymax;
+                    const bool hot = act && (a > thi || ((wni >> lane) & 1u));
+                    hotbits |= (hot ? 1u : 0u) << i;
+                }
+                s_cm[q * BN + cbase + k * 32 + lane] = mymax;
+                // pass 2 (rare): append the hot entries of this lane's atom
+                if (__any_sync(0xffffffffu, hotbits != 0u)) {
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) {
+                        if ((hotbits >> i) & 1u) {
+                            const int j = nb * BN + cbase + k * 32 + i;
+                            const int e = atomicAdd(&g.hot_cnt[j], 1);
+                            if (e < g.hcap) {
+                                g.hot_idx[(size_t)j * g.hcap + e] = m;
+                                g.hot_val[(size_t)j * g.hcap + e] = __uint_as_float(r[i]);
+                            }
+                        }
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[ab]);
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
+            for (int i = et; i < BN; i += EPI_THREADS) {
+                const uint32_t v = max(max(s_cm[i], s_cm[BN + i]), max(s_cm[2 * BN + i], s_cm[3 * BN + i]));
+                if (v) atomicMax(&g.cmax[nb * BN + i], v);
+            }
+            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
         }
     }
     tc_fence_before();
@@ -176,7 +257,7 @@ static int make_map(CUtensorMap* map, const void* ptr, int inner, int rows, int 
 }
 
 int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K, int S, float* C, int ldc,
-            cudaStream_t s) {
+            cudaStream_t s, const GemmArgs* fused = nullptr) {
     if (M % BM || Nb % BN || K % BK || S < 1 || lda < K || ldb < K || lda % 8 || ldb % 8 || ldc < M) {
         err_store() = "batched gemm: need M%128==0, N%256==0, K%64==0, 16-byte aligned rows";
         return DSCR_EINVAL;
@@ -186,14 +267,19 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
     if (rc) return rc;
     rc = make_map(&mb, B, K, Nb * S, ldb, BK, BN);
     if (rc) return rc;
-    GemmArgs g;
+    GemmArgs g{};
     g.Nb = Nb;
     g.KB = K / BK;
     g.S = S;
     g.num_m = M / BM;
     g.num_n = Nb / BN;
     g.num_tiles = g.num_m * g.num_n;
-    g.C = C;
+    if (fused) {
+        g.mask = fused->mask; g.nzm = fused->nzm; g.thr = fused->thr; g.cmax = fused->cmax;
+        g.hot_cnt = fused->hot_cnt; g.hot_idx = fused->hot_idx; g.hot_val = fused->hot_val;
+        g.hcap = fused->hcap; g.words = M / 32;
+    }
+    g.C = fused ? nullptr : C;
     g.ldc = ldc;
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
@@ -247,49 +333,63 @@ struct BParams {
     double* anorm;             // [K] column norms of the bf16 dictionary (fp64)
     int *istar, *nnz, *kept, *status;
     const double* beta;        // [iters]
+    int fused;                 // GEMM epilogue emits hot entries (no dense C round trip)
+    uint32_t* nzm;             // [B][K/32] atoms present in the observation's u or x list
+    float* thr;                // [B] lam_j (1 - 1e-6)
+    uint32_t* cmax;            // [B] max |c| over active atoms (float bits)
+    int* hot_cnt;              // [B]
+    int* hot_idx;              // [B][hcap]
+    float* hot_val;            // [B][hcap]
+    int hcap;
     double* trace;             // [iters][4]: sum F, sum gap, sum nnz, sum kept
     int* it;                   // device iteration counter
 };
 
 // fp64 correlations: out[j][i] = sum_n Dt[i][n] V[j][n]; mode 1 writes the
 // DST3 centre correlation cc[j][i] = ycorr[j][i]/lam_j - shift_j * out (fp32).
-constexpr int DG_T = 64, DG_K = 16;
+// CTA tile 128 atoms x 128 observations, 8 x 8 outputs per thread (strided by 16
+// so shared-memory reads are conflict free), K slices of 16 staged as fp64.
+constexpr int DG_T = 128, DG_K = 16;
 __global__ void __launch_bounds__(256) k_dgemm_corr(BParams P, const double* V, int ldv, double* out, int mode) {
-    __shared__ double sD[DG_K][DG_T + 1], sV[DG_K][DG_T + 1];
+    __shared__ double sD[DG_K][DG_T], sV[DG_K][DG_T];
     const int i0 = blockIdx.x * DG_T, j0 = blockIdx.y * DG_T;
     const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
-    double acc[4][4] = {};
+    double acc[8][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc[q][p] = 0.0;
+    const int la = threadIdx.x >> 1, lk = (threadIdx.x & 1) * 8;   // loader: row la, 8 consecutive k
     for (int n0 = 0; n0 < P.N; n0 += DG_K) {
         {
-            const int a = threadIdx.x / 4, kk = (threadIdx.x % 4) * 4;
-            const __nv_bfloat16* dp = P.Dt + (size_t)(i0 + a) * P.ldd + n0 + kk;
-            const double* vp = V + (size_t)(j0 + a) * ldv + n0 + kk;
+            const __nv_bfloat16* dp = P.Dt + (size_t)(i0 + la) * P.ldd + n0 + lk;
+            const double* vp = V + (size_t)(j0 + la) * ldv + n0 + lk;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const bool ok = n0 + kk + q < P.N;
-                sD[kk + q][a] = ok ? (double)__bfloat162float(dp[q]) : 0.0;
-                sV[kk + q][a] = ok ? vp[q] : 0.0;
+            for (int q = 0; q < 8; ++q) {
+                const bool ok = n0 + lk + q < P.N;
+                sD[lk + q][la] = ok ? (double)__bfloat162float(dp[q]) : 0.0;
+                sV[lk + q][la] = ok ? vp[q] : 0.0;
             }
         }
         __syncthreads();
 #pragma unroll
         for (int kk = 0; kk < DG_K; ++kk) {
-            double a4[4], b4[4];
+            double a8[8], b8[8];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) { a4[q] = sD[kk][tx * 4 + q]; b4[q] = sV[kk][ty * 4 + q]; }
+            for (int q = 0; q < 8; ++q) { a8[q] = sD[kk][tx + 16 * q]; b8[q] = sV[kk][ty + 16 * q]; }
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
+            for (int q = 0; q < 8; ++q)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) acc[q][p] = fma(a4[p], b4[q], acc[q][p]);
+                for (int p = 0; p < 8; ++p) acc[q][p] = fma(a8[p], b8[q], acc[q][p]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int j = j0 + ty * 4 + q;
+    for (int q = 0; q < 8; ++q) {
+        const int j = j0 + ty + 16 * q;
 #pragma unroll
-        for (int p = 0; p < 4; ++p) {
-            const int i = i0 + tx * 4 + p;
+        for (int p = 0; p < 8; ++p) {
+            const int i = i0 + tx + 16 * p;
             if (mode == 0) {
                 out[(size_t)j * P.K + i] = acc[q][p];
             } else {
@@ -402,12 +502,18 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
     double v3[3] = {a, b, c};
     block_sum_n<3>(v3, s_sh);
     const bool trivial = P.status[j] == 1;
-    for (int w = threadIdx.x; w < P.K / 32; w += BT) P.mask[(size_t)j * (P.K / 32) + w] = trivial ? 0u : 0xffffffffu;
+    for (int w = threadIdx.x; w < P.K / 32; w += BT) {
+        P.mask[(size_t)j * (P.K / 32) + w] = trivial ? 0u : 0xffffffffu;
+        P.nzm[(size_t)j * (P.K / 32) + w] = 0u;
+    }
     if (threadIdx.x == 0) {
         P.yy[j] = v3[0]; P.sq[j] = v3[1]; P.ty[j] = v3[2];
         P.xc[0][j] = 0; P.uc[0][j] = 0; P.xc[1][j] = 0; P.uc[1][j] = 0;
         P.F[j] = 0.5 * v3[0]; P.gap[j] = NAN; P.nnz[j] = 0; P.kept[j] = trivial ? 0 : P.K;
         P.radius[j] = NAN;
+        P.thr[j] = (float)(P.lam[j] * (1.0 - 1e-6));
+        P.cmax[j] = 0u;
+        P.hot_cnt[j] = 0;
         if (j == 0) *P.it = 0;
     }
 }
@@ -601,6 +707,161 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     }
 }
 
+// Per-observation update on the hot entries emitted by the fused GEMM epilogue.
+// Entries not emitted have u = x = 0 and |c| <= lam_j (1 - 1e-6): their candidate,
+// momentum and list contributions are exactly zero, so only hot entries are processed.
+constexpr int HMAX = 2048;
+
+__device__ __forceinline__ int find_in(const int* a, int n, int key) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (a[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return (lo < n && a[lo] == key) ? lo : -1;
+}
+
+__global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
+    __shared__ int s_idx[HMAX];
+    __shared__ float s_val[HMAX];
+    __shared__ double s_sh[64];
+    __shared__ int s_scan[2 * BW + 1];
+    const int j = blockIdx.x;
+    const int words = P.K / 32;
+    const int par = t & 1;
+    const size_t lo = (size_t)j * P.cap;
+    uint32_t* mrow = P.mask + (size_t)j * words;
+    uint32_t* nrow = P.nzm + (size_t)j * words;
+    const int hc = P.hot_cnt[j];
+    if (P.status[j] != 0) {
+        __syncthreads();
+        if (threadIdx.x == 0) { P.hot_cnt[j] = 0; P.cmax[j] = 0u; }
+        return;
+    }
+    const int cnt = min(hc, P.hcap);
+    int npow = 1;
+    while (npow < cnt) npow <<= 1;
+    for (int e = threadIdx.x; e < npow; e += BT) {
+        s_idx[e] = (e < cnt) ? P.hot_idx[(size_t)j * P.hcap + e] : 0x7fffffff;
+        s_val[e] = (e < cnt) ? P.hot_val[(size_t)j * P.hcap + e] : 0.0f;
+    }
+    __syncthreads();
+    // bitonic sort of (atom, c) by atom: the emission order is arbitrary, the lists are ordered
+    for (int k = 2; k <= npow; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            for (int e = threadIdx.x; e < npow; e += BT) {
+                const int o = e ^ jj;
+                if (o > e) {
+                    const bool up = (e & k) == 0;
+                    const int a = s_idx[e], b = s_idx[o];
+                    if ((a > b) == up) {
+                        s_idx[e] = b; s_idx[o] = a;
+                        const float tv = s_val[e]; s_val[e] = s_val[o]; s_val[o] = tv;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // dual scaling with the inflated correlation bound, r_SAFE^2, test radius (screening.py:115-205)
+    const double lam = P.lam[j], L = P.L;
+    const double sq = P.sq[j], tyv = P.ty[j];
+    const double cinf = (double)__uint_as_float(P.cmax[j]) + P.err_rel * sqrt(sq);
+    const double bound = (cinf == 0.0) ? INFINITY : 1.0 / cinf;
+    const double mu = (sq != 0.0) ? clip(tyv / (lam * sq), bound) : 0.0;
+    double acc = 0.0;
+    for (int n = threadIdx.x; n < P.N; n += BT) {
+        const double v = (sq != 0.0) ? mu * P.theta[(size_t)j * P.ldy + n] : 0.0;
+        const double d = P.Y[(size_t)j * P.ldy + n] / lam - v;
+        acc = fma(d, d, acc);
+    }
+    const double rsq = block_sum(acc, s_sh);
+    double rho = NAN;
+    if (P.test == DSCR_SAFE) rho = sqrt(rsq);
+    else if (P.test == DSCR_DST3) {
+        const double arg = rsq - P.shift_sq[j];
+        if (arg < -RADIUS_GUARD && threadIdx.x == 0) P.status[j] = 3;
+        rho = sqrt(fmax(arg, 0.0));
+    }
+    const double margin = SCREEN_MARGIN + 1e-6;
+    const bool can_screen = (P.test != DSCR_TEST_OFF) && (P.ccmin[j] - rho > margin);
+    double kept = (double)P.kept[j];
+    if (can_screen) {       // rare: test every active atom of this observation
+        double lost = 0.0;
+        for (int w = threadIdx.x; w < words; w += BT) {
+            uint32_t m = mrow[w];
+            uint32_t keepw = m;
+            while (m) {
+                const int bit = __ffs(m) - 1;
+                m &= m - 1;
+                const int i = w * 32 + bit;
+                const double ccv = (double)P.cc[(size_t)j * P.K + i];
+                if ((1.0 - fabs(ccv)) / P.anorm[i] - rho > margin) keepw &= ~(1u << bit);   // screening.py:359
+            }
+            if (keepw != mrow[w]) { lost += __popc(mrow[w] ^ keepw); mrow[w] = keepw; }
+        }
+        kept -= block_sum(lost, s_sh);
+    }
+    __syncthreads();
+    // hot entries in atom order: prox, momentum, ordered compaction into the new lists
+    const double thr = lam / L, beta = P.beta[t];
+    const int* xi = P.xi[par] + lo; const double* xv = P.xv[par] + lo; const int xcnt = P.xc[par][j];
+    const int* ui = P.ui[par] + lo; const double* uv = P.uv[par] + lo; const int ucnt = P.uc[par][j];
+    int nx = 0, nu = 0;
+    double pen = 0.0, nnz = 0.0;
+    for (int e0 = 0; e0 < cnt; e0 += BT) {
+        const int e = e0 + threadIdx.x;
+        double cand = 0.0, un = 0.0;
+        int i = -1;
+        if (e < cnt) {
+            i = s_idx[e];
+            if ((mrow[i >> 5] >> (i & 31)) & 1u) {
+                const int pu = find_in(ui, ucnt, i), px = find_in(xi, xcnt, i);
+                const double u = pu >= 0 ? uv[pu] : 0.0, x = px >= 0 ? xv[px] : 0.0;
+                const double c = (double)s_val[e];
+                cand = soft(u - c / L, thr);
+                un = cand + beta * (cand - x);
+            }
+        }
+        int tx, tu;
+        const int ox = block_exscan(cand != 0.0 ? 1 : 0, s_scan, &tx);
+        const int ou = block_exscan(un != 0.0 ? 1 : 0, s_scan, &tu);
+        if (cand != 0.0 && nx + ox < P.cap) { P.xi[par ^ 1][lo + nx + ox] = i; P.xv[par ^ 1][lo + nx + ox] = cand; }
+        if (un != 0.0 && nu + ou < P.cap) { P.ui[par ^ 1][lo + nu + ou] = i; P.uv[par ^ 1][lo + nu + ou] = un; }
+        pen += fabs(cand);
+        nnz += (cand != 0.0) ? 1.0 : 0.0;
+        nx += tx;
+        nu += tu;
+    }
+    // nonzero bitmap: clear the old lists' atoms, then set the new lists' atoms
+    for (int e = threadIdx.x; e < ucnt; e += BT) atomicAnd(&nrow[ui[e] >> 5], ~(1u << (ui[e] & 31)));
+    for (int e = threadIdx.x; e < xcnt; e += BT) atomicAnd(&nrow[xi[e] >> 5], ~(1u << (xi[e] & 31)));
+    __syncthreads();
+    const int nxc = min(nx, P.cap), nuc = min(nu, P.cap);
+    for (int e = threadIdx.x; e < nuc; e += BT) {
+        const int a = P.ui[par ^ 1][lo + e];
+        atomicOr(&nrow[a >> 5], 1u << (a & 31));
+    }
+    for (int e = threadIdx.x; e < nxc; e += BT) {
+        const int a = P.xi[par ^ 1][lo + e];
+        atomicOr(&nrow[a >> 5], 1u << (a & 31));
+    }
+    double v2[2] = {pen, nnz};
+    block_sum_n<2>(v2, s_sh);
+    if (threadIdx.x == 0) {
+        if (hc > P.hcap || nx > P.cap || nu > P.cap) P.status[j] = 4;
+        P.xc[par ^ 1][j] = nxc;
+        P.uc[par ^ 1][j] = nuc;
+        P.pen[j] = v2[0];
+        P.nnz[j] = (int)v2[1];
+        P.kept[j] = (int)kept;
+        P.rsq[j] = rsq;
+        P.radius[j] = rho;
+        P.hot_cnt[j] = 0;       // re-arm for the next GEMM
+        P.cmax[j] = 0u;
+    }
+}
+
 // sparse residuals D x - y and D u - y; objective, gap, next theta (+ bf16 terms)
 __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
     __shared__ double s_sh[64];
@@ -613,10 +874,13 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
         return;
     }
     const size_t lo = (size_t)j * P.cap;
+    // thread t owns rows 4t..4t+3 (+1024 for the second chunk); one 8-byte load per entry and
+    // chunk, four entries in flight
     constexpr int RPT = 8;            // rows per thread (N <= 2048)
     double rx[RPT], ru[RPT];
 #pragma unroll
     for (int q = 0; q < RPT; ++q) { rx[q] = 0.0; ru[q] = 0.0; }
+    const int nch = (P.N + 1023) / 1024;
     for (int which = 0; which < 2; ++which) {
         const int* idx = (which ? P.ui[par] : P.xi[par]) + lo;
         const double* val = (which ? P.uv[par] : P.xv[par]) + lo;
@@ -626,24 +890,42 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
             if (e0 + threadIdx.x < cnt) { s_idx[threadIdx.x] = idx[e0 + threadIdx.x]; s_val[threadIdx.x] = val[e0 + threadIdx.x]; }
             __syncthreads();
             const int m = min(BT, cnt - e0);
-            for (int e = 0; e < m; ++e) {
-                const __nv_bfloat16* col = P.Dt + (size_t)s_idx[e] * P.ldd;
-                const double v = s_val[e];
+            for (int ch = 0; ch < nch; ++ch) {
+                const int r0 = ch * 1024 + 4 * threadIdx.x;
+                if (r0 >= P.N) continue;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                int e = 0;
+                for (; e + 4 <= m; e += 4) {
+                    uint2 w[4];
 #pragma unroll
-                for (int q = 0; q < RPT; ++q) {
-                    const int n = threadIdx.x + q * BT;
-                    if (n < P.N) {
-                        const double d = (double)__bfloat162float(col[n]);
-                        if (which) ru[q] = fma(v, d, ru[q]); else rx[q] = fma(v, d, rx[q]);
+                    for (int q = 0; q < 4; ++q)
+                        w[q] = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0));
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const double v = s_val[e + q];
+                        a0 = fma(v, (double)__uint_as_float(w[q].x << 16), a0);
+                        a1 = fma(v, (double)__uint_as_float(w[q].x & 0xffff0000u), a1);
+                        a2 = fma(v, (double)__uint_as_float(w[q].y << 16), a2);
+                        a3 = fma(v, (double)__uint_as_float(w[q].y & 0xffff0000u), a3);
                     }
                 }
+                for (; e < m; ++e) {
+                    const uint2 w = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e] * P.ldd + r0));
+                    const double v = s_val[e];
+                    a0 = fma(v, (double)__uint_as_float(w.x << 16), a0);
+                    a1 = fma(v, (double)__uint_as_float(w.x & 0xffff0000u), a1);
+                    a2 = fma(v, (double)__uint_as_float(w.y << 16), a2);
+                    a3 = fma(v, (double)__uint_as_float(w.y & 0xffff0000u), a3);
+                }
+                double* dst = which ? ru : rx;
+                dst[ch * 4 + 0] += a0; dst[ch * 4 + 1] += a1; dst[ch * 4 + 2] += a2; dst[ch * 4 + 3] += a3;
             }
         }
     }
     double f2 = 0.0, sq = 0.0, tyv = 0.0;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-        const int n = threadIdx.x + q * BT;
+        const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
         if (n < P.N) {
             const double yn = P.Y[(size_t)j * P.ldy + n];
             const double qa = rx[q] - yn;
@@ -654,6 +936,7 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
             tyv = fma(tn, yn, tyv);
         }
     }
+    for (int n = P.N + threadIdx.x; n < P.ldy; n += BT) write_theta(P, j, n, 0.0);
     double v3[3] = {f2, sq, tyv};
     block_sum_n<3>(v3, s_sh);
     if (threadIdx.x == 0) {
@@ -718,6 +1001,13 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     p.anorm = (double*)take(K * 8);
     int** iv[] = {&p.istar, &p.nnz, &p.kept, &p.status};
     for (int** q : iv) *q = (int*)take(B * 4);
+    p.nzm = (uint32_t*)take(B * K / 8);
+    p.thr = (float*)take(B * 4);
+    p.cmax = (uint32_t*)take(B * 4);
+    p.hot_cnt = (int*)take(B * 4);
+    p.hcap = 2048;
+    p.hot_idx = (int*)take(B * (size_t)p.hcap * 4);
+    p.hot_val = (float*)take(B * (size_t)p.hcap * 4);
     p.beta = (const double*)take((size_t)d->max_iters * 8);
     p.trace = (double*)take((size_t)d->max_iters * 4 * 8);
     p.it = (int*)take(64);
@@ -752,6 +1042,7 @@ int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void
     P.N = d->n_rows; P.K = d->n_atoms; P.B = d->n_obs; P.ldd = d->ldd;
     P.Y = d->Y; P.ldy = d->ldy; P.lam = d->lam; P.L = d->L; P.test = d->test;
     P.splits = d->splits; P.cap = d->cap;
+    P.fused = d->fused;
     // |c~ - c| <= ||d_i|| (||theta - theta~|| + fp32 accumulation) <= err_rel ||theta||
     P.err_rel = (d->splits == 1 ? 0.00391 : 1.6e-5) + 2.0 * d->n_rows * 5.96e-8;
     h->max_iters = d->max_iters;
@@ -782,10 +1073,14 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
 
 static int enqueue_iterations(dscr_batched* h, int t0, int n, cudaStream_t s) {
     BParams& P = h->P;
+    GemmArgs fz{};
+    fz.mask = P.mask; fz.nzm = P.nzm; fz.thr = P.thr; fz.cmax = P.cmax;
+    fz.hot_cnt = P.hot_cnt; fz.hot_idx = P.hot_idx; fz.hot_val = P.hot_val; fz.hcap = P.hcap;
     for (int t = t0; t < t0 + n; ++t) {
-        int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s);
+        int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s, P.fused ? &fz : nullptr);
         if (rc) return rc;
-        k_bupdate<<<P.B, BT, 0, s>>>(P, t);
+        if (P.fused) k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);
+        else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
         k_bresid<<<P.B, BT, 0, s>>>(P, t);
         k_btrace<<<1, BT, 0, s>>>(P, t);
         cudaError_t e = cudaGetLastError();
@@ -823,10 +1118,14 @@ int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out) {
     BParams& P = h->P;
     cudaEvent_t ev[4];
     for (int i = 0; i < 4; ++i) cudaEventCreate(&ev[i]);
+    GemmArgs fz{};
+    fz.mask = P.mask; fz.nzm = P.nzm; fz.thr = P.thr; fz.cmax = P.cmax;
+    fz.hot_cnt = P.hot_cnt; fz.hot_idx = P.hot_idx; fz.hot_val = P.hot_val; fz.hcap = P.hcap;
     cudaEventRecord(ev[0], s);
-    int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s);
+    int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s, P.fused ? &fz : nullptr);
     cudaEventRecord(ev[1], s);
-    k_bupdate<<<P.B, BT, 0, s>>>(P, t);
+    if (P.fused) k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);
+    else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
     cudaEventRecord(ev[2], s);
     k_bresid<<<P.B, BT, 0, s>>>(P, t);
     cudaEventRecord(ev[3], s);

@@ -105,3 +105,18 @@ def test_batched_c5_shape_runs():
                                      rel_tol=1e-300, L0=L, norm_aware=True))
         assert abs(res.objective[j] - ref.final_objective) <= 2e-2 * ref.final_objective
     print(f"\nc5-shape batch of 512: {res.device_seconds * 1e3:.1f} ms for 100 iterations")
+
+
+@pytest.mark.parametrize("ratio", [0.4, 0.85])
+def test_fused_epilogue_matches_dense_update(ratio):
+    """Hot-entry epilogue (no dense C round trip) == dense C + full per-atom update."""
+    w, dic, D64, L = _batch_problem(256, 2048, 512, ratio, seed=3)
+    a = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2, fused=True)
+    b = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2, fused=False)
+    np.testing.assert_allclose(a.objective, b.objective, rtol=1e-13)
+    assert np.array_equal(a.kept, b.kept) and np.array_equal(a.nnz, b.nnz)
+    for j in range(0, 512, 37):
+        assert np.array_equal(a.x_idx[j], b.x_idx[j])
+        np.testing.assert_allclose(a.x_val[j], b.x_val[j], rtol=1e-13, atol=1e-15)
+    if ratio > 0.5:
+        assert a.kept.min() < 2048
