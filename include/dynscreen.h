@@ -251,6 +251,16 @@ int dscr_solver_destroy(dscr_solver* h);
 int dscr_batched_gemm_bf16(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K,
                            int splits, float* C, int ldc, void* stream);
 
+/* Correlations D^T V of a bf16 dictionary (D^T = atoms x rows, row stride ldd) with fp64
+ * vectors (V = n_obs x rows, stride ldv) to ~fp64 accuracy on the integer tensor cores:
+ * int8 slices of both operands, exact int32 products, fp64 recombination (relative error
+ * ~2^-30 of sum |d||v|).  out[j][i] (stride ldo).  Atoms, observations and rows multiples of
+ * 128, rows <= 2048.  The fp64 setup correlations of a batch (problems.py:75-86 lambda_max,
+ * screening.py:214-231 centre correlations) for many observations at once. */
+size_t dscr_corr_exact_work_size(int n_atoms, int n_rows, int n_obs);
+int dscr_corr_exact_bf16(const void* Dt, int n_atoms, int n_rows, int ldd, const double* V, int n_obs, int ldv,
+                         double* out, int ldo, void* work, size_t work_bytes, void* stream);
+
 /* Batched FISTA with per-observation dynamic screening: shared bf16 dictionary
  * (stored as D^T = atoms x features, i.e. column-major D), many observations.
  * Iterates are sparse per observation; c = D^T theta runs on tcgen05 tensor cores;

@@ -15,6 +15,8 @@
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include <algorithm>
 
@@ -236,15 +238,16 @@ static EncodeTiledFn encode_fn() {
     return fn;
 }
 
-// 2-D bf16 tensor [rows][ld] (inner dimension `inner` elements), box = box_inner x box_rows, 128B swizzle
-static int make_map(CUtensorMap* map, const void* ptr, int inner, int rows, int ld, int box_inner, int box_rows) {
+// 2-D tensor [rows][ld] (inner dimension `inner` elements), box = box_inner x box_rows, 128B swizzle
+static int make_map(CUtensorMap* map, const void* ptr, int inner, int rows, int ld, int box_inner, int box_rows,
+                    CUtensorMapDataType dt = CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, int esize = 2) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) { err_store() = "cuTensorMapEncodeTiled unavailable"; return DSCR_ECUDA; }
     cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)ld * 2};
+    cuuint64_t strides[1] = {(cuuint64_t)ld * esize};
     cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr), dims, strides, box, estr,
+    CUresult r = fn(map, dt, 2, const_cast<void*>(ptr), dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) {
@@ -293,6 +296,253 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
 }
 
 // ---------------------------------------------------------------------------
+// Exact correlations on the integer tensor cores (setup of config 5)
+// ---------------------------------------------------------------------------
+//
+// out[j][i] = sum_n D[n][i] V[j][n] to ~fp64 accuracy without fp64 GEMM throughput:
+// each row of D^T (bf16) and of V (fp64 or bf16) is written as a power-of-two scale times
+// 7-bit signed slices, x = 2^E sum_s q_s 2^{-7(s+1)}, q_s in [-127, 127] (truncation).  A bf16
+// entry is represented exactly by S = 4 slices when it lies within 2^21 of its row maximum;
+// V = fp64 rows keep 35 bits with T = 5 slices.  Slice products are int8 x int8 GEMMs with
+// exact int32 accumulation (tcgen05 kind::i8); the pairs of one diagonal s + t share one TMEM
+// accumulator (<= 4 pairs x N 127^2 < 2^31 for N <= 2048) and the epilogue combines the
+// diagonals in fp64: out = 2^{E_i + F_j - 14} sum_d 2^{-7d} C_d.  Pairs with s + t > 5 are
+// dropped (weight below 2^-49 of the leading term per product).
+constexpr int OZ_BM = 128, OZ_BN = 128, OZ_BK = 128, OZ_STAGES = 6;
+constexpr int OZ_A = OZ_BM * OZ_BK, OZ_B = OZ_BN * OZ_BK, OZ_STAGE = OZ_A + OZ_B;
+constexpr int OZ_THREADS = 320;     // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue
+constexpr int OZ_EPI = OZ_THREADS - 64;
+constexpr size_t OZ_SMEM = (size_t)OZ_STAGES * OZ_STAGE + 1024 + 256;
+constexpr int OZ_DMAX = 5, OZ_MAXP = 32;
+
+struct OzArgs {
+    int K, B;                  // atoms (rows of the A slices), observations (rows of the B slices)
+    int KB;                    // N / 128
+    int np, nd;                // slice pairs, diagonals
+    int ps[OZ_MAXP], pt[OZ_MAXP];
+    int dend[OZ_DMAX + 2];     // pairs [dend[d-1], dend[d]) lie on diagonal d
+    int num_m, num_tiles;
+    const int* eA;             // [K] row exponents of the A slices
+    const int* eB;             // [B] row exponents of the B slices
+    int mode;                  // 0: out[j][i] fp64 ; 1: DST3 centre correlation cc (fp32)
+    double* out; int ldo;
+    const double *ycorr, *lam, *lmax, *anorm, *sgn;
+    const int* istar;
+    float* cc;
+};
+
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+    k_ozaki(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, OzArgs g) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* sA = base;
+    uint8_t* sB = base + OZ_STAGES * OZ_A;
+    uint64_t* full = (uint64_t*)(sB + OZ_STAGES * OZ_B);
+    uint64_t* empty = full + OZ_STAGES;
+    uint64_t* tfull = empty + OZ_STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tslot = (uint32_t*)(tempty + 2);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tmA);
+        tma_prefetch(&tmB);
+        for (int s = 0; s < OZ_STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], OZ_EPI); }
+        fence_barrier_init();
+    }
+    if (warp == 1) tmem_alloc(tslot, 2 * OZ_BN);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tslot;
+
+    if (warp == 0) {
+        if (lane == 0) {   // ---- TMA producer: pairs in diagonal order, k-blocks inside
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
+                const int mb = tile % g.num_m, nb = tile / g.num_m;
+                for (int p = 0; p < g.np; ++p)
+                    for (int kb = 0; kb < g.KB; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        mbar_expect_tx(&full[stage], OZ_STAGE);
+                        tma_load_2d(sA + stage * OZ_A, &tmA, &full[stage], kb * OZ_BK, g.ps[p] * g.K + mb * OZ_BM);
+                        tma_load_2d(sB + stage * OZ_B, &tmB, &full[stage], kb * OZ_BK, g.pt[p] * g.B + nb * OZ_BN);
+                        if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+                    }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {   // ---- MMA issuer: one TMEM accumulator per diagonal
+            const uint32_t idesc = idesc_s8_s32(OZ_BM, OZ_BN);
+            int stage = 0;
+            uint32_t phase = 0;
+            int gd = 0;
+            for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
+                int p = 0;
+                for (int d = 0; d < g.nd; ++d, ++gd) {
+                    const int ab = gd & 1;
+                    mbar_wait(&tempty[ab], ((gd >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t dcol = tmem + ab * OZ_BN;
+                    bool first = true;
+                    for (; p < g.dend[d]; ++p)
+                        for (int kb = 0; kb < g.KB; ++kb) {
+                            mbar_wait(&full[stage], phase);
+                            tc_fence_after();
+                            const uint64_t da = desc_kmajor_sw128(smem_u32(sA + stage * OZ_A));
+                            const uint64_t db = desc_kmajor_sw128(smem_u32(sB + stage * OZ_B));
+#pragma unroll
+                            for (int k = 0; k < OZ_BK / 32; ++k) {   // +32 B along K inside the swizzle atom
+                                mma_s8(dcol, da + 2 * k, db + 2 * k, idesc, first ? 0u : 1u);
+                                first = false;
+                            }
+                            mma_commit(&empty[stage]);
+                            if (++stage == OZ_STAGES) { stage = 0; phase ^= 1; }
+                        }
+                    mma_commit(&tfull[ab]);
+                }
+            }
+        }
+    } else {   // ---- epilogue: fp64 combination of the diagonals, scaled store
+        const int q = warp & 3;                  // TMEM lane quarter
+        const int half = (warp - 2) >> 2;        // 64-column half of the tile
+        int gd = 0;
+        for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
+            const int mb = tile % g.num_m, nb = tile / g.num_m;
+            double acc[64];
+#pragma unroll
+            for (int c = 0; c < 64; ++c) acc[c] = 0.0;
+            for (int d = 0; d < g.nd; ++d, ++gd) {
+                const int ab = gd & 1;
+                mbar_wait(&tfull[ab], (gd >> 1) & 1);
+                tc_fence_after();
+                const double w = ldexp(1.0, -7 * d);
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    uint32_t r[32];
+                    tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * OZ_BN + half * 64 + c * 32, r);
+#pragma unroll
+                    for (int i = 0; i < 32; ++i) acc[c * 32 + i] = fma((double)(int)r[i], w, acc[c * 32 + i]);
+                }
+                tc_fence_before();
+                mbar_arrive(&tempty[ab]);
+            }
+            const int i = mb * OZ_BM + q * 32 + lane;
+            const int ei = g.eA[i] - 14;
+            const int j0 = nb * OZ_BN + half * 64;
+            if (g.mode == 0) {
+                double* o = g.out + (size_t)j0 * g.ldo + i;
+#pragma unroll
+                for (int c = 0; c < 64; ++c) o[(size_t)c * g.ldo] = ldexp(acc[c], ei + g.eB[j0 + c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < 64; ++c) {
+                    const int j = j0 + c;
+                    const double lam = g.lam[j];
+                    const double a = g.anorm[g.istar[j]];
+                    const double coef = (g.lmax[j] / lam - 1.0) / (a * a) * g.sgn[j];
+                    const double v = ldexp(acc[c], ei + g.eB[j]);
+                    g.cc[(size_t)j * g.K + i] = (float)(g.ycorr[(size_t)j * g.K + i] / lam - coef * v);
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc(tmem, 2 * OZ_BN);
+}
+
+__device__ __forceinline__ double to_f64(double v) { return v; }
+__device__ __forceinline__ double to_f64(__nv_bfloat16 v) { return (double)__bfloat162float(v); }
+
+// rows of src (bf16 or fp64, row stride ld, N used) -> S int8 slices [S][rows][N] + exponents
+template <typename T>
+__global__ void __launch_bounds__(256) k_slice_rows(const T* src, int rows, int N, int ld, int S, int8_t* dst,
+                                                    int* ex) {
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * 256 + threadIdx.x) >> 5;
+    if (r >= rows) return;
+    const T* row = src + (size_t)r * ld;
+    double m = 0.0;
+    for (int n = lane; n < N; n += 32) m = fmax(m, fabs(to_f64(row[n])));
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    int e = 0;
+    if (m > 0.0) frexp(m, &e);                  // m < 2^e
+    if (lane == 0) ex[r] = e;
+    for (int n = lane; n < N; n += 32) {
+        double x = ldexp(to_f64(row[n]), -e);   // |x| < 1, exact
+        for (int s = 0; s < S; ++s) {
+            x *= 128.0;
+            const double qv = trunc(x);
+            x -= qv;
+            dst[((size_t)s * rows + r) * N + n] = (int8_t)(int)qv;
+        }
+    }
+}
+
+// B slices of the DST3 atoms: row j of slice s = row istar[j] of the dictionary's slice s
+__global__ void __launch_bounds__(256) k_gather_slices(const int8_t* Ds, const int* eD, int K, int N, int S,
+                                                       const int* istar, int B, int8_t* dst, int* ex) {
+    const int j = blockIdx.x;
+    const int i = istar[j];
+    if (threadIdx.x == 0) ex[j] = eD[i];
+    const int nw = N / 16;
+    for (int s = 0; s < S; ++s) {
+        const uint4* srow = reinterpret_cast<const uint4*>(Ds + ((size_t)s * K + i) * N);
+        uint4* drow = reinterpret_cast<uint4*>(dst + ((size_t)s * B + j) * N);
+        for (int w = threadIdx.x; w < nw; w += 256) drow[w] = srow[w];
+    }
+}
+
+// pairs (s, t), s < S, t < T, s + t <= OZ_DMAX, in diagonal order
+static void oz_pairs(OzArgs& g, int S, int T) {
+    g.np = 0;
+    g.nd = 0;
+    for (int d = 0; d <= OZ_DMAX; ++d) {
+        for (int s = 0; s < S; ++s) {
+            const int t = d - s;
+            if (t < 0 || t >= T) continue;
+            g.ps[g.np] = s;
+            g.pt[g.np] = t;
+            ++g.np;
+        }
+        g.dend[g.nd++] = g.np;
+    }
+}
+
+// A slices [S][K][N], B slices [T][B][N]; K, B, N multiples of 128
+static int ozaki_launch(const int8_t* As, int K, int S, const int8_t* Bs, int B, int T, int N, OzArgs& g, cudaStream_t s) {
+    if (K % OZ_BM || B % OZ_BN || N % OZ_BK || N > 2048) {
+        err_store() = "exact correlation: need atoms, observations, rows multiples of 128 and rows <= 2048";
+        return DSCR_EINVAL;
+    }
+    CUtensorMap ma, mb;
+    int rc = make_map(&ma, As, N, S * K, N, OZ_BK, OZ_BM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1);
+    if (rc) return rc;
+    rc = make_map(&mb, Bs, N, T * B, N, OZ_BK, OZ_BN, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1);
+    if (rc) return rc;
+    oz_pairs(g, S, T);
+    g.K = K;
+    g.B = B;
+    g.KB = N / OZ_BK;
+    g.num_m = K / OZ_BM;
+    g.num_tiles = g.num_m * (B / OZ_BN);
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaError_t e = cudaFuncSetAttribute(k_ozaki, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)OZ_SMEM);
+    if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+    k_ozaki<<<std::min(g.num_tiles, sms), OZ_THREADS, OZ_SMEM, s>>>(ma, mb, g);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+    return DSCR_OK;
+}
+
+constexpr int OZ_SD = 4, OZ_SV = 5;    // slices of the bf16 dictionary / of fp64 observations
+
+// ---------------------------------------------------------------------------
 // batched FISTA with per-observation dynamic DST3 screening (config 5)
 // ---------------------------------------------------------------------------
 //
@@ -320,16 +570,20 @@ struct BParams {
     int cap;
     double err_rel;            // |c~ - c| <= err_rel * ||theta||
     // state
-    double* theta;             // [B][ldy]
     __nv_bfloat16* tb;         // [S][B][ldy]
     float* C;                  // [B][K]  c^T from the GEMM
     float* cc;                 // [B][K]  test centre correlations (fp32)
     double* ycorr;             // [B][K]  fp64 setup scratch
-    double* astar;             // [B][ldy]
+    double* astar;             // [B][ldy] (fp64 setup path only)
+    int8_t* Ds;                // [OZ_SD][K][N] int8 slices of the dictionary (exact setup path)
+    int* eD;                   // [K]
+    int8_t* Vs;                // [OZ_SV][B][N] int8 slices of y / of the DST3 atoms
+    int* eV;                   // [B]
+    int oz;                    // setup correlations on the integer tensor cores
     uint32_t* mask;            // [B][K/32]
     int* xi[2]; double* xv[2]; int* xc[2];   // x lists (parity)
     int* ui[2]; double* uv[2]; int* uc[2];   // u lists
-    double *sq, *ty, *yy, *lmax, *sgn, *shift_sq, *rsq, *radius, *F, *gap, *pen, *ccmin;
+    double *sq, *ty, *mu0, *rsq0, *yy, *lmax, *sgn, *shift_sq, *rsq, *radius, *F, *gap, *pen, *ccmin;
     double* anorm;             // [K] column norms of the bf16 dictionary (fp64)
     int *istar, *nnz, *kept, *status;
     const double* beta;        // [iters]
@@ -419,6 +673,7 @@ __global__ void __launch_bounds__(BT) k_bnorms(BParams P) {
 
 // lambda_* = max_i |D^T y_j| (lowest index), a_* sign, DST3 shift^2 (problems.py:75-86, screening.py:221-231)
 __global__ void __launch_bounds__(BT) k_blmax(BParams P) {
+    __shared__ double s_sh[64];
     __shared__ double s_v[BT];
     __shared__ int s_i[BT];
     const int j = blockIdx.x;
@@ -443,18 +698,26 @@ __global__ void __launch_bounds__(BT) k_blmax(BParams P) {
         }
         __syncthreads();
     }
+    const int i = s_i[0];
+    // lambda_* of the chosen atom recomputed directly in fp64 (the integer-slice correlations
+    // carry ~2^-30 relative error; this keeps lambda_* and the DST3 shift at fp64 accuracy)
+    double dot = 0.0;
+    for (int n = threadIdx.x; n < P.N; n += BT)
+        dot = fma((double)__bfloat162float(P.Dt[(size_t)i * P.ldd + n]), P.Y[(size_t)j * P.ldy + n], dot);
+    dot = block_sum(dot, s_sh);
+    const double lm = P.oz ? fabs(dot) : s_v[0];
+    const double sg = P.oz ? (dot >= 0.0 ? 1.0 : -1.0) : (row[i] >= 0.0 ? 1.0 : -1.0);
     if (threadIdx.x == 0) {
-        const int i = s_i[0];
-        P.lmax[j] = s_v[0];
+        P.lmax[j] = lm;
         P.istar[j] = i;
-        P.sgn[j] = row[i] >= 0.0 ? 1.0 : -1.0;
-        const double shift = s_v[0] / P.lam[j] - 1.0;
+        P.sgn[j] = sg;
+        const double shift = lm / P.lam[j] - 1.0;
         const double an = P.anorm[i];
         P.shift_sq[j] = (P.test == DSCR_DST3) ? shift * shift / (an * an) : 0.0;   // normal a_*/||a_*||
-        P.status[j] = (P.lam[j] > s_v[0]) ? 1 : 0;     // 1 = trivial (solvers.py:384-397)
+        P.status[j] = (P.lam[j] > lm) ? 1 : 0;     // 1 = trivial (solvers.py:384-397)
     }
-    __syncthreads();
-    const int ist = P.istar[j];
+    if (P.oz) return;
+    const int ist = i;
     for (int n = threadIdx.x; n < P.ldy; n += BT)
         P.astar[(size_t)j * P.ldy + n] = (n < P.N) ? (double)__bfloat162float(P.Dt[(size_t)ist * P.ldd + n]) : 0.0;
 }
@@ -478,8 +741,16 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
     }
 }
 
+// r_SAFE^2 = ||y/lam - mu theta||^2 (screening.py:115-140) from the residual kernel's
+// exact ||y/lam - mu0 theta||^2 at the unclipped mu0 = <theta,y>/(lam ||theta||^2):
+// y/lam - mu0 theta is orthogonal to theta, so the clipped value adds (mu - mu0)^2 ||theta||^2
+// (two non-negative terms; no cancellation).
+__device__ __forceinline__ double radius_sq(const BParams& P, int j, double mu, double sq) {
+    const double dm = mu - P.mu0[j];
+    return fma(dm * dm, sq, P.rsq0[j]);
+}
+
 __device__ __forceinline__ void write_theta(const BParams& P, int j, int n, double t) {
-    P.theta[(size_t)j * P.ldy + n] = t;
     const __nv_bfloat16 hi = __double2bfloat16(t);
     P.tb[(size_t)j * P.ldy + n] = hi;
     if (P.splits > 1) {
@@ -501,13 +772,22 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
     }
     double v3[3] = {a, b, c};
     block_sum_n<3>(v3, s_sh);
+    const double lam = P.lam[j];
+    const double mu0 = (v3[1] != 0.0) ? v3[2] / (lam * v3[1]) : 0.0;
+    double d2 = 0.0;
+    for (int n = threadIdx.x; n < P.N; n += BT) {
+        const double yn = P.Y[(size_t)j * P.ldy + n];
+        const double d = yn / lam - mu0 * (0.0 - yn);
+        d2 = fma(d, d, d2);
+    }
+    d2 = block_sum(d2, s_sh);
     const bool trivial = P.status[j] == 1;
     for (int w = threadIdx.x; w < P.K / 32; w += BT) {
         P.mask[(size_t)j * (P.K / 32) + w] = trivial ? 0u : 0xffffffffu;
         P.nzm[(size_t)j * (P.K / 32) + w] = 0u;
     }
     if (threadIdx.x == 0) {
-        P.yy[j] = v3[0]; P.sq[j] = v3[1]; P.ty[j] = v3[2];
+        P.yy[j] = v3[0]; P.sq[j] = v3[1]; P.ty[j] = v3[2]; P.mu0[j] = mu0; P.rsq0[j] = d2;
         P.xc[0][j] = 0; P.uc[0][j] = 0; P.xc[1][j] = 0; P.uc[1][j] = 0;
         P.F[j] = 0.5 * v3[0]; P.gap[j] = NAN; P.nnz[j] = 0; P.kept[j] = trivial ? 0 : P.K;
         P.radius[j] = NAN;
@@ -665,13 +945,7 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     const double cinf = s_scal[0] + P.err_rel * sqrt(sq);
     const double bound = (cinf == 0.0) ? INFINITY : 1.0 / cinf;
     const double mu = (sq != 0.0) ? clip(tyv / (lam * sq), bound) : 0.0;
-    double acc = 0.0;
-    for (int n = threadIdx.x; n < P.N; n += BT) {
-        const double v = (sq != 0.0) ? mu * P.theta[(size_t)j * P.ldy + n] : 0.0;
-        const double d = P.Y[(size_t)j * P.ldy + n] / lam - v;
-        acc = fma(d, d, acc);
-    }
-    const double rsq = block_sum(acc, s_sh);
+    const double rsq = radius_sq(P, j, mu, sq);
     if (P.test == DSCR_SAFE) rho = sqrt(rsq);
     else if (P.test == DSCR_DST3) {
         const double arg = rsq - P.shift_sq[j];
@@ -721,9 +995,13 @@ __device__ __forceinline__ int find_in(const int* a, int n, int key) {
     return (lo < n && a[lo] == key) ? lo : -1;
 }
 
+constexpr int LSM = 512;       // old-list entries staged in shared memory (longer lists search global)
+
 __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     __shared__ int s_idx[HMAX];
     __shared__ float s_val[HMAX];
+    __shared__ int s_xi[LSM], s_ui[LSM];
+    __shared__ double s_xv[LSM], s_uv[LSM];
     __shared__ double s_sh[64];
     __shared__ int s_scan[2 * BW + 1];
     const int j = blockIdx.x;
@@ -733,11 +1011,20 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     uint32_t* mrow = P.mask + (size_t)j * words;
     uint32_t* nrow = P.nzm + (size_t)j * words;
     const int hc = P.hot_cnt[j];
-    if (P.status[j] != 0) {
+    const int st = P.status[j];
+    const int xcnt = P.xc[par][j], ucnt = P.uc[par][j];
+    const double lam = P.lam[j], L = P.L;
+    const double sq = P.sq[j], tyv = P.ty[j];
+    const uint32_t cmx = P.cmax[j];
+    const double ccmin = P.ccmin[j], shsq = P.shift_sq[j], beta = P.beta[t];
+    const int kept0 = P.kept[j];
+    if (st != 0) {
         __syncthreads();
         if (threadIdx.x == 0) { P.hot_cnt[j] = 0; P.cmax[j] = 0u; }
         return;
     }
+    const int* xi = P.xi[par] + lo; const double* xv = P.xv[par] + lo;
+    const int* ui = P.ui[par] + lo; const double* uv = P.uv[par] + lo;
     const int cnt = min(hc, P.hcap);
     int npow = 1;
     while (npow < cnt) npow <<= 1;
@@ -745,7 +1032,20 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
         s_idx[e] = (e < cnt) ? P.hot_idx[(size_t)j * P.hcap + e] : 0x7fffffff;
         s_val[e] = (e < cnt) ? P.hot_val[(size_t)j * P.hcap + e] : 0.0f;
     }
+    const bool xs = xcnt <= LSM, us = ucnt <= LSM;
+    if (xs) for (int e = threadIdx.x; e < xcnt; e += BT) { s_xi[e] = xi[e]; s_xv[e] = xv[e]; }
+    if (us) for (int e = threadIdx.x; e < ucnt; e += BT) { s_ui[e] = ui[e]; s_uv[e] = uv[e]; }
+    // dual scaling with the inflated correlation bound, r_SAFE^2, test radius (screening.py:115-205)
+    const double cinf = (double)__uint_as_float(cmx) + P.err_rel * sqrt(sq);
+    const double bound = (cinf == 0.0) ? INFINITY : 1.0 / cinf;
+    const double mu = (sq != 0.0) ? clip(tyv / (lam * sq), bound) : 0.0;
+    const double rsq = radius_sq(P, j, mu, sq);
     __syncthreads();
+    if (xs) xi = s_xi, xv = s_xv;
+    if (us) ui = s_ui, uv = s_uv;
+    // nonzero bitmap: clear the old lists' atoms (set again below for the new lists)
+    for (int e = threadIdx.x; e < ucnt; e += BT) atomicAnd(&nrow[ui[e] >> 5], ~(1u << (ui[e] & 31)));
+    for (int e = threadIdx.x; e < xcnt; e += BT) atomicAnd(&nrow[xi[e] >> 5], ~(1u << (xi[e] & 31)));
     // bitonic sort of (atom, c) by atom: the emission order is arbitrary, the lists are ordered
     for (int k = 2; k <= npow; k <<= 1) {
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
@@ -763,29 +1063,16 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
             __syncthreads();
         }
     }
-    // dual scaling with the inflated correlation bound, r_SAFE^2, test radius (screening.py:115-205)
-    const double lam = P.lam[j], L = P.L;
-    const double sq = P.sq[j], tyv = P.ty[j];
-    const double cinf = (double)__uint_as_float(P.cmax[j]) + P.err_rel * sqrt(sq);
-    const double bound = (cinf == 0.0) ? INFINITY : 1.0 / cinf;
-    const double mu = (sq != 0.0) ? clip(tyv / (lam * sq), bound) : 0.0;
-    double acc = 0.0;
-    for (int n = threadIdx.x; n < P.N; n += BT) {
-        const double v = (sq != 0.0) ? mu * P.theta[(size_t)j * P.ldy + n] : 0.0;
-        const double d = P.Y[(size_t)j * P.ldy + n] / lam - v;
-        acc = fma(d, d, acc);
-    }
-    const double rsq = block_sum(acc, s_sh);
     double rho = NAN;
     if (P.test == DSCR_SAFE) rho = sqrt(rsq);
     else if (P.test == DSCR_DST3) {
-        const double arg = rsq - P.shift_sq[j];
+        const double arg = rsq - shsq;
         if (arg < -RADIUS_GUARD && threadIdx.x == 0) P.status[j] = 3;
         rho = sqrt(fmax(arg, 0.0));
     }
     const double margin = SCREEN_MARGIN + 1e-6;
-    const bool can_screen = (P.test != DSCR_TEST_OFF) && (P.ccmin[j] - rho > margin);
-    double kept = (double)P.kept[j];
+    const bool can_screen = (P.test != DSCR_TEST_OFF) && (ccmin - rho > margin);
+    double kept = (double)kept0;
     if (can_screen) {       // rare: test every active atom of this observation
         double lost = 0.0;
         for (int w = threadIdx.x; w < words; w += BT) {
@@ -801,12 +1088,10 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
             if (keepw != mrow[w]) { lost += __popc(mrow[w] ^ keepw); mrow[w] = keepw; }
         }
         kept -= block_sum(lost, s_sh);
+        __syncthreads();
     }
-    __syncthreads();
     // hot entries in atom order: prox, momentum, ordered compaction into the new lists
-    const double thr = lam / L, beta = P.beta[t];
-    const int* xi = P.xi[par] + lo; const double* xv = P.xv[par] + lo; const int xcnt = P.xc[par][j];
-    const int* ui = P.ui[par] + lo; const double* uv = P.uv[par] + lo; const int ucnt = P.uc[par][j];
+    const double thr = lam / L;
     int nx = 0, nu = 0;
     double pen = 0.0, nnz = 0.0;
     for (int e0 = 0; e0 < cnt; e0 += BT) {
@@ -826,32 +1111,21 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
         int tx, tu;
         const int ox = block_exscan(cand != 0.0 ? 1 : 0, s_scan, &tx);
         const int ou = block_exscan(un != 0.0 ? 1 : 0, s_scan, &tu);
-        if (cand != 0.0 && nx + ox < P.cap) { P.xi[par ^ 1][lo + nx + ox] = i; P.xv[par ^ 1][lo + nx + ox] = cand; }
-        if (un != 0.0 && nu + ou < P.cap) { P.ui[par ^ 1][lo + nu + ou] = i; P.uv[par ^ 1][lo + nu + ou] = un; }
+        const bool wx = cand != 0.0 && nx + ox < P.cap, wu = un != 0.0 && nu + ou < P.cap;
+        if (wx) { P.xi[par ^ 1][lo + nx + ox] = i; P.xv[par ^ 1][lo + nx + ox] = cand; }
+        if (wu) { P.ui[par ^ 1][lo + nu + ou] = i; P.uv[par ^ 1][lo + nu + ou] = un; }
+        if (wx || wu) atomicOr(&nrow[i >> 5], 1u << (i & 31));
         pen += fabs(cand);
         nnz += (cand != 0.0) ? 1.0 : 0.0;
         nx += tx;
         nu += tu;
     }
-    // nonzero bitmap: clear the old lists' atoms, then set the new lists' atoms
-    for (int e = threadIdx.x; e < ucnt; e += BT) atomicAnd(&nrow[ui[e] >> 5], ~(1u << (ui[e] & 31)));
-    for (int e = threadIdx.x; e < xcnt; e += BT) atomicAnd(&nrow[xi[e] >> 5], ~(1u << (xi[e] & 31)));
-    __syncthreads();
-    const int nxc = min(nx, P.cap), nuc = min(nu, P.cap);
-    for (int e = threadIdx.x; e < nuc; e += BT) {
-        const int a = P.ui[par ^ 1][lo + e];
-        atomicOr(&nrow[a >> 5], 1u << (a & 31));
-    }
-    for (int e = threadIdx.x; e < nxc; e += BT) {
-        const int a = P.xi[par ^ 1][lo + e];
-        atomicOr(&nrow[a >> 5], 1u << (a & 31));
-    }
     double v2[2] = {pen, nnz};
     block_sum_n<2>(v2, s_sh);
     if (threadIdx.x == 0) {
         if (hc > P.hcap || nx > P.cap || nu > P.cap) P.status[j] = 4;
-        P.xc[par ^ 1][j] = nxc;
-        P.uc[par ^ 1][j] = nuc;
+        P.xc[par ^ 1][j] = min(nx, P.cap);
+        P.uc[par ^ 1][j] = min(nu, P.cap);
         P.pen[j] = v2[0];
         P.nnz[j] = (int)v2[1];
         P.kept[j] = (int)kept;
@@ -934,13 +1208,28 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
             f2 = fma(qa, qa, f2);
             sq = fma(tn, tn, sq);
             tyv = fma(tn, yn, tyv);
+            rx[q] = yn;                        // keep y and theta for the r_SAFE^2 pass
+            ru[q] = tn;
         }
     }
     for (int n = P.N + threadIdx.x; n < P.ldy; n += BT) write_theta(P, j, n, 0.0);
     double v3[3] = {f2, sq, tyv};
     block_sum_n<3>(v3, s_sh);
+    const double lam = P.lam[j];
+    const double mu0 = (v3[1] != 0.0) ? v3[2] / (lam * v3[1]) : 0.0;
+    double d2 = 0.0;
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) {
+        const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
+        if (n < P.N) {
+            const double d = rx[q] / lam - mu0 * ru[q];
+            d2 = fma(d, d, d2);
+        }
+    }
+    d2 = block_sum(d2, s_sh);
     if (threadIdx.x == 0) {
-        const double lam = P.lam[j];
+        P.mu0[j] = mu0;
+        P.rsq0[j] = d2;
         const double F = 0.5 * v3[0] + lam * P.pen[j];
         P.F[j] = F;
         P.gap[j] = F - 0.5 * P.yy[j] + 0.5 * lam * lam * P.rsq[j];
@@ -985,18 +1274,21 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     auto take = [&](size_t bytes) { size_t o = off; off = bw_align(off + bytes); return base ? base + o : nullptr; };
     const size_t B = d->n_obs, K = d->n_atoms, ly = d->ldy, cap = d->cap;
     BParams p{};
-    p.theta = (double*)take(B * ly * 8);
     p.tb = (__nv_bfloat16*)take((size_t)d->splits * B * ly * 2);
     p.C = (float*)take(B * K * 4);
     p.cc = (float*)take(B * K * 4);
     p.ycorr = (double*)take(B * K * 8);
     p.astar = (double*)take(B * ly * 8);
+    p.Ds = (int8_t*)take((size_t)OZ_SD * K * d->n_rows);
+    p.eD = (int*)take(K * 4);
+    p.Vs = (int8_t*)take((size_t)std::max(OZ_SD, OZ_SV) * B * d->n_rows);
+    p.eV = (int*)take(B * 4);
     p.mask = (uint32_t*)take(B * K / 8);
     for (int q = 0; q < 2; ++q) {
         p.xi[q] = (int*)take(B * cap * 4); p.xv[q] = (double*)take(B * cap * 8); p.xc[q] = (int*)take(B * 4);
         p.ui[q] = (int*)take(B * cap * 4); p.uv[q] = (double*)take(B * cap * 8); p.uc[q] = (int*)take(B * 4);
     }
-    double** dv[] = {&p.sq, &p.ty, &p.yy, &p.lmax, &p.sgn, &p.shift_sq, &p.rsq, &p.radius, &p.F, &p.gap, &p.pen, &p.ccmin};
+    double** dv[] = {&p.sq, &p.ty, &p.mu0, &p.rsq0, &p.yy, &p.lmax, &p.sgn, &p.shift_sq, &p.rsq, &p.radius, &p.F, &p.gap, &p.pen, &p.ccmin};
     for (double** q : dv) *q = (double*)take(B * 8);
     p.anorm = (double*)take(K * 8);
     int** iv[] = {&p.istar, &p.nnz, &p.kept, &p.status};
@@ -1043,6 +1335,12 @@ int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void
     P.Y = d->Y; P.ldy = d->ldy; P.lam = d->lam; P.L = d->L; P.test = d->test;
     P.splits = d->splits; P.cap = d->cap;
     P.fused = d->fused;
+    {   // setup correlations: integer-slice tensor-core products unless DSCR_BATCHED_SETUP=fp64
+        const char* ev = getenv("DSCR_BATCHED_SETUP");
+        const bool fp64 = ev && !strcmp(ev, "fp64");
+        P.oz = (!fp64 && d->n_rows % OZ_BK == 0 && d->n_rows <= 2048 && d->n_obs % OZ_BN == 0 &&
+                d->n_atoms % OZ_BM == 0) ? 1 : 0;
+    }
     // |c~ - c| <= ||d_i|| (||theta - theta~|| + fp32 accumulation) <= err_rel ||theta||
     P.err_rel = (d->splits == 1 ? 0.00391 : 1.6e-5) + 2.0 * d->n_rows * 5.96e-8;
     h->max_iters = d->max_iters;
@@ -1061,9 +1359,28 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
     BParams& P = h->P;
     dim3 g(P.K / DG_T, P.B / DG_T);
     k_bnorms<<<std::max(1, P.K / BW / 4), BT, 0, s>>>(P);
-    k_dgemm_corr<<<g, 256, 0, s>>>(P, P.Y, P.ldy, P.ycorr, 0);                 // D^T y_j (fp64)
-    k_blmax<<<P.B, BT, 0, s>>>(P);
-    if (P.test == DSCR_DST3) k_dgemm_corr<<<g, 256, 0, s>>>(P, P.astar, P.ldy, nullptr, 1);   // cc = y/lam - shift a_*
+    if (P.oz) {   // exact slice products on the integer tensor cores
+        k_slice_rows<<<P.K / 8, 256, 0, s>>>(P.Dt, P.K, P.N, P.ldd, OZ_SD, P.Ds, P.eD);
+        k_slice_rows<<<P.B / 8, 256, 0, s>>>(P.Y, P.B, P.N, P.ldy, OZ_SV, P.Vs, P.eV);
+        OzArgs oa{};
+        oa.eA = P.eD; oa.eB = P.eV; oa.mode = 0; oa.out = P.ycorr; oa.ldo = P.K;
+        int rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, OZ_SV, P.N, oa, s);   // D^T y_j
+        if (rc) return rc;
+        k_blmax<<<P.B, BT, 0, s>>>(P);
+        if (P.test == DSCR_DST3) {   // cc = y/lam - shift a_* (a_* = dictionary row: exact slices)
+            k_gather_slices<<<P.B, 256, 0, s>>>(P.Ds, P.eD, P.K, P.N, OZ_SD, P.istar, P.B, P.Vs, P.eV);
+            OzArgs ob{};
+            ob.eA = P.eD; ob.eB = P.eV; ob.mode = 1;
+            ob.ycorr = P.ycorr; ob.lam = P.lam; ob.lmax = P.lmax; ob.anorm = P.anorm; ob.sgn = P.sgn;
+            ob.istar = P.istar; ob.cc = P.cc;
+            rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, OZ_SD, P.N, ob, s);
+            if (rc) return rc;
+        }
+    } else {
+        k_dgemm_corr<<<g, 256, 0, s>>>(P, P.Y, P.ldy, P.ycorr, 0);                 // D^T y_j (fp64)
+        k_blmax<<<P.B, BT, 0, s>>>(P);
+        if (P.test == DSCR_DST3) k_dgemm_corr<<<g, 256, 0, s>>>(P, P.astar, P.ldy, nullptr, 1);   // cc = y/lam - shift a_*
+    }
     if (P.test != DSCR_TEST_OFF) k_bcc<<<P.B, BT, 0, s>>>(P);
     k_binit<<<P.B, BT, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
@@ -1159,6 +1476,48 @@ int dscr_batched_destroy(dscr_batched* h) {
 }
 
 }  // extern "C"
+
+static size_t oz_work_layout(int K, int N, int B, int8_t** Ds, int** eD, int8_t** Vs, int** eV, char* base) {
+    size_t off = 0;
+    auto take = [&](size_t bytes) { size_t o = off; off = bw_align(off + bytes); return base ? base + o : nullptr; };
+    int8_t* a = (int8_t*)take((size_t)OZ_SD * K * N);
+    int* b = (int*)take((size_t)K * 4);
+    int8_t* c = (int8_t*)take((size_t)OZ_SV * B * N);
+    int* d = (int*)take((size_t)B * 4);
+    if (Ds) { *Ds = a; *eD = b; *Vs = c; *eV = d; }
+    return off;
+}
+
+extern "C" size_t dscr_corr_exact_work_size(int n_atoms, int n_rows, int n_obs) {
+    if (n_atoms <= 0 || n_rows <= 0 || n_obs <= 0) return 0;
+    return oz_work_layout(n_atoms, n_rows, n_obs, nullptr, nullptr, nullptr, nullptr, nullptr);
+}
+
+extern "C" int dscr_corr_exact_bf16(const void* Dt, int n_atoms, int n_rows, int ldd, const double* V, int n_obs,
+                                    int ldv, double* out, int ldo, void* work, size_t work_bytes, void* stream) {
+    if (!Dt || !V || !out || !work || ldd < n_rows || ldv < n_rows || ldo < n_atoms) {
+        err_store() = "exact correlation: null pointer or bad leading dimension";
+        return DSCR_EINVAL;
+    }
+    if (n_atoms % OZ_BM || n_obs % OZ_BN || n_rows % OZ_BK || n_rows > 2048) {
+        err_store() = "exact correlation: need atoms, observations, rows multiples of 128 and rows <= 2048";
+        return DSCR_EINVAL;
+    }
+    if (work_bytes < dscr_corr_exact_work_size(n_atoms, n_rows, n_obs) || ((uintptr_t)work & 255)) {
+        err_store() = "exact correlation: workspace too small or not 256-byte aligned";
+        return DSCR_EINVAL;
+    }
+    cudaStream_t s = (cudaStream_t)stream;
+    int8_t *Ds, *Vs;
+    int *eD, *eV;
+    oz_work_layout(n_atoms, n_rows, n_obs, &Ds, &eD, &Vs, &eV, (char*)work);
+    using namespace dscr::batched;
+    k_slice_rows<<<(n_atoms + 7) / 8, 256, 0, s>>>((const __nv_bfloat16*)Dt, n_atoms, n_rows, ldd, OZ_SD, Ds, eD);
+    k_slice_rows<<<(n_obs + 7) / 8, 256, 0, s>>>(V, n_obs, n_rows, ldv, OZ_SV, Vs, eV);
+    OzArgs g{};
+    g.eA = eD; g.eB = eV; g.mode = 0; g.out = out; g.ldo = ldo;
+    return ozaki_launch(Ds, n_atoms, OZ_SD, Vs, n_obs, OZ_SV, n_rows, g, s);
+}
 
 extern "C" int dscr_batched_gemm_bf16(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K,
                                       int splits, float* C, int ldc, void* stream) {

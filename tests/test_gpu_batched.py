@@ -54,6 +54,88 @@ def test_gemm_c5_shape_throughput():
     assert tflops > 200
 
 
+def _corr_exact(Dt, V):
+    L = nat.lib()
+    K, N = Dt.shape
+    B = V.shape[0]
+    out = torch.empty((B, K), dtype=torch.float64, device=Dt.device)
+    ws = L.dscr_corr_exact_work_size(K, N, B)
+    work = torch.empty(ws, dtype=torch.uint8, device=Dt.device)
+    nat.check(L.dscr_corr_exact_bf16(Dt.data_ptr(), K, N, N, V.data_ptr(), B, N, out.data_ptr(), K,
+                                     work.data_ptr(), ws, nat.stream_ptr()))
+    return out
+
+
+def _slices(X, S):
+    """Row scale 2^e (max|x| < 2^e) and S truncated 7-bit slices: x = 2^e sum_s q_s 2^-7(s+1)."""
+    m = np.abs(X).max(axis=1)
+    e = np.zeros(len(X), dtype=np.int64)
+    nz = m > 0
+    e[nz] = np.frexp(m[nz])[1]
+    x = np.ldexp(X, -e[:, None])
+    qs = []
+    for _ in range(S):
+        x = x * 128.0
+        q = np.trunc(x)
+        x = x - q
+        qs.append(q)
+    return qs, e
+
+
+def _slice_emulation(D, V, S=4, T=5, dmax=5):
+    """numpy restatement of the integer-slice correlation (same fp64 combination order)."""
+    Ds, eD = _slices(D, S)
+    Vs, eV = _slices(V, T)
+    acc = np.zeros((V.shape[0], D.shape[0]))
+    for d in range(dmax + 1):
+        C = np.zeros_like(acc)
+        for s_ in range(S):
+            t = d - s_
+            if 0 <= t < T:
+                C += Vs[t] @ Ds[s_].T          # exact: integers < 2^53
+        acc = acc + C * 2.0 ** (-7 * d)
+    return np.ldexp(acc, eD[None, :] + eV[:, None] - 14), eD, eV
+
+
+@pytest.mark.parametrize("K,N,B,hard", [(128, 128, 128, True), (384, 256, 256, True), (1024, 1024, 512, False),
+                                        (256, 2048, 128, True)])
+def test_corr_exact_matches_fp64(K, N, B, hard):
+    """Integer-slice tensor-core correlations: bit-identical to the numpy restatement of the
+    slice algorithm, and within its rigorous error bound of fp64 (fp32 GEMM: ~2^-13)."""
+    rng = np.random.default_rng(K + N + B)
+    D = rng.standard_normal((K, N))
+    V = rng.standard_normal((B, N))
+    if hard:
+        D *= np.exp(rng.uniform(-6, 6, size=(K, 1)))         # per-atom scales
+        D[:, ::7] *= 1e-5                                     # entries below 2^-21 of the row max: truncated
+        D[1] = 0.0                                            # empty atom
+        V *= np.exp(rng.uniform(-20, 20, size=(B, 1)))
+        V[:, ::5] *= 1e-7
+        V[2] = 0.0
+    Dt = torch.from_numpy(D).to(torch.bfloat16).cuda()
+    out = _corr_exact(Dt, torch.from_numpy(V).cuda()).cpu().numpy()
+    Dh = Dt.double().cpu().numpy()
+    emu, eD, eV = _slice_emulation(Dh, V)
+    assert np.array_equal(out, emu)
+    ref = V @ Dh.T
+    # |err| <= 2^(E_i - 28) ||v_j||_1 + 2^(F_j - 35) ||d_i||_1 (+ dropped pairs, fp64 rounding)
+    bound = (np.ldexp(1.0, eD - 28)[None, :] * np.abs(V).sum(1)[:, None]
+             + np.ldexp(1.0, eV - 35)[:, None] * np.abs(Dh).sum(1)[None, :])
+    err = np.abs(out - ref)
+    assert np.all(err <= 1.01 * bound + 1e-12 * np.abs(ref) + 1e-300)
+    if hard:
+        assert np.all(out[2] == 0.0) and np.all(out[:, 1] == 0.0)
+    else:   # unit-scale Gaussian dictionary (every bf16 entry sliced exactly): ~fp64 accuracy
+        rel = err / (np.abs(V) @ np.abs(Dh).T)
+        assert rel.max() < 2.0 ** -30, rel.max()
+
+
+def test_corr_exact_rejects_bad_shapes():
+    L = nat.lib()
+    assert L.dscr_corr_exact_bf16(None, 128, 128, 128, None, 128, 128, None, 128, None, 0, None) == nat.DSCR_EINVAL
+    assert L.dscr_corr_exact_work_size(0, 128, 128) == 0
+
+
 # ---------------------------------------------------------------- batched solver vs oracle
 
 import paper_1412_4080_b200 as ds  # noqa: E402
@@ -120,3 +202,18 @@ def test_fused_epilogue_matches_dense_update(ratio):
         np.testing.assert_allclose(a.x_val[j], b.x_val[j], rtol=1e-13, atol=1e-15)
     if ratio > 0.5:
         assert a.kept.min() < 2048
+
+
+@pytest.mark.parametrize("ratio", [0.4, 0.85])
+def test_integer_slice_setup_matches_fp64_setup(ratio, monkeypatch):
+    """Setup correlations on the integer tensor cores (default) vs the fp64 FMA path: same
+    screening decisions, support and trace (centres differ by < 2^-30, far inside the test slack)."""
+    w, dic, D64, L = _batch_problem(256, 2048, 512, ratio, seed=5)
+    a = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    monkeypatch.setenv("DSCR_BATCHED_SETUP", "fp64")
+    b = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    assert np.array_equal(a.kept, b.kept) and np.array_equal(a.nnz, b.nnz)
+    np.testing.assert_allclose(a.objective, b.objective, rtol=1e-12)
+    np.testing.assert_allclose(a.gap, b.gap, rtol=1e-9, atol=1e-12)
+    for j in range(0, 512, 41):
+        assert np.array_equal(a.x_idx[j], b.x_idx[j])
