@@ -612,8 +612,9 @@ def run_c5(args):
             r = solve_batched(dic, w.y, w.lam, L, iterations=iters, test="dst3", splits=args.splits)
         torch.cuda.synchronize()
         es = (time.perf_counter() - t0) / args.steps
-        e2e = {"value": world * iters / es, "unit": "iters/s", "h2d_bytes_per_step": int(w.D.nbytes + b * n * 8 + b * 8),
-               "d2h_bytes_per_step": int(b * (1024 * 12 + 64)), "seconds_per_step": es}
+        e2e = {"value": world * iters / es, "unit": "iters/s",
+               "h2d_bytes_per_step": int(dic.data.nbytes + w.y.nbytes + w.lam.nbytes),
+               "d2h_bytes_per_step": int(r.d2h_bytes), "seconds_per_step": es}
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         from oracle import screen_oracle as so

@@ -45,9 +45,24 @@ class BatchedResult:
     lambda_max: np.ndarray
     radius: np.ndarray
     trace: np.ndarray            # [iterations][4]: sum F, sum gap, sum nnz, sum kept
-    x_idx: list
-    x_val: list
+    x_ptr: np.ndarray            # CSR over observations: x_j = (x_indices, x_values)[x_ptr[j]:x_ptr[j+1]]
+    x_indices: np.ndarray
+    x_values: np.ndarray
     device_seconds: float = float("nan")
+    d2h_bytes: int = 0           # bytes copied device -> host by result()
+
+    @property
+    def x_idx(self):
+        """Per-observation support (sorted atom indices), split from the CSR arrays on first use."""
+        if not hasattr(self, "_x_idx"):
+            self._x_idx = np.split(self.x_indices, self.x_ptr[1:-1])
+        return self._x_idx
+
+    @property
+    def x_val(self):
+        if not hasattr(self, "_x_val"):
+            self._x_val = np.split(self.x_values, self.x_ptr[1:-1])
+        return self._x_val
 
     def x_dense(self, j, k):
         out = np.zeros(k)
@@ -77,10 +92,15 @@ class BatchedEngine:
         self.iterations, self.cap = int(iterations), int(cap)
         self.Dt = dictionary.device_data(self.device)                      # (K, ldd) bf16 bits
         ldy = (n + 63) // 64 * 64
-        yh = np.zeros((b, ldy))
-        yh[:, :n] = Y.T
-        self.Yd = torch.from_numpy(yh).to(self.device)
+        # upload Y as given (n x b) and transpose on the device into observation rows [b][ldy]
+        Yh = torch.from_numpy(Y.T if Y.flags.f_contiguous else np.ascontiguousarray(Y))
+        self.Yd = torch.zeros((b, ldy), dtype=torch.float64, device=self.device)
+        if Y.flags.f_contiguous:
+            self.Yd[:, :n].copy_(Yh.to(self.device))
+        else:
+            self.Yd[:, :n].copy_(Yh.to(self.device).T)
         self.lamd = torch.from_numpy(lam.copy()).to(self.device)
+        self.h2d_bytes = int(Y.nbytes + lam.nbytes)
         self.betas = fista_betas(self.iterations)
         d = nat.BatchedDesc()
         d.n_rows, d.n_atoms, d.n_obs, d.ldd = n, self.k, b, dictionary.ldd
@@ -113,33 +133,34 @@ class BatchedEngine:
         return self.ws[off: off + count * isz].view(dtype)
 
     def result(self, device_seconds=float("nan")):
+        """Copy the solution back: device-side CSR compaction of the x lists, then a few
+        packed transfers (self.d2h_bytes counts them)."""
         torch = self.torch
-        self.stream.synchronize()
-        b, bf = self.b, self.bufs
+        b, bf, cap = self.b, self.bufs, self.cap
         par = self.iterations & 1
-        cnt = self._view(bf.x_cnt[par], b, torch.int32).cpu().numpy()
-        idx = self._view(bf.x_idx[par], b * self.cap, torch.int32).cpu().numpy().reshape(b, self.cap)
-        val = self._view(bf.x_val[par], b * self.cap, torch.float64).cpu().numpy().reshape(b, self.cap)
-        its = int(self._view(bf.iterations, 1, torch.int32).cpu().item())
-        status = self._view(bf.status, b, torch.int32).cpu().numpy()
+        cnt = self._view(bf.x_cnt[par], b, torch.int32)
+        live = torch.arange(cap, device=self.device, dtype=torch.int32)[None, :] < cnt[:, None]
+        idx = self._view(bf.x_idx[par], b * cap, torch.int32).view(b, cap)[live].cpu().numpy()
+        val = self._view(bf.x_val[par], b * cap, torch.float64).view(b, cap)[live].cpu().numpy()
+        f64 = torch.stack([self._view(p, b, torch.float64) for p in (bf.F, bf.gap, bf.lmax, bf.radius)]).cpu().numpy()
+        i32 = torch.cat([self._view(p, b, torch.int32) for p in (bf.nnz, bf.kept, bf.status, bf.x_cnt[par])]
+                        + [self._view(bf.iterations, 1, torch.int32)]).cpu().numpy()
+        trace = self._view(bf.trace, self.iterations * 4, torch.float64).cpu().numpy().reshape(-1, 4)
+        self.d2h_bytes = int(idx.nbytes + val.nbytes + f64.nbytes + i32.nbytes + trace.nbytes)
+        nnz, kept, status, counts = (i32[q * b:(q + 1) * b] for q in range(4))
         if np.any(status >= 3):
             bad = np.flatnonzero(status >= 3)
             code = int(status[bad[0]])
             raise RuntimeError(f"batched solve failed on {bad.size} observations (status {code}: "
                                f"{'radius guard' if code == 3 else 'nonzero capacity exceeded'})")
+        ptr = np.zeros(b + 1, dtype=np.int64)
+        np.cumsum(counts, out=ptr[1:])
         return BatchedResult(
-            iterations=its,
-            objective=self._view(bf.F, b, torch.float64).cpu().numpy(),
-            gap=self._view(bf.gap, b, torch.float64).cpu().numpy(),
-            nnz=self._view(bf.nnz, b, torch.int32).cpu().numpy(),
-            kept=self._view(bf.kept, b, torch.int32).cpu().numpy(),
-            status=status,
-            lambda_max=self._view(bf.lmax, b, torch.float64).cpu().numpy(),
-            radius=self._view(bf.radius, b, torch.float64).cpu().numpy(),
-            trace=self._view(bf.trace, self.iterations * 4, torch.float64).cpu().numpy().reshape(-1, 4),
-            x_idx=[idx[j, : cnt[j]].astype(np.int64) for j in range(b)],
-            x_val=[val[j, : cnt[j]].copy() for j in range(b)],
-            device_seconds=device_seconds,
+            iterations=int(i32[4 * b]),
+            objective=f64[0], gap=f64[1], nnz=nnz, kept=kept, status=status,
+            lambda_max=f64[2], radius=f64[3], trace=trace,
+            x_ptr=ptr, x_indices=idx.astype(np.int64), x_values=val,
+            device_seconds=device_seconds, d2h_bytes=self.d2h_bytes,
         )
 
     def close(self):
