@@ -705,11 +705,47 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
 // ---------------------------------------------------------------------------
 
 constexpr int K3_CHUNK = 128;
+constexpr int K3_WIN = 256;     // slot offsets staged in shared memory per chunk
+
+// slot of flat entry f (last s with off[s] <= f), one warp: 32-ary search, ~log32(G) rounds
+__device__ __forceinline__ int warp_find_slot(const int* off, int G, int f, int lane) {
+    int lo = 0, hi = G;   // off[lo] <= f < off[hi]
+    while (hi - lo > 1) {
+        const int span = hi - lo;
+        const int probe = lo + (int)(((long long)span * lane) / 32);
+        const bool le = (lane == 0) || (probe > lo && off[probe] <= f);
+        const unsigned bal = __ballot_sync(0xffffffffu, le);
+        const int l = 31 - __clz(bal);                        // last lane whose probe is <= f
+        const int nlo = lo + (int)(((long long)span * l) / 32);
+        const int nhi = (l == 31) ? hi : lo + (int)(((long long)span * (l + 1)) / 32);
+        lo = max(nlo, lo);
+        hi = max(nhi, lo + 1);
+    }
+    return lo;
+}
+
+template <typename T>
+__device__ __forceinline__ void k3a_acc(const typename Vec<T>::Raw (&d)[4], const double* sa, const double* sb,
+                                        double* acc_a, double* acc_b) {
+    constexpr int V = Vec<T>::V;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const double a = sa[q], bb = sb[q];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const double x = Vec<T>::get(d[q], v);
+            acc_a[v] = fma(a, x, acc_a[v]);
+            acc_b[v] = fma(bb, x, acc_b[v]);
+        }
+    }
+}
 
 template <typename T>
 __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     __shared__ int s_idx[K3_CHUNK];
     __shared__ double s_a[K3_CHUNK], s_b[K3_CHUNK];
+    __shared__ int s_off[K3_WIN];
+    __shared__ int s_s0;
     dscr_scalars* sc = P.sc;
     const bool fix = (sc->mode == MODE_FIXUP);
     const int pe = sc->p_eff;
@@ -728,9 +764,25 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     for (int c0 = lo; c0 < hi; c0 += K3_CHUNK) {
         const int cn = min(K3_CHUNK, hi - c0);
         __syncthreads();
+        if (threadIdx.x < 32) {
+            const int s0 = warp_find_slot(off, P.G, c0, threadIdx.x);
+            if (threadIdx.x == 0) s_s0 = s0;
+        }
+        __syncthreads();
+        const int s0 = s_s0;
+        for (int i = threadIdx.x; i < K3_WIN; i += NT) s_off[i] = (s0 + i <= P.G) ? off[s0 + i] : INT_MAX;
+        __syncthreads();
+        const int wend = s_off[K3_WIN - 1];
         for (int i = threadIdx.x; i < cn; i += NT) {
             const int f = c0 + i;
-            const int s = find_slot(off, P.G, f);
+            int s;
+            if (f < wend) {   // last window slot with offset <= f
+                int a = 0, b = K3_WIN - 1;
+                while (b - a > 1) { const int m = (a + b) >> 1; if (s_off[m] <= f) a = m; else b = m; }
+                s = s0 + a;
+            } else {
+                s = find_slot(off, P.G, f);
+            }
             const size_t e = (size_t)s * P.sup_cap + (f - off[s]);
             int idx = P.sidx[e];
             double a = P.sa[e], bb = P.sb[e];
@@ -744,29 +796,35 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
         }
         __syncthreads();
         if (rows_ok) {
-            int i = 0;
-            for (; i + 4 <= cn; i += 4) {
-                double d[4][V];
+            // groups of 4 columns, next group's loads in flight while this group accumulates
+            const int ng = cn / 4;
+            typename Vec<T>::Raw d0[4], d1[4];
+            if (ng > 0) {
 #pragma unroll
-                for (int q = 0; q < 4; ++q) Vec<T>::load(D + (size_t)s_idx[i + q] * P.ldd + r0, d[q], pol);
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const double a = s_a[i + q], bb = s_b[i + q];
-#pragma unroll
-                    for (int v = 0; v < V; ++v) {
-                        acc_a[v] = fma(a, d[q][v], acc_a[v]);
-                        acc_b[v] = fma(bb, d[q][v], acc_b[v]);
-                    }
-                }
+                for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[q] * P.ldd + r0, d0[q], pol);
             }
-            for (; i < cn; ++i) {
-                double d[V];
-                Vec<T>::load(D + (size_t)s_idx[i] * P.ldd + r0, d, pol);
+            int g = 0;
+            for (; g + 2 <= ng; g += 2) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[4 * g + 4 + q] * P.ldd + r0, d1[q], pol);
+                k3a_acc<T>(d0, s_a + 4 * g, s_b + 4 * g, acc_a, acc_b);
+                if (g + 2 < ng) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q)
+                        Vec<T>::load_raw(D + (size_t)s_idx[4 * g + 8 + q] * P.ldd + r0, d0[q], pol);
+                }
+                k3a_acc<T>(d1, s_a + 4 * g + 4, s_b + 4 * g + 4, acc_a, acc_b);
+            }
+            if (g < ng) k3a_acc<T>(d0, s_a + 4 * g, s_b + 4 * g, acc_a, acc_b);   // odd group count
+            for (int i = 4 * ng; i < cn; ++i) {
+                typename Vec<T>::Raw d;
+                Vec<T>::load_raw(D + (size_t)s_idx[i] * P.ldd + r0, d, pol);
                 const double a = s_a[i], bb = s_b[i];
 #pragma unroll
                 for (int v = 0; v < V; ++v) {
-                    acc_a[v] = fma(a, d[v], acc_a[v]);
-                    acc_b[v] = fma(bb, d[v], acc_b[v]);
+                    const double x = Vec<T>::get(d, v);
+                    acc_a[v] = fma(a, x, acc_a[v]);
+                    acc_b[v] = fma(bb, x, acc_b[v]);
                 }
             }
         }
@@ -1493,6 +1551,19 @@ static int pers_occupancy(int dtype, bool group, int smem) {
     return pers_occ_t<__nv_bfloat16>(group, smem);
 }
 
+template <typename T>
+static int k3a_occ_t() {
+    int n = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k3a_residual<T>, NT, 0);
+    return std::max(1, n);
+}
+
+static int k3a_occupancy(int dtype) {
+    if (dtype == DSCR_F64) return k3a_occ_t<double>();
+    if (dtype == DSCR_F32) return k3a_occ_t<float>();
+    return k3a_occ_t<__nv_bfloat16>();
+}
+
 static int k1_occupancy(int dtype, bool group, int smem) {
     if (dtype == DSCR_F64) return k1_occ_t<double>(group, smem);
     if (dtype == DSCR_F32) return k1_occ_t<float>(group, smem);
@@ -1518,7 +1589,7 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     const int V = 32 / dtype_size(pr->dtype);   // Vec<T>::V (32-byte loads)
     g.TR = NT * V;
     g.R = (pr->n_rows + g.TR - 1) / g.TR;
-    g.P = std::max(1, (sms * 4) / g.R);
+    g.P = std::max(1, (sms * k3a_occupancy(pr->dtype)) / g.R);   // (row tile x split) CTAs: one wave
     g.G3b = (pr->n_rows + K3B_ROWS - 1) / K3B_ROWS;
     return g;
 }

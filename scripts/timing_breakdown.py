@@ -1,6 +1,6 @@
 """In-graph per-kernel timing of one solve from the engine's %globaltimer stamps.
 
-    python scripts/timing_breakdown.py c1|c2|c3|c4proxy
+    python scripts/timing_breakdown.py c1|c2|c3|c4|c4proxy
 """
 import sys
 
@@ -22,6 +22,8 @@ def workload(name):
         return wl.config2(ratio=0.5)
     if name == "c3":
         return wl.config3()
+    if name == "c4":
+        return wl.config4()
     D = wl.gaussian_dictionary_f32(1024, 32768, 0)
     y = wl.gaussian_observation(1024, 0)
     lam = 0.2 * float(np.max(np.abs(D.astype(np.float64).T @ y)))
@@ -49,6 +51,7 @@ for rep in range(3):
     b = eng.bufs
     trips = min(sc.trips, b.max_kts)
     ts = eng.view(b.kts, trips * 8, torch.int64).cpu().numpy().reshape(trips, 8).astype(np.float64)
+    rows = eng.trace_rows(sc.t)
     eng.close()
 t = sc.t
 setup_ms = ev0.elapsed_time(ev1)
@@ -64,3 +67,10 @@ print(f"{name}: {t} iterations, {sc.trips} trips, setup {setup_ms:.3f} ms, loop 
       f"= {1e3 * loop_ms / max(t, 1):.2f} us/iteration")
 for k, v in cols.items():
     print(f"  {k:14s} median {np.nanmedian(v) / 1e3:8.2f} us   mean {np.nanmean(v) / 1e3:8.2f} us")
+from paper_1412_4080_b200 import _native as nat  # noqa: E402
+sup = rows[:, nat.TR_SUPPORT].astype(np.float64)
+elem = {"f64": 8, "f32": 4, "bf16": 2}[w.dtype]
+k3a = (d[:, 6] - d[:, 4]) / 1e9
+print(f"  support (x or u nonzero) median {np.median(sup):.0f}, final nnz {int(rows[-1, nat.TR_NNZ])}, "
+      f"kept {int(rows[-1, nat.TR_KEPT])}; K3a reads {np.median(sup) * w.D.shape[0] * elem / 1e6:.1f} MB "
+      f"-> {np.median(sup[1:len(k3a) + 1] * w.D.shape[0] * elem / k3a) / 1e9:.0f} GB/s")
