@@ -216,6 +216,14 @@ int dscr_test_group(const double* w, const double* cnorm, const double* snorm,
                     void* stream);
 /* Largest singular value of D by 2-vector block power iteration (dictionary.py:120-171);
  * blocking; `work` must hold dscr_operator_norm_work_size() bytes of device memory. */
+/* Spectral norms of column groups of D (GroupPartition.build, dictionary.py:120-160 per group):
+ * group g = columns group_cols[group_ptr[g] .. group_ptr[g+1]) (device arrays).  One kernel for
+ * all groups: fp64 Gram per group + the 2-vector block power iteration of dscr_operator_norm on
+ * it.  out[g] (device) = ||D_g||_2, or -1 for groups of more than 32 columns or more columns
+ * than rows (use dscr_operator_norm on those). */
+int dscr_group_spectral_norms(int dtype, const void* D, int ldd, int n_rows, int n_groups, const int32_t* group_ptr,
+                              const int32_t* group_cols, double tol, int max_iters, double* out, void* stream);
+
 size_t dscr_operator_norm_work_size(int ldd, int k);
 int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double tol, int max_iters,
                        void* work, double* out_host, void* stream);

@@ -9,8 +9,8 @@ device is missing.
 """
 
 from .instrument import DYNAMIC, NONE, STATIC, STRATEGIES, SolveTrace, flops_iteration, flops_static_init
-from .problem import (GROUP, LASSO, Dictionary, GroupPartition, LambdaMax, Problem, expand, index_set,
-                      operator_norm, spectral_norm)
+from .problem import (GROUP, LASSO, Dictionary, GroupPartition, LambdaMax, Problem, expand, group_spectral_norms,
+                      index_set, operator_norm, spectral_norm)
 from .solver import (ALGORITHMS, CP, DOME, DST3, FISTA, GROUP_TESTS, GSAFE, GST3, ISTA, LASSO_TESTS, SAFE,
                      SPARSA, TWIST, DeviceContext, IterationInfo, ScreenState, SolveResult, SolverConfig, run)
 from .ops import (lambda_max, prox_group, prox_l1, screen_update, test_dome, test_sphere_group,

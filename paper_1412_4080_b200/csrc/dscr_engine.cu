@@ -518,11 +518,61 @@ __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* s
     return false;
 }
 
+// Flat index -> slot of a segmented list (slot s holds entries [off[s], off[s+1])).
+// A CTA stages a window of K3_WIN consecutive slot offsets in shared memory, starting at
+// the slot of its first entry (one warp, 32-ary search), and resolves entries inside the
+// window with a shared-memory search; entries past the window fall back to find_slot.
+constexpr int K3_WIN = 256;
+
+
+// slot of flat entry f (last s with off[s] <= f), one warp: 32-ary search, ~log32(G) rounds
+__device__ __forceinline__ int warp_find_slot(const int* off, int G, int f, int lane) {
+    int lo = 0, hi = G;   // off[lo] <= f < off[hi]
+    while (hi - lo > 1) {
+        const int span = hi - lo;
+        const int probe = lo + (int)(((long long)span * lane) / 32);
+        const bool le = (lane == 0) || (probe > lo && off[probe] <= f);
+        const unsigned bal = __ballot_sync(0xffffffffu, le);
+        const int l = 31 - __clz(bal);                        // last lane whose probe is <= f
+        const int nlo = lo + (int)(((long long)span * l) / 32);
+        const int nhi = (l == 31) ? hi : lo + (int)(((long long)span * (l + 1)) / 32);
+        lo = max(nlo, lo);
+        hi = max(nhi, lo + 1);
+    }
+    return lo;
+}
+
+// all threads: stage the window starting at the slot of flat entry f0; returns the window end
+__device__ __forceinline__ int stage_window(const int* off, int G, int f0, int* s_off, int* s_s0) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int s0 = warp_find_slot(off, G, f0, threadIdx.x);
+        if (threadIdx.x == 0) *s_s0 = s0;
+    }
+    __syncthreads();
+    const int s0 = *s_s0;
+    for (int i = threadIdx.x; i < K3_WIN; i += NT) s_off[i] = (s0 + i <= G) ? off[s0 + i] : INT_MAX;
+    __syncthreads();
+    return s_off[K3_WIN - 1];
+}
+
+__device__ __forceinline__ int window_slot(const int* off, int G, const int* s_off, int s0, int wend, int f) {
+    if (f >= wend) return find_slot(off, G, f);
+    int a = 0, b = K3_WIN - 1;   // s_off[a] <= f < s_off[b]
+    while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (s_off[m] <= f) a = m; else b = m;
+    }
+    return s0 + a;
+}
+
 // K2 per-CTA work: test, compaction into slot b, vectors, support list, partials
 template <bool GROUP>
 __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     __shared__ int s_scan[2 * NW + 1];
     __shared__ double s_sh[64];
+    __shared__ int s_off[K3_WIN];
+    __shared__ int s_s0;
     dscr_scalars* sc = P.sc;
     const bool static_mode = (sc->mode == MODE_STATIC);
     const int p = sc->parity, xi = sc->xi;
@@ -544,12 +594,14 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
 
     int n_keep = 0, n_sup = 0;
     double pen = 0.0, nnz = 0.0, kept_atoms = 0.0, ssr = 0.0, dropped = 0.0;
+    int wend = INT_MIN;
     for (int base = lo; base < hi; base += NT) {
+        if (base >= wend) wend = stage_window(off, P.G, base, s_off, &s_s0);   // uniform
         const int f = base + threadIdx.x;
         const bool valid = f < hi;
         int unit = -1;
         if (valid) {
-            const int s = find_slot(off, P.G, f);
+            const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
             unit = act[s * P.cap + (f - off[s])];
         }
         const bool masked = valid && test_on && unit_test(P, sc, unit);
@@ -705,25 +757,6 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
 // ---------------------------------------------------------------------------
 
 constexpr int K3_CHUNK = 128;
-constexpr int K3_WIN = 256;     // slot offsets staged in shared memory per chunk
-
-// slot of flat entry f (last s with off[s] <= f), one warp: 32-ary search, ~log32(G) rounds
-__device__ __forceinline__ int warp_find_slot(const int* off, int G, int f, int lane) {
-    int lo = 0, hi = G;   // off[lo] <= f < off[hi]
-    while (hi - lo > 1) {
-        const int span = hi - lo;
-        const int probe = lo + (int)(((long long)span * lane) / 32);
-        const bool le = (lane == 0) || (probe > lo && off[probe] <= f);
-        const unsigned bal = __ballot_sync(0xffffffffu, le);
-        const int l = 31 - __clz(bal);                        // last lane whose probe is <= f
-        const int nlo = lo + (int)(((long long)span * l) / 32);
-        const int nhi = (l == 31) ? hi : lo + (int)(((long long)span * (l + 1)) / 32);
-        lo = max(nlo, lo);
-        hi = max(nhi, lo + 1);
-    }
-    return lo;
-}
-
 template <typename T>
 __device__ __forceinline__ void k3a_acc(const typename Vec<T>::Raw (&d)[4], const double* sa, const double* sb,
                                         double* acc_a, double* acc_b) {
@@ -763,26 +796,10 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     const int* off = P.sup_off;
     for (int c0 = lo; c0 < hi; c0 += K3_CHUNK) {
         const int cn = min(K3_CHUNK, hi - c0);
-        __syncthreads();
-        if (threadIdx.x < 32) {
-            const int s0 = warp_find_slot(off, P.G, c0, threadIdx.x);
-            if (threadIdx.x == 0) s_s0 = s0;
-        }
-        __syncthreads();
-        const int s0 = s_s0;
-        for (int i = threadIdx.x; i < K3_WIN; i += NT) s_off[i] = (s0 + i <= P.G) ? off[s0 + i] : INT_MAX;
-        __syncthreads();
-        const int wend = s_off[K3_WIN - 1];
+        const int wend = stage_window(off, P.G, c0, s_off, &s_s0);
         for (int i = threadIdx.x; i < cn; i += NT) {
             const int f = c0 + i;
-            int s;
-            if (f < wend) {   // last window slot with offset <= f
-                int a = 0, b = K3_WIN - 1;
-                while (b - a > 1) { const int m = (a + b) >> 1; if (s_off[m] <= f) a = m; else b = m; }
-                s = s0 + a;
-            } else {
-                s = find_slot(off, P.G, f);
-            }
+            const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
             const size_t e = (size_t)s * P.sup_cap + (f - off[s]);
             int idx = P.sidx[e];
             double a = P.sa[e], bb = P.sb[e];

@@ -257,6 +257,112 @@ static size_t apply_part_bytes(int dt, int ldd, int k) {
     return (size_t)apply_splits(k, ldd, V) * 2 * ldd * sizeof(double);
 }
 
+// Spectral norms of many small column groups at once (GroupPartition.build,
+// dictionary.py:120-160 _power_top_eig per group): one CTA per group forms the m x m
+// Gram D_g^T D_g in fp64 (columns staged through shared memory, fixed-order sums), then
+// one warp runs the reference's 2-vector block power iteration on it (start block
+// [ones, alternating] orthonormalised, Rayleigh 2 x 2 top eigenvalue, stop when stable to
+// tol * max(1, value), basis-axis restart if the block falls into the null space).
+// Groups with m > GN_MAXM or m > n get -1 (the host runs the general path for them).
+constexpr int GN_MAXM = 32, GN_ROWS = 64, GN_PAIRS = 3;   // 3 x 256 >= 32 * 33 / 2
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_group_norms(const T* D, int ldd, int n, int ng, const int* gptr,
+                                                     const int* gcols, double tol, int max_iters, double* out) {
+    __shared__ double sX[GN_ROWS][GN_MAXM + 1];
+    __shared__ double sG[GN_MAXM][GN_MAXM + 1];
+    __shared__ int scol[GN_MAXM];
+    const int g = blockIdx.x;
+    if (g >= ng) return;
+    const int c0 = gptr[g], m = gptr[g + 1] - c0;
+    if (m < 1 || m > GN_MAXM || m > n) {
+        if (threadIdx.x == 0) out[g] = -1.0;
+        return;
+    }
+    if (threadIdx.x < m) scol[threadIdx.x] = gcols[c0 + threadIdx.x];
+    const int npairs = m * (m + 1) / 2;
+    int pk[GN_PAIRS], pl[GN_PAIRS];
+    double acc[GN_PAIRS];
+#pragma unroll
+    for (int q = 0; q < GN_PAIRS; ++q) {
+        int e = threadIdx.x + q * NT, k = 0;
+        pk[q] = -1; pl[q] = -1; acc[q] = 0.0;
+        if (e < npairs) {           // row-major upper triangle: (k, l), k <= l
+            while (e >= m - k) { e -= m - k; ++k; }
+            pk[q] = k; pl[q] = k + e;
+        }
+    }
+    for (int r0 = 0; r0 < n; r0 += GN_ROWS) {
+        __syncthreads();
+        for (int e = threadIdx.x; e < GN_ROWS * m; e += NT) {
+            const int rr = e % GN_ROWS, kk = e / GN_ROWS, row = r0 + rr;
+            sX[rr][kk] = row < n ? elem(D + (size_t)scol[kk] * ldd + row) : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < GN_PAIRS; ++q) {
+            if (pk[q] < 0) continue;
+            double a = acc[q];
+            for (int rr = 0; rr < GN_ROWS; ++rr) a = fma(sX[rr][pk[q]], sX[rr][pl[q]], a);
+            acc[q] = a;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < GN_PAIRS; ++q)
+        if (pk[q] >= 0) { sG[pk[q]][pl[q]] = acc[q]; sG[pl[q]][pk[q]] = acc[q]; }
+    __syncthreads();
+    if (threadIdx.x >= 32) return;
+    const int lane = threadIdx.x;
+    const bool in = lane < m;
+    const int nvec = m > 1 ? 2 : 1;
+    // start block: ones and (+1, -1, +1, ...), Gram-Schmidt
+    const double n1 = sqrt((double)m);
+    double q1 = in ? 1.0 / n1 : 0.0;
+    double alt = in ? ((lane & 1) ? -1.0 : 1.0) : 0.0;
+    const double dot0 = warp_sum(alt * q1);
+    double q2 = alt - dot0 * q1;
+    const double n2 = sqrt(warp_sum(q2 * q2));
+    q2 = (nvec > 1 && n2 > 0.0) ? q2 / n2 : 0.0;
+    double val = NAN;
+    bool have = false;
+    for (int it = 0; it < max_iters; ++it) {
+        double z1 = 0.0, z2 = 0.0;
+        for (int j = 0; j < m; ++j) {
+            const double a = in ? sG[lane][j] : 0.0;
+            z1 = fma(a, __shfl_sync(0xffffffffu, q1, j), z1);
+            z2 = fma(a, __shfl_sync(0xffffffffu, q2, j), z2);
+        }
+        const double h11 = warp_sum(q1 * z1), h12 = warp_sum(q1 * z2), h21 = warp_sum(q2 * z1),
+                     h22 = warp_sum(q2 * z2);
+        double top;
+        if (nvec > 1) {
+            const double b = 0.5 * (h12 + h21);
+            top = 0.5 * (h11 + h22) + sqrt(0.25 * (h11 - h22) * (h11 - h22) + b * b);
+        } else {
+            top = h11;
+        }
+        if (have && fabs(top - val) <= tol * fmax(1.0, fabs(top))) {
+            if (lane == 0) out[g] = sqrt(fmax(top, 0.0));
+            return;
+        }
+        val = top;
+        have = true;
+        const double z11 = warp_sum(z1 * z1), z12 = warp_sum(z1 * z2), z22 = warp_sum(z2 * z2);
+        const double r11 = sqrt(z11);
+        if (!(r11 > 0.0)) {   // block fell into the null space: restart on basis axes
+            q1 = (lane == it % m) ? 1.0 : 0.0;
+            q2 = (nvec > 1 && lane == (it + 1) % m) ? 1.0 : 0.0;
+            have = false;
+            continue;
+        }
+        const double r12 = z12 / r11;
+        const double r22 = sqrt(fmax(z22 - r12 * r12, 0.0));
+        q1 = z1 / r11;
+        q2 = (nvec > 1) ? (z2 - r12 * q1) / (r22 > 0.0 ? r22 : 1.0) : 0.0;
+    }
+    if (lane == 0) out[g] = sqrt(fmax(val, 0.0));
+}
+
 static int check_dict(int dt, const void* D, int ldd, int n, int k) {
     if (dt < DSCR_F64 || dt > DSCR_BF16) return inval("unknown dtype");
     if (!D || n < 1 || k < 1 || ldd < n || ldd % 16) return inval("bad dictionary shape or ldd");
@@ -326,6 +432,23 @@ int dscr_test_group(const double* w, const double* cn, const double* sn, const i
                     uint8_t* m, void* stream) {
     if (nk <= 0) return DSCR_OK;
     k_test_group<<<std::max(1, std::min((nk + 255) / 256, 4096)), 256, 0, (cudaStream_t)stream>>>(w, cn, sn, kg, nk, r, m);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_group_spectral_norms(int dtype, const void* D, int ldd, int n, int n_groups, const int32_t* group_ptr,
+                              const int32_t* group_cols, double tol, int max_iters, double* out, void* stream) {
+    if (dtype < DSCR_F64 || dtype > DSCR_BF16) return inval("unknown dtype");
+    if (!D || n < 1 || ldd < n || ldd % 16) return inval("bad dictionary shape or ldd");
+    if (n_groups <= 0) return DSCR_OK;
+    if (!group_ptr || !group_cols || !out || max_iters < 1 || !(tol >= 0)) return inval("bad group arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (dtype == DSCR_F64)
+        k_group_norms<double><<<n_groups, NT, 0, s>>>((const double*)D, ldd, n, n_groups, group_ptr, group_cols, tol, max_iters, out);
+    else if (dtype == DSCR_F32)
+        k_group_norms<float><<<n_groups, NT, 0, s>>>((const float*)D, ldd, n, n_groups, group_ptr, group_cols, tol, max_iters, out);
+    else
+        k_group_norms<__nv_bfloat16><<<n_groups, NT, 0, s>>>((const __nv_bfloat16*)D, ldd, n, n_groups, group_ptr, group_cols, tol, max_iters, out);
     OCK(cudaGetLastError());
     return DSCR_OK;
 }

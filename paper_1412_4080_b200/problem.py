@@ -190,7 +190,9 @@ def operator_norm(dictionary, cols=None, tol=1e-10, max_iters=5000):
         cols = index_set(cols, dictionary.n_cols)
         if cols.size == 0:
             raise ValueError("spectral_norm requires a nonempty column set")
-        Dd = dictionary.device_data(dev)[torch.from_numpy(cols).to(dev)].contiguous()
+        base = dictionary.device_data(dev)
+        src = base.view(torch.int16) if base.dtype == torch.uint16 else base    # bf16 bits: gather as int16
+        Dd = src[torch.from_numpy(cols).to(dev)].contiguous().view(base.dtype)
         k = int(cols.size)
     ldd = dictionary.ldd
     work = torch.empty(int(L.dscr_operator_norm_work_size(ldd, k)), dtype=torch.uint8, device=dev)
@@ -202,6 +204,31 @@ def operator_norm(dictionary, cols=None, tol=1e-10, max_iters=5000):
 
 def spectral_norm(dictionary, cols):
     return operator_norm(dictionary, cols)
+
+
+def group_spectral_norms(dictionary, groups, tol=1e-10, max_iters=5000):
+    """||D_g||_2 for every group in one kernel (dscr_group_spectral_norms: per-group fp64 Gram
+    + the same block power iteration); groups the kernel does not take (> 32 columns or more
+    columns than rows) go through operator_norm."""
+    import torch
+    L = nat.lib()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    groups = [index_set(g, dictionary.n_cols) for g in groups]
+    if any(g.size == 0 for g in groups):
+        raise ValueError("spectral_norm requires a nonempty column set")
+    ptr = np.zeros(len(groups) + 1, dtype=np.int32)
+    ptr[1:] = np.cumsum([g.size for g in groups])
+    cols = np.concatenate(groups).astype(np.int32)
+    Dd = dictionary.device_data(dev)
+    ptr_d, cols_d = torch.from_numpy(ptr).to(dev), torch.from_numpy(cols).to(dev)
+    out = torch.empty(len(groups), dtype=torch.float64, device=dev)
+    nat.check(L.dscr_group_spectral_norms(dictionary.dtype_code, Dd.data_ptr(), dictionary.ldd, dictionary.n_rows,
+                                          len(groups), ptr_d.data_ptr(), cols_d.data_ptr(), float(tol),
+                                          int(max_iters), out.data_ptr(), nat.stream_ptr()))
+    norms = out.cpu().numpy()
+    for gi in np.flatnonzero(norms < 0):
+        norms[gi] = operator_norm(dictionary, groups[gi], tol=tol, max_iters=max_iters)
+    return norms
 
 
 @dataclass(frozen=True)
@@ -234,7 +261,7 @@ class GroupPartition:
         if weights.shape != (len(groups),) or np.any(weights <= 0):
             raise ValueError("need one strictly positive weight per group")
         if spectral_norms is None:
-            spectral_norms = np.array([operator_norm(dictionary, g) for g in groups])
+            spectral_norms = group_spectral_norms(dictionary, groups)
         norms = np.asarray(spectral_norms, dtype=np.float64)
         sizes = np.array([g.size for g in groups], dtype=np.int64)
         offsets = np.concatenate(([0], np.cumsum(sizes)[:-1]))

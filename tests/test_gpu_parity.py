@@ -112,6 +112,44 @@ def test_operator_norm_matches_reference():
     assert got == pytest.approx(np.linalg.norm(D, 2), rel=1e-8)
 
 
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+def test_group_spectral_norms_match_reference_power_iteration(dtype):
+    """Batched group norms (one kernel: Gram + block power iteration) vs the reference
+    algorithm per group (oracle power_top_eig, dictionary.py:120-160) and exact SVD."""
+    rng = np.random.default_rng(11)
+    n, sizes = 300, [1, 2, 3, 5, 10, 10, 16, 31, 32, 33, 40, 7, 1, 10]
+    k = int(sum(sizes))
+    D = rng.standard_normal((n, k))
+    D /= np.linalg.norm(D, axis=0)
+    ptr = np.concatenate(([0], np.cumsum(sizes)))
+    D[:, ptr[4]:ptr[5]] = 0.0      # all-zero group: null-space restarts; the reference's loop ends with lam=None
+                                   # (TypeError at max(None, 0.0), dictionary.py:160), ours returns 0
+    D[:, ptr[5] + 1:ptr[6]] = D[:, [ptr[5]]]                            # rank-1 group
+    perm = rng.permutation(k)                                            # groups are scattered column sets
+    groups = [np.sort(perm[ptr[g]:ptr[g + 1]]) for g in range(len(sizes))]
+    Dp = np.empty_like(D)
+    Dp[:, perm] = D
+    if dtype == "f64":
+        dic = ds.Dictionary(Dp, check_unit_norms=False)
+    elif dtype == "f32":
+        dic = ds.Dictionary(Dp.astype(np.float32), check_unit_norms=False, dtype="f32")
+    else:
+        bits = (Dp.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16)
+        dic = ds.Dictionary(bits, check_unit_norms=False, dtype="bf16")
+    D64 = dic.as_float64()
+    got = ds.group_spectral_norms(dic, groups)
+    for g, cols in enumerate(groups):
+        if g == 4:
+            assert got[g] == 0.0
+            continue
+        ref = np.sqrt(so.power_top_eig(D64[:, cols]))
+        exact = np.linalg.norm(D64[:, cols], 2)
+        assert got[g] == pytest.approx(ref, rel=1e-8, abs=1e-300), (g, got[g], ref)
+        assert got[g] == pytest.approx(exact, rel=1e-7, abs=1e-300)
+    part = ds.GroupPartition.build(dic, groups)
+    assert np.array_equal(part.spectral_norms, got)
+
+
 # ---------------------------------------------------------------- solver vs reference fixtures
 
 
