@@ -215,6 +215,177 @@ __global__ void k_pw_qr(double* q, const double* z, int dim, int ld, int nvec, d
     }
 }
 
+// ---- operator norm, device-resident loop --------------------------------------
+// State of the block power iteration (dictionary.py:120-160) kept on the device.
+struct PwState {
+    double val;        // previous top Rayleigh value
+    double result;     // ||D||_2 when done
+    int have;          // val valid
+    int it;            // iterations done
+    int done;
+    int pad;
+};
+
+// Gram of the smaller side, fp64, upper-triangle tiles mirrored:
+//   ROWS = true : H[a][b] = sum_k D[a][k] D[b][k]   (dim = n; rows of Dt are atoms)
+//   ROWS = false: H[i][j] = sum_n D[n][i] D[n][j]   (dim = k; contraction along Dt rows)
+// 128 x 128 tile per CTA, 8 x 8 outputs per thread strided by 16, 16-deep slices in smem.
+constexpr int GR_T = 128, GR_K = 16;
+template <typename T, bool ROWS>
+__global__ void __launch_bounds__(256) k_gram(const T* D, int ldd, int n, int k, int dim, double* H) {
+    __shared__ double sA[GR_K][GR_T], sB[GR_K][GR_T];
+    const int bx = blockIdx.x, by = blockIdx.y;
+    if (bx > by) return;                       // upper triangle of tiles
+    const int i0 = bx * GR_T, j0 = by * GR_T;
+    const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+    double acc[8][8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+#pragma unroll
+        for (int p = 0; p < 8; ++p) acc[q][p] = 0.0;
+    const int klen = ROWS ? k : n;             // contraction length
+    for (int c0 = 0; c0 < klen; c0 += GR_K) {
+        if (ROWS) {   // slice = rows c0..c0+15 of Dt, columns i0.. / j0.. (contiguous along n)
+            const int kk = threadIdx.x / 16, cc = (threadIdx.x % 16) * 8;
+            const int row = c0 + kk;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int a = i0 + cc + q, b = j0 + cc + q;
+                sA[kk][cc + q] = (row < k && a < dim) ? elem(D + (size_t)row * ldd + a) : 0.0;
+                sB[kk][cc + q] = (row < k && b < dim) ? elem(D + (size_t)row * ldd + b) : 0.0;
+            }
+        } else {      // slice = entries c0..c0+15 of Dt rows i0.. / j0..
+            const int la = threadIdx.x >> 1, lk = (threadIdx.x & 1) * 8;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                const int nn = c0 + lk + q;
+                const int a = i0 + la, b = j0 + la;
+                sA[lk + q][la] = (nn < n && a < dim) ? elem(D + (size_t)a * ldd + nn) : 0.0;
+                sB[lk + q][la] = (nn < n && b < dim) ? elem(D + (size_t)b * ldd + nn) : 0.0;
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < GR_K; ++kk) {
+            double a8[8], b8[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) { a8[q] = sA[kk][tx + 16 * q]; b8[q] = sB[kk][ty + 16 * q]; }
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+#pragma unroll
+                for (int p = 0; p < 8; ++p) acc[q][p] = fma(a8[p], b8[q], acc[q][p]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+        const int j = j0 + ty + 16 * q;
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            const int i = i0 + tx + 16 * p;
+            if (i < dim && j < dim) {
+                H[(size_t)j * dim + i] = acc[q][p];
+                H[(size_t)i * dim + j] = acc[q][p];
+            }
+        }
+    }
+}
+
+// z_v = H q_v for the two block vectors (H symmetric dim x dim, one warp per row)
+__global__ void __launch_bounds__(NT) k_gram_mv(const double* H, int dim, const double* q, double* z, int ld,
+                                                 int nvec, const PwState* st) {
+    if (st->done) return;
+    const int lane = threadIdx.x & 31;
+    const int r = (blockIdx.x * NT + threadIdx.x) >> 5;
+    if (r >= dim) return;
+    const double* row = H + (size_t)r * dim;
+    double a1 = 0.0, a2 = 0.0;
+    for (int c = lane; c < dim; c += 32) {
+        const double h = row[c];
+        a1 = fma(h, q[c], a1);
+        if (nvec > 1) a2 = fma(h, q[ld + c], a2);
+    }
+    a1 = warp_sum(a1);
+    a2 = warp_sum(a2);
+    if (lane == 0) { z[r] = a1; if (nvec > 1) z[ld + r] = a2; }
+}
+
+__global__ void __launch_bounds__(NT) k_pw_init(double* q, int dim, int ld, int nvec, PwState* st) {
+    __shared__ double s_sh[64];
+    // start block [ones, (+1, -1, +1, ...)], orthonormalised (same span as np.linalg.qr)
+    const double n1 = sqrt((double)dim);
+    double dot = 0.0;
+    for (int i = threadIdx.x; i < dim; i += NT) dot += ((i & 1) ? -1.0 : 1.0) / n1;
+    dot = block_sum(dot, s_sh);
+    double n2 = 0.0;
+    for (int i = threadIdx.x; i < dim; i += NT) {
+        const double v = ((i & 1) ? -1.0 : 1.0) - dot * (1.0 / n1);
+        n2 = fma(v, v, n2);
+    }
+    n2 = sqrt(block_sum(n2, s_sh));
+    for (int i = threadIdx.x; i < dim; i += NT) {
+        q[i] = 1.0 / n1;
+        if (nvec > 1) q[ld + i] = n2 > 0.0 ? (((i & 1) ? -1.0 : 1.0) - dot * (1.0 / n1)) / n2 : 0.0;
+    }
+    if (threadIdx.x == 0) { st->val = NAN; st->result = NAN; st->have = 0; st->it = 0; st->done = 0; }
+}
+
+// one step after z = op(q): Rayleigh 2 x 2 top value, stop test, restart, q <- QR(z); single CTA
+__global__ void __launch_bounds__(NT) k_pw_step(double* q, const double* z, int dim, int ld, int nvec, double tol,
+                                                 int max_iters, PwState* st, cudaGraphConditionalHandle h) {
+    __shared__ double s_sh[64];
+    if (st->done) return;
+    double a[7] = {0, 0, 0, 0, 0, 0, 0};
+    for (int i = threadIdx.x; i < dim; i += NT) {
+        const double q1 = q[i], z1 = z[i];
+        const double q2 = nvec > 1 ? q[ld + i] : 0.0, z2 = nvec > 1 ? z[ld + i] : 0.0;
+        a[0] = fma(q1, z1, a[0]); a[1] = fma(q1, z2, a[1]); a[2] = fma(q2, z1, a[2]); a[3] = fma(q2, z2, a[3]);
+        a[4] = fma(z1, z1, a[4]); a[5] = fma(z1, z2, a[5]); a[6] = fma(z2, z2, a[6]);
+    }
+    block_sum_n<7>(a, s_sh);
+    double top;
+    if (nvec > 1) {
+        const double b = 0.5 * (a[1] + a[2]);
+        top = 0.5 * (a[0] + a[3]) + sqrt(0.25 * (a[0] - a[3]) * (a[0] - a[3]) + b * b);
+    } else {
+        top = a[0];
+    }
+    const int it = st->it;
+    const bool conv = st->have && fabs(top - st->val) <= tol * fmax(1.0, fabs(top));
+    const double r11 = sqrt(a[4]);
+    const bool restart = !conv && !(r11 > 0.0);
+    __syncthreads();
+    if (conv) {
+        if (threadIdx.x == 0) { st->result = sqrt(fmax(top, 0.0)); st->done = 1; cudaGraphSetConditional(h, 0); }
+        return;
+    }
+    if (restart) {   // block fell into the null space: restart on basis axes
+        for (int i = threadIdx.x; i < dim; i += NT) {
+            q[i] = (i == it % dim) ? 1.0 : 0.0;
+            if (nvec > 1) q[ld + i] = (i == (it + 1) % dim) ? 1.0 : 0.0;
+        }
+    } else {
+        const double r12 = a[5] / r11;
+        const double r22 = sqrt(fmax(a[6] - r12 * r12, 0.0));
+        const double d22 = r22 > 0.0 ? r22 : 1.0;
+        for (int i = threadIdx.x; i < dim; i += NT) {
+            const double q1 = z[i] / r11;
+            q[i] = q1;
+            if (nvec > 1) q[ld + i] = (z[ld + i] - r12 * q1) / d22;
+        }
+    }
+    if (threadIdx.x == 0) {
+        st->val = top;
+        st->have = restart ? 0 : 1;
+        st->it = it + 1;
+        if (it + 1 >= max_iters) {
+            st->result = sqrt(fmax(restart ? NAN : top, 0.0));
+            st->done = 1;
+            cudaGraphSetConditional(h, 0);
+        }
+    }
+}
+
 template <typename T>
 static int corr_launch(const void* D, int ldd, int n, int k, const double* v, double* out, int nvec,
                        int ldv, int ldo, cudaStream_t s) {
@@ -369,6 +540,40 @@ static int check_dict(int dt, const void* D, int ldd, int n, int k) {
     return DSCR_OK;
 }
 
+// Gram path when one side is small and the other much longer: iterate on the dim x dim
+// Gram (L2 / HBM resident) instead of two passes over D per iteration.
+static bool pw_use_gram(int n, int k) {
+    const long long dim = std::min(n, k), other = std::max(n, k);
+    return dim <= 16384 && other >= 4 * dim;
+}
+
+static size_t pw_layout(int ldd, int n, int k, size_t* off_q, size_t* off_z, size_t* off_w, size_t* off_st,
+                        size_t* off_part, size_t* off_h, int dt) {
+    const size_t M = (size_t)std::max(ldd, k);
+    size_t o = 0;
+    auto take = [&](size_t bytes) { size_t r = o; o = (o + bytes + 255) / 256 * 256; return r; };
+    *off_q = take(2 * M * 8);
+    *off_z = take(2 * M * 8);
+    *off_w = take(2 * M * 8);
+    *off_st = take(sizeof(PwState));
+    if (pw_use_gram(n, k)) {
+        const size_t dim = (size_t)std::min(n, k);
+        *off_part = 0;
+        *off_h = take(dim * dim * 8);
+    } else {
+        *off_h = 0;
+        *off_part = take(apply_part_bytes(dt, ldd, k) * 2);
+    }
+    return o;
+}
+
+template <typename T>
+static void gram_launch(const void* D, int ldd, int n, int k, int dim, double* H, cudaStream_t s) {
+    const int tiles = (dim + GR_T - 1) / GR_T;
+    if (k >= n) k_gram<T, true><<<dim3(tiles, tiles), 256, 0, s>>>((const T*)D, ldd, n, k, dim, H);
+    else k_gram<T, false><<<dim3(tiles, tiles), 256, 0, s>>>((const T*)D, ldd, n, k, dim, H);
+}
+
 }  // namespace ops
 }  // namespace dscr
 
@@ -454,89 +659,119 @@ int dscr_group_spectral_norms(int dtype, const void* D, int ldd, int n, int n_gr
 }
 
 size_t dscr_operator_norm_work_size(int ldd, int k) {
-    return (6 * (size_t)std::max(ldd, k) + 64) * sizeof(double) + apply_part_bytes(DSCR_F64, ldd, k) * 4;
+    // n <= ldd < n + 16: size for n = ldd (largest Gram) and the apply partials of the widest dtype
+    size_t q, z, w, st, part, h;
+    const size_t a = pw_layout(ldd, ldd, k, &q, &z, &w, &st, &part, &h, DSCR_BF16);
+    const size_t b = pw_layout(ldd, std::max(1, ldd - 15), k, &q, &z, &w, &st, &part, &h, DSCR_BF16);
+    const size_t c = pw_layout(ldd, ldd, k, &q, &z, &w, &st, &part, &h, DSCR_F64);
+    return std::max(a, std::max(b, c)) + 256;
 }
 
-// 2-vector block power iteration for the top eigenvalue of D^T D
-// (dictionary.py:120-171): start block [ones, alternating], orthonormalised;
-// stop when the top Rayleigh value is stable to tol * max(1, value).
+// 2-vector block power iteration for the top eigenvalue of D^T D (dictionary.py:120-160):
+// start block [ones, alternating], orthonormalised; stop when the top Rayleigh value is
+// stable to tol * max(1, value); basis-axis restart when the block falls into the null space.
+// The loop runs on the device inside a CUDA graph (conditional WHILE node, 4 steps per body):
+// one host synchronisation per call.
 int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double tol, int max_iters, void* work,
                        double* out_host, void* stream) {
     int rc = check_dict(dtype, D, ldd, n, k);
     if (rc) return rc;
     if (!work || !out_host) return inval("null work or output");
+    if (max_iters < 1 || !(tol >= 0)) return inval("bad tolerance or iteration cap");
     cudaStream_t s = (cudaStream_t)stream;
     const bool small_cols = k <= n;           // operate on the smaller side of the Gram operator
     const int dim = small_cols ? k : n;
     const int ldq = small_cols ? k : ldd;     // leading dim of q and z (length-dim vectors)
     const int ldw = small_cols ? ldd : k;     // leading dim of the intermediate
     const int nvec = dim > 1 ? 2 : 1;
-    const size_t M = (size_t)std::max(ldd, k);
-    double* q = (double*)work;      // [2][ldq]
-    double* z = q + 2 * M;          // [2][ldq]
-    double* w = z + 2 * M;          // [2][ldw]
-    double* sums = w + 2 * M;       // 7 inner products
-    double* part = sums + 64;       // split-K partials of the apply
-    // start block: ones and (+1,-1,+1,...) ; Gram-Schmidt QR (same span as np.linalg.qr)
-    std::vector<double> h0(2 * (size_t)ldq, 0.0);
-    for (int i = 0; i < dim; ++i) { h0[i] = 1.0; h0[ldq + i] = (i & 1) ? -1.0 : 1.0; }
-    {
-        double n1 = std::sqrt((double)dim);
-        double dot = 0.0;
-        for (int i = 0; i < dim; ++i) dot += h0[ldq + i] / n1;
-        double n2 = 0.0;
-        std::vector<double> q2(dim);
-        for (int i = 0; i < dim; ++i) { q2[i] = h0[ldq + i] - dot * (1.0 / n1); n2 += q2[i] * q2[i]; }
-        n2 = std::sqrt(n2);
-        for (int i = 0; i < dim; ++i) { h0[i] = 1.0 / n1; h0[ldq + i] = (nvec > 1 && n2 > 0) ? q2[i] / n2 : 0.0; }
+    const bool gram = pw_use_gram(n, k);
+    size_t oq, oz, ow, ost, opart, oh;
+    pw_layout(ldd, n, k, &oq, &oz, &ow, &ost, &opart, &oh, dtype);
+    char* base = (char*)work;
+    double* q = (double*)(base + oq);
+    double* z = (double*)(base + oz);
+    double* w = (double*)(base + ow);
+    PwState* st = (PwState*)(base + ost);
+    double* part = (double*)(base + opart);
+    double* H = (double*)(base + oh);
+    // function attributes before capture
+    if (!gram) {
+        const size_t smem = (size_t)ldd * 8 * nvec;
+        if (dtype == DSCR_F64) OCK(cudaFuncSetAttribute(k_corr<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        else if (dtype == DSCR_F32) OCK(cudaFuncSetAttribute(k_corr<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        else OCK(cudaFuncSetAttribute(k_corr<__nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     }
-    OCK(cudaMemsetAsync(work, 0, (6 * M + 64) * sizeof(double), s));
-    OCK(cudaMemcpyAsync(q, h0.data(), sizeof(double) * h0.size(), cudaMemcpyHostToDevice, s));
-    double val = NAN;
-    bool have = false;
-    double hs[7];
-    for (int it = 0; it < max_iters; ++it) {
-        if (small_cols) {
-            if ((rc = apply_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, part, s))) return rc;
-            if ((rc = corr_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, s))) return rc;
-        } else {
-            if ((rc = corr_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, s))) return rc;
-            if ((rc = apply_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, part, s))) return rc;
-        }
-        k_pw_dots<<<1, NT, 0, s>>>(q, z, dim, ldq, nvec, sums);
-        OCK(cudaGetLastError());
-        OCK(cudaMemcpyAsync(hs, sums, sizeof hs, cudaMemcpyDeviceToHost, s));
-        OCK(cudaStreamSynchronize(s));
-        double top;
-        if (nvec > 1) {
-            const double a = hs[0], b = 0.5 * (hs[1] + hs[2]), c = hs[3];
-            top = 0.5 * (a + c) + std::sqrt(0.25 * (a - c) * (a - c) + b * b);
-        } else {
-            top = hs[0];
-        }
-        if (have && std::fabs(top - val) <= tol * std::max(1.0, std::fabs(top))) {
-            *out_host = std::sqrt(std::max(top, 0.0));
-            return DSCR_OK;
-        }
-        val = top;
-        have = true;
-        const double r11 = std::sqrt(hs[4]);
-        if (!(r11 > 0)) {   // block fell into the null space: restart on basis axes
-            std::vector<double> hb(2 * (size_t)ldq, 0.0);
-            hb[(size_t)(it % dim)] = 1.0;
-            if (nvec > 1) hb[ldq + (size_t)((it + 1) % dim)] = 1.0;
-            OCK(cudaMemcpyAsync(q, hb.data(), sizeof(double) * hb.size(), cudaMemcpyHostToDevice, s));
-            OCK(cudaStreamSynchronize(s));
-            have = false;
-            continue;
-        }
-        const double r12 = hs[5] / r11;
-        const double r22 = std::sqrt(std::max(hs[6] - r12 * r12, 0.0));
-        k_pw_qr<<<std::max(1, std::min((dim + 255) / 256, 1024)), 256, 0, s>>>(q, z, dim, ldq, nvec, r11, r12,
-                                                                                r22 > 0 ? r22 : 1.0);
-        OCK(cudaGetLastError());
+    cudaGraph_t g = nullptr;
+    cudaGraphExec_t ge = nullptr;
+    cudaStream_t cs = nullptr;
+    cudaGraphConditionalHandle h;
+    cudaError_t e = cudaStreamCreateWithFlags(&cs, cudaStreamNonBlocking);
+    auto fail = [&](const char* what, cudaError_t err) {
+        if (ge) cudaGraphExecDestroy(ge);
+        if (g) cudaGraphDestroy(g);
+        if (cs) cudaStreamDestroy(cs);
+        return cuda_err(what, err);
+    };
+    if (e != cudaSuccess) return fail("stream create", e);
+    if ((e = cudaGraphCreate(&g, 0)) != cudaSuccess) return fail("graph create", e);
+    if ((e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault)) != cudaSuccess)
+        return fail("conditional handle", e);
+    // prologue: Gram (if used) and the start block
+    if ((e = cudaStreamBeginCaptureToGraph(cs, g, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        return fail("capture", e);
+    if (gram) {
+        if (dtype == DSCR_F64) gram_launch<double>(D, ldd, n, k, dim, H, cs);
+        else if (dtype == DSCR_F32) gram_launch<float>(D, ldd, n, k, dim, H, cs);
+        else gram_launch<__nv_bfloat16>(D, ldd, n, k, dim, H, cs);
     }
-    *out_host = std::sqrt(std::max(val, 0.0));
+    k_pw_init<<<1, NT, 0, cs>>>(q, dim, ldq, nvec, st);
+    cudaGraph_t tmp = nullptr;
+    e = cudaStreamEndCapture(cs, &tmp);
+    if (e != cudaSuccess) return fail("end capture", e);
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    std::vector<cudaGraphNode_t> nodes(nn);
+    cudaGraphGetNodes(g, nodes.data(), &nn);
+    cudaGraphNode_t last = nodes.back();
+    // WHILE node: body = 4 x (op; step)
+    cudaGraphNodeParams cp = {};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t cnode;
+    if ((e = cudaGraphAddNode(&cnode, g, &last, 1, &cp)) != cudaSuccess) return fail("add WHILE node", e);
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    if ((e = cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal)) != cudaSuccess)
+        return fail("capture body", e);
+    for (int r = 0; r < 4 && rc == DSCR_OK; ++r) {
+        if (gram) {
+            k_gram_mv<<<(dim + NW - 1) / NW, NT, 0, cs>>>(H, dim, q, z, ldq, nvec, st);
+        } else if (small_cols) {
+            if ((rc = apply_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, part, cs)) == DSCR_OK)
+                rc = corr_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, cs);
+        } else {
+            if ((rc = corr_any(dtype, D, ldd, n, k, q, w, nvec, ldq, ldw, cs)) == DSCR_OK)
+                rc = apply_any(dtype, D, ldd, n, k, w, z, nvec, ldw, ldq, part, cs);
+        }
+        k_pw_step<<<1, NT, 0, cs>>>(q, z, dim, ldq, nvec, tol, max_iters, st, h);
+    }
+    e = cudaStreamEndCapture(cs, &tmp);
+    if (rc) {
+        if (g) cudaGraphDestroy(g);
+        cudaStreamDestroy(cs);
+        return rc;
+    }
+    if (e != cudaSuccess) return fail("end capture body", e);
+    if ((e = cudaGraphInstantiate(&ge, g, 0)) != cudaSuccess) return fail("instantiate", e);
+    if ((e = cudaGraphLaunch(ge, s)) != cudaSuccess) return fail("launch", e);
+    PwState hs;
+    if ((e = cudaMemcpyAsync(&hs, st, sizeof hs, cudaMemcpyDeviceToHost, s)) != cudaSuccess) return fail("read result", e);
+    if ((e = cudaStreamSynchronize(s)) != cudaSuccess) return fail("sync", e);
+    cudaGraphExecDestroy(ge);
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cs);
+    *out_host = hs.result;
     return DSCR_OK;
 }
 }

@@ -112,6 +112,29 @@ def test_operator_norm_matches_reference():
     assert got == pytest.approx(np.linalg.norm(D, 2), rel=1e-8)
 
 
+@pytest.mark.parametrize("shape", [(64, 600), (600, 64), (300, 500), (1, 40), (40, 1), (128, 128)])
+@pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
+def test_operator_norm_paths_match_reference_power_iteration(shape, dtype):
+    """Device-resident power iteration: Gram path (one side >= 4x the other) and the
+    apply/correlate path, vs the reference algorithm (oracle power_top_eig)."""
+    rng = np.random.default_rng(shape[0] * 7 + shape[1])
+    D = rng.standard_normal(shape)
+    if dtype == "f64":
+        dic = ds.Dictionary(D, check_unit_norms=False)
+    elif dtype == "f32":
+        dic = ds.Dictionary(D.astype(np.float32), check_unit_norms=False, dtype="f32")
+    else:
+        dic = ds.Dictionary((D.astype(np.float32).view(np.uint32) >> 16).astype(np.uint16), check_unit_norms=False,
+                            dtype="bf16")
+    D64 = dic.as_float64()
+    got = ds.operator_norm(dic)
+    assert got == pytest.approx(np.sqrt(so.power_top_eig(D64)), rel=1e-8)
+    assert got == pytest.approx(np.linalg.norm(D64, 2), rel=1e-7)
+    # iteration cap: value of the last Rayleigh step, as the reference returns it
+    capped = ds.operator_norm(dic, max_iters=3)
+    assert capped == pytest.approx(np.sqrt(so.power_top_eig(D64, max_iters=3)), rel=1e-10)
+
+
 @pytest.mark.parametrize("dtype", ["f64", "f32", "bf16"])
 def test_group_spectral_norms_match_reference_power_iteration(dtype):
     """Batched group norms (one kernel: Gram + block power iteration) vs the reference
