@@ -293,7 +293,10 @@ typedef struct dscr_batched_desc {
 } dscr_batched_desc;
 
 typedef struct dscr_batched_buffers {
-    int32_t* x_idx[2]; double* x_val[2]; int32_t* x_cnt[2];   /* x lists by parity ([B][cap]) */
+    /* support lists by parity ([B][cap]): sorted atoms with x or u nonzero, their x and u
+     * values, and the count per observation; after t iterations the solution is the entries of
+     * parity t & 1 with x != 0 */
+    int32_t* s_idx[2]; double* s_x[2]; double* s_u[2]; int32_t* s_cnt[2];
     double* F; double* gap; int32_t* nnz; int32_t* kept; int32_t* status; double* lmax; double* radius;
     double* trace;            /* [max_iters][4]: sum F, sum gap, sum nnz, sum kept */
     int32_t* iterations;      /* device counter */

@@ -93,7 +93,7 @@ class BatchedDesc(C.Structure):
 
 class BatchedBuffers(C.Structure):
     _fields_ = [
-        ("x_idx", C.c_void_p * 2), ("x_val", C.c_void_p * 2), ("x_cnt", C.c_void_p * 2),
+        ("s_idx", C.c_void_p * 2), ("s_x", C.c_void_p * 2), ("s_u", C.c_void_p * 2), ("s_cnt", C.c_void_p * 2),
         ("F", C.c_void_p), ("gap", C.c_void_p), ("nnz", C.c_void_p), ("kept", C.c_void_p),
         ("status", C.c_void_p), ("lmax", C.c_void_p), ("radius", C.c_void_p), ("trace", C.c_void_p),
         ("iterations", C.c_void_p), ("C", C.c_void_p), ("mask", C.c_void_p),

@@ -138,12 +138,14 @@ class BatchedEngine:
         torch = self.torch
         b, bf, cap = self.b, self.bufs, self.cap
         par = self.iterations & 1
-        cnt = self._view(bf.x_cnt[par], b, torch.int32)
-        live = torch.arange(cap, device=self.device, dtype=torch.int32)[None, :] < cnt[:, None]
-        idx = self._view(bf.x_idx[par], b * cap, torch.int32).view(b, cap)[live].cpu().numpy()
-        val = self._view(bf.x_val[par], b * cap, torch.float64).view(b, cap)[live].cpu().numpy()
+        cnt = self._view(bf.s_cnt[par], b, torch.int32)
+        xs = self._view(bf.s_x[par], b * cap, torch.float64).view(b, cap)
+        live = (torch.arange(cap, device=self.device, dtype=torch.int32)[None, :] < cnt[:, None]) & (xs != 0.0)
+        counts_d = live.sum(dim=1, dtype=torch.int32)
+        idx = self._view(bf.s_idx[par], b * cap, torch.int32).view(b, cap)[live].cpu().numpy()
+        val = xs[live].cpu().numpy()
         f64 = torch.stack([self._view(p, b, torch.float64) for p in (bf.F, bf.gap, bf.lmax, bf.radius)]).cpu().numpy()
-        i32 = torch.cat([self._view(p, b, torch.int32) for p in (bf.nnz, bf.kept, bf.status, bf.x_cnt[par])]
+        i32 = torch.cat([self._view(p, b, torch.int32) for p in (bf.nnz, bf.kept, bf.status)] + [counts_d]
                         + [self._view(bf.iterations, 1, torch.int32)]).cpu().numpy()
         trace = self._view(bf.trace, self.iterations * 4, torch.float64).cpu().numpy().reshape(-1, 4)
         self.d2h_bytes = int(idx.nbytes + val.nbytes + f64.nbytes + i32.nbytes + trace.nbytes)

@@ -581,8 +581,8 @@ struct BParams {
     int* eV;                   // [B]
     int oz;                    // setup correlations on the integer tensor cores
     uint32_t* mask;            // [B][K/32]
-    int* xi[2]; double* xv[2]; int* xc[2];   // x lists (parity)
-    int* ui[2]; double* uv[2]; int* uc[2];   // u lists
+    // support lists by parity: sorted atoms with x or u nonzero, their x and u values, count
+    int* si[2]; double* sx[2]; double* su[2]; int* sn[2];
     double *sq, *ty, *mu0, *rsq0, *yy, *lmax, *sgn, *shift_sq, *rsq, *radius, *F, *gap, *pen, *ccmin;
     double* anorm;             // [K] column norms of the bf16 dictionary (fp64)
     int *istar, *nnz, *kept, *status;
@@ -788,7 +788,7 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
     }
     if (threadIdx.x == 0) {
         P.yy[j] = v3[0]; P.sq[j] = v3[1]; P.ty[j] = v3[2]; P.mu0[j] = mu0; P.rsq0[j] = d2;
-        P.xc[0][j] = 0; P.uc[0][j] = 0; P.xc[1][j] = 0; P.uc[1][j] = 0;
+        P.sn[0][j] = 0; P.sn[1][j] = 0;
         P.F[j] = 0.5 * v3[0]; P.gap[j] = NAN; P.nnz[j] = 0; P.kept[j] = trivial ? 0 : P.K;
         P.radius[j] = NAN;
         P.thr[j] = (float)(P.lam[j] * (1.0 - 1e-6));
@@ -819,6 +819,29 @@ __device__ __forceinline__ double list_gather(const int* idx, const double* val,
     return v;
 }
 
+// x and u values of a sorted support list at atoms g0..g0+31 (one per lane), advancing *ptr
+__device__ __forceinline__ void list_gather2(const int* idx, const double* xv, const double* uv, int cnt, int& ptr,
+                                             int g0, double* sxs, double* sus, int lane, double& x, double& u) {
+    x = 0.0; u = 0.0;
+    if (ptr >= cnt || idx[ptr] >= g0 + 32) return;      // warp-uniform: no entry in this group
+    sxs[lane] = 0.0;
+    sus[lane] = 0.0;
+    __syncwarp();
+    for (;;) {
+        const int e = ptr + lane;
+        const int a = (e < cnt) ? idx[e] : 0x7fffffff;
+        const bool in = a < g0 + 32;
+        if (in) { sxs[a - g0] = xv[e]; sus[a - g0] = uv[e]; }
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        ptr += __popc(bal);
+        if (bal != 0xffffffffu) break;
+    }
+    __syncwarp();
+    x = sxs[lane];
+    u = sus[lane];
+    __syncwarp();
+}
+
 __device__ __forceinline__ int lower_bound_dev(const int* a, int n, int key) {
     int lo = 0, hi = n;
     while (lo < hi) {
@@ -832,7 +855,8 @@ __device__ __forceinline__ int lower_bound_dev(const int* a, int n, int key) {
 __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     __shared__ double s_sh[64];
     __shared__ double s_scr[BW][32];
-    __shared__ int s_cnt[2][BW + 1];
+    __shared__ double s_scr2[BW][32];
+    __shared__ int s_cnt[BW + 1];
     __shared__ double s_scal[4];
     const int j = blockIdx.x;
     if (P.status[j] != 0) return;
@@ -844,18 +868,17 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     const int a0 = warp * span;
     const double lam = P.lam[j], L = P.L;
     const double thr = lam / L, beta = P.beta[t];
-    const int* xi = P.xi[par]; const double* xv = P.xv[par]; const int xcnt = P.xc[par][j];
-    const int* ui = P.ui[par]; const double* uv = P.uv[par]; const int ucnt = P.uc[par][j];
     const size_t lo = (size_t)j * P.cap;
-    int pu0 = 0, px0 = 0;
-    if (lane == 0) { pu0 = lower_bound_dev(ui + lo, ucnt, a0); px0 = lower_bound_dev(xi + lo, xcnt, a0); }
-    pu0 = __shfl_sync(0xffffffffu, pu0, 0);
-    px0 = __shfl_sync(0xffffffffu, px0, 0);
+    const int* si = P.si[par] + lo; const double* sx = P.sx[par] + lo; const double* su = P.su[par] + lo;
+    const int scnt = P.sn[par][j];
+    int ps0 = 0;
+    if (lane == 0) ps0 = lower_bound_dev(si, scnt, a0);
+    ps0 = __shfl_sync(0xffffffffu, ps0, 0);
     // One sweep of the warp's atoms.  mode 0: max|c| and list counts assuming no atom is screened;
     // mode 1: counts with the test; mode 2: write lists and mask words.
     double rho = NAN, margin = SCREEN_MARGIN + 1e-6;
     bool can_screen = false;
-    int nx_off = 0, nu_off = 0;
+    int ns_off = 0;
     double pen = 0.0, nnz = 0.0, kept = 0.0;
     double m = 0.0;
     // with u_i = x_i = 0 the candidate is nonzero only if |c_i| > lam (soft threshold of -c/L at lam/L):
@@ -863,11 +886,10 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     // exact fp64 path
     const float hot_f = (float)(lam * (1.0 - 1e-6));
     float mf = 0.0f;
-    auto sweep = [&](int mode, int& cx, int& cu) {
-        int pu = pu0, px = px0;
-        cx = 0; cu = 0;
-        int nu_at = (pu < ucnt) ? ui[lo + pu] : 0x7fffffff;     // next list atoms (cached)
-        int nx_at = (px < xcnt) ? xi[lo + px] : 0x7fffffff;
+    auto sweep = [&](int mode, int& cs) {
+        int ps = ps0;
+        cs = 0;
+        int ns_at = (ps < scnt) ? si[ps] : 0x7fffffff;     // next list atom (cached)
         constexpr int PF = 8;                                    // groups prefetched per step
         for (int gb = a0; gb < a0 + span; gb += 32 * PF) {
             float cfs[PF];
@@ -886,17 +908,16 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
                 bool active = (w >> lane) & 1u;
                 const float cf = cfs[q];
                 if (mode == 0 && active) mf = fmaxf(mf, fabsf(cf));
-                const bool lists = nu_at < g0 + 32 || nx_at < g0 + 32;
+                const bool lists = ns_at < g0 + 32;
                 const bool screen_here = mode > 0 && can_screen && w != 0u;
                 if (!lists && !screen_here && !__any_sync(0xffffffffu, active && fabsf(cf) > hot_f)) {
                     if (mode == 2 && lane == 0) kept += __popc(w);
                     continue;
                 }
                 const double c = (double)cf;
-                const double u = list_gather(ui + lo, uv + lo, ucnt, pu, g0, s_scr[warp], lane);
-                const double x = list_gather(xi + lo, xv + lo, xcnt, px, g0, s_scr[warp], lane);
-                nu_at = (pu < ucnt) ? ui[lo + pu] : 0x7fffffff;
-                nx_at = (px < xcnt) ? xi[lo + px] : 0x7fffffff;
+                double x, u;
+                list_gather2(si, sx, su, scnt, ps, g0, s_scr[warp], s_scr2[warp], lane, x, u);
+                ns_at = (ps < scnt) ? si[ps] : 0x7fffffff;
                 if (screen_here && active) {
                     const double ccv = (double)P.cc[(size_t)j * P.K + i];
                     if ((1.0 - fabs(ccv)) / P.anorm[i] - rho > margin) active = false;   // screening.py:359, norm-aware
@@ -906,31 +927,27 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
                     cand = soft(u - c / L, thr);
                     un = cand + beta * (cand - x);
                 }
-                const unsigned bx = __ballot_sync(0xffffffffu, cand != 0.0);
-                const unsigned bu = __ballot_sync(0xffffffffu, un != 0.0);
+                const unsigned bs = __ballot_sync(0xffffffffu, cand != 0.0 || un != 0.0);
                 if (mode == 2) {
                     const unsigned ba = __ballot_sync(0xffffffffu, active);
                     const unsigned ltm = (1u << lane) - 1u;
-                    if (cand != 0.0) {
-                        const int e = nx_off + cx + __popc(bx & ltm);
-                        if (e < P.cap) { P.xi[par ^ 1][lo + e] = i; P.xv[par ^ 1][lo + e] = cand; }
-                    }
-                    if (un != 0.0) {
-                        const int e = nu_off + cu + __popc(bu & ltm);
-                        if (e < P.cap) { P.ui[par ^ 1][lo + e] = i; P.uv[par ^ 1][lo + e] = un; }
+                    if (cand != 0.0 || un != 0.0) {
+                        const int e = ns_off + cs + __popc(bs & ltm);
+                        if (e < P.cap) {
+                            P.si[par ^ 1][lo + e] = i; P.sx[par ^ 1][lo + e] = cand; P.su[par ^ 1][lo + e] = un;
+                        }
                     }
                     if (lane == 0 && ba != w) mrow[g0 >> 5] = ba;
                     pen += fabs(cand);
                     nnz += (cand != 0.0) ? 1.0 : 0.0;
                     if (lane == 0) kept += __popc(ba);
                 }
-                cx += __popc(bx);
-                cu += __popc(bu);
+                cs += __popc(bs);
             }
         }
     };
-    int cx, cu;
-    sweep(0, cx, cu);
+    int cs;
+    sweep(0, cs);
     m = warp_max((double)mf);
     if (lane == 0) s_scr[warp][0] = m;
     __syncthreads();
@@ -954,25 +971,23 @@ __global__ void __launch_bounds__(BT) k_bupdate(BParams P, int t) {
     }
     // fp32 centre correlations: screen only with a 1e-6 extra margin
     if (P.test != DSCR_TEST_OFF) can_screen = P.ccmin[j] - rho > margin;
-    if (can_screen) sweep(1, cx, cu);
-    if (lane == 0) { s_cnt[0][warp] = cx; s_cnt[1][warp] = cu; }
+    if (can_screen) sweep(1, cs);
+    if (lane == 0) s_cnt[warp] = cs;
     __syncthreads();
-    for (int w = 0; w < warp; ++w) { nx_off += s_cnt[0][w]; nu_off += s_cnt[1][w]; }
+    for (int w = 0; w < warp; ++w) ns_off += s_cnt[w];
     if (threadIdx.x == 0) {
-        int tx = 0, tu = 0;
-        for (int w = 0; w < BW; ++w) { tx += s_cnt[0][w]; tu += s_cnt[1][w]; }
-        s_cnt[0][BW] = tx;
-        s_cnt[1][BW] = tu;
+        int ts = 0;
+        for (int w = 0; w < BW; ++w) ts += s_cnt[w];
+        s_cnt[BW] = ts;
     }
     __syncthreads();
-    sweep(2, cx, cu);
+    sweep(2, cs);
     double v3[3] = {pen, nnz, kept};
     block_sum_n<3>(v3, s_sh);
     if (threadIdx.x == 0) {
-        const int tx = s_cnt[0][BW], tu = s_cnt[1][BW];
-        if (tx > P.cap || tu > P.cap) P.status[j] = 4;     // list capacity exceeded
-        P.xc[par ^ 1][j] = min(tx, P.cap);
-        P.uc[par ^ 1][j] = min(tu, P.cap);
+        const int ts = s_cnt[BW];
+        if (ts > P.cap) P.status[j] = 4;     // list capacity exceeded
+        P.sn[par ^ 1][j] = min(ts, P.cap);
         P.pen[j] = v3[0];
         P.nnz[j] = (int)v3[1];
         P.kept[j] = (int)v3[2];
@@ -1000,8 +1015,8 @@ constexpr int LSM = 512;       // old-list entries staged in shared memory (long
 __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     __shared__ int s_idx[HMAX];
     __shared__ float s_val[HMAX];
-    __shared__ int s_xi[LSM], s_ui[LSM];
-    __shared__ double s_xv[LSM], s_uv[LSM];
+    __shared__ int s_si[LSM];
+    __shared__ double s_sx[LSM], s_su[LSM];
     __shared__ double s_sh[64];
     __shared__ int s_scan[2 * BW + 1];
     const int j = blockIdx.x;
@@ -1012,7 +1027,7 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     uint32_t* nrow = P.nzm + (size_t)j * words;
     const int hc = P.hot_cnt[j];
     const int st = P.status[j];
-    const int xcnt = P.xc[par][j], ucnt = P.uc[par][j];
+    const int scnt = P.sn[par][j];
     const double lam = P.lam[j], L = P.L;
     const double sq = P.sq[j], tyv = P.ty[j];
     const uint32_t cmx = P.cmax[j];
@@ -1023,8 +1038,7 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
         if (threadIdx.x == 0) { P.hot_cnt[j] = 0; P.cmax[j] = 0u; }
         return;
     }
-    const int* xi = P.xi[par] + lo; const double* xv = P.xv[par] + lo;
-    const int* ui = P.ui[par] + lo; const double* uv = P.uv[par] + lo;
+    const int* si = P.si[par] + lo; const double* sx = P.sx[par] + lo; const double* su = P.su[par] + lo;
     const int cnt = min(hc, P.hcap);
     int npow = 1;
     while (npow < cnt) npow <<= 1;
@@ -1032,20 +1046,17 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
         s_idx[e] = (e < cnt) ? P.hot_idx[(size_t)j * P.hcap + e] : 0x7fffffff;
         s_val[e] = (e < cnt) ? P.hot_val[(size_t)j * P.hcap + e] : 0.0f;
     }
-    const bool xs = xcnt <= LSM, us = ucnt <= LSM;
-    if (xs) for (int e = threadIdx.x; e < xcnt; e += BT) { s_xi[e] = xi[e]; s_xv[e] = xv[e]; }
-    if (us) for (int e = threadIdx.x; e < ucnt; e += BT) { s_ui[e] = ui[e]; s_uv[e] = uv[e]; }
+    const bool ss = scnt <= LSM;
+    if (ss) for (int e = threadIdx.x; e < scnt; e += BT) { s_si[e] = si[e]; s_sx[e] = sx[e]; s_su[e] = su[e]; }
     // dual scaling with the inflated correlation bound, r_SAFE^2, test radius (screening.py:115-205)
     const double cinf = (double)__uint_as_float(cmx) + P.err_rel * sqrt(sq);
     const double bound = (cinf == 0.0) ? INFINITY : 1.0 / cinf;
     const double mu = (sq != 0.0) ? clip(tyv / (lam * sq), bound) : 0.0;
     const double rsq = radius_sq(P, j, mu, sq);
     __syncthreads();
-    if (xs) xi = s_xi, xv = s_xv;
-    if (us) ui = s_ui, uv = s_uv;
-    // nonzero bitmap: clear the old lists' atoms (set again below for the new lists)
-    for (int e = threadIdx.x; e < ucnt; e += BT) atomicAnd(&nrow[ui[e] >> 5], ~(1u << (ui[e] & 31)));
-    for (int e = threadIdx.x; e < xcnt; e += BT) atomicAnd(&nrow[xi[e] >> 5], ~(1u << (xi[e] & 31)));
+    if (ss) si = s_si, sx = s_sx, su = s_su;
+    // nonzero bitmap: clear the old list's atoms (set again below for the new list)
+    for (int e = threadIdx.x; e < scnt; e += BT) atomicAnd(&nrow[si[e] >> 5], ~(1u << (si[e] & 31)));
     // bitonic sort of (atom, c) by atom: the emission order is arbitrary, the lists are ordered
     for (int k = 2; k <= npow; k <<= 1) {
         for (int jj = k >> 1; jj > 0; jj >>= 1) {
@@ -1092,7 +1103,7 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     }
     // hot entries in atom order: prox, momentum, ordered compaction into the new lists
     const double thr = lam / L;
-    int nx = 0, nu = 0;
+    int ns = 0;
     double pen = 0.0, nnz = 0.0;
     for (int e0 = 0; e0 < cnt; e0 += BT) {
         const int e = e0 + threadIdx.x;
@@ -1101,31 +1112,29 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
         if (e < cnt) {
             i = s_idx[e];
             if ((mrow[i >> 5] >> (i & 31)) & 1u) {
-                const int pu = find_in(ui, ucnt, i), px = find_in(xi, xcnt, i);
-                const double u = pu >= 0 ? uv[pu] : 0.0, x = px >= 0 ? xv[px] : 0.0;
+                const int ps = find_in(si, scnt, i);
+                const double u = ps >= 0 ? su[ps] : 0.0, x = ps >= 0 ? sx[ps] : 0.0;
                 const double c = (double)s_val[e];
                 cand = soft(u - c / L, thr);
                 un = cand + beta * (cand - x);
             }
         }
-        int tx, tu;
-        const int ox = block_exscan(cand != 0.0 ? 1 : 0, s_scan, &tx);
-        const int ou = block_exscan(un != 0.0 ? 1 : 0, s_scan, &tu);
-        const bool wx = cand != 0.0 && nx + ox < P.cap, wu = un != 0.0 && nu + ou < P.cap;
-        if (wx) { P.xi[par ^ 1][lo + nx + ox] = i; P.xv[par ^ 1][lo + nx + ox] = cand; }
-        if (wu) { P.ui[par ^ 1][lo + nu + ou] = i; P.uv[par ^ 1][lo + nu + ou] = un; }
-        if (wx || wu) atomicOr(&nrow[i >> 5], 1u << (i & 31));
+        const bool keep = cand != 0.0 || un != 0.0;
+        int ts;
+        const int os = block_exscan(keep ? 1 : 0, s_scan, &ts);
+        if (keep && ns + os < P.cap) {
+            P.si[par ^ 1][lo + ns + os] = i; P.sx[par ^ 1][lo + ns + os] = cand; P.su[par ^ 1][lo + ns + os] = un;
+            atomicOr(&nrow[i >> 5], 1u << (i & 31));
+        }
         pen += fabs(cand);
         nnz += (cand != 0.0) ? 1.0 : 0.0;
-        nx += tx;
-        nu += tu;
+        ns += ts;
     }
     double v2[2] = {pen, nnz};
     block_sum_n<2>(v2, s_sh);
     if (threadIdx.x == 0) {
-        if (hc > P.hcap || nx > P.cap || nu > P.cap) P.status[j] = 4;
-        P.xc[par ^ 1][j] = min(nx, P.cap);
-        P.uc[par ^ 1][j] = min(nu, P.cap);
+        if (hc > P.hcap || ns > P.cap) P.status[j] = 4;
+        P.sn[par ^ 1][j] = min(ns, P.cap);
         P.pen[j] = v2[0];
         P.nnz[j] = (int)v2[1];
         P.kept[j] = (int)kept;
@@ -1140,60 +1149,63 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
 __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
     __shared__ double s_sh[64];
     __shared__ int s_idx[BT];
-    __shared__ double s_val[BT];
+    __shared__ double s_a[BT], s_b[BT];
     const int j = blockIdx.x;
-    const int par = (t + 1) & 1;      // lists written by this iteration's update
+    const int par = (t + 1) & 1;      // list written by this iteration's update
     if (P.status[j] != 0) {
         if (threadIdx.x == 0 && j == 0) *P.it = t + 1;
         return;
     }
     const size_t lo = (size_t)j * P.cap;
-    // thread t owns rows 4t..4t+3 (+1024 for the second chunk); one 8-byte load per entry and
-    // chunk, four entries in flight
+    // thread t owns rows 4t..4t+3 (+1024 for the second chunk); one pass over the support list
+    // (x and u share each column load), one 8-byte load per entry and chunk, 8 entries in flight
     constexpr int RPT = 8;            // rows per thread (N <= 2048)
-    double rx[RPT], ru[RPT];
-#pragma unroll
-    for (int q = 0; q < RPT; ++q) { rx[q] = 0.0; ru[q] = 0.0; }
+    double rx[RPT], ru[RPT], yv[RPT];
     const int nch = (P.N + 1023) / 1024;
-    for (int which = 0; which < 2; ++which) {
-        const int* idx = (which ? P.ui[par] : P.xi[par]) + lo;
-        const double* val = (which ? P.uv[par] : P.xv[par]) + lo;
-        const int cnt = which ? P.uc[par][j] : P.xc[par][j];
-        for (int e0 = 0; e0 < cnt; e0 += BT) {
-            __syncthreads();
-            if (e0 + threadIdx.x < cnt) { s_idx[threadIdx.x] = idx[e0 + threadIdx.x]; s_val[threadIdx.x] = val[e0 + threadIdx.x]; }
-            __syncthreads();
-            const int m = min(BT, cnt - e0);
-            for (int ch = 0; ch < nch; ++ch) {
-                const int r0 = ch * 1024 + 4 * threadIdx.x;
-                if (r0 >= P.N) continue;
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
-                int e = 0;
-                for (; e + 4 <= m; e += 4) {
-                    uint2 w[4];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        w[q] = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0));
+    for (int q = 0; q < RPT; ++q) {
+        rx[q] = 0.0; ru[q] = 0.0;
+        const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
+        yv[q] = (n < P.N) ? P.Y[(size_t)j * P.ldy + n] : 0.0;       // independent of the list: issue early
+    }
+    const int* idx = P.si[par] + lo;
+    const double* xa = P.sx[par] + lo;
+    const double* ub = P.su[par] + lo;
+    const int cnt = P.sn[par][j];
+    for (int e0 = 0; e0 < cnt; e0 += BT) {
+        __syncthreads();
+        if (e0 + threadIdx.x < cnt) {
+            s_idx[threadIdx.x] = idx[e0 + threadIdx.x];
+            s_a[threadIdx.x] = xa[e0 + threadIdx.x];
+            s_b[threadIdx.x] = ub[e0 + threadIdx.x];
+        }
+        __syncthreads();
+        const int m = min(BT, cnt - e0);
+        for (int ch = 0; ch < nch; ++ch) {
+            const int r0 = ch * 1024 + 4 * threadIdx.x;
+            if (r0 >= P.N) continue;
+            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
+            auto acc = [&](const uint2& w, double va, double vb) {
+                const double d0 = (double)__uint_as_float(w.x << 16), d1 = (double)__uint_as_float(w.x & 0xffff0000u);
+                const double d2 = (double)__uint_as_float(w.y << 16), d3 = (double)__uint_as_float(w.y & 0xffff0000u);
+                a0 = fma(va, d0, a0); a1 = fma(va, d1, a1); a2 = fma(va, d2, a2); a3 = fma(va, d3, a3);
+                b0 = fma(vb, d0, b0); b1 = fma(vb, d1, b1); b2 = fma(vb, d2, b2); b3 = fma(vb, d3, b3);
+            };
+            int e = 0;
+            for (; e + 8 <= m; e += 8) {
+                uint2 w[8];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const double v = s_val[e + q];
-                        a0 = fma(v, (double)__uint_as_float(w[q].x << 16), a0);
-                        a1 = fma(v, (double)__uint_as_float(w[q].x & 0xffff0000u), a1);
-                        a2 = fma(v, (double)__uint_as_float(w[q].y << 16), a2);
-                        a3 = fma(v, (double)__uint_as_float(w[q].y & 0xffff0000u), a3);
-                    }
-                }
-                for (; e < m; ++e) {
-                    const uint2 w = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e] * P.ldd + r0));
-                    const double v = s_val[e];
-                    a0 = fma(v, (double)__uint_as_float(w.x << 16), a0);
-                    a1 = fma(v, (double)__uint_as_float(w.x & 0xffff0000u), a1);
-                    a2 = fma(v, (double)__uint_as_float(w.y << 16), a2);
-                    a3 = fma(v, (double)__uint_as_float(w.y & 0xffff0000u), a3);
-                }
-                double* dst = which ? ru : rx;
-                dst[ch * 4 + 0] += a0; dst[ch * 4 + 1] += a1; dst[ch * 4 + 2] += a2; dst[ch * 4 + 3] += a3;
+                for (int q = 0; q < 8; ++q)
+                    w[q] = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0));
+#pragma unroll
+                for (int q = 0; q < 8; ++q) acc(w[q], s_a[e + q], s_b[e + q]);
             }
+            for (; e < m; ++e) {
+                const uint2 w = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e] * P.ldd + r0));
+                acc(w, s_a[e], s_b[e]);
+            }
+            rx[ch * 4 + 0] += a0; rx[ch * 4 + 1] += a1; rx[ch * 4 + 2] += a2; rx[ch * 4 + 3] += a3;
+            ru[ch * 4 + 0] += b0; ru[ch * 4 + 1] += b1; ru[ch * 4 + 2] += b2; ru[ch * 4 + 3] += b3;
         }
     }
     double f2 = 0.0, sq = 0.0, tyv = 0.0;
@@ -1201,7 +1213,7 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
     for (int q = 0; q < RPT; ++q) {
         const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
         if (n < P.N) {
-            const double yn = P.Y[(size_t)j * P.ldy + n];
+            const double yn = yv[q];
             const double qa = rx[q] - yn;
             const double tn = ru[q] - yn;      // theta_{t+1} = D u - y (solvers.py:212)
             write_theta(P, j, n, tn);
@@ -1285,8 +1297,8 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     p.eV = (int*)take(B * 4);
     p.mask = (uint32_t*)take(B * K / 8);
     for (int q = 0; q < 2; ++q) {
-        p.xi[q] = (int*)take(B * cap * 4); p.xv[q] = (double*)take(B * cap * 8); p.xc[q] = (int*)take(B * 4);
-        p.ui[q] = (int*)take(B * cap * 4); p.uv[q] = (double*)take(B * cap * 8); p.uc[q] = (int*)take(B * 4);
+        p.si[q] = (int*)take(B * cap * 4); p.sx[q] = (double*)take(B * cap * 8);
+        p.su[q] = (double*)take(B * cap * 8); p.sn[q] = (int*)take(B * 4);
     }
     double** dv[] = {&p.sq, &p.ty, &p.mu0, &p.rsq0, &p.yy, &p.lmax, &p.sgn, &p.shift_sq, &p.rsq, &p.radius, &p.F, &p.gap, &p.pen, &p.ccmin};
     for (double** q : dv) *q = (double*)take(B * 8);
@@ -1459,7 +1471,7 @@ int dscr_batched_get_buffers(dscr_batched* h, dscr_batched_buffers* b) {
     if (!h || !b) { err_store() = "null argument"; return DSCR_EINVAL; }
     const BParams& P = h->P;
     for (int q = 0; q < 2; ++q) {
-        b->x_idx[q] = P.xi[q]; b->x_val[q] = P.xv[q]; b->x_cnt[q] = P.xc[q];
+        b->s_idx[q] = P.si[q]; b->s_x[q] = P.sx[q]; b->s_u[q] = P.su[q]; b->s_cnt[q] = P.sn[q];
     }
     b->F = P.F; b->gap = P.gap; b->nnz = P.nnz; b->kept = P.kept; b->status = P.status; b->lmax = P.lmax;
     b->radius = P.radius; b->trace = P.trace; b->iterations = P.it; b->C = P.C; b->mask = P.mask;
