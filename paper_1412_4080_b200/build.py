@@ -50,6 +50,7 @@ def build(force=False, verbose=False):
                 "-I", os.path.join(HERE, "csrc")]
     if verbose:
         cmd_base += ["-Xptxas", "-v"]
+    cmd_base += os.environ.get("DSCR_NVCC_EXTRA", "").split()   # experiment knobs (-D...), empty by default
     build_dir = os.path.join(LIB_DIR, "obj")
     os.makedirs(build_dir, exist_ok=True)
     procs = []

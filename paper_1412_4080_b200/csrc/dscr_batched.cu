@@ -1146,7 +1146,22 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
 }
 
 // sparse residuals D x - y and D u - y; objective, gap, next theta (+ bf16 terms)
-__global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
+// 4 consecutive bf16 rows of one column (w) times the entry's x and u values
+__device__ __forceinline__ void resid_acc(const uint2& w, double va, double vb, double (&a)[4], double (&b)[4]) {
+    const double d[4] = {(double)__uint_as_float(w.x << 16), (double)__uint_as_float(w.x & 0xffff0000u),
+                         (double)__uint_as_float(w.y << 16), (double)__uint_as_float(w.y & 0xffff0000u)};
+#pragma unroll
+    for (int v = 0; v < 4; ++v) { a[v] = fma(va, d[v], a[v]); b[v] = fma(vb, d[v], b[v]); }
+}
+
+#ifndef BRESID_EB
+#define BRESID_EB 4
+#endif
+#ifndef BRESID_MINB
+#define BRESID_MINB 5
+#endif
+template <int NCH>      // 1024-row chunks (N <= NCH * 1024)
+__global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BParams P, int t) {
     __shared__ double s_sh[64];
     __shared__ int s_idx[BT];
     __shared__ double s_a[BT], s_b[BT];
@@ -1159,9 +1174,9 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
     const size_t lo = (size_t)j * P.cap;
     // thread t owns rows 4t..4t+3 (+1024 for the second chunk); one pass over the support list
     // (x and u share each column load), one 8-byte load per entry and chunk, 8 entries in flight
-    constexpr int RPT = 8;            // rows per thread (N <= 2048)
+    constexpr int RPT = 4 * NCH;      // rows per thread
     double rx[RPT], ru[RPT], yv[RPT];
-    const int nch = (P.N + 1023) / 1024;
+    constexpr int nch = NCH;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         rx[q] = 0.0; ru[q] = 0.0;
@@ -1181,31 +1196,27 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
         }
         __syncthreads();
         const int m = min(BT, cnt - e0);
+#pragma unroll
         for (int ch = 0; ch < nch; ++ch) {
             const int r0 = ch * 1024 + 4 * threadIdx.x;
             if (r0 >= P.N) continue;
-            double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, b0 = 0.0, b1 = 0.0, b2 = 0.0, b3 = 0.0;
-            auto acc = [&](const uint2& w, double va, double vb) {
-                const double d0 = (double)__uint_as_float(w.x << 16), d1 = (double)__uint_as_float(w.x & 0xffff0000u);
-                const double d2 = (double)__uint_as_float(w.y << 16), d3 = (double)__uint_as_float(w.y & 0xffff0000u);
-                a0 = fma(va, d0, a0); a1 = fma(va, d1, a1); a2 = fma(va, d2, a2); a3 = fma(va, d3, a3);
-                b0 = fma(vb, d0, b0); b1 = fma(vb, d1, b1); b2 = fma(vb, d2, b2); b3 = fma(vb, d3, b3);
-            };
+            double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
             int e = 0;
-            for (; e + 8 <= m; e += 8) {
-                uint2 w[8];
+            constexpr int EB = BRESID_EB;    // list entries in flight
+            for (; e + EB <= m; e += EB) {
+                uint2 w[EB];
 #pragma unroll
-                for (int q = 0; q < 8; ++q)
+                for (int q = 0; q < EB; ++q)
                     w[q] = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0));
 #pragma unroll
-                for (int q = 0; q < 8; ++q) acc(w[q], s_a[e + q], s_b[e + q]);
+                for (int q = 0; q < EB; ++q) resid_acc(w[q], s_a[e + q], s_b[e + q], a, b);
             }
             for (; e < m; ++e) {
                 const uint2 w = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e] * P.ldd + r0));
-                acc(w, s_a[e], s_b[e]);
+                resid_acc(w, s_a[e], s_b[e], a, b);
             }
-            rx[ch * 4 + 0] += a0; rx[ch * 4 + 1] += a1; rx[ch * 4 + 2] += a2; rx[ch * 4 + 3] += a3;
-            ru[ch * 4 + 0] += b0; ru[ch * 4 + 1] += b1; ru[ch * 4 + 2] += b2; ru[ch * 4 + 3] += b3;
+#pragma unroll
+            for (int v = 0; v < 4; ++v) { rx[ch * 4 + v] += a[v]; ru[ch * 4 + v] += b[v]; }
         }
     }
     double f2 = 0.0, sq = 0.0, tyv = 0.0;
@@ -1249,6 +1260,11 @@ __global__ void __launch_bounds__(BT) k_bresid(BParams P, int t) {
         P.ty[j] = v3[2];
         if (j == 0) *P.it = t + 1;
     }
+}
+
+static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
+    if (P.N <= 1024) k_bresid<1><<<P.B, BT, 0, s>>>(P, t);
+    else k_bresid<2><<<P.B, BT, 0, s>>>(P, t);
 }
 
 // per-iteration batch aggregates (fixed order)
@@ -1410,7 +1426,7 @@ static int enqueue_iterations(dscr_batched* h, int t0, int n, cudaStream_t s) {
         if (rc) return rc;
         if (P.fused) k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);
         else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
-        k_bresid<<<P.B, BT, 0, s>>>(P, t);
+        launch_bresid(P, t, s);
         k_btrace<<<1, BT, 0, s>>>(P, t);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
@@ -1456,7 +1472,7 @@ int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out) {
     if (P.fused) k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);
     else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
     cudaEventRecord(ev[2], s);
-    k_bresid<<<P.B, BT, 0, s>>>(P, t);
+    launch_bresid(P, t, s);
     cudaEventRecord(ev[3], s);
     cudaEventSynchronize(ev[3]);
     for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
