@@ -14,6 +14,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cub/device/device_segmented_radix_sort.cuh>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -592,6 +593,23 @@ struct BParams {
     float* thr;                // [B] lam_j (1 - 1e-6)
     uint32_t* cmax;            // [B] max |c| over active atoms (float bits)
     int* hot_cnt;              // [B]
+    int* big;                  // [B] observations left to the CTA update (too many entries for a warp)
+    int* nbig;
+    int wu_max;                // largest hot / list count the warp update takes (0: CTA update only)
+    // screening order: atoms of each observation sorted by their test value
+    // v_i = (1 - |cc_i|) / ||a_i|| (descending); at radius rho the screened set is a prefix
+    float* skey;               // [B][K] sorted v (fp32)
+    int* sorder;               // [B][K] atom of each sorted position
+    int* sptr;                 // [B] leading sorted positions already out of the active set
+    float* skey_in;            // setup scratch (aliases C)
+    int* sval_in;              // setup scratch
+    int* soff;                 // [B + 1] segment offsets
+    void* cub_tmp;
+    size_t cub_bytes;
+    // screening work list of an iteration: (item count << 32 | positions) and per item the
+    // observation, its first sorted position and the item's offset in the flattened positions
+    unsigned long long* scr_ctr;
+    int *scr_j, *scr_p, *scr_off;
     int* hot_idx;              // [B][hcap]
     float* hot_val;            // [B][hcap]
     int hcap;
@@ -729,8 +747,12 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
     float m = -INFINITY;   // best (1 - |cc_i|)/||a_i|| of the column
     for (int i = threadIdx.x; i < P.K; i += BT) {
         if (P.test == DSCR_SAFE) P.cc[(size_t)j * P.K + i] = (float)(P.ycorr[(size_t)j * P.K + i] / P.lam[j]);
-        m = fmaxf(m, (float)((1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / P.anorm[i]));
+        const float v = (float)((1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / P.anorm[i]);
+        m = fmaxf(m, v);
+        P.skey_in[(size_t)j * P.K + i] = v;      // sort key of the screening order
+        P.sval_in[(size_t)j * P.K + i] = i;
     }
+    if (threadIdx.x == 0) { P.soff[j] = j * P.K; P.sptr[j] = 0; if (j == P.B - 1) P.soff[P.B] = P.B * P.K; }
     for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
     if ((threadIdx.x & 31) == 0) s_m[threadIdx.x >> 5] = m;
     __syncthreads();
@@ -741,7 +763,7 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
     }
 }
 
-// r_SAFE^2 = ||y/lam - mu theta||^2 (screening.py:115-140) from the residual kernel's
+// r_SAFE^2 = ||y/lam - mu theta||^2 (screening.py:115-141, 189-197) from the residual kernel's
 // exact ||y/lam - mu0 theta||^2 at the unclipped mu0 = <theta,y>/(lam ||theta||^2):
 // y/lam - mu0 theta is orthogonal to theta, so the clipped value adds (mu - mu0)^2 ||theta||^2
 // (two non-negative terms; no cancellation).
@@ -794,7 +816,7 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
         P.thr[j] = (float)(P.lam[j] * (1.0 - 1e-6));
         P.cmax[j] = 0u;
         P.hot_cnt[j] = 0;
-        if (j == 0) *P.it = 0;
+        if (j == 0) { *P.it = 0; *P.nbig = 0; *P.scr_ctr = 0ull; }
     }
 }
 
@@ -1012,14 +1034,114 @@ __device__ __forceinline__ int find_in(const int* a, int n, int key) {
 
 constexpr int LSM = 512;       // old-list entries staged in shared memory (longer lists search global)
 
-__global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
+// Screening at radius rho from the observation's sorted order (keys fl32(v) descending,
+// v_i = (1 - |cc_i|)/||a_i||).  Rounding is monotone, so every atom that can pass the exact
+// fp64 test (v_i - rho > margin, screening.py:359 norm-aware) lies before the first position
+// whose key is below fl32(threshold): that position is found by a 32-ary search, and the range
+// [pointer, end) is tested in parallel.  The result equals testing every active atom.  The
+// pointer then moves to the first position still active (everything before it is screened).
+
+// The screening order is sorted on the top 32 - SORT_BIT0 bits of the radix image of the fp32
+// key (sign-adjusted so unsigned order = float order); okey() is that truncated image, monotone
+// non-decreasing in v, so v > t implies okey(fl32(v)) >= okey(fl32(t)).
+constexpr int SORT_BIT0 = 8;
+__device__ __forceinline__ uint32_t okey(float v) {
+    const uint32_t b = __float_as_uint(v);
+    const uint32_t f = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return f >> SORT_BIT0;
+}
+
+// first position q in (lo, hi] with key[q] < tk (hi if none), keys descending, key[lo] >= tk;
+// one warp, 32 probes per round spread over [lo + 1, hi)
+__device__ __forceinline__ int warp_first_below(const float* key, int lo, int hi, float tk, int lane) {
+    while (hi - lo > 1) {
+        const int span = hi - lo;
+        const int probe = lo + 1 + (int)(((long long)(span - 1) * lane) / 32);
+        const unsigned bal = __ballot_sync(0xffffffffu, okey(key[probe]) < okey(tk));
+        if (bal == 0u) {                 // every probe still at or above: move past the last one
+            lo = lo + 1 + (int)(((long long)(span - 1) * 31) / 32);
+            continue;
+        }
+        const int f = __ffs(bal) - 1;    // first probe below
+        const int nhi = lo + 1 + (int)(((long long)(span - 1) * f) / 32);
+        const int nlo = (f == 0) ? lo : lo + 1 + (int)(((long long)(span - 1) * (f - 1)) / 32);
+        lo = nlo;
+        hi = nhi;
+    }
+    return hi;
+}
+
+struct ScanRange { int p, end; };
+
+__device__ __forceinline__ ScanRange screen_range(const BParams& P, int j, double rho, double margin, int lane) {
+    const float* key = P.skey + (size_t)j * P.K;
+    const float tkey = (float)((rho + margin) - 1e-12 * (1.0 + fabs(rho)));
+    const int p = P.sptr[j];
+    ScanRange r{p, p};
+    if (p < P.K && okey(key[p]) >= okey(tkey)) r.end = warp_first_below(key, p, P.K, tkey, lane);
+    return r;
+}
+
+// Enqueue the observation's screening range [pointer, end) for k_bscreen (lane 0 of the
+// calling warp); the pointer is provisionally moved to end and lowered there by the first
+// position that fails.
+__device__ __forceinline__ void screen_enqueue(const BParams& P, int j, const ScanRange& r, int lane) {
+    if (lane != 0 || r.end <= r.p) return;
+    const unsigned long long old = atomicAdd(P.scr_ctr, (1ull << 32) | (unsigned long long)(r.end - r.p));
+    const int item = (int)(old >> 32);
+    P.scr_j[item] = j;
+    P.scr_p[item] = r.p;
+    P.scr_off[item] = (int)(old & 0xffffffffull);
+    P.sptr[j] = r.end;
+}
+
+// the screening test of one atom (screening.py:359, norm-aware), same fp64 expression as sv
+__device__ __forceinline__ bool screened_now(const BParams& P, int j, int i, double rho, double margin) {
+    return (1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / P.anorm[i] - rho > margin;
+}
+
+// All screening ranges of the iteration, flattened over the whole GPU: exact test per sorted
+// position, mask bits of passing atoms cleared, kept counts lowered
+// (one atomic per group of lanes on the same observation), pointer = first failing position.
+__global__ void __launch_bounds__(256) k_bscreen(BParams P) {
+    const unsigned long long c = *P.scr_ctr;
+    const int items = (int)(c >> 32), T = (int)(c & 0xffffffffull);
+    if (T == 0) return;
+    const double margin = SCREEN_MARGIN + 1e-6;
+    const int lane = threadIdx.x & 31;
+    const int stride = gridDim.x * 256;
+    for (int g0 = blockIdx.x * 256 + (threadIdx.x & ~31); g0 < T; g0 += stride) {
+        const int g = g0 + lane;
+        int j = -1, lost = 0;
+        if (g < T) {
+            int a = 0, b = items;                        // last item with offset <= g
+            while (b - a > 1) { const int m = (a + b) >> 1; if (P.scr_off[m] <= g) a = m; else b = m; }
+            j = P.scr_j[a];
+            const int q = P.scr_p[a] + (g - P.scr_off[a]);
+            const double rho = P.radius[j];
+            const int i = P.sorder[(size_t)j * P.K + q];
+            if (screened_now(P, j, i, rho, margin)) {
+                const uint32_t bit = 1u << (i & 31);
+                const uint32_t old = atomicAnd(&P.mask[(size_t)j * (P.K / 32) + (i >> 5)], ~bit);
+                lost = (old & bit) ? 1 : 0;
+            } else {
+                atomicMin(&P.sptr[j], q);
+            }
+        }
+        const unsigned grp = __match_any_sync(0xffffffffu, j);
+        int tot = 0;
+        for (int o = 0; o < 32; ++o) tot += __shfl_sync(0xffffffffu, lost, o) * (int)((grp >> o) & 1u);
+        if (j >= 0 && lane == __ffs(grp) - 1 && tot) atomicSub(&P.kept[j], tot);
+    }
+}
+
+__device__ void update_hot_cta(const BParams& P, int t, int j) {
     __shared__ int s_idx[HMAX];
     __shared__ float s_val[HMAX];
     __shared__ int s_si[LSM];
     __shared__ double s_sx[LSM], s_su[LSM];
     __shared__ double s_sh[64];
     __shared__ int s_scan[2 * BW + 1];
-    const int j = blockIdx.x;
     const int words = P.K / 32;
     const int par = t & 1;
     const size_t lo = (size_t)j * P.cap;
@@ -1083,24 +1205,8 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     }
     const double margin = SCREEN_MARGIN + 1e-6;
     const bool can_screen = (P.test != DSCR_TEST_OFF) && (ccmin - rho > margin);
-    double kept = (double)kept0;
-    if (can_screen) {       // rare: test every active atom of this observation
-        double lost = 0.0;
-        for (int w = threadIdx.x; w < words; w += BT) {
-            uint32_t m = mrow[w];
-            uint32_t keepw = m;
-            while (m) {
-                const int bit = __ffs(m) - 1;
-                m &= m - 1;
-                const int i = w * 32 + bit;
-                const double ccv = (double)P.cc[(size_t)j * P.K + i];
-                if ((1.0 - fabs(ccv)) / P.anorm[i] - rho > margin) keepw &= ~(1u << bit);   // screening.py:359
-            }
-            if (keepw != mrow[w]) { lost += __popc(mrow[w] ^ keepw); mrow[w] = keepw; }
-        }
-        kept -= block_sum(lost, s_sh);
-        __syncthreads();
-    }
+    const double kept = (double)kept0;     // k_bscreen lowers it by this iteration's screened atoms
+    if (can_screen && threadIdx.x < 32) screen_enqueue(P, j, screen_range(P, j, rho, margin, threadIdx.x), threadIdx.x);
     // hot entries in atom order: prox, momentum, ordered compaction into the new lists
     const double thr = lam / L;
     int ns = 0;
@@ -1111,7 +1217,7 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
         int i = -1;
         if (e < cnt) {
             i = s_idx[e];
-            if ((mrow[i >> 5] >> (i & 31)) & 1u) {
+            if (((mrow[i >> 5] >> (i & 31)) & 1u) && !(can_screen && screened_now(P, j, i, rho, margin))) {
                 const int ps = find_in(si, scnt, i);
                 const double u = ps >= 0 ? su[ps] : 0.0, x = ps >= 0 ? sx[ps] : 0.0;
                 const double c = (double)s_val[e];
@@ -1146,6 +1252,141 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
 }
 
 // sparse residuals D x - y and D u - y; objective, gap, next theta (+ bf16 terms)
+// observations the warp path left (more than WU hot or list entries): one CTA each
+__global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
+    if (blockIdx.x < *P.nbig) update_hot_cta(P, t, P.big[blockIdx.x]);   // one CTA per listed observation
+}
+
+// Warp-per-observation update on the hot entries (the common case: <= WU hot entries and
+// <= WU support-list entries): register bitonic sort of the hot entries by atom, radius from
+// the residual kernel's scalars, prox + momentum, ballot compaction in atom order; no block
+// barriers.  Same arithmetic per entry as update_hot_cta.
+constexpr int WU = 64;
+constexpr int UW = 8;            // observations (warps) per CTA
+
+__device__ __forceinline__ void warp_cas(int& k, float& v, int partner_lane_mask, bool take_min) {
+    const int ok = __shfl_xor_sync(0xffffffffu, k, partner_lane_mask);
+    const float ov = __shfl_xor_sync(0xffffffffu, v, partner_lane_mask);
+    const bool swap = take_min ? (ok < k) : (ok > k);
+    if (swap) { k = ok; v = ov; }
+}
+
+__global__ void __launch_bounds__(UW * 32) k_bupdate_warp(BParams P, int t) {
+    __shared__ int s_si[UW][WU];
+    __shared__ double s_sx[UW][WU], s_su[UW][WU];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int j = blockIdx.x * UW + warp;
+    if (j >= P.B) return;
+    const int par = t & 1;
+    const int hc = P.hot_cnt[j];
+    const int st = P.status[j];
+    const int scnt = P.sn[par][j];
+    if (st != 0) {
+        if (lane == 0) { P.hot_cnt[j] = 0; P.cmax[j] = 0u; }
+        return;
+    }
+    const int cnt = min(hc, P.hcap);
+    if (cnt > P.wu_max || scnt > P.wu_max) {     // the CTA kernel takes it
+        if (lane == 0) P.big[atomicAdd(P.nbig, 1)] = j;
+        return;
+    }
+    const int words = P.K / 32;
+    const size_t lo = (size_t)j * P.cap;
+    uint32_t* mrow = P.mask + (size_t)j * words;
+    uint32_t* nrow = P.nzm + (size_t)j * words;
+    // hot entries: element e = h * 32 + lane, padded with INT_MAX
+    int k0 = INT_MAX, k1 = INT_MAX;
+    float v0 = 0.0f, v1 = 0.0f;
+    if (lane < cnt) { k0 = P.hot_idx[(size_t)j * P.hcap + lane]; v0 = P.hot_val[(size_t)j * P.hcap + lane]; }
+    if (lane + 32 < cnt) { k1 = P.hot_idx[(size_t)j * P.hcap + lane + 32]; v1 = P.hot_val[(size_t)j * P.hcap + lane + 32]; }
+    // old support list (sorted) into this warp's shared memory; clear its atoms in the nonzero bitmap
+    const int* si = P.si[par] + lo;
+    for (int e = lane; e < scnt; e += 32) {
+        const int a = si[e];
+        s_si[warp][e] = a;
+        s_sx[warp][e] = P.sx[par][lo + e];
+        s_su[warp][e] = P.su[par][lo + e];
+        atomicAnd(&nrow[a >> 5], ~(1u << (a & 31)));
+    }
+    // scalars
+    const double lam = P.lam[j], L = P.L;
+    const double sq = P.sq[j], tyv = P.ty[j];
+    const uint32_t cmx = P.cmax[j];
+    const double ccmin = P.ccmin[j], shsq = P.shift_sq[j], beta = P.beta[t];
+    double kept = (double)P.kept[j];
+    // bitonic sort of the 64 (atom, c) pairs by atom
+    for (int k = 2; k <= 64; k <<= 1) {
+        for (int jj = k >> 1; jj > 0; jj >>= 1) {
+            if (jj == 32) {               // partner in the other half of the same lane (k = 64: ascending)
+                if (k1 < k0) { const int tk = k0; k0 = k1; k1 = tk; const float tv = v0; v0 = v1; v1 = tv; }
+            } else {
+                const bool lower = (lane & jj) == 0;
+                const bool up0 = ((lane & k) == 0), up1 = (((lane + 32) & k) == 0);
+                warp_cas(k0, v0, jj, lower == up0);
+                warp_cas(k1, v1, jj, lower == up1);
+            }
+        }
+    }
+    // dual scaling with the inflated correlation bound, radius (screening.py:115-205)
+    const double cinf = (double)__uint_as_float(cmx) + P.err_rel * sqrt(sq);
+    const double bound = (cinf == 0.0) ? INFINITY : 1.0 / cinf;
+    const double mu = (sq != 0.0) ? clip(tyv / (lam * sq), bound) : 0.0;
+    const double rsq = radius_sq(P, j, mu, sq);
+    double rho = NAN;
+    if (P.test == DSCR_SAFE) rho = sqrt(rsq);
+    else if (P.test == DSCR_DST3) {
+        const double arg = rsq - shsq;
+        if (arg < -RADIUS_GUARD && lane == 0) P.status[j] = 3;
+        rho = sqrt(fmax(arg, 0.0));
+    }
+    const double margin = SCREEN_MARGIN + 1e-6;
+    const bool can_screen = P.test != DSCR_TEST_OFF && ccmin - rho > margin;
+    if (can_screen) screen_enqueue(P, j, screen_range(P, j, rho, margin, lane), lane);   // k_bscreen applies it
+    __syncwarp();     // list staging and bitmap clears visible to the whole warp
+    const double thr = lam / L;
+    const int ns = scnt;
+    auto update_entry = [&](int i, float cv, double& cand, double& un) {
+        cand = 0.0; un = 0.0;
+        if (i == INT_MAX || !((mrow[i >> 5] >> (i & 31)) & 1u)) return;
+        if (can_screen && screened_now(P, j, i, rho, margin)) return;     // screened this iteration
+        int a = 0, b = ns;                        // lower bound in the old list
+        while (a < b) { const int m = (a + b) >> 1; if (s_si[warp][m] < i) a = m + 1; else b = m; }
+        const bool hit = a < ns && s_si[warp][a] == i;
+        const double u = hit ? s_su[warp][a] : 0.0, x = hit ? s_sx[warp][a] : 0.0;
+        cand = soft(u - (double)cv / L, thr);
+        un = cand + beta * (cand - x);
+    };
+    double c0, u0, c1, u1;
+    update_entry(k0, v0, c0, u0);
+    update_entry(k1, v1, c1, u1);
+    const bool keep0 = c0 != 0.0 || u0 != 0.0, keep1 = c1 != 0.0 || u1 != 0.0;
+    const unsigned b0 = __ballot_sync(0xffffffffu, keep0), b1 = __ballot_sync(0xffffffffu, keep1);
+    const unsigned ltm = (1u << lane) - 1u;
+    const int p0 = __popc(b0 & ltm), p1 = __popc(b0) + __popc(b1 & ltm);
+    const int total = __popc(b0) + __popc(b1);
+    if (keep0 && p0 < P.cap) {
+        P.si[par ^ 1][lo + p0] = k0; P.sx[par ^ 1][lo + p0] = c0; P.su[par ^ 1][lo + p0] = u0;
+        atomicOr(&nrow[k0 >> 5], 1u << (k0 & 31));
+    }
+    if (keep1 && p1 < P.cap) {
+        P.si[par ^ 1][lo + p1] = k1; P.sx[par ^ 1][lo + p1] = c1; P.su[par ^ 1][lo + p1] = u1;
+        atomicOr(&nrow[k1 >> 5], 1u << (k1 & 31));
+    }
+    const double pen = warp_sum(fabs(c0) + fabs(c1));
+    const double nnz = warp_sum((c0 != 0.0 ? 1.0 : 0.0) + (c1 != 0.0 ? 1.0 : 0.0));
+    if (lane == 0) {
+        if (hc > P.hcap || total > P.cap) P.status[j] = 4;
+        P.sn[par ^ 1][j] = min(total, P.cap);
+        P.pen[j] = pen;
+        P.nnz[j] = (int)nnz;
+        P.kept[j] = (int)kept;
+        P.rsq[j] = rsq;
+        P.radius[j] = rho;
+        P.hot_cnt[j] = 0;       // re-arm for the next GEMM
+        P.cmax[j] = 0u;
+    }
+}
+
 // 4 consecutive bf16 rows of one column (w) times the entry's x and u values
 __device__ __forceinline__ void resid_acc(const uint2& w, double va, double vb, double (&a)[4], double (&b)[4]) {
     const double d[4] = {(double)__uint_as_float(w.x << 16), (double)__uint_as_float(w.x & 0xffff0000u),
@@ -1167,6 +1408,7 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
     __shared__ double s_a[BT], s_b[BT];
     const int j = blockIdx.x;
     const int par = (t + 1) & 1;      // list written by this iteration's update
+    if (j == 0 && threadIdx.x == 0) { *P.nbig = 0; *P.scr_ctr = 0ull; }   // this iteration's lists are consumed
     if (P.status[j] != 0) {
         if (threadIdx.x == 0 && j == 0) *P.it = t + 1;
         return;
@@ -1262,6 +1504,12 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
     }
 }
 
+static void launch_update_hot(const BParams& P, int t, cudaStream_t s) {
+    k_bupdate_warp<<<(P.B + UW - 1) / UW, UW * 32, 0, s>>>(P, t);
+    k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);     // CTAs past the big-list count exit at once
+    k_bscreen<<<4 * 148, 256, 0, s>>>(P);        // this iteration's screening, whole GPU
+}
+
 static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
     if (P.N <= 1024) k_bresid<1><<<P.B, BT, 0, s>>>(P, t);
     else k_bresid<2><<<P.B, BT, 0, s>>>(P, t);
@@ -1304,6 +1552,24 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     BParams p{};
     p.tb = (__nv_bfloat16*)take((size_t)d->splits * B * ly * 2);
     p.C = (float*)take(B * K * 4);
+    p.skey_in = p.C;
+    p.skey = (float*)take(B * K * 4);
+    p.sorder = (int*)take(B * K * 4);
+    p.sval_in = (int*)take(B * K * 4);
+    p.soff = (int*)take((B + 1) * 4);
+    p.sptr = (int*)take(B * 4);
+    p.scr_ctr = (unsigned long long*)take(8);
+    p.scr_j = (int*)take(B * 4);
+    p.scr_p = (int*)take(B * 4);
+    p.scr_off = (int*)take(B * 4);
+    {
+        size_t tb = 0;
+        cub::DeviceSegmentedRadixSort::SortPairsDescending((void*)nullptr, tb, (const float*)nullptr, (float*)nullptr,
+                                                           (const int*)nullptr, (int*)nullptr, (int)(B * K), (int)B,
+                                                           (const int*)nullptr, (const int*)nullptr);
+        p.cub_bytes = tb;
+        p.cub_tmp = take(tb + 256);
+    }
     p.cc = (float*)take(B * K * 4);
     p.ycorr = (double*)take(B * K * 8);
     p.astar = (double*)take(B * ly * 8);
@@ -1325,6 +1591,8 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     p.thr = (float*)take(B * 4);
     p.cmax = (uint32_t*)take(B * 4);
     p.hot_cnt = (int*)take(B * 4);
+    p.big = (int*)take(B * 4);
+    p.nbig = (int*)take(4);
     p.hcap = 2048;
     p.hot_idx = (int*)take(B * (size_t)p.hcap * 4);
     p.hot_val = (float*)take(B * (size_t)p.hcap * 4);
@@ -1368,6 +1636,8 @@ int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void
         const bool fp64 = ev && !strcmp(ev, "fp64");
         P.oz = (!fp64 && d->n_rows % OZ_BK == 0 && d->n_rows <= 2048 && d->n_obs % OZ_BN == 0 &&
                 d->n_atoms % OZ_BM == 0) ? 1 : 0;
+        const char* eu = getenv("DSCR_BATCHED_UPDATE");   // "cta": every observation on the CTA update
+        P.wu_max = (eu && !strcmp(eu, "cta")) ? 0 : WU;
     }
     // |c~ - c| <= ||d_i|| (||theta - theta~|| + fp32 accumulation) <= err_rel ||theta||
     P.err_rel = (d->splits == 1 ? 0.00391 : 1.6e-5) + 2.0 * d->n_rows * 5.96e-8;
@@ -1409,7 +1679,13 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
         k_blmax<<<P.B, BT, 0, s>>>(P);
         if (P.test == DSCR_DST3) k_dgemm_corr<<<g, 256, 0, s>>>(P, P.astar, P.ldy, nullptr, 1);   // cc = y/lam - shift a_*
     }
-    if (P.test != DSCR_TEST_OFF) k_bcc<<<P.B, BT, 0, s>>>(P);
+    if (P.test != DSCR_TEST_OFF) {
+        k_bcc<<<P.B, BT, 0, s>>>(P);
+        size_t tb = P.cub_bytes;
+        cudaError_t ce = cub::DeviceSegmentedRadixSort::SortPairsDescending(
+            P.cub_tmp, tb, P.skey_in, P.skey, P.sval_in, P.sorder, P.B * P.K, P.B, P.soff, P.soff + 1, SORT_BIT0, 32, s);
+        if (ce != cudaSuccess) { err_store() = cudaGetErrorString(ce); return DSCR_ECUDA; }
+    }
     k_binit<<<P.B, BT, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
@@ -1424,7 +1700,7 @@ static int enqueue_iterations(dscr_batched* h, int t0, int n, cudaStream_t s) {
     for (int t = t0; t < t0 + n; ++t) {
         int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s, P.fused ? &fz : nullptr);
         if (rc) return rc;
-        if (P.fused) k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);
+        if (P.fused) launch_update_hot(P, t, s);
         else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
         launch_bresid(P, t, s);
         k_btrace<<<1, BT, 0, s>>>(P, t);
@@ -1469,7 +1745,7 @@ int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out) {
     cudaEventRecord(ev[0], s);
     int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s, P.fused ? &fz : nullptr);
     cudaEventRecord(ev[1], s);
-    if (P.fused) k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);
+    if (P.fused) launch_update_hot(P, t, s);
     else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
     cudaEventRecord(ev[2], s);
     launch_bresid(P, t, s);

@@ -217,3 +217,18 @@ def test_integer_slice_setup_matches_fp64_setup(ratio, monkeypatch):
     np.testing.assert_allclose(a.gap, b.gap, rtol=1e-9, atol=1e-12)
     for j in range(0, 512, 41):
         assert np.array_equal(a.x_idx[j], b.x_idx[j])
+
+
+@pytest.mark.parametrize("ratio", [0.4, 0.85])
+def test_warp_update_matches_cta_update(ratio, monkeypatch):
+    """Warp-per-observation update (<= 64 hot/list entries) vs the CTA update for every
+    observation: same lists, screening and trace (penalty sums differ only in reduction order)."""
+    w, dic, D64, L = _batch_problem(256, 2048, 512, ratio, seed=9)
+    a = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    monkeypatch.setenv("DSCR_BATCHED_UPDATE", "cta")
+    b = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    assert np.array_equal(a.kept, b.kept) and np.array_equal(a.nnz, b.nnz)
+    np.testing.assert_allclose(a.objective, b.objective, rtol=1e-13)
+    for j in range(0, 512, 23):
+        assert np.array_equal(a.x_idx[j], b.x_idx[j])
+        np.testing.assert_allclose(a.x_val[j], b.x_val[j], rtol=1e-13, atol=1e-15)
