@@ -35,7 +35,7 @@ constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTE
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int GEMM_THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int EPI_THREADS = GEMM_THREADS - 64;
-constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 16 * BN + 64;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 32 * BN + 64;
 
 struct GemmArgs {
     int Nb;          // observations per split (rows of one Theta block)
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
         const int q = warp & 3;
         const int half = (warp - 2) >> 2;                             // which half of the tile's columns
-        uint32_t* s_cm = reinterpret_cast<uint32_t*>(tslot + 1);     // [4 quarters][BN] tile max per observation
+        uint32_t* s_cm0 = reinterpret_cast<uint32_t*>(tslot + 1);    // [2 parities][4 quarters][BN] tile max per observation
         const int et = threadIdx.x - 64;                              // 0..EPI_THREADS-1
         constexpr int KC = BN / 64;                                   // 32-column chunks per warp
         int lt = 0;
@@ -161,29 +161,38 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int m0 = mb * BM + q * 32;                  // this warp's 32 atoms
             const int m = m0 + lane;
             const int cbase = half * (BN / 2);
-            // per-observation words of this warp's columns, fetched before waiting on the accumulator
-            uint32_t wa[KC], wn[KC];
-            float th[KC];
-#pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const int jl = nb * BN + cbase + k * 32 + lane;
-                wa[k] = g.mask[(size_t)jl * g.words + (m0 >> 5)];
-                wn[k] = g.nzm[(size_t)jl * g.words + (m0 >> 5)];
-                th[k] = g.thr[jl];
+            uint32_t* s_cm = s_cm0 + ab * 4 * BN;   // double-buffered by tile parity: one barrier per tile
+            // per-observation words of this warp's columns: chunk 0 fetched before waiting on the
+            // accumulator, chunk k+1 while chunk k is processed (rotating scalars, no local memory)
+            uint32_t wa_c, wn_c;
+            float th_c;
+            {
+                const int jl = nb * BN + cbase + lane;
+                wa_c = g.mask[(size_t)jl * g.words + (m0 >> 5)];
+                wn_c = g.nzm[(size_t)jl * g.words + (m0 >> 5)];
+                th_c = g.thr[jl];
             }
             mbar_wait(&tfull[ab], aphase);
             tc_fence_after();
 #pragma unroll 1
             for (int k = 0; k < KC; ++k) {
+                uint32_t wa_n = 0u, wn_n = 0u;
+                float th_n = 0.0f;
+                if (k + 1 < KC) {
+                    const int jl = nb * BN + cbase + (k + 1) * 32 + lane;
+                    wa_n = g.mask[(size_t)jl * g.words + (m0 >> 5)];
+                    wn_n = g.nzm[(size_t)jl * g.words + (m0 >> 5)];
+                    th_n = g.thr[jl];
+                }
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + cbase + k * 32, r);
                 // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms
                 uint32_t hotbits = 0u, mymax = 0u;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const uint32_t wai = __shfl_sync(0xffffffffu, wa[k], i);
-                    const uint32_t wni = __shfl_sync(0xffffffffu, wn[k], i);
-                    const float thi = __shfl_sync(0xffffffffu, th[k], i);
+                    const uint32_t wai = __shfl_sync(0xffffffffu, wa_c, i);
+                    const uint32_t wni = __shfl_sync(0xffffffffu, wn_c, i);
+                    const float thi = __shfl_sync(0xffffffffu, th_c, i);
                     const float a = fabsf(__uint_as_float(r[i]));
                     const bool act = (wai >> lane) & 1u;
                     const uint32_t mv = __reduce_max_sync(0xffffffffu, act ? __float_as_uint(a) : 0u);
@@ -206,6 +215,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                         }
                     }
                 }
+                wa_c = wa_n; wn_c = wn_n; th_c = th_n;
             }
             tc_fence_before();
             mbar_arrive(&tempty[ab]);
@@ -214,7 +224,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 const uint32_t v = max(max(s_cm[i], s_cm[BN + i]), max(s_cm[2 * BN + i], s_cm[3 * BN + i]));
                 if (v) atomicMax(&g.cmax[nb * BN + i], v);
             }
-            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
         }
     }
     tc_fence_before();
