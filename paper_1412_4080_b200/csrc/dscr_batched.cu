@@ -35,7 +35,7 @@ constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTE
 constexpr int TMEM_COLS = 2 * BN;
 constexpr int GEMM_THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
 constexpr int EPI_THREADS = GEMM_THREADS - 64;
-constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 32 * BN + 64;
+constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 64;
 
 struct GemmArgs {
     int Nb;          // observations per split (rows of one Theta block)
@@ -56,6 +56,10 @@ struct GemmArgs {
     int words;              // M/32
 };
 
+// CL: CTA pairs (2-CTA clusters along the atom blocks) share each Theta tile: every CTA loads
+// its half of the tile with TMA multicast into both CTAs' shared memory, and the MMA commit
+// releases the stage in both CTAs (empty barriers count 2).  Halves the Theta L2 traffic.
+template <bool CL>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_dt(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
     extern __shared__ uint8_t smem_raw[];
@@ -69,10 +73,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint32_t* tslot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+    const uint32_t crank = CL ? cluster_rank() : 0u;
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL ? 2 : 1); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_THREADS); }
         fence_barrier_init();
     }
@@ -80,21 +85,35 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (CL) cluster_sync();          // peer barriers initialised before any multicast / remote arrive
     const uint32_t tmem = *tslot;
     const int kbs = g.KB * g.S;
+    // tile sequence of this CTA: pairs of atom blocks per cluster when clustered
+    const int t_first = CL ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+    const int t_step = CL ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+    const int t_count = CL ? g.num_tiles / 2 : g.num_tiles;
+    auto tile_mn = [&](int tt, int& mb, int& nb) {
+        if (CL) { const int hm = g.num_m >> 1; mb = 2 * (tt % hm) + (int)crank; nb = tt / hm; }
+        else { mb = tt % g.num_m; nb = tt / g.num_m; }
+    };
 
     if (warp == 0) {
         if (lane == 0) {   // ---- TMA producer
             int stage = 0;
             uint32_t phase = 0;
-            for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
-                const int mb = tile % g.num_m, nb = tile / g.num_m;
+            for (int tt = t_first; tt < t_count; tt += t_step) {
+                int mb, nb;
+                tile_mn(tt, mb, nb);
                 for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_expect_tx(&full[stage], STAGE_BYTES);
                     const int s = kb / g.KB, k = (kb % g.KB) * BK;
                     tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], k, mb * BM);
-                    tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], k, s * g.Nb + nb * BN);
+                    if (CL)
+                        tma_load_2d_mc(sB + stage * B_BYTES + crank * (B_BYTES / 2), &tmB, &full[stage], k,
+                                       s * g.Nb + nb * BN + (int)crank * (BN / 2), (uint16_t)0x3);
+                    else
+                        tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], k, s * g.Nb + nb * BN);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
             }
@@ -105,7 +124,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             int stage = 0;
             uint32_t phase = 0;
             int lt = 0;
-            for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++lt) {
+            for (int tt = t_first; tt < t_count; tt += t_step, ++lt) {
                 const int ab = lt & 1;
                 const uint32_t aphase = (lt >> 1) & 1;
                 mbar_wait(&tempty[ab], aphase ^ 1);
@@ -119,7 +138,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the swizzle atom
                         mma_bf16(dcol, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-                    mma_commit(&empty[stage]);
+                    if (CL) mma_commit_mc(&empty[stage], (uint16_t)0x3);   // release the stage in both CTAs
+                    else mma_commit(&empty[stage]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
                 }
                 mma_commit(&tfull[ab]);
@@ -129,8 +149,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int q = warp & 3;   // TMEM lane quarter this warp may access
         const int half = (warp - 2) >> 2;   // which half of the tile's columns
         int lt = 0;
-        for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++lt) {
-            const int mb = tile % g.num_m, nb = tile / g.num_m;
+        for (int tt = t_first; tt < t_count; tt += t_step, ++lt) {
+            int mb, nb;
+            tile_mn(tt, mb, nb);
             const int ab = lt & 1;
             const uint32_t aphase = (lt >> 1) & 1;
             mbar_wait(&tfull[ab], aphase);
@@ -150,18 +171,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
         const int q = warp & 3;
         const int half = (warp - 2) >> 2;                             // which half of the tile's columns
-        uint32_t* s_cm0 = reinterpret_cast<uint32_t*>(tslot + 1);    // [2 parities][4 quarters][BN] tile max per observation
-        const int et = threadIdx.x - 64;                              // 0..EPI_THREADS-1
         constexpr int KC = BN / 64;                                   // 32-column chunks per warp
         int lt = 0;
-        for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++lt) {
-            const int mb = tile % g.num_m, nb = tile / g.num_m;
+        for (int tt = t_first; tt < t_count; tt += t_step, ++lt) {
+            int mb, nb;
+            tile_mn(tt, mb, nb);
             const int ab = lt & 1;
             const uint32_t aphase = (lt >> 1) & 1;
             const int m0 = mb * BM + q * 32;                  // this warp's 32 atoms
             const int m = m0 + lane;
             const int cbase = half * (BN / 2);
-            uint32_t* s_cm = s_cm0 + ab * 4 * BN;   // double-buffered by tile parity: one barrier per tile
             // per-observation words of this warp's columns: chunk 0 fetched before waiting on the
             // accumulator, chunk k+1 while chunk k is processed (rotating scalars, no local memory)
             uint32_t wa_c, wn_c;
@@ -200,7 +219,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     const bool hot = act && (a > thi || ((wni >> lane) & 1u));
                     hotbits |= (hot ? 1u : 0u) << i;
                 }
-                s_cm[q * BN + cbase + k * 32 + lane] = mymax;
+                if (mymax) atomicMax(&g.cmax[nb * BN + cbase + k * 32 + lane], mymax);   // reduction, no return
                 // pass 2 (rare): append the hot entries of this lane's atom
                 if (__any_sync(0xffffffffu, hotbits != 0u)) {
 #pragma unroll
@@ -219,16 +238,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             tc_fence_before();
             mbar_arrive(&tempty[ab]);
-            asm volatile("bar.sync 1, %0;" ::"n"(EPI_THREADS) : "memory");
-            for (int i = et; i < BN; i += EPI_THREADS) {
-                const uint32_t v = max(max(s_cm[i], s_cm[BN + i]), max(s_cm[2 * BN + i], s_cm[3 * BN + i]));
-                if (v) atomicMax(&g.cmax[nb * BN + i], v);
-            }
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    if (CL) cluster_sync();          // no CTA leaves while its peer may still arrive on its barriers
     if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
 }
 
@@ -275,10 +290,12 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
         err_store() = "batched gemm: need M%128==0, N%256==0, K%64==0, 16-byte aligned rows";
         return DSCR_EINVAL;
     }
+    const char* ecl = getenv("DSCR_GEMM_CLUSTER");
+    const bool cl = (M / BM) % 2 == 0 && !(ecl && !strcmp(ecl, "0"));
     CUtensorMap ma, mb;
     int rc = make_map(&ma, A, K, M, lda, BK, BM);
     if (rc) return rc;
-    rc = make_map(&mb, B, K, Nb * S, ldb, BK, BN);
+    rc = make_map(&mb, B, K, Nb * S, ldb, BK, cl ? BN / 2 : BN);
     if (rc) return rc;
     GemmArgs g{};
     g.Nb = Nb;
@@ -297,9 +314,27 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaError_t e = cudaFuncSetAttribute(k_gemm_dt, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
-    if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
-    k_gemm_dt<<<std::min(g.num_tiles, sms), GEMM_THREADS, GEMM_SMEM, s>>>(ma, mb, g);
+    cudaError_t e;
+    if (cl) {
+        e = cudaFuncSetAttribute(k_gemm_dt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+        if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(std::min(g.num_tiles, sms & ~1));
+        lc.blockDim = dim3(GEMM_THREADS);
+        lc.dynamicSmemBytes = GEMM_SMEM;
+        lc.stream = s;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        lc.attrs = at;
+        lc.numAttrs = 1;
+        e = cudaLaunchKernelEx(&lc, k_gemm_dt<true>, ma, mb, g);
+        if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+    } else {
+        e = cudaFuncSetAttribute(k_gemm_dt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+        if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+        k_gemm_dt<false><<<std::min(g.num_tiles, sms), GEMM_THREADS, GEMM_SMEM, s>>>(ma, mb, g);
+    }
     e = cudaGetLastError();
     if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     return DSCR_OK;
