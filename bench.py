@@ -456,6 +456,11 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         its, h2d, d2h = 0, 0, 0
+        for _ in range(min(args.warmup, 1)):    # untimed: first-use allocations (one solve per problem)
+            for p, c in problems:
+                p.dictionary.drop_device()
+                p.dictionary.__dict__.pop("_problem_cache", None)
+                ds.run(p, c, device=dev)
         torch.cuda.synchronize()
         barrier()
         t0 = time.perf_counter()
@@ -605,6 +610,9 @@ def run_c5(args):
     achieved = flop / (ms[0] / 1e3) / 1e12
     e2e = None
     if not args.no_e2e:
+        for _ in range(args.warmup):       # untimed: first-use allocations and kernel loads
+            dic.drop_device()
+            solve_batched(dic, w.y, w.lam, L, iterations=iters, test="dst3", splits=args.splits)
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         for _ in range(args.steps):
@@ -645,7 +653,10 @@ def run_c5(args):
                          "frac": achieved / peak, "traffic": None, "peak_source": src,
                          "kernel": "k_gemm_dt (tcgen05)", "kernel_ms": ms[0], "flop_per_launch": flop,
                          "per_kernel_ms": list(ms)},
-            "gpu_launches": args.steps * (iters * 4 + 5),
+            # ours per step: 9 setup kernels (norms, 2 slicings, 2 integer-slice GEMMs, lambda_*, gather,
+            # centres, init; the CUB sort is library code) + 6 per iteration (GEMM, warp update, CTA
+            # update, screening, residual, trace)
+            "gpu_launches": args.steps * (iters * 6 + 9),
             "clocks": clocks.summary(), "e2e": e2e, "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)

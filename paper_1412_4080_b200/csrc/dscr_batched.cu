@@ -541,11 +541,11 @@ __global__ void __launch_bounds__(256) k_gather_slices(const int8_t* Ds, const i
     }
 }
 
-// pairs (s, t), s < S, t < T, s + t <= OZ_DMAX, in diagonal order
-static void oz_pairs(OzArgs& g, int S, int T) {
+// pairs (s, t), s < S, t < T, s + t <= dmax (<= OZ_DMAX), in diagonal order
+static void oz_pairs(OzArgs& g, int S, int T, int dmax) {
     g.np = 0;
     g.nd = 0;
-    for (int d = 0; d <= OZ_DMAX; ++d) {
+    for (int d = 0; d <= dmax; ++d) {
         for (int s = 0; s < S; ++s) {
             const int t = d - s;
             if (t < 0 || t >= T) continue;
@@ -558,7 +558,8 @@ static void oz_pairs(OzArgs& g, int S, int T) {
 }
 
 // A slices [S][K][N], B slices [T][B][N]; K, B, N multiples of 128
-static int ozaki_launch(const int8_t* As, int K, int S, const int8_t* Bs, int B, int T, int N, OzArgs& g, cudaStream_t s) {
+static int ozaki_launch(const int8_t* As, int K, int S, const int8_t* Bs, int B, int T, int N, OzArgs& g, cudaStream_t s,
+                        int dmax = OZ_DMAX) {
     if (K % OZ_BM || B % OZ_BN || N % OZ_BK || N > 2048) {
         err_store() = "exact correlation: need atoms, observations, rows multiples of 128 and rows <= 2048";
         return DSCR_EINVAL;
@@ -568,7 +569,7 @@ static int ozaki_launch(const int8_t* As, int K, int S, const int8_t* Bs, int B,
     if (rc) return rc;
     rc = make_map(&mb, Bs, N, T * B, N, OZ_BK, OZ_BN, CU_TENSOR_MAP_DATA_TYPE_UINT8, 1);
     if (rc) return rc;
-    oz_pairs(g, S, T);
+    oz_pairs(g, S, T, std::min(dmax, OZ_DMAX));
     g.K = K;
     g.B = B;
     g.KB = N / OZ_BK;
@@ -1703,10 +1704,13 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
     k_bnorms<<<std::max(1, P.K / BW / 4), BT, 0, s>>>(P);
     if (P.oz) {   // exact slice products on the integer tensor cores
         k_slice_rows<<<P.K / 8, 256, 0, s>>>(P.Dt, P.K, P.N, P.ldd, OZ_SD, P.Ds, P.eD);
-        k_slice_rows<<<P.B / 8, 256, 0, s>>>(P.Y, P.B, P.N, P.ldy, OZ_SV, P.Vs, P.eV);
+        // The centre correlations are stored in fp32 and tested with a 1e-6 slack, and lambda_* is
+        // recomputed in fp64: y keeps 28 bits (T = 4) and pairs with s + t <= 4 (13 pairs), the
+        // D^T a_* products s + t <= 3 (10 pairs); errors ~1e-9, three orders inside the slack.
+        k_slice_rows<<<P.B / 8, 256, 0, s>>>(P.Y, P.B, P.N, P.ldy, 4, P.Vs, P.eV);
         OzArgs oa{};
         oa.eA = P.eD; oa.eB = P.eV; oa.mode = 0; oa.out = P.ycorr; oa.ldo = P.K;
-        int rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, OZ_SV, P.N, oa, s);   // D^T y_j
+        int rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, 4, P.N, oa, s, 4);   // D^T y_j
         if (rc) return rc;
         k_blmax<<<P.B, BT, 0, s>>>(P);
         if (P.test == DSCR_DST3) {   // cc = y/lam - shift a_* (a_* = dictionary row: exact slices)
@@ -1715,7 +1719,7 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
             ob.eA = P.eD; ob.eB = P.eV; ob.mode = 1;
             ob.ycorr = P.ycorr; ob.lam = P.lam; ob.lmax = P.lmax; ob.anorm = P.anorm; ob.sgn = P.sgn;
             ob.istar = P.istar; ob.cc = P.cc;
-            rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, OZ_SD, P.N, ob, s);
+            rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, OZ_SD, P.N, ob, s, 3);
             if (rc) return rc;
         }
     } else {
