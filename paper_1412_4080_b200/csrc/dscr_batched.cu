@@ -1446,11 +1446,16 @@ __device__ __forceinline__ void resid_acc(const uint2& w, double va, double vb, 
 #ifndef BRESID_MINB
 #define BRESID_MINB 5
 #endif
-template <int NCH>      // 1024-row chunks (N <= NCH * 1024)
-__global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BParams P, int t) {
+template <int NCH, int TPB>      // chunks of 4 * TPB rows (N <= NCH * 4 * TPB), TPB threads
+#ifndef BRESID_MINB128
+#define BRESID_MINB128 8
+#endif
+__global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2) : (NCH <= 2 ? BRESID_MINB128 : 4))
+    k_bresid(BParams P, int t) {
+    constexpr int RC = 4 * TPB;      // rows per chunk
     __shared__ double s_sh[64];
-    __shared__ int s_idx[BT];
-    __shared__ double s_a[BT], s_b[BT];
+    __shared__ int s_idx[TPB];
+    __shared__ double s_a[TPB], s_b[TPB];
     const int j = blockIdx.x;
     const int par = (t + 1) & 1;      // list written by this iteration's update
     if (j == 0 && threadIdx.x == 0) { *P.nbig = 0; *P.scr_ctr = 0ull; }   // this iteration's lists are consumed
@@ -1459,7 +1464,7 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
         return;
     }
     const size_t lo = (size_t)j * P.cap;
-    // thread t owns rows 4t..4t+3 (+1024 for the second chunk); one pass over the support list
+    // thread t owns rows 4t..4t+3 of each RC-row chunk; one pass over the support list
     // (x and u share each column load), one 8-byte load per entry and chunk, 8 entries in flight
     constexpr int RPT = 4 * NCH;      // rows per thread
     double rx[RPT], ru[RPT], yv[RPT];
@@ -1467,14 +1472,14 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         rx[q] = 0.0; ru[q] = 0.0;
-        const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
+        const int n = (q >> 2) * RC + 4 * threadIdx.x + (q & 3);
         yv[q] = (n < P.N) ? P.Y[(size_t)j * P.ldy + n] : 0.0;       // independent of the list: issue early
     }
     const int* idx = P.si[par] + lo;
     const double* xa = P.sx[par] + lo;
     const double* ub = P.su[par] + lo;
     const int cnt = P.sn[par][j];
-    for (int e0 = 0; e0 < cnt; e0 += BT) {
+    for (int e0 = 0; e0 < cnt; e0 += TPB) {
         __syncthreads();
         if (e0 + threadIdx.x < cnt) {
             s_idx[threadIdx.x] = idx[e0 + threadIdx.x];
@@ -1482,10 +1487,10 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
             s_b[threadIdx.x] = ub[e0 + threadIdx.x];
         }
         __syncthreads();
-        const int m = min(BT, cnt - e0);
+        const int m = min(TPB, cnt - e0);
 #pragma unroll
         for (int ch = 0; ch < nch; ++ch) {
-            const int r0 = ch * 1024 + 4 * threadIdx.x;
+            const int r0 = ch * RC + 4 * threadIdx.x;
             if (r0 >= P.N) continue;
             double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
             int e = 0;
@@ -1509,7 +1514,7 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
     double f2 = 0.0, sq = 0.0, tyv = 0.0;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-        const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
+        const int n = (q >> 2) * RC + 4 * threadIdx.x + (q & 3);
         if (n < P.N) {
             const double yn = yv[q];
             const double qa = rx[q] - yn;
@@ -1522,21 +1527,25 @@ __global__ void __launch_bounds__(BT, NCH == 1 ? BRESID_MINB : 2) k_bresid(BPara
             ru[q] = tn;
         }
     }
-    for (int n = P.N + threadIdx.x; n < P.ldy; n += BT) write_theta(P, j, n, 0.0);
+    for (int n = P.N + threadIdx.x; n < P.ldy; n += TPB) write_theta(P, j, n, 0.0);
     double v3[3] = {f2, sq, tyv};
-    block_sum_n<3>(v3, s_sh);
+    block_sum_nt<3, TPB>(v3, s_sh);
     const double lam = P.lam[j];
     const double mu0 = (v3[1] != 0.0) ? v3[2] / (lam * v3[1]) : 0.0;
     double d2 = 0.0;
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
-        const int n = (q >> 2) * 1024 + 4 * threadIdx.x + (q & 3);
+        const int n = (q >> 2) * RC + 4 * threadIdx.x + (q & 3);
         if (n < P.N) {
             const double d = rx[q] / lam - mu0 * ru[q];
             d2 = fma(d, d, d2);
         }
     }
-    d2 = block_sum(d2, s_sh);
+    {
+        double d1[1] = {d2};
+        block_sum_nt<1, TPB>(d1, s_sh);
+        d2 = d1[0];
+    }
     if (threadIdx.x == 0) {
         P.mu0[j] = mu0;
         P.rsq0[j] = d2;
@@ -1555,20 +1564,44 @@ static void launch_update_hot(const BParams& P, int t, cudaStream_t s) {
     k_bscreen<<<4 * 148, 256, 0, s>>>(P);        // this iteration's screening, whole GPU
 }
 
+#ifndef BRESID_TPB
+#define BRESID_TPB 256
+#endif
 static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
-    if (P.N <= 1024) k_bresid<1><<<P.B, BT, 0, s>>>(P, t);
-    else k_bresid<2><<<P.B, BT, 0, s>>>(P, t);
+    constexpr int TPB = BRESID_TPB;
+    constexpr int RC = 4 * TPB;
+    if (P.N <= RC) k_bresid<1, TPB><<<P.B, TPB, 0, s>>>(P, t);
+    else if (P.N <= 2 * RC) k_bresid<2, TPB><<<P.B, TPB, 0, s>>>(P, t);
+    else if (P.N <= 3 * RC) k_bresid<3, TPB><<<P.B, TPB, 0, s>>>(P, t);
+    else k_bresid<4, TPB><<<P.B, TPB, 0, s>>>(P, t);
 }
 
-// per-iteration batch aggregates (fixed order)
-__global__ void __launch_bounds__(BT) k_btrace(BParams P, int t) {
-    __shared__ double s_sh[64];
+// per-iteration batch aggregates (fixed order): 1024 threads, loads of 4 observations in flight
+constexpr int TR_T = 1024;
+__global__ void __launch_bounds__(TR_T) k_btrace(BParams P, int t) {
+    __shared__ double s_sh[4 * (TR_T / 32)];
     double a[4] = {0, 0, 0, 0};
-    for (int j = threadIdx.x; j < P.B; j += BT) {
-        if (P.status[j] != 0) continue;
-        a[0] += P.F[j]; a[1] += P.gap[j]; a[2] += P.nnz[j]; a[3] += P.kept[j];
+    for (int j0 = threadIdx.x; j0 < P.B; j0 += 4 * TR_T) {
+        int st[4];
+        double f[4], gp[4];
+        int nz[4], kp[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int j = j0 + u * TR_T;
+            const bool ok = j < P.B;
+            st[u] = ok ? P.status[j] : 1;
+            f[u] = ok ? P.F[j] : 0.0;
+            gp[u] = ok ? P.gap[j] : 0.0;
+            nz[u] = ok ? P.nnz[j] : 0;
+            kp[u] = ok ? P.kept[j] : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (st[u] != 0) continue;
+            a[0] += f[u]; a[1] += gp[u]; a[2] += nz[u]; a[3] += kp[u];
+        }
     }
-    block_sum_n<4>(a, s_sh);
+    block_sum_nt<4, TR_T>(a, s_sh);
     if (threadIdx.x == 0)
         for (int q = 0; q < 4; ++q) P.trace[(size_t)t * 4 + q] = a[q];
 }
@@ -1751,7 +1784,7 @@ static int enqueue_iterations(dscr_batched* h, int t0, int n, cudaStream_t s) {
         if (P.fused) launch_update_hot(P, t, s);
         else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
         launch_bresid(P, t, s);
-        k_btrace<<<1, BT, 0, s>>>(P, t);
+        k_btrace<<<1, TR_T, 0, s>>>(P, t);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     }

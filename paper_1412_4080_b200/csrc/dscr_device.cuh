@@ -164,6 +164,29 @@ __device__ __forceinline__ void block_sum_n(double (&v)[M], double* sh) {
     __syncthreads();
 }
 
+// block_sum_n for a CTA of TPB threads (TPB a multiple of 32); sh holds (TPB/32)*M doubles
+template <int M, int TPB>
+__device__ __forceinline__ void block_sum_nt(double (&v)[M], double* sh) {
+    constexpr int W = TPB / 32;
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = warp_sum(v[m]);
+    __syncthreads();
+    if (l == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) sh[m * W + w] = v[m];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        double r = 0.0;
+#pragma unroll
+        for (int q = 0; q < W; ++q) r += sh[m * W + q];
+        v[m] = r;
+    }
+    __syncthreads();
+}
+
 // Exclusive scan of an int over the CTA; returns prefix, *total gets the sum.
 __device__ __forceinline__ int block_exscan(int v, int* sh, int* total) {
     const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
