@@ -56,19 +56,29 @@ struct GemmArgs {
     int words;              // M/32
 };
 
-// CL: CTA pairs (2-CTA clusters along the atom blocks) share each Theta tile: every CTA loads
-// its half of the tile with TMA multicast into both CTAs' shared memory, and the MMA commit
-// releases the stage in both CTAs (empty barriers count 2).  Halves the Theta L2 traffic.
-template <bool CL>
+// MODE 0: one CTA per tile (128 atoms x 256 observations).
+// MODE 1: 2-CTA clusters along the atom blocks share each Theta tile: every CTA loads its half
+//   with TMA multicast into both CTAs' shared memory; the MMA commit releases the stage in both
+//   CTAs (empty barriers count 2).
+// MODE 2: CTA pair (cta_group::2): the pair computes a 256 x 256 tile with one
+//   tcgen05.mma.cta_group::2 stream issued by the leader (rank 0).  Each CTA holds its 128 atom
+//   rows and half of the Theta tile (6 stages x 32 KB); both CTAs' TMA complete on the leader's
+//   full barrier; the leader's commits are multicast to both CTAs' empty / TMEM-full barriers;
+//   each CTA's TMEM holds its 128 rows x 256 columns and both epilogues arrive on the leader's
+//   TMEM-empty barrier.
+template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_dt(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
+    constexpr bool CL = MODE >= 1, TWO = MODE == 2;
+    constexpr int NSTG = TWO ? 6 : STAGES;
+    constexpr int SB_BYTES = TWO ? B_BYTES / 2 : B_BYTES;   // Theta bytes per stage in this CTA
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* sA = base;
-    uint8_t* sB = base + STAGES * A_BYTES;
-    uint64_t* full = (uint64_t*)(sB + STAGES * B_BYTES);
-    uint64_t* empty = full + STAGES;
-    uint64_t* tfull = empty + STAGES;
+    uint8_t* sB = base + NSTG * A_BYTES;
+    uint64_t* full = (uint64_t*)(sB + NSTG * SB_BYTES);
+    uint64_t* empty = full + NSTG;
+    uint64_t* tfull = empty + NSTG;
     uint64_t* tempty = tfull + 2;
     uint32_t* tslot = (uint32_t*)(tempty + 2);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -77,11 +87,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmB);
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL ? 2 : 1); }
-        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], EPI_THREADS); }
+        for (int s = 0; s < NSTG; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], MODE == 1 ? 2 : 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], TWO ? 2 * (EPI_THREADS / 32) : EPI_THREADS); }
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc(tslot, TMEM_COLS);
+    if (warp == 1) {
+        if (TWO) tmem_alloc_2sm(tslot, TMEM_COLS);
+        else tmem_alloc(tslot, TMEM_COLS);
+    }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -106,21 +119,28 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 tile_mn(tt, mb, nb);
                 for (int kb = 0; kb < kbs; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_expect_tx(&full[stage], STAGE_BYTES);
                     const int s = kb / g.KB, k = (kb % g.KB) * BK;
-                    tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], k, mb * BM);
-                    if (CL)
-                        tma_load_2d_mc(sB + stage * B_BYTES + crank * (B_BYTES / 2), &tmB, &full[stage], k,
-                                       s * g.Nb + nb * BN + (int)crank * (BN / 2), (uint16_t)0x3);
-                    else
-                        tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], k, s * g.Nb + nb * BN);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (TWO) {
+                        const uint32_t lfull = mapa_rank(smem_u32(&full[stage]), 0);   // leader's barrier
+                        if (crank == 0) mbar_expect_tx(&full[stage], 2 * (A_BYTES + SB_BYTES));
+                        tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, lfull, k, mb * BM);
+                        tma_load_2d_2sm(sB + stage * SB_BYTES, &tmB, lfull, k, s * g.Nb + nb * BN + (int)crank * (BN / 2));
+                    } else {
+                        mbar_expect_tx(&full[stage], STAGE_BYTES);
+                        tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], k, mb * BM);
+                        if (CL)
+                            tma_load_2d_mc(sB + stage * B_BYTES + crank * (B_BYTES / 2), &tmB, &full[stage], k,
+                                           s * g.Nb + nb * BN + (int)crank * (BN / 2), (uint16_t)0x3);
+                        else
+                            tma_load_2d(sB + stage * B_BYTES, &tmB, &full[stage], k, s * g.Nb + nb * BN);
+                    }
+                    if (++stage == NSTG) { stage = 0; phase ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {   // ---- MMA issuer (single thread)
-            const uint32_t idesc = idesc_bf16_f32(BM, BN);
+        if (lane == 0 && (!TWO || crank == 0)) {   // ---- MMA issuer (single thread; the leader of a pair)
+            const uint32_t idesc = idesc_bf16_f32(TWO ? 2 * BM : BM, BN);
             int stage = 0;
             uint32_t phase = 0;
             int lt = 0;
@@ -134,15 +154,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint64_t da = desc_kmajor_sw128(smem_u32(sA + stage * A_BYTES));
-                    const uint64_t db = desc_kmajor_sw128(smem_u32(sB + stage * B_BYTES));
+                    const uint64_t db = desc_kmajor_sw128(smem_u32(sB + stage * SB_BYTES));
 #pragma unroll
-                    for (int k = 0; k < BK / 16; ++k)   // +32 B along K inside the swizzle atom
-                        mma_bf16(dcol, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
-                    if (CL) mma_commit_mc(&empty[stage], (uint16_t)0x3);   // release the stage in both CTAs
+                    for (int k = 0; k < BK / 16; ++k) {  // +32 B along K inside the swizzle atom
+                        if (TWO) mma_bf16_2sm(dcol, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                        else mma_bf16(dcol, da + 2 * k, db + 2 * k, idesc, (kb | k) != 0);
+                    }
+                    if (TWO) mma_commit_2sm(&empty[stage], (uint16_t)0x3);     // both CTAs' stage
+                    else if (CL) mma_commit_mc(&empty[stage], (uint16_t)0x3);  // release the stage in both CTAs
                     else mma_commit(&empty[stage]);
-                    if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    if (++stage == NSTG) { stage = 0; phase ^= 1; }
                 }
-                mma_commit(&tfull[ab]);
+                if (TWO) mma_commit_2sm(&tfull[ab], (uint16_t)0x3);
+                else mma_commit(&tfull[ab]);
             }
         }
     } else if (g.C) {   // ---- epilogue: TMEM -> registers -> C^T[obs][atom]
@@ -166,7 +190,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 for (int i = 0; i < 32; ++i) crow[(size_t)(c0 + i) * g.ldc] = __uint_as_float(r[i]);
             }
             tc_fence_before();
-            mbar_arrive(&tempty[ab]);
+            if (TWO) {                    // one arrival per warp on the leader's barrier (its MMA waits)
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[ab]), 0));
+            } else {
+                mbar_arrive(&tempty[ab]);
+            }
         }
     } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
         const int q = warp & 3;
@@ -237,14 +266,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 wa_c = wa_n; wn_c = wn_n; th_c = th_n;
             }
             tc_fence_before();
-            mbar_arrive(&tempty[ab]);
+            if (TWO) {                    // one arrival per warp on the leader's barrier (its MMA waits)
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[ab]), 0));
+            } else {
+                mbar_arrive(&tempty[ab]);
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     if (CL) cluster_sync();          // no CTA leaves while its peer may still arrive on its barriers
-    if (warp == 1) tmem_dealloc(tmem, TMEM_COLS);
+    if (warp == 1) {
+        if (TWO) tmem_dealloc_2sm(tmem, TMEM_COLS);
+        else tmem_dealloc(tmem, TMEM_COLS);
+    }
 }
 
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -290,8 +327,13 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
         err_store() = "batched gemm: need M%128==0, N%256==0, K%64==0, 16-byte aligned rows";
         return DSCR_EINVAL;
     }
+    // GEMM mode: 2 (CTA pair, default) / 1 (cluster multicast, DSCR_GEMM_CLUSTER=mc) / 0 (single
+    // CTA, DSCR_GEMM_CLUSTER=0 or an odd number of atom blocks)
     const char* ecl = getenv("DSCR_GEMM_CLUSTER");
-    const bool cl = (M / BM) % 2 == 0 && !(ecl && !strcmp(ecl, "0"));
+    int mode = (M / BM) % 2 == 0 ? 2 : 0;
+    if (ecl && !strcmp(ecl, "0")) mode = 0;
+    if (ecl && !strcmp(ecl, "mc") && mode) mode = 1;
+    const bool cl = mode > 0;
     CUtensorMap ma, mb;
     int rc = make_map(&ma, A, K, M, lda, BK, BM);
     if (rc) return rc;
@@ -316,7 +358,8 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e;
     if (cl) {
-        e = cudaFuncSetAttribute(k_gemm_dt<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+        auto kern = (mode == 2) ? k_gemm_dt<2> : k_gemm_dt<1>;
+        e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
         cudaLaunchConfig_t lc = {};
         lc.gridDim = dim3(std::min(g.num_tiles, sms & ~1));
@@ -328,12 +371,12 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
         at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
         lc.attrs = at;
         lc.numAttrs = 1;
-        e = cudaLaunchKernelEx(&lc, k_gemm_dt<true>, ma, mb, g);
+        e = cudaLaunchKernelEx(&lc, kern, ma, mb, g);
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     } else {
-        e = cudaFuncSetAttribute(k_gemm_dt<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
+        e = cudaFuncSetAttribute(k_gemm_dt<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
-        k_gemm_dt<false><<<std::min(g.num_tiles, sms), GEMM_THREADS, GEMM_SMEM, s>>>(ma, mb, g);
+        k_gemm_dt<0><<<std::min(g.num_tiles, sms), GEMM_THREADS, GEMM_SMEM, s>>>(ma, mb, g);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
