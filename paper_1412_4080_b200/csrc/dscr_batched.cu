@@ -1129,10 +1129,10 @@ constexpr int LSM = 512;       // old-list entries staged in shared memory (long
 // [pointer, end) is tested in parallel.  The result equals testing every active atom.  The
 // pointer then moves to the first position still active (everything before it is screened).
 
-// The screening order is sorted on the top 32 - SORT_BIT0 bits of the radix image of the fp32
+// The screening order is sorted on the top 32 - SORT_BIT0 = 16 bits of the radix image of the fp32
 // key (sign-adjusted so unsigned order = float order); okey() is that truncated image, monotone
 // non-decreasing in v, so v > t implies okey(fl32(v)) >= okey(fl32(t)).
-constexpr int SORT_BIT0 = 8;
+constexpr int SORT_BIT0 = 16;
 __device__ __forceinline__ uint32_t okey(float v) {
     const uint32_t b = __float_as_uint(v);
     const uint32_t f = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
