@@ -83,18 +83,18 @@ def _slices(X, S):
 
 
 def _slice_emulation(D, V, S=4, T=5, dmax=5):
-    """numpy restatement of the integer-slice correlation (same fp64 combination order)."""
+    """numpy restatement of the integer-slice correlation (exact int64 combination, one rounding)."""
     Ds, eD = _slices(D, S)
     Vs, eV = _slices(V, T)
-    acc = np.zeros((V.shape[0], D.shape[0]))
+    acc = np.zeros((V.shape[0], D.shape[0]), dtype=np.int64)
     for d in range(dmax + 1):
         C = np.zeros_like(acc)
         for s_ in range(S):
             t = d - s_
             if 0 <= t < T:
-                C += Vs[t] @ Ds[s_].T          # exact: integers < 2^53
-        acc = acc + C * 2.0 ** (-7 * d)
-    return np.ldexp(acc, eD[None, :] + eV[:, None] - 14), eD, eV
+                C += Vs[t].astype(np.int64) @ Ds[s_].astype(np.int64).T     # exact integer products
+        acc += C << (7 * (dmax - d))                                         # exact, < 2^63
+    return np.ldexp(acc.astype(np.float64), eD[None, :] + eV[:, None] - 14 - 7 * dmax), eD, eV
 
 
 @pytest.mark.parametrize("K,N,B,hard", [(128, 128, 128, True), (384, 256, 256, True), (1024, 1024, 512, False),
