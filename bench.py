@@ -542,7 +542,13 @@ def run_c5(args):
     from paper_1412_4080_b200.batched import BatchedEngine, solve_batched
 
     w = wl.config5(seed=args.seed + rank)      # each rank: its own 4096 observations (data parallel)
-    dic = ds.Dictionary(w.D, check_unit_norms=False, dtype="bf16")
+    # inputs in pinned host memory (the e2e copies): dictionary bits (K, N) and observations (B, N)
+    host_d = torch.empty((w.D.shape[1], w.D.shape[0]), dtype=torch.uint16, pin_memory=True)
+    host_d.numpy()[:] = w.D.T
+    host_y = torch.empty((w.y.shape[1], w.y.shape[0]), dtype=torch.float64, pin_memory=True)
+    host_y.numpy()[:] = w.y.T
+    dic = ds.Dictionary(host_d.numpy().T, check_unit_norms=False, dtype="bf16")
+    dic._host_tensor = host_d
     nrm = ds.operator_norm(dic, tol=1e-11, max_iters=20000)
     L = nrm * nrm * (1.0 + 1e-6)
     iters = 100
@@ -610,16 +616,20 @@ def run_c5(args):
     achieved = flop / (ms[0] / 1e3) / 1e12
     e2e = None
     if not args.no_e2e:
+        import gc
+        del engs, engs2, e                  # release the device-timed engines' workspaces
+        gc.collect()
         for _ in range(args.warmup):       # untimed: first-use allocations and kernel loads
             dic.drop_device()
-            solve_batched(dic, w.y, w.lam, L, iterations=iters, test="dst3", splits=args.splits)
+            solve_batched(dic, host_y.T, w.lam, L, iterations=iters, test="dst3", splits=args.splits)
         torch.cuda.synchronize()
+        e2e_steps = max(args.steps, 5)
         t0 = time.perf_counter()
-        for _ in range(args.steps):
+        for _ in range(e2e_steps):
             dic.drop_device()
-            r = solve_batched(dic, w.y, w.lam, L, iterations=iters, test="dst3", splits=args.splits)
+            r = solve_batched(dic, host_y.T, w.lam, L, iterations=iters, test="dst3", splits=args.splits)
         torch.cuda.synchronize()
-        es = (time.perf_counter() - t0) / args.steps
+        es = (time.perf_counter() - t0) / e2e_steps
         e2e = {"value": world * iters / es, "unit": "iters/s",
                "h2d_bytes_per_step": int(dic.data.nbytes + w.y.nbytes + w.lam.nbytes),
                "d2h_bytes_per_step": int(r.d2h_bytes), "seconds_per_step": es}

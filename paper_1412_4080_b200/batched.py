@@ -78,7 +78,12 @@ class BatchedEngine:
         import torch
         if dictionary.dtype != "bf16":
             raise ValueError("the batched path takes a bf16 dictionary (Dictionary(..., dtype='bf16'))")
-        Y = np.asarray(Y, dtype=np.float64)
+        y_torch = torch.is_tensor(Y)          # e.g. the transposed view of a pinned (b, n) host buffer
+        if y_torch:
+            if Y.dtype != torch.float64 or Y.dim() != 2 or Y.device.type != "cpu":
+                raise ValueError("observations must be a 2-D float64 host tensor or array")
+        else:
+            Y = np.asarray(Y, dtype=np.float64)
         n, b = Y.shape
         if n != dictionary.n_rows:
             raise ValueError("observations must have the dictionary's row count")
@@ -93,14 +98,20 @@ class BatchedEngine:
         self.Dt = dictionary.device_data(self.device)                      # (K, ldd) bf16 bits
         ldy = (n + 63) // 64 * 64
         # upload Y as given (n x b) and transpose on the device into observation rows [b][ldy]
-        Yh = torch.from_numpy(Y.T if Y.flags.f_contiguous else np.ascontiguousarray(Y))
         self.Yd = torch.zeros((b, ldy), dtype=torch.float64, device=self.device)
-        if Y.flags.f_contiguous:
-            self.Yd[:, :n].copy_(Yh.to(self.device))
+        if y_torch:
+            rows = Y.T if Y.T.is_contiguous() else Y.T.contiguous()              # (b, n)
+            self.Yd[:, :n].copy_(rows.to(self.device, non_blocking=rows.is_pinned()))
+            y_bytes = int(Y.numel() * 8)
         else:
-            self.Yd[:, :n].copy_(Yh.to(self.device).T)
+            Yh = torch.from_numpy(Y.T if Y.flags.f_contiguous else np.ascontiguousarray(Y))
+            if Y.flags.f_contiguous:
+                self.Yd[:, :n].copy_(Yh.to(self.device))
+            else:
+                self.Yd[:, :n].copy_(Yh.to(self.device).T)
+            y_bytes = int(Y.nbytes)
         self.lamd = torch.from_numpy(lam.copy()).to(self.device)
-        self.h2d_bytes = int(Y.nbytes + lam.nbytes)
+        self.h2d_bytes = int(y_bytes + lam.nbytes)
         self.betas = fista_betas(self.iterations)
         d = nat.BatchedDesc()
         d.n_rows, d.n_atoms, d.n_obs, d.ldd = n, self.k, b, dictionary.ldd
