@@ -33,7 +33,11 @@ using namespace umma;
 constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
 constexpr int A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int TMEM_COLS = 2 * BN;
-constexpr int GEMM_THREADS = 320;   // warp 0 TMA, warp 1 MMA, warps 2..9 epilogue (2 per TMEM lane quarter)
+#ifndef GEMM_EPI_WARPS
+#define GEMM_EPI_WARPS 16
+#endif
+constexpr int EPI_WARPS = GEMM_EPI_WARPS;   // epilogue warps: EPI_WARPS / 4 per TMEM lane quarter
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;   // warp 0 TMA, warp 1 MMA, then the epilogue warps
 constexpr int EPI_THREADS = GEMM_THREADS - 64;
 constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 64;
 
@@ -55,6 +59,22 @@ struct GemmArgs {
     int hcap;
     int words;              // M/32
 };
+
+#ifndef EPI_TRANSPOSE
+#define EPI_TRANSPOSE 0
+#endif
+// 32 x 32 bit-matrix transpose across a warp: lane l holds row l; returns column `lane`
+// (bit i of the result = bit `lane` of lane i's input).  5 butterfly stages.
+__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
+#pragma unroll
+    for (int s = 16; s >= 1; s >>= 1) {
+        const uint32_t lo = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
+                          : (s == 2) ? 0x33333333u : 0x55555555u;
+        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
+        x = (lane & s) ? ((x & ~lo) | ((y >> s) & lo)) : ((x & lo) | ((y << s) & ~lo));
+    }
+    return x;
+}
 
 // MODE 0: one CTA per tile (128 atoms x 256 observations).
 // MODE 1: 2-CTA clusters along the atom blocks share each Theta tile: every CTA loads its half
@@ -171,7 +191,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
     } else if (g.C) {   // ---- epilogue: TMEM -> registers -> C^T[obs][atom]
         const int q = warp & 3;   // TMEM lane quarter this warp may access
-        const int half = (warp - 2) >> 2;   // which half of the tile's columns
+        constexpr int PARTS = EPI_WARPS / 4;
+        const int half = (warp - 2) >> 2;   // which part of the tile's columns
         int lt = 0;
         for (int tt = t_first; tt < t_count; tt += t_step, ++lt) {
             int mb, nb;
@@ -183,7 +204,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const int m = mb * BM + q * 32 + lane;
             float* crow = g.C + (size_t)(nb * BN) * g.ldc + m;
 #pragma unroll 1
-            for (int c0 = half * (BN / 2); c0 < (half + 1) * (BN / 2); c0 += 32) {
+            for (int c0 = half * (BN / PARTS); c0 < (half + 1) * (BN / PARTS); c0 += 32) {
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + c0, r);
 #pragma unroll
@@ -199,8 +220,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
     } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
         const int q = warp & 3;
-        const int half = (warp - 2) >> 2;                             // which half of the tile's columns
-        constexpr int KC = BN / 64;                                   // 32-column chunks per warp
+        constexpr int PARTS = EPI_WARPS / 4;
+        const int half = (warp - 2) >> 2;                             // which part of the tile's columns
+        constexpr int KC = BN / (32 * PARTS);                         // 32-column chunks per warp
         int lt = 0;
         for (int tt = t_first; tt < t_count; tt += t_step, ++lt) {
             int mb, nb;
@@ -209,7 +231,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t aphase = (lt >> 1) & 1;
             const int m0 = mb * BM + q * 32;                  // this warp's 32 atoms
             const int m = m0 + lane;
-            const int cbase = half * (BN / 2);
+            const int cbase = half * (BN / PARTS);
             // per-observation words of this warp's columns: chunk 0 fetched before waiting on the
             // accumulator, chunk k+1 while chunk k is processed (rotating scalars, no local memory)
             uint32_t wa_c, wn_c;
@@ -234,18 +256,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + cbase + k * 32, r);
-                // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms
+                // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms.
+                // The mask / list words arrive one per column (lane = column); a warp bit transpose
+                // gives each lane its own atom's bits for all 32 columns.
                 uint32_t hotbits = 0u, mymax = 0u;
+#if EPI_TRANSPOSE
+                const uint32_t actw = warp_transpose32(wa_c, lane), nzw = warp_transpose32(wn_c, lane);
+#endif
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const uint32_t wai = __shfl_sync(0xffffffffu, wa_c, i);
-                    const uint32_t wni = __shfl_sync(0xffffffffu, wn_c, i);
                     const float thi = __shfl_sync(0xffffffffu, th_c, i);
-                    const float a = fabsf(__uint_as_float(r[i]));
-                    const bool act = (wai >> lane) & 1u;
-                    const uint32_t mv = __reduce_max_sync(0xffffffffu, act ? __float_as_uint(a) : 0u);
+                    const uint32_t abits = r[i] & 0x7fffffffu;          // |c| (float bits, monotone)
+#if EPI_TRANSPOSE
+                    const bool act = (actw >> i) & 1u;
+                    const bool nz = (nzw >> i) & 1u;
+#else
+                    const bool act = (__shfl_sync(0xffffffffu, wa_c, i) >> lane) & 1u;
+                    const bool nz = (__shfl_sync(0xffffffffu, wn_c, i) >> lane) & 1u;
+#endif
+                    const uint32_t mv = __reduce_max_sync(0xffffffffu, act ? abits : 0u);
                     mymax = (lane == i) ? mv : mymax;
-                    const bool hot = act && (a > thi || ((wni >> lane) & 1u));
+                    const bool hot = act && (__uint_as_float(abits) > thi || nz);
                     hotbits |= (hot ? 1u : 0u) << i;
                 }
                 if (mymax) atomicMax(&g.cmax[nb * BN + cbase + k * 32 + lane], mymax);   // reduction, no return
