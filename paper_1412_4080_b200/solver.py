@@ -20,7 +20,8 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as nat
-from .instrument import DYNAMIC, NONE, STATIC, STRATEGIES, SolveTrace, flops_iteration, flops_static_init
+from .instrument import (DYNAMIC, NONE, STATIC, STRATEGIES, SolveTrace, flops_iteration, flops_static_init,
+                         problem_digest)
 from .problem import GROUP, LASSO, LambdaMax, Problem
 
 ISTA, FISTA, TWIST, SPARSA, CP = "ista", "fista", "twist", "sparsa", "cp"
@@ -411,7 +412,7 @@ def _solve(eng, problem, cfg, iteration_hook):
     _raise_status(eng.L, sc)
     device_s = start.elapsed_time(stop) / 1e3 if iteration_hook is None else float("nan")
     trace = SolveTrace(kind=problem.kind, strategy=cfg.strategy, n_rows=n, n_cols=k,
-                       group_count=group_count, lam=problem.lam)
+                       group_count=group_count, lam=problem.lam, digest=problem_digest(problem))
     if sc.trivial:
         st = ScreenState(np.arange(k, dtype=np.int64), np.empty(0, dtype=np.int64), cfg.test)
         return SolveResult(np.zeros(k), 0, trace, 0.5 * float(problem.y @ problem.y), st,
