@@ -216,6 +216,13 @@ int dscr_test_group(const double* w, const double* cnorm, const double* snorm,
                     void* stream);
 /* Largest singular value of D by 2-vector block power iteration (dictionary.py:120-171);
  * blocking; `work` must hold dscr_operator_norm_work_size() bytes of device memory. */
+/* DSMX ingestion (dictionary.py:304-335: row-major little-endian fp64 payload): `nr` file rows
+ * starting at row0 (device, nr x ncols row-major) transposed into the column-major dictionary
+ * layout dst[col * ldd + row0 + r] in the storage dtype (fp64; fp32 round-to-nearest; bf16 bit
+ * patterns via fp32, round-to-nearest-even). */
+int dscr_ingest_rows_f64(const double* rows, int nr, int ncols, int row0, int dtype, void* dst, int ldd,
+                         void* stream);
+
 /* Spectral norms of column groups of D (GroupPartition.build, dictionary.py:120-160 per group):
  * group g = columns group_cols[group_ptr[g] .. group_ptr[g+1]) (device arrays).  One kernel for
  * all groups: fp64 Gram per group + the 2-vector block power iteration of dscr_operator_norm on

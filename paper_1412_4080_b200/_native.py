@@ -34,7 +34,7 @@ ABI_FUNCTIONS = (
     "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_phase", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
     "dscr_batched_gemm_bf16", "dscr_batched_workspace_size", "dscr_batched_create", "dscr_batched_setup",
     "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_profile", "dscr_batched_destroy",
-    "dscr_corr_exact_work_size", "dscr_corr_exact_bf16", "dscr_group_spectral_norms",
+    "dscr_corr_exact_work_size", "dscr_corr_exact_bf16", "dscr_group_spectral_norms", "dscr_ingest_rows_f64",
 )
 
 
@@ -141,6 +141,7 @@ def _declare(lib):
         "dscr_corr_exact_work_size": (sz, [i32, i32, i32]),
         "dscr_corr_exact_bf16": (i32, [vp, i32, i32, i32, vp, i32, i32, vp, i32, vp, sz, vp]),
         "dscr_group_spectral_norms": (i32, [i32, vp, i32, i32, i32, vp, vp, dbl, i32, vp, vp]),
+        "dscr_ingest_rows_f64": (i32, [vp, i32, i32, i32, i32, vp, i32, vp]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)

@@ -534,6 +534,40 @@ __global__ void __launch_bounds__(NT) k_group_norms(const T* D, int ldd, int n, 
     if (lane == 0) out[g] = sqrt(fmax(val, 0.0));
 }
 
+// DSMX ingestion (dictionary.py:304-335 layout: row-major fp64): a block of `nr` file rows
+// (nr x ncols, row-major, on the device) transposed into the column-major dictionary layout
+// dst[col][row0 + r] (row stride ldd) with the storage conversion: fp64 as is, fp32 round to
+// nearest, bf16 = fp64 -> fp32 -> bf16 round-to-nearest-even (workloads.bf16_round).
+// 32 x 32 tiles through shared memory so both sides are coalesced.
+template <typename T>
+__device__ __forceinline__ T ingest_cvt(double v);
+template <>
+__device__ __forceinline__ double ingest_cvt<double>(double v) { return v; }
+template <>
+__device__ __forceinline__ float ingest_cvt<float>(double v) { return __double2float_rn(v); }
+template <>
+__device__ __forceinline__ uint16_t ingest_cvt<uint16_t>(double v) {
+    const uint32_t b = __float_as_uint(__double2float_rn(v));
+    return (uint16_t)((b + 0x7FFFu + ((b >> 16) & 1u)) >> 16);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_ingest_rows(const double* __restrict__ src, int nr, int ncols, int row0,
+                                                     T* __restrict__ dst, int ldd) {
+    __shared__ double tile[32][33];
+    const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;     // 32 x 8
+    for (int j = ty; j < 32; j += 8) {
+        const int r = r0 + j, c = c0 + tx;
+        tile[j][tx] = (r < nr && c < ncols) ? src[(size_t)r * ncols + c] : 0.0;
+    }
+    __syncthreads();
+    for (int j = ty; j < 32; j += 8) {
+        const int c = c0 + j, r = r0 + tx;
+        if (c < ncols && r < nr) dst[(size_t)c * ldd + row0 + r] = ingest_cvt<T>(tile[tx][j]);
+    }
+}
+
 static int check_dict(int dt, const void* D, int ldd, int n, int k) {
     if (dt < DSCR_F64 || dt > DSCR_BF16) return inval("unknown dtype");
     if (!D || n < 1 || k < 1 || ldd < n || ldd % 16) return inval("bad dictionary shape or ldd");
@@ -637,6 +671,20 @@ int dscr_test_group(const double* w, const double* cn, const double* sn, const i
                     uint8_t* m, void* stream) {
     if (nk <= 0) return DSCR_OK;
     k_test_group<<<std::max(1, std::min((nk + 255) / 256, 4096)), 256, 0, (cudaStream_t)stream>>>(w, cn, sn, kg, nk, r, m);
+    OCK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_ingest_rows_f64(const double* rows, int nr, int ncols, int row0, int dtype, void* dst, int ldd,
+                         void* stream) {
+    if (!rows || !dst || nr < 0 || ncols < 1 || row0 < 0 || row0 + nr > ldd) return inval("bad ingestion block");
+    if (nr == 0) return DSCR_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    const dim3 grid((ncols + 31) / 32, (nr + 31) / 32);
+    if (dtype == DSCR_F64) k_ingest_rows<double><<<grid, 256, 0, s>>>(rows, nr, ncols, row0, (double*)dst, ldd);
+    else if (dtype == DSCR_F32) k_ingest_rows<float><<<grid, 256, 0, s>>>(rows, nr, ncols, row0, (float*)dst, ldd);
+    else if (dtype == DSCR_BF16) k_ingest_rows<uint16_t><<<grid, 256, 0, s>>>(rows, nr, ncols, row0, (uint16_t*)dst, ldd);
+    else return inval("unknown dtype");
     OCK(cudaGetLastError());
     return DSCR_OK;
 }
