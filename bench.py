@@ -289,7 +289,7 @@ def run_c4_sharded(args, world, rank, local):
     import paper_1412_4080_b200 as ds
     from paper_1412_4080_b200 import dist as pdist
     from paper_1412_4080_b200 import workloads as wl
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", torch.cuda.current_device())
     n, k, blk = 8192, 262144, 4096
     c0, c1 = pdist.shard_ranges(k // blk, world)[rank]      # whole generator blocks per rank
     c0, c1 = c0 * blk, c1 * blk
@@ -317,18 +317,55 @@ def run_c4_sharded(args, world, rank, local):
         pdist.orchestrate(shard, cfg, lam, dist.group.WORLD)
     torch.cuda.synchronize()
     dist.barrier()
-    with ClockSampler(local) as clocks:
-        t0 = time.perf_counter()
+    stream = torch.cuda.current_stream(dev)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    calls0 = shard.phase_calls
+    with ClockSampler(torch.cuda.current_device()) as clocks:
+        ev0.record(stream)
         its = 0
         for _ in range(args.steps):
             sc = pdist.orchestrate(shard, cfg, lam, dist.group.WORLD)
             its += sc.t
+        ev1.record(stream)
         torch.cuda.synchronize()
-        el = time.perf_counter() - t0
-    t = torch.tensor([el], device=dev)
+    dist.barrier()
+    launches = shard.phase_calls - calls0
+    t = torch.tensor([ev0.elapsed_time(ev1) / 1e3], device=dev)      # device time, max over ranks
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     el = float(t.item())
     shard.close()
+    # whole-step HBM rate per GPU of the dominant stream (K1 reads every local active column per
+    # iteration; no screening fires on c4): local bytes x iterations / device time
+    k1_bytes_local = (c1 - c0) * n * 4
+    per_gpu = k1_bytes_local * (its / args.steps) / (el / args.steps) / 1e9
+    peaks_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    peak, peak_src = 6650.0, "fallback"
+    if os.path.exists(peaks_path):
+        with open(peaks_path) as fh:
+            peak = float(json.load(fh).get("hbm_gbs", peak))
+        peak_src = "measured"
+    # end to end per step: local dictionary re-uploaded from pinned host memory, solve, solution read back
+    e2e = None
+    if not args.no_e2e:
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0 = time.perf_counter()
+        e_its, d2h = 0, 0
+        for _ in range(args.steps):
+            dic.drop_device()
+            sh = pdist.GpuShard(prob, cfg, c0, k, device=dev)
+            sc = pdist.orchestrate(sh, cfg, lam, dist.group.WORLD)
+            kept_l, x_l, rows, sc = sh.local_solution()
+            sh.close()
+            e_its += sc.t
+            d2h += kept_l.nbytes + x_l.nbytes + rows.nbytes
+        torch.cuda.synchronize()
+        es = torch.tensor([time.perf_counter() - t0], device=dev)
+        dist.all_reduce(es, op=dist.ReduceOp.MAX)
+        es = float(es.item())
+        e2e = {"value": e_its / es, "unit": "iters/s", "h2d_bytes_per_step": int(host.numel() * 4 + n * 8),
+               "d2h_bytes_per_step": int(d2h // args.steps), "seconds_per_step": es / args.steps,
+               "note": "per rank; value uses rank 0's iteration count and the slowest rank's time"}
     if rank == 0:
         line = {
             "metric": METRIC, "value": its / el, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
@@ -336,8 +373,13 @@ def run_c4_sharded(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox, see DESIGN.md)",
             "config": {"workload": "c4", "n": n, "k": k, "iterations_per_step": its / args.steps,
                        "time_to_gap_s": el / args.steps, "parallelism": f"colshard{world}",
-                       "columns_per_rank": c1 - c0, "collectives_per_iteration": 2},
-            "roofline": None, "gpu_launches": None, "clocks": clocks.summary(), "e2e": None, "cpu_baseline": None,
+                       "columns_per_rank": c1 - c0, "collectives_per_iteration": 2,
+                       "l2": "dictionary shard larger than the 126 MB L2"},
+            "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
+                         "traffic": None, "peak_source": peak_src,
+                         "kernel": "k1 stream, whole-step average per GPU (local columns x iterations / device time)"},
+            "gpu_launches": int(launches), "gpu_launches_note": "dscr_solver_phase launches on rank 0 (>= 1 kernel each)",
+            "clocks": clocks.summary(), "e2e": e2e, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
@@ -347,10 +389,22 @@ def run_ours(args):
     import torch
     world, rank, local = dist_env()
     if (world > 1 or args.sharded) and args.workload == "c4":
-        torch.cuda.set_device(local)
+        # DSCR_BENCH_BACKEND / DSCR_BENCH_DEVICE: test overrides (gloo ranks sharing one GPU)
+        dev_index = int(os.environ.get("DSCR_BENCH_DEVICE", local))
+        torch.cuda.set_device(dev_index)
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        return run_c4_sharded(args, world, rank, local)
+        backend = os.environ.get("DSCR_BENCH_BACKEND", "nccl")
+        kw = {}
+        if "RANK" not in os.environ:           # --sharded without a launcher: a one-rank group
+            import socket
+            with socket.socket() as sk:
+                sk.bind(("127.0.0.1", 0))
+                kw = {"init_method": f"tcp://127.0.0.1:{sk.getsockname()[1]}", "rank": 0, "world_size": 1}
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index), **kw)
+        else:
+            dist.init_process_group(backend, **kw)
+        return run_c4_sharded(args, world, rank, dev_index)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:

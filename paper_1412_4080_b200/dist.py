@@ -123,9 +123,11 @@ class GpuShard:
         self.comm = self.eng.view(b.comm, b.comm_len, torch.float64)
         self.vec = self.eng.view(b.vec, problem_local.dictionary.ldd, torch.float64)
         self.unit_offset = group_offset if problem_local.kind == GROUP else col_offset
+        self.phase_calls = 0          # dscr_solver_phase launches (each enqueues >= 1 kernel)
 
     def phase(self, ph):
         nat.check(self.eng.L.dscr_solver_phase(self.eng.h, int(ph), self.eng.sptr))
+        self.phase_calls += 1
 
     def scalars(self):
         return self.eng.scalars()
