@@ -60,22 +60,6 @@ struct GemmArgs {
     int words;              // M/32
 };
 
-#ifndef EPI_TRANSPOSE
-#define EPI_TRANSPOSE 0
-#endif
-// 32 x 32 bit-matrix transpose across a warp: lane l holds row l; returns column `lane`
-// (bit i of the result = bit `lane` of lane i's input).  5 butterfly stages.
-__device__ __forceinline__ uint32_t warp_transpose32(uint32_t x, int lane) {
-#pragma unroll
-    for (int s = 16; s >= 1; s >>= 1) {
-        const uint32_t lo = (s == 16) ? 0x0000FFFFu : (s == 8) ? 0x00FF00FFu : (s == 4) ? 0x0F0F0F0Fu
-                          : (s == 2) ? 0x33333333u : 0x55555555u;
-        const uint32_t y = __shfl_xor_sync(0xffffffffu, x, s);
-        x = (lane & s) ? ((x & ~lo) | ((y >> s) & lo)) : ((x & lo) | ((y << s) & ~lo));
-    }
-    return x;
-}
-
 // MODE 0: one CTA per tile (128 atoms x 256 observations).
 // MODE 1: 2-CTA clusters along the atom blocks share each Theta tile: every CTA loads its half
 //   with TMA multicast into both CTAs' shared memory; the MMA commit releases the stage in both
@@ -256,24 +240,15 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 }
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + cbase + k * 32, r);
-                // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms.
-                // The mask / list words arrive one per column (lane = column); a warp bit transpose
-                // gives each lane its own atom's bits for all 32 columns.
+                // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms
+                // (the mask / list words arrive one per column, lane = column; shuffled per column)
                 uint32_t hotbits = 0u, mymax = 0u;
-#if EPI_TRANSPOSE
-                const uint32_t actw = warp_transpose32(wa_c, lane), nzw = warp_transpose32(wn_c, lane);
-#endif
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
                     const float thi = __shfl_sync(0xffffffffu, th_c, i);
                     const uint32_t abits = r[i] & 0x7fffffffu;          // |c| (float bits, monotone)
-#if EPI_TRANSPOSE
-                    const bool act = (actw >> i) & 1u;
-                    const bool nz = (nzw >> i) & 1u;
-#else
                     const bool act = (__shfl_sync(0xffffffffu, wa_c, i) >> lane) & 1u;
                     const bool nz = (__shfl_sync(0xffffffffu, wn_c, i) >> lane) & 1u;
-#endif
                     const uint32_t mv = __reduce_max_sync(0xffffffffu, act ? abits : 0u);
                     mymax = (lane == i) ? mv : mymax;
                     const bool hot = act && (__uint_as_float(abits) > thi || nz);
