@@ -231,6 +231,8 @@ def run_reference(args):
     if rank != 0:
         return
     import paper_1412_4080_b200 as ds  # noqa: F401  (host types / generators only)
+    if args.workload == "c5":
+        return run_reference_c5(args, world)
     works = build_workload(args.workload, args.seed)
     # the reference arm shares the host problem definition; L from the host power iteration
     from oracle import screen_oracle as so
@@ -272,10 +274,57 @@ def run_reference(args):
         "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(1, len(samples)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": args.workload},
+        "data": "synthetic", "config": workload_config(args.workload, works),
         "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port",
                          "sample": f"first {args.cpu_sample_iters} iterations of each solve of {args.workload} "
                                    f"(setup included, as reference run() times it), fp64 numpy oracle"},
+        "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(name, works):
+    """Input description of a workload, shared by both arms' JSON lines."""
+    w = works[0]
+    cfg = {"workload": name, "n": int(w.D.shape[0]), "k": int(w.D.shape[1]), "algorithm": w.algorithm,
+           "test": w.test, "gap_tol": w.gap_tol, "dictionary_dtype": w.dtype}
+    if len(works) > 1:
+        cfg["instances"] = len(works)
+    return cfg
+
+
+def run_reference_c5(args, world):
+    """Reference arm on c5: the fp64 oracle (the reference's algorithm, per observation, as
+    screenlab.run would solve them) on a sample of the batch, extrapolated to batch-iterations/s."""
+    from oracle import screen_oracle as so
+    from paper_1412_4080_b200 import workloads as wl
+    w = wl.config5(seed=args.seed)
+    D64 = (np.asarray(w.D, dtype=np.uint32) << 16).view(np.float32).astype(np.float64)
+    n, k = D64.shape
+    b = w.y.shape[1]
+    iters, sample = 100, 4
+    L = (1.0 + np.sqrt(k / n)) ** 2 * 1.01          # Marchenko-Pastur edge; only the timing uses it
+    samples = []
+    for i in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        for j in range(sample):
+            jj = (i * sample + j) % b
+            so.solve(so.make_problem(D64, w.y[:, jj], w.lam[jj]),
+                     so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=iters,
+                               rel_tol=1e-300, L0=L, norm_aware=True))
+        if i >= args.warmup:
+            samples.append(time.perf_counter() - t0)
+    obs_iters_s = sample * iters * len(samples) / sum(samples)
+    v = obs_iters_s / b
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * iters / v,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "c5", "n": n, "k": k, "batch": b, "iterations_per_step": iters,
+                   "algorithm": "fista", "test": "dst3", "dictionary_dtype": "bf16"},
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cpu_cores(), "kind": "port",
+                         "sample": f"{sample} of {b} observations x {iters} FISTA+DST3 iterations per step, fp64 "
+                                   f"oracle on the bf16-upcast dictionary, extrapolated to the batch"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
