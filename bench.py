@@ -498,10 +498,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    # inputs that fit in the 126 MB L2: flush it (write a 256 MB buffer) before every timed solve
+    fits_l2 = works[0].D.nbytes <= 126e6
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if fits_l2 else None
     with ClockSampler(local) as clocks:
         ev0.record(stream)
         for engs in steps:
             for e in engs:
+                if flush is not None:
+                    flush.zero_()
                 e.setup()
                 e.launch(0)
         ev1.record(stream)
@@ -602,7 +607,7 @@ def run_ours(args):
                        "iterations_per_step": per_step_iters, "time_to_gap_s": dev_s / args.steps,
                        "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
                        "l2": "dictionary larger than the 126 MB L2" if works[0].D.nbytes > 126e6
-                             else "dictionary fits in L2 (no flush between steps)",
+                             else "L2 flushed (256 MB write) before every timed solve",
                        "accumulate": "fp64"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
@@ -683,9 +688,11 @@ def run_c5(args):
     if world > 1:
         torch.distributed.barrier()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # D + Y (67 MB) fit in the L2
     with ClockSampler(local) as clocks:
         ev0.record()
         for e in engs2:
+            flush.zero_()
             e.setup()
             e.run()
         ev1.record()
@@ -761,7 +768,7 @@ def run_c5(args):
                        "splits": args.splits, "parallelism": f"dp{world}" if world > 1 else "single-gpu",
                        "mean_objective": float(np.mean(res.objective)), "kept_min": int(res.kept.min()),
                        "nnz_mean": float(np.mean(res.nnz)), "accumulate": "fp32 (TMEM), fp64 state",
-                       "setup_ms": setup_ms},
+                       "setup_ms": setup_ms, "l2": "L2 flushed (256 MB write) before every timed solve"},
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                          "frac": achieved / peak, "traffic": None, "peak_source": src,
                          "kernel": "k_gemm_dt (tcgen05)", "kernel_ms": ms[0], "flop_per_launch": flop,
