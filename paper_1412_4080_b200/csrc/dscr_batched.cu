@@ -14,6 +14,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
+#include <cub/block/block_radix_sort.cuh>
 #include <cub/device/device_segmented_radix_sort.cuh>
 #include <stdio.h>
 #include <stdlib.h>
@@ -695,10 +696,10 @@ struct BParams {
     int wu_max;                // largest hot / list count the warp update takes (0: CTA update only)
     // screening order: atoms of each observation sorted by their test value
     // v_i = (1 - |cc_i|) / ||a_i|| (descending); at radius rho the screened set is a prefix
-    float* skey;               // [B][K] sorted v (fp32)
+    uint16_t* skey;            // [B][K] sorted 16-bit order keys of v (okey, descending)
     int* sorder;               // [B][K] atom of each sorted position
     int* sptr;                 // [B] leading sorted positions already out of the active set
-    float* skey_in;            // setup scratch (aliases C)
+    uint16_t* skey_in;         // setup scratch (aliases C)
     int* sval_in;              // setup scratch
     int* soff;                 // [B + 1] segment offsets
     void* cub_tmp;
@@ -837,6 +838,14 @@ __global__ void __launch_bounds__(BT) k_blmax(BParams P) {
         P.astar[(size_t)j * P.ldy + n] = (n < P.N) ? (double)__bfloat162float(P.Dt[(size_t)ist * P.ldd + n]) : 0.0;
 }
 
+// 16-bit order-preserving image of an fp32 value (unsigned order = float order, top 16 bits of
+// the radix image), monotone non-decreasing: v > t implies okey16(v) >= okey16(t).
+__device__ __forceinline__ uint16_t okey16(float v) {
+    const uint32_t b = __float_as_uint(v);
+    const uint32_t f = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+    return (uint16_t)(f >> 16);
+}
+
 // SAFE centre correlations (cc = ycorr/lam) and per-observation min |cc|
 __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
     __shared__ float s_m[BW];
@@ -846,7 +855,7 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
         if (P.test == DSCR_SAFE) P.cc[(size_t)j * P.K + i] = (float)(P.ycorr[(size_t)j * P.K + i] / P.lam[j]);
         const float v = (float)((1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / P.anorm[i]);
         m = fmaxf(m, v);
-        P.skey_in[(size_t)j * P.K + i] = v;      // sort key of the screening order
+        P.skey_in[(size_t)j * P.K + i] = okey16(v);   // sort key of the screening order
         P.sval_in[(size_t)j * P.K + i] = i;
     }
     if (threadIdx.x == 0) { P.soff[j] = j * P.K; P.sptr[j] = 0; if (j == P.B - 1) P.soff[P.B] = P.B * P.K; }
@@ -857,6 +866,32 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
         float mm = s_m[0];
         for (int w = 1; w < BW; ++w) mm = fmaxf(mm, s_m[w]);
         P.ccmin[j] = (double)mm + 1e-6;    // slack for the fp32 rounding of the margin itself
+    }
+}
+
+// Screening order of one observation in shared memory (K <= BS_T * BS_I): (okey16, atom) packed in
+// a word, block radix sort on the key bits (descending; stable, so ties keep the atom order and
+// padding entries stay last), order and sorted keys written once.
+constexpr int BS_T = 512, BS_I = 32;
+using BlockSort = cub::BlockRadixSort<uint32_t, BS_T, BS_I>;
+__global__ void __launch_bounds__(BS_T, 1) k_bsort(BParams P) {
+    extern __shared__ __align__(16) uint8_t bs_raw[];
+    typename BlockSort::TempStorage& tmp = *reinterpret_cast<typename BlockSort::TempStorage*>(bs_raw);
+    const int j = blockIdx.x;
+    uint32_t keys[BS_I];
+#pragma unroll
+    for (int it = 0; it < BS_I; ++it) {
+        const int i = threadIdx.x * BS_I + it;             // blocked arrangement = atom order
+        keys[it] = (i < P.K) ? ((uint32_t)P.skey_in[(size_t)j * P.K + i] << 16) | (uint32_t)i : 0u;
+    }
+    BlockSort(tmp).SortDescending(keys, 16, 32);
+#pragma unroll
+    for (int it = 0; it < BS_I; ++it) {
+        const int q = threadIdx.x * BS_I + it;
+        if (q < P.K) {
+            P.sorder[(size_t)j * P.K + q] = (int)(keys[it] & 0xffffu);
+            P.skey[(size_t)j * P.K + q] = (uint16_t)(keys[it] >> 16);
+        }
     }
 }
 
@@ -1138,23 +1173,16 @@ constexpr int LSM = 512;       // old-list entries staged in shared memory (long
 // [pointer, end) is tested in parallel.  The result equals testing every active atom.  The
 // pointer then moves to the first position still active (everything before it is screened).
 
-// The screening order is sorted on the top 32 - SORT_BIT0 = 16 bits of the radix image of the fp32
-// key (sign-adjusted so unsigned order = float order); okey() is that truncated image, monotone
-// non-decreasing in v, so v > t implies okey(fl32(v)) >= okey(fl32(t)).
-constexpr int SORT_BIT0 = 16;
-__device__ __forceinline__ uint32_t okey(float v) {
-    const uint32_t b = __float_as_uint(v);
-    const uint32_t f = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-    return f >> SORT_BIT0;
-}
+// The screening order is sorted on okey16 (16-bit order-preserving image of the fp32 key), so a
+// threshold t maps to okey16(fl32(t)) and every atom that can pass lies before the first smaller key.
 
 // first position q in (lo, hi] with key[q] < tk (hi if none), keys descending, key[lo] >= tk;
 // one warp, 32 probes per round spread over [lo + 1, hi)
-__device__ __forceinline__ int warp_first_below(const float* key, int lo, int hi, float tk, int lane) {
+__device__ __forceinline__ int warp_first_below(const uint16_t* key, int lo, int hi, uint16_t tk, int lane) {
     while (hi - lo > 1) {
         const int span = hi - lo;
         const int probe = lo + 1 + (int)(((long long)(span - 1) * lane) / 32);
-        const unsigned bal = __ballot_sync(0xffffffffu, okey(key[probe]) < okey(tk));
+        const unsigned bal = __ballot_sync(0xffffffffu, key[probe] < tk);
         if (bal == 0u) {                 // every probe still at or above: move past the last one
             lo = lo + 1 + (int)(((long long)(span - 1) * 31) / 32);
             continue;
@@ -1171,11 +1199,11 @@ __device__ __forceinline__ int warp_first_below(const float* key, int lo, int hi
 struct ScanRange { int p, end; };
 
 __device__ __forceinline__ ScanRange screen_range(const BParams& P, int j, double rho, double margin, int lane) {
-    const float* key = P.skey + (size_t)j * P.K;
-    const float tkey = (float)((rho + margin) - 1e-12 * (1.0 + fabs(rho)));
+    const uint16_t* key = P.skey + (size_t)j * P.K;
+    const uint16_t tkey = okey16((float)((rho + margin) - 1e-12 * (1.0 + fabs(rho))));
     const int p = P.sptr[j];
     ScanRange r{p, p};
-    if (p < P.K && okey(key[p]) >= okey(tkey)) r.end = warp_first_below(key, p, P.K, tkey, lane);
+    if (p < P.K && key[p] >= tkey) r.end = warp_first_below(key, p, P.K, tkey, lane);
     return r;
 }
 
@@ -1682,8 +1710,8 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     BParams p{};
     p.tb = (__nv_bfloat16*)take((size_t)d->splits * B * ly * 2);
     p.C = (float*)take(B * K * 4);
-    p.skey_in = p.C;
-    p.skey = (float*)take(B * K * 4);
+    p.skey_in = reinterpret_cast<uint16_t*>(p.C);
+    p.skey = (uint16_t*)take(B * K * 2);
     p.sorder = (int*)take(B * K * 4);
     p.sval_in = (int*)take(B * K * 4);
     p.soff = (int*)take((B + 1) * 4);
@@ -1694,7 +1722,7 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     p.scr_off = (int*)take(B * 4);
     {
         size_t tb = 0;
-        cub::DeviceSegmentedRadixSort::SortPairsDescending((void*)nullptr, tb, (const float*)nullptr, (float*)nullptr,
+        cub::DeviceSegmentedRadixSort::SortPairsDescending((void*)nullptr, tb, (const uint16_t*)nullptr, (uint16_t*)nullptr,
                                                            (const int*)nullptr, (int*)nullptr, (int)(B * K), (int)B,
                                                            (const int*)nullptr, (const int*)nullptr);
         p.cub_bytes = tb;
@@ -1814,10 +1842,19 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
     }
     if (P.test != DSCR_TEST_OFF) {
         k_bcc<<<P.B, BT, 0, s>>>(P);
-        size_t tb = P.cub_bytes;
-        cudaError_t ce = cub::DeviceSegmentedRadixSort::SortPairsDescending(
-            P.cub_tmp, tb, P.skey_in, P.skey, P.sval_in, P.sorder, P.B * P.K, P.B, P.soff, P.soff + 1, SORT_BIT0, 32, s);
-        if (ce != cudaSuccess) { err_store() = cudaGetErrorString(ce); return DSCR_ECUDA; }
+        cudaError_t ce;
+        const char* es = getenv("DSCR_BATCHED_SORT");          // "device": the segmented device sort
+        if (P.K <= BS_T * BS_I && !(es && !strcmp(es, "device"))) {   // one block per observation, in smem
+            const int smem = (int)sizeof(typename BlockSort::TempStorage);
+            ce = cudaFuncSetAttribute(k_bsort, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+            if (ce != cudaSuccess) { err_store() = cudaGetErrorString(ce); return DSCR_ECUDA; }
+            k_bsort<<<P.B, BS_T, smem, s>>>(P);
+        } else {
+            size_t tb = P.cub_bytes;
+            ce = cub::DeviceSegmentedRadixSort::SortPairsDescending(
+                P.cub_tmp, tb, P.skey_in, P.skey, P.sval_in, P.sorder, P.B * P.K, P.B, P.soff, P.soff + 1, 0, 16, s);
+            if (ce != cudaSuccess) { err_store() = cudaGetErrorString(ce); return DSCR_ECUDA; }
+        }
     }
     k_binit<<<P.B, BT, 0, s>>>(P);
     cudaError_t e = cudaGetLastError();

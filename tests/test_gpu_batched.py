@@ -232,3 +232,16 @@ def test_warp_update_matches_cta_update(ratio, monkeypatch):
     for j in range(0, 512, 23):
         assert np.array_equal(a.x_idx[j], b.x_idx[j])
         np.testing.assert_allclose(a.x_val[j], b.x_val[j], rtol=1e-13, atol=1e-15)
+
+
+def test_block_sort_matches_device_sort(monkeypatch):
+    """Screening order by the per-observation shared-memory sort == the segmented device sort."""
+    w, dic, D64, L = _batch_problem(256, 2048, 512, 0.85, seed=13)
+    a = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    monkeypatch.setenv("DSCR_BATCHED_SORT", "device")
+    b = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    assert np.array_equal(a.kept, b.kept) and np.array_equal(a.nnz, b.nnz)
+    assert np.array_equal(a.objective, b.objective)
+    assert a.kept.min() < 2048
+    for j in range(0, 512, 29):
+        assert np.array_equal(a.x_idx[j], b.x_idx[j])
