@@ -245,3 +245,16 @@ def test_block_sort_matches_device_sort(monkeypatch):
     assert a.kept.min() < 2048
     for j in range(0, 512, 29):
         assert np.array_equal(a.x_idx[j], b.x_idx[j])
+
+
+def test_batched_max_rows_matches_oracle():
+    """N = 2048 (the batched path's maximum): two-chunk residual, integer-slice setup at its limit."""
+    w, dic, D64, L = _batch_problem(2048, 1024, 256, 0.5, seed=17)
+    res = solve_batched(dic, w.y, w.lam, L, iterations=40, test="dst3", splits=2)
+    for j in (0, 77, 255):
+        ref = so.solve(so.make_problem(D64, w.y[:, j], w.lam[j]),
+                       so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=40, rel_tol=1e-300,
+                                 L0=L, norm_aware=True))
+        assert abs(res.objective[j] - ref.final_objective) <= 1e-4 * ref.final_objective
+        x = res.x_dense(j, 1024)
+        assert np.linalg.norm(x - ref.x_star) <= 1e-3 * max(np.linalg.norm(ref.x_star), 1e-12)
