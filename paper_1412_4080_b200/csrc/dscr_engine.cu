@@ -292,10 +292,70 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
             }
         }
     }
+    constexpr int GMAX = 64;                 // groups up to GMAX atoms: lane-parallel, staged in smem
+    __shared__ double s_gc[GROUP ? NW : 1][GROUP ? GMAX : 1], s_gv[GROUP ? NW : 1][GROUP ? GMAX : 1];
     for (int f = lo + warp; GROUP && f < hi; f += NW) {
         const int s = find_slot(off, P.G, f);
         const int unit = act[s * P.cap + (f - off[s])];
         const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+        const int gs = j1 - j0;
+        if (gs <= GMAX) {
+            // correlations (4 columns in flight) and prox arguments staged per warp, group norms in
+            // numpy's reduceat order from shared memory, the block soft threshold lane-parallel
+            for (int jb = j0; jb < j1; jb += 4) {
+                double cs4[4] = {0.0, 0.0, 0.0, 0.0};
+                if (need_dot) {
+                    const T* cols[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) cols[c] = (jb + c < j1) ? D + (size_t)(jb + c) * P.ldd : nullptr;
+                    warp_dots<T, 4, (sizeof(T) == 8 ? 2 : 1)>(cols, P.n, s_theta, lane, pol, cs4);
+                }
+                if (lane < 4 && jb + lane < j1) {
+                    double cc = cs4[0];
+#pragma unroll
+                    for (int q = 1; q < 4; ++q) if (lane == q) cc = cs4[q];
+                    s_gc[warp][jb - j0 + lane] = need_dot ? cc : P.corr[jb + lane];
+                }
+            }
+            __syncwarp();
+            for (int c0 = lane; c0 < gs; c0 += 32) {
+                const int j = j0 + c0;
+                const double cc = s_gc[warp][c0];
+                if (need_dot) P.corr[j] = cc;
+                double v;
+                if (algo == DSCR_FISTA) v = uc[j] - cc / L;
+                else if (algo == DSCR_CP) v = xc[j] - tau * cc;
+                else if (algo == DSCR_TWIST) v = xc[j] - tws * cc;
+                else v = xc[j] - cc / L;
+                s_gv[warp][c0] = v;
+            }
+            __syncwarp();
+            double fac = 0.0;
+            if (lane == 0) {   // group soft threshold (dictionary.py:290-301), numpy reduceat summation order
+                const double nv = sqrt(np_segment_sum([&](int i) { double t = s_gv[warp][i - j0]; return t * t; }, j0, gs));
+                const double nc = sqrt(np_segment_sum([&](int i) { double t = s_gc[warp][i - j0]; return t * t; }, j0, gs));
+                if (nc > 0.0) { wmax = fmin(wmax, P.gw[unit] / nc); wany = 1.0; }
+                fac = (nv > 0.0) ? fmax(1.0 - thr * P.gw[unit] / nv, 0.0) : 0.0;
+            }
+            fac = __shfl_sync(0xffffffffu, fac, 0);
+            for (int c0 = lane; c0 < gs; c0 += 32) {
+                const int j = j0 + c0;
+                double cand = s_gv[warp][c0] * fac;
+                if (algo == DSCR_TWIST && !first) {
+                    const double a = P.twa, bb = P.twb;
+                    cand = ((1.0 - a) * xp[j] + (a - bb) * xc[j]) + bb * cand;
+                }
+                xn[j] = cand;
+                if (!isfinite(cand)) wnf = 1.0;
+                const double point = (algo == DSCR_FISTA) ? uc[j] : xc[j];
+                const double st = cand - point;
+                wcs += s_gc[warp][c0] * st;
+                wss += st * st;
+            }
+            __syncwarp();
+            continue;
+        }
+        // larger groups: serial per-group path through global memory
         // correlations of the group's atoms (4 columns in flight), provisional prox argument in xn
         for (int jb = j0; jb < j1; jb += 4) {
             double cs4[4];
