@@ -1658,7 +1658,8 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     // one full wave; also co-resident for the persistent kernel (grid barriers)
     const int per_sm = std::max(1, std::min(k1_occupancy(pr->dtype, pr->n_groups > 0, g.smem1),
                                             std::max(1, pers_occupancy(pr->dtype, pr->n_groups > 0, g.smem1))));
-    g.G = std::max(1, std::min((n_units + 15) / 16, sms * per_sm));
+    // >= 16 atoms per CTA (group problems: count atoms, not groups), at most one CTA per unit
+    g.G = std::max(1, std::min(std::min((pr->n_cols + 15) / 16, n_units), sms * per_sm));
     if (const char* e = getenv("DSCR_MAX_CTAS")) g.G = std::max(1, std::min(g.G, atoi(e)));
     g.cap = (n_units + g.G - 1) / g.G;
     g.max_gsize = max_gsize;
