@@ -693,6 +693,7 @@ struct BParams {
     int* hot_cnt;              // [B]
     int* big;                  // [B] observations left to the CTA update (too many entries for a warp)
     int* nbig;
+    int* big_next;             // work counter of the CTA update
     int wu_max;                // largest hot / list count the warp update takes (0: CTA update only)
     // screening order: atoms of each observation sorted by their test value
     // v_i = (1 - |cc_i|) / ||a_i|| (descending); at radius rho the screened set is a prefix
@@ -948,7 +949,7 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
         P.thr[j] = (float)(P.lam[j] * (1.0 - 1e-6));
         P.cmax[j] = 0u;
         P.hot_cnt[j] = 0;
-        if (j == 0) { *P.it = 0; *P.nbig = 0; *P.scr_ctr = 0ull; }
+        if (j == 0) { *P.it = 0; *P.nbig = 0; *P.big_next = 0; *P.scr_ctr = 0ull; }
     }
 }
 
@@ -1228,14 +1229,14 @@ __device__ __forceinline__ bool screened_now(const BParams& P, int j, int i, dou
 // All screening ranges of the iteration, flattened over the whole GPU: exact test per sorted
 // position, mask bits of passing atoms cleared, kept counts lowered
 // (one atomic per group of lanes on the same observation), pointer = first failing position.
-__global__ void __launch_bounds__(256) k_bscreen(BParams P) {
+__device__ __forceinline__ void bscreen_body(const BParams& P, int bid, int nblk) {   // 256 threads
     const unsigned long long c = *P.scr_ctr;
     const int items = (int)(c >> 32), T = (int)(c & 0xffffffffull);
     if (T == 0) return;
     const double margin = SCREEN_MARGIN + 1e-6;
     const int lane = threadIdx.x & 31;
-    const int stride = gridDim.x * 256;
-    for (int g0 = blockIdx.x * 256 + (threadIdx.x & ~31); g0 < T; g0 += stride) {
+    const int stride = nblk * 256;
+    for (int g0 = bid * 256 + (threadIdx.x & ~31); g0 < T; g0 += stride) {
         const int g = g0 + lane;
         int j = -1, lost = 0;
         if (g < T) {
@@ -1259,6 +1260,10 @@ __global__ void __launch_bounds__(256) k_bscreen(BParams P) {
         if (j >= 0 && lane == __ffs(grp) - 1 && tot) atomicSub(&P.kept[j], tot);
     }
 }
+
+__global__ void __launch_bounds__(256) k_bscreen(BParams P) { bscreen_body(P, blockIdx.x, gridDim.x); }
+
+constexpr int NSCR = 4 * 148;    // screening blocks appended to the residual launch
 
 __device__ void update_hot_cta(const BParams& P, int t, int j) {
     __shared__ int s_idx[HMAX];
@@ -1379,7 +1384,16 @@ __device__ void update_hot_cta(const BParams& P, int t, int j) {
 // sparse residuals D x - y and D u - y; objective, gap, next theta (+ bf16 terms)
 // observations the warp path left (more than WU hot or list entries): one CTA each
 __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
-    if (blockIdx.x < *P.nbig) update_hot_cta(P, t, P.big[blockIdx.x]);   // one CTA per listed observation
+    __shared__ int s_b;
+    const int nb = *P.nbig;                      // final: the warp kernel ran before this launch
+    for (;;) {                                   // a resident-sized grid pulls observations off the list
+        __syncthreads();
+        if (threadIdx.x == 0) s_b = atomicAdd(P.big_next, 1);
+        __syncthreads();
+        const int b = s_b;
+        if (b >= nb) break;
+        update_hot_cta(P, t, P.big[b]);
+    }
 }
 
 // Warp-per-observation update on the hot entries (the common case: <= WU hot entries and
@@ -1523,6 +1537,9 @@ __device__ __forceinline__ void resid_acc(const uint2& w, double va, double vb, 
 #ifndef BRESID_EB
 #define BRESID_EB 4
 #endif
+#ifndef BRESID_TPB
+#define BRESID_TPB 256
+#endif
 #ifndef BRESID_MINB
 #define BRESID_MINB 5
 #endif
@@ -1536,9 +1553,12 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
     __shared__ double s_sh[64];
     __shared__ int s_idx[TPB];
     __shared__ double s_a[TPB], s_b[TPB];
+    if (blockIdx.x >= P.B) {          // appended blocks: this iteration's screening (k_bscreen)
+        if (TPB == 256) bscreen_body(P, blockIdx.x - P.B, gridDim.x - P.B);
+        return;
+    }
     const int j = blockIdx.x;
     const int par = (t + 1) & 1;      // list written by this iteration's update
-    if (j == 0 && threadIdx.x == 0) { *P.nbig = 0; *P.scr_ctr = 0ull; }   // this iteration's lists are consumed
     if (P.status[j] != 0) {
         if (threadIdx.x == 0 && j == 0) *P.it = t + 1;
         return;
@@ -1640,26 +1660,25 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
 
 static void launch_update_hot(const BParams& P, int t, cudaStream_t s) {
     k_bupdate_warp<<<(P.B + UW - 1) / UW, UW * 32, 0, s>>>(P, t);
-    k_bupdate_hot<<<P.B, BT, 0, s>>>(P, t);     // CTAs past the big-list count exit at once
-    k_bscreen<<<4 * 148, 256, 0, s>>>(P);        // this iteration's screening, whole GPU
+    k_bupdate_hot<<<std::min(P.B, 5 * 148), BT, 0, s>>>(P, t);   // resident grid, dynamic work list
+    if (BRESID_TPB != 256) k_bscreen<<<NSCR, 256, 0, s>>>(P);   // else: blocks of the residual launch
 }
 
-#ifndef BRESID_TPB
-#define BRESID_TPB 256
-#endif
 static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
     constexpr int TPB = BRESID_TPB;
     constexpr int RC = 4 * TPB;
-    if (P.N <= RC) k_bresid<1, TPB><<<P.B, TPB, 0, s>>>(P, t);
-    else if (P.N <= 2 * RC) k_bresid<2, TPB><<<P.B, TPB, 0, s>>>(P, t);
-    else if (P.N <= 3 * RC) k_bresid<3, TPB><<<P.B, TPB, 0, s>>>(P, t);
-    else k_bresid<4, TPB><<<P.B, TPB, 0, s>>>(P, t);
+    const int grid = P.B + (TPB == 256 ? NSCR : 0);
+    if (P.N <= RC) k_bresid<1, TPB><<<grid, TPB, 0, s>>>(P, t);
+    else if (P.N <= 2 * RC) k_bresid<2, TPB><<<grid, TPB, 0, s>>>(P, t);
+    else if (P.N <= 3 * RC) k_bresid<3, TPB><<<grid, TPB, 0, s>>>(P, t);
+    else k_bresid<4, TPB><<<grid, TPB, 0, s>>>(P, t);
 }
 
 // per-iteration batch aggregates (fixed order): 1024 threads, loads of 4 observations in flight
 constexpr int TR_T = 1024;
 __global__ void __launch_bounds__(TR_T) k_btrace(BParams P, int t) {
     __shared__ double s_sh[4 * (TR_T / 32)];
+    if (threadIdx.x == 0) { *P.nbig = 0; *P.big_next = 0; *P.scr_ctr = 0ull; }   // this iteration's lists consumed
     double a[4] = {0, 0, 0, 0};
     for (int j0 = threadIdx.x; j0 < P.B; j0 += 4 * TR_T) {
         int st[4];
@@ -1751,6 +1770,7 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     p.hot_cnt = (int*)take(B * 4);
     p.big = (int*)take(B * 4);
     p.nbig = (int*)take(4);
+    p.big_next = (int*)take(4);
     p.hcap = 2048;
     p.hot_idx = (int*)take(B * (size_t)p.hcap * 4);
     p.hot_val = (float*)take(B * (size_t)p.hcap * 4);
@@ -1920,6 +1940,7 @@ int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out) {
     cudaEventRecord(ev[2], s);
     launch_bresid(P, t, s);
     cudaEventRecord(ev[3], s);
+    k_btrace<<<1, TR_T, 0, s>>>(P, t);          // resets the iteration's work lists
     cudaEventSynchronize(ev[3]);
     for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
     for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
