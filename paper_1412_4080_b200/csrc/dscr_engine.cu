@@ -153,6 +153,54 @@ __device__ __forceinline__ int find_slot(const int* off, int G, int f) {
 __device__ __forceinline__ int unit_atom_lo(const Params& P, int u) { return P.n_groups ? P.gptr[u] : u; }
 __device__ __forceinline__ int unit_atom_hi(const Params& P, int u) { return P.n_groups ? P.gptr[u + 1] : u + 1; }
 
+// Flat index -> slot of a segmented list (slot s holds entries [off[s], off[s+1])).
+// A CTA stages a window of K3_WIN consecutive slot offsets in shared memory, starting at
+// the slot of its first entry (one warp, 32-ary search), and resolves entries inside the
+// window with a shared-memory search; entries past the window fall back to find_slot.
+constexpr int K3_WIN = 256;
+
+
+// slot of flat entry f (last s with off[s] <= f), one warp: 32-ary search, ~log32(G) rounds
+__device__ __forceinline__ int warp_find_slot(const int* off, int G, int f, int lane) {
+    int lo = 0, hi = G;   // off[lo] <= f < off[hi]
+    while (hi - lo > 1) {
+        const int span = hi - lo;
+        const int probe = lo + (int)(((long long)span * lane) / 32);
+        const bool le = (lane == 0) || (probe > lo && off[probe] <= f);
+        const unsigned bal = __ballot_sync(0xffffffffu, le);
+        const int l = 31 - __clz(bal);                        // last lane whose probe is <= f
+        const int nlo = lo + (int)(((long long)span * l) / 32);
+        const int nhi = (l == 31) ? hi : lo + (int)(((long long)span * (l + 1)) / 32);
+        lo = max(nlo, lo);
+        hi = max(nhi, lo + 1);
+    }
+    return lo;
+}
+
+// all threads: stage the window starting at the slot of flat entry f0; returns the window end
+__device__ __forceinline__ int stage_window(const int* off, int G, int f0, int* s_off, int* s_s0) {
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        const int s0 = warp_find_slot(off, G, f0, threadIdx.x);
+        if (threadIdx.x == 0) *s_s0 = s0;
+    }
+    __syncthreads();
+    const int s0 = *s_s0;
+    for (int i = threadIdx.x; i < K3_WIN; i += NT) s_off[i] = (s0 + i <= G) ? off[s0 + i] : INT_MAX;
+    __syncthreads();
+    return s_off[K3_WIN - 1];
+}
+
+__device__ __forceinline__ int window_slot(const int* off, int G, const int* s_off, int s0, int wend, int f) {
+    if (f >= wend) return find_slot(off, G, f);
+    int a = 0, b = K3_WIN - 1;   // s_off[a] <= f < s_off[b]
+    while (b - a > 1) {
+        const int m = (a + b) >> 1;
+        if (s_off[m] <= f) a = m; else b = m;
+    }
+    return s0 + a;
+}
+
 // test radius from the dual-scaling bound; whole CTA participates.
 // Restates dual_scale_lasso/group + _safe_radius_sq + _shifted_radius
 // (screening.py:115-205).  bound = 1/corr_inf (Lasso) or min_g w_g/||c_g||.
@@ -244,6 +292,9 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     double wcs = 0.0, wss = 0.0, wnf = 0.0, wany = 0.0;
 
     const uint64_t pol = make_policy(P.l2_keep);
+    __shared__ int s_off[K3_WIN];
+    __shared__ int s_s0;
+    const int wend = stage_window(off, P.G, lo, s_off, &s_s0);   // slot offsets of this CTA's range
     if (!GROUP) {
         // Lasso: each warp streams C columns at once (C*U 32-byte loads in flight per lane);
         // lane c applies the update of column c.
@@ -251,7 +302,7 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
         for (int f0 = lo + warp * C; f0 < hi; f0 += NW * C) {
             int myj = -1;
             if (lane < C && f0 + lane < hi) {
-                const int s = find_slot(off, P.G, f0 + lane);
+                const int s = window_slot(off, P.G, s_off, s_s0, wend, f0 + lane);
                 myj = act[s * P.cap + (f0 + lane - off[s])];
             }
             int js[C];
@@ -295,7 +346,7 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     constexpr int GMAX = 64;                 // groups up to GMAX atoms: lane-parallel, staged in smem
     __shared__ double s_gc[GROUP ? NW : 1][GROUP ? GMAX : 1], s_gv[GROUP ? NW : 1][GROUP ? GMAX : 1];
     for (int f = lo + warp; GROUP && f < hi; f += NW) {
-        const int s = find_slot(off, P.G, f);
+        const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
         const int unit = act[s * P.cap + (f - off[s])];
         const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
         const int gs = j1 - j0;
@@ -576,54 +627,6 @@ __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* s
         return (P.gw[unit] - P.cnorm[unit]) / P.gsn[unit] - r > SCREEN_MARGIN;
     }
     return false;
-}
-
-// Flat index -> slot of a segmented list (slot s holds entries [off[s], off[s+1])).
-// A CTA stages a window of K3_WIN consecutive slot offsets in shared memory, starting at
-// the slot of its first entry (one warp, 32-ary search), and resolves entries inside the
-// window with a shared-memory search; entries past the window fall back to find_slot.
-constexpr int K3_WIN = 256;
-
-
-// slot of flat entry f (last s with off[s] <= f), one warp: 32-ary search, ~log32(G) rounds
-__device__ __forceinline__ int warp_find_slot(const int* off, int G, int f, int lane) {
-    int lo = 0, hi = G;   // off[lo] <= f < off[hi]
-    while (hi - lo > 1) {
-        const int span = hi - lo;
-        const int probe = lo + (int)(((long long)span * lane) / 32);
-        const bool le = (lane == 0) || (probe > lo && off[probe] <= f);
-        const unsigned bal = __ballot_sync(0xffffffffu, le);
-        const int l = 31 - __clz(bal);                        // last lane whose probe is <= f
-        const int nlo = lo + (int)(((long long)span * l) / 32);
-        const int nhi = (l == 31) ? hi : lo + (int)(((long long)span * (l + 1)) / 32);
-        lo = max(nlo, lo);
-        hi = max(nhi, lo + 1);
-    }
-    return lo;
-}
-
-// all threads: stage the window starting at the slot of flat entry f0; returns the window end
-__device__ __forceinline__ int stage_window(const int* off, int G, int f0, int* s_off, int* s_s0) {
-    __syncthreads();
-    if (threadIdx.x < 32) {
-        const int s0 = warp_find_slot(off, G, f0, threadIdx.x);
-        if (threadIdx.x == 0) *s_s0 = s0;
-    }
-    __syncthreads();
-    const int s0 = *s_s0;
-    for (int i = threadIdx.x; i < K3_WIN; i += NT) s_off[i] = (s0 + i <= G) ? off[s0 + i] : INT_MAX;
-    __syncthreads();
-    return s_off[K3_WIN - 1];
-}
-
-__device__ __forceinline__ int window_slot(const int* off, int G, const int* s_off, int s0, int wend, int f) {
-    if (f >= wend) return find_slot(off, G, f);
-    int a = 0, b = K3_WIN - 1;   // s_off[a] <= f < s_off[b]
-    while (b - a > 1) {
-        const int m = (a + b) >> 1;
-        if (s_off[m] <= f) a = m; else b = m;
-    }
-    return s0 + a;
 }
 
 // K2 per-CTA work: test, compaction into slot b, vectors, support list, partials
