@@ -25,6 +25,8 @@
 // (run loop), screening.py:115-413 (dual scaling, regions, tests),
 // problems.py:75-177, dictionary.py:82-117, 280-301.
 
+#include <map>
+#include <mutex>
 #include <cuda_runtime.h>
 #include <cuda_bf16.h>
 #include <dlfcn.h>
@@ -118,6 +120,8 @@ struct Params {
     double* trace;
     unsigned long long* kts;   // per-trip kernel timestamps [trips][8]
     int max_kts;
+    int max_gsize;
+    int k1_tile;       // K1 tiled path: row segments per column (0 = per-warp column path)
     int max_iters;
     int G, cap, TR, R, P, G3b;
     int col_offset, group_offset;
@@ -140,6 +144,12 @@ __device__ __forceinline__ void stamp(const Params& P, int slot) {
     const int trip = P.sc->trips;
     if (P.kts && trip < P.max_kts) P.kts[(size_t)trip * 8 + slot] = globaltimer();
 }
+
+// Programmatic dependent launch: the chain kernels are launched with programmatic stream
+// serialization, so the next kernel's CTAs are scheduled while this one drains; every chain
+// kernel waits for its predecessor's completion (and memory flush) before touching state.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 __device__ __forceinline__ int find_slot(const int* off, int G, int f) {
     int lo = 0, hi = G;   // off[lo] <= f < off[hi]
@@ -294,7 +304,9 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     const uint64_t pol = make_policy(P.l2_keep);
     __shared__ int s_off[K3_WIN];
     __shared__ int s_s0;
-    const int wend = stage_window(off, P.G, lo, s_off, &s_s0);   // slot offsets of this CTA's range
+    // nothing screened yet: the order-preserving list is the identity (no slot lookups)
+    const bool ident = (nu == P.n_units);
+    const int wend = ident ? 0 : stage_window(off, P.G, lo, s_off, &s_s0);   // slot offsets of this CTA's range
     if (!GROUP) {
         // Lasso: each warp streams C columns at once (C*U 32-byte loads in flight per lane);
         // lane c applies the update of column c.
@@ -302,8 +314,12 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
         for (int f0 = lo + warp * C; f0 < hi; f0 += NW * C) {
             int myj = -1;
             if (lane < C && f0 + lane < hi) {
-                const int s = window_slot(off, P.G, s_off, s_s0, wend, f0 + lane);
-                myj = act[s * P.cap + (f0 + lane - off[s])];
+                if (ident) {
+                    myj = f0 + lane;
+                } else {
+                    const int s = window_slot(off, P.G, s_off, s_s0, wend, f0 + lane);
+                    myj = act[s * P.cap + (f0 + lane - off[s])];
+                }
             }
             int js[C];
 #pragma unroll
@@ -346,8 +362,11 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     constexpr int GMAX = 64;                 // groups up to GMAX atoms: lane-parallel, staged in smem
     __shared__ double s_gc[GROUP ? NW : 1][GROUP ? GMAX : 1], s_gv[GROUP ? NW : 1][GROUP ? GMAX : 1];
     for (int f = lo + warp; GROUP && f < hi; f += NW) {
-        const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
-        const int unit = act[s * P.cap + (f - off[s])];
+        int unit = f;
+        if (!ident) {
+            const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
+            unit = act[s * P.cap + (f - off[s])];
+        }
         const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
         const int gs = j1 - j0;
         if (gs <= GMAX) {
@@ -473,6 +492,240 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     }
 }
 
+// K1 tiled path, for short columns (at most K1T_SEGS segments of 32*V*U rows; c1-c3 shapes).
+// The per-warp column path gives each warp whole columns, so a CTA whose share is a few
+// columns more than a multiple of 4*NW waits a second full column chain on one warp (c2:
+// 34 columns per CTA = 16 round trips).  Here the CTA's atoms are resolved into shared
+// memory in batches of K1T_ATOMS, the correlations are (atom quad x row segment) items dealt
+// evenly over the warps -- one round trip of 4*U loads per lane per item -- and the segment
+// partials are combined in fixed segment order (independent of the grid), then the update
+// runs per atom (Lasso) or per group (one warp per group, correlations read from shared).
+constexpr int K1T_ATOMS = 256;
+constexpr int K1T_SEGS = 16;
+
+template <typename T>
+__device__ __forceinline__ void warp_dots_seg(const T* const (&col)[4], int n, const double* sv, int lane,
+                                              uint64_t pol, int row0, double (&out)[4]) {
+    constexpr int V = Vec<T>::V, U = K1Cfg<T>::U;
+    typename Vec<T>::Raw d[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int i = row0 + u * 32 * V + lane * V;
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (i < n && col[c]) Vec<T>::load_raw(col[c] + i, d[u][c], pol);
+            else Vec<T>::zero(d[u][c]);
+        }
+    }
+    double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int i = row0 + u * 32 * V + lane * V;
+        if (i < n) {
+#pragma unroll
+            for (int v = 0; v < V; ++v) {
+                const double t = sv[i + v];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) acc[c] = fma(Vec<T>::get(d[u][c], v), t, acc[c]);
+            }
+        }
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) out[c] = warp_sum(acc[c]);
+}
+
+template <typename T, bool GROUP>
+__device__ __forceinline__ void k1_body_tile(const Params& P, int b, int G, double* s_theta) {
+    __shared__ double s_red[NW][NP1];
+    __shared__ int s_atom[K1T_ATOMS];
+    __shared__ int s_unit[K1T_ATOMS], s_uoff[K1T_ATOMS + 1];
+    __shared__ int s_scan[2 * NW + 1];
+    __shared__ int s_off[K3_WIN];
+    __shared__ int s_s0;
+    constexpr int GMAX = 64;
+    __shared__ double s_gv[GROUP ? NW : 1][GROUP ? GMAX : 1];
+    double* s_part = s_theta + P.ldd;                 // [K1T_SEGS][K1T_ATOMS] after theta
+    dscr_scalars* sc = P.sc;
+    const int mode = sc->mode;
+    const int p = sc->parity, xi = sc->xi;
+    const int nu = sc->n_units;
+    const int lo = (int)(((long long)nu * b) / G), hi = (int)(((long long)nu * (b + 1)) / G);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool need_dot = (mode == MODE_NORMAL);
+    if (need_dot && hi > lo) {
+        const double* th = P.theta[p];
+        for (int i = threadIdx.x; i < P.ldd; i += NT) s_theta[i] = th[i];
+    }
+    const T* D = static_cast<const T*>(P.D);
+    const int* act = P.act[p];
+    const int* off = P.act_off[p];
+    const double* xc = P.x[xi];
+    double* xn = P.x[(xi + 1) % 3];
+    const double* xp = P.x[(xi + 2) % 3];
+    const double* uc = P.u[p];
+    const int algo = P.algo;
+    const double L = sc->L, lam = P.lam;
+    const double tau = sc->tau, tws = P.tw_step;
+    const bool first = (sc->t == 0);
+    double thr;
+    if (algo == DSCR_CP) thr = lam * tau;
+    else if (algo == DSCR_TWIST) thr = lam * tws;
+    else thr = lam / L;
+    const int nseg = P.k1_tile;
+    constexpr int SEGR = 32 * Vec<T>::V * K1Cfg<T>::U;   // rows per segment
+
+    double wmax = GROUP ? INFINITY : 0.0;
+    double wcs = 0.0, wss = 0.0, wnf = 0.0, wany = 0.0;
+    const uint64_t pol = make_policy(P.l2_keep);
+    const bool ident = (nu == P.n_units);
+    int wend = 0;
+    if (ident) __syncthreads();   // theta staged
+    else wend = stage_window(off, P.G, lo, s_off, &s_s0);   // (syncs: theta staged)
+    const int ub = GROUP ? max(1, K1T_ATOMS / max(1, P.max_gsize)) : K1T_ATOMS;
+
+    for (int b0 = lo; b0 < hi; b0 += ub) {
+        const int nb = min(ub, hi - b0);
+        // ---- resolve the batch's units and atoms
+        int unit = -1, gs = 0;
+        if (threadIdx.x < nb) {
+            const int f = b0 + threadIdx.x;
+            if (ident) {
+                unit = f;
+            } else {
+                const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
+                unit = act[s * P.cap + (f - off[s])];
+            }
+            gs = GROUP ? (P.gptr[unit + 1] - P.gptr[unit]) : 1;
+        }
+        int na;
+        const int aoff = GROUP ? block_exscan(gs, s_scan, &na) : (int)threadIdx.x;   // (syncs)
+        if (!GROUP) na = nb;
+        if (threadIdx.x < nb) {
+            s_unit[threadIdx.x] = unit;
+            s_uoff[threadIdx.x] = aoff;
+            if (GROUP) { const int j0 = P.gptr[unit]; for (int k = 0; k < gs; ++k) s_atom[aoff + k] = j0 + k; }
+            else s_atom[threadIdx.x] = unit;
+        }
+        if (threadIdx.x == 0) s_uoff[nb] = na;
+        __syncthreads();
+        // ---- correlation items: (atom quad, row segment), dealt round-robin over the warps
+        if (need_dot) {
+            const int nq = (na + 3) >> 2;
+            for (int it = warp; it < nq * nseg; it += NW) {
+                const int q = it / nseg, sg = it - q * nseg;
+                const T* cols[4];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int a = 4 * q + c;
+                    cols[c] = (a < na) ? D + (size_t)s_atom[a] * P.ldd : nullptr;
+                }
+                double cs[4];
+                warp_dots_seg<T>(cols, P.n, s_theta, lane, pol, sg * SEGR, cs);
+                if (lane < 4 && 4 * q + lane < na) {
+                    double v = cs[0];
+#pragma unroll
+                    for (int c = 1; c < 4; ++c) if (lane == c) v = cs[c];
+                    s_part[sg * K1T_ATOMS + 4 * q + lane] = v;
+                }
+            }
+        }
+        __syncthreads();
+        // ---- fixed-order segment combination
+        for (int a = threadIdx.x; a < na; a += NT) {
+            const int j = s_atom[a];
+            double c;
+            if (need_dot) {
+                c = s_part[a];
+                for (int sg = 1; sg < nseg; ++sg) c += s_part[sg * K1T_ATOMS + a];
+                P.corr[j] = c;
+            } else {
+                c = P.corr[j];
+            }
+            if (GROUP) { s_part[a] = c; continue; }
+            // Lasso update of atom j (as in k1_body)
+            wmax = fmax(wmax, fabs(c));
+            double point, v;
+            if (algo == DSCR_FISTA) { point = uc[j]; v = point - c / L; }
+            else if (algo == DSCR_CP) { point = xc[j]; v = point - tau * c; }
+            else if (algo == DSCR_TWIST) { point = xc[j]; v = point - tws * c; }
+            else { point = xc[j]; v = point - c / L; }
+            double cand = soft(v, thr);
+            if (algo == DSCR_TWIST && !first) {
+                const double a2 = P.twa, bb = P.twb;
+                cand = ((1.0 - a2) * xp[j] + (a2 - bb) * xc[j]) + bb * cand;
+            }
+            xn[j] = cand;
+            if (!isfinite(cand)) wnf = 1.0;
+            const double st = cand - point;
+            wcs += c * st;
+            wss += st * st;
+        }
+        if (GROUP) {
+            __syncthreads();
+            // ---- group update: one warp per group (sizes <= GMAX), as the k1_body group path
+            for (int t = warp; t < nb; t += NW) {
+                const int u = s_unit[t], a0 = s_uoff[t], g = s_uoff[t + 1] - a0;
+                const int j0 = P.gptr[u];
+                const double* gc = s_part + a0;
+                for (int c0 = lane; c0 < g; c0 += 32) {
+                    const int j = j0 + c0;
+                    const double cc = gc[c0];
+                    double v;
+                    if (algo == DSCR_FISTA) v = uc[j] - cc / L;
+                    else if (algo == DSCR_CP) v = xc[j] - tau * cc;
+                    else if (algo == DSCR_TWIST) v = xc[j] - tws * cc;
+                    else v = xc[j] - cc / L;
+                    s_gv[warp][c0] = v;
+                }
+                __syncwarp();
+                double fac = 0.0;
+                if (lane == 0) {   // group soft threshold (dictionary.py:290-301), numpy reduceat order
+                    const double nv = sqrt(np_segment_sum([&](int i) { double q = s_gv[warp][i - j0]; return q * q; }, j0, g));
+                    const double nc = sqrt(np_segment_sum([&](int i) { double q = gc[i - j0]; return q * q; }, j0, g));
+                    if (nc > 0.0) { wmax = fmin(wmax, P.gw[u] / nc); wany = 1.0; }
+                    fac = (nv > 0.0) ? fmax(1.0 - thr * P.gw[u] / nv, 0.0) : 0.0;
+                }
+                fac = __shfl_sync(0xffffffffu, fac, 0);
+                for (int c0 = lane; c0 < g; c0 += 32) {
+                    const int j = j0 + c0;
+                    double cand = s_gv[warp][c0] * fac;
+                    if (algo == DSCR_TWIST && !first) {
+                        const double a2 = P.twa, bb = P.twb;
+                        cand = ((1.0 - a2) * xp[j] + (a2 - bb) * xc[j]) + bb * cand;
+                    }
+                    xn[j] = cand;
+                    if (!isfinite(cand)) wnf = 1.0;
+                    const double point = (algo == DSCR_FISTA) ? uc[j] : xc[j];
+                    const double st = cand - point;
+                    wcs += gc[c0] * st;
+                    wss += st * st;
+                }
+                __syncwarp();
+            }
+        }
+        __syncthreads();   // s_atom / s_part reuse by the next batch
+    }
+    wmax = GROUP ? warp_min(wmax) : warp_max(wmax);
+    wcs = warp_sum(wcs);
+    wss = warp_sum(wss);
+    wnf = warp_max(wnf);
+    wany = warp_max(wany);
+    if (lane == 0) {
+        s_red[warp][0] = wmax; s_red[warp][1] = wcs; s_red[warp][2] = wss;
+        s_red[warp][3] = wnf; s_red[warp][4] = wany;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double m = GROUP ? INFINITY : 0.0, cs = 0.0, ss = 0.0, nf = 0.0, any = 0.0;
+        for (int w = 0; w < NW; ++w) {
+            m = GROUP ? fmin(m, s_red[w][0]) : fmax(m, s_red[w][0]);
+            cs += s_red[w][1]; ss += s_red[w][2]; nf = fmax(nf, s_red[w][3]); any = fmax(any, s_red[w][4]);
+        }
+        double* o = P.p1 + (size_t)b * NP1;
+        o[0] = m; o[1] = cs; o[2] = ss; o[3] = nf; o[4] = any;
+    }
+}
+
 // K1 tail: fixed-order reduction of the G partials, FISTA/CP scalars, radius.  Run by the
 // last CTA (graph path) or redundantly by every CTA (persistent path).
 template <bool GROUP>
@@ -549,12 +802,15 @@ template <typename T, bool GROUP>
 __global__ void __launch_bounds__(NT, K1Cfg<T>::MINB) k1_corr_update(Params P) {
     extern __shared__ double s_theta[];
     __shared__ int s_flag;
+    pdl_wait();
+    pdl_trigger();
     dscr_scalars* sc = P.sc;
     if (sc->stop || sc->t >= sc->run_limit) return;
     const int mode = sc->mode;
     if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 0);
-    k1_body<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
+    if (P.k1_tile) k1_body_tile<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
+    else k1_body<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
     if (!last_block(P.tickets + 0, gridDim.x, &s_flag)) return;
     k1_final<GROUP>(P, gridDim.x);
 }
@@ -658,14 +914,19 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     int n_keep = 0, n_sup = 0;
     double pen = 0.0, nnz = 0.0, kept_atoms = 0.0, ssr = 0.0, dropped = 0.0;
     int wend = INT_MIN;
+    const bool ident = (nu == P.n_units);   // nothing screened yet: identity list
     for (int base = lo; base < hi; base += NT) {
-        if (base >= wend) wend = stage_window(off, P.G, base, s_off, &s_s0);   // uniform
+        if (!ident && base >= wend) wend = stage_window(off, P.G, base, s_off, &s_s0);   // uniform
         const int f = base + threadIdx.x;
         const bool valid = f < hi;
         int unit = -1;
         if (valid) {
-            const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
-            unit = act[s * P.cap + (f - off[s])];
+            if (ident) {
+                unit = f;
+            } else {
+                const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
+                unit = act[s * P.cap + (f - off[s])];
+            }
         }
         const bool masked = valid && test_on && unit_test(P, sc, unit);
         if (valid && !static_mode) P.mask[f] = masked ? 1 : 0;
@@ -803,6 +1064,8 @@ __device__ void k2_final(const Params& P, int G) {
 template <bool GROUP>
 __global__ void __launch_bounds__(NT) k2_screen(Params P) {
     __shared__ int s_flag;
+    pdl_wait();
+    pdl_trigger();
     dscr_scalars* sc = P.sc;
     if (sc->stop) return;
     const int mode = sc->mode;
@@ -921,6 +1184,8 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
 
 template <typename T>
 __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
+    pdl_wait();
+    pdl_trigger();
     dscr_scalars* sc = P.sc;
     if (sc->stop || sc->t >= sc->run_limit) return;
     if (sc->mode == MODE_STATIC) return;
@@ -1137,6 +1402,8 @@ __device__ void k3b_final(const Params& P, int G3) {
 
 __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     __shared__ int s_flag;
+    pdl_wait();
+    pdl_trigger();
     dscr_scalars* sc = P.sc;
     if (sc->stop || sc->t >= sc->run_limit) return;
     if (sc->mode == MODE_STATIC) return;
@@ -1581,7 +1848,7 @@ struct Layout {
 };
 
 struct Geometry {
-    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1;
+    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1, tile;
 };
 
 static int dtype_size(int dt) { return dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2); }
@@ -1599,14 +1866,28 @@ static float l2_keep_fraction(size_t dict_bytes) {
     return 0.0f;
 }
 
+// Max dynamic shared memory attribute of a kernel.  The attribute is global per function and
+// graphs created earlier keep launching with their own sizes, so it only ever grows (a later,
+// smaller problem must not invalidate an earlier engine's launches).
+static cudaError_t raise_smem(const void* fn, int smem) {
+    static std::mutex mu;
+    static std::map<const void*, int> cur;
+    std::lock_guard<std::mutex> lk(mu);
+    int& c = cur[fn];
+    if (smem <= c) return cudaSuccess;
+    cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e == cudaSuccess) c = smem;
+    return e;
+}
+
 template <typename T>
 static int k1_occ_t(bool group, int smem) {
     int n = 0;
     if (group) {
-        cudaFuncSetAttribute(k1_corr_update<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        raise_smem((const void*)k1_corr_update<T, true>, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_corr_update<T, true>, NT, smem);
     } else {
-        cudaFuncSetAttribute(k1_corr_update<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        raise_smem((const void*)k1_corr_update<T, false>, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k1_corr_update<T, false>, NT, smem);
     }
     return std::max(1, n);
@@ -1616,10 +1897,10 @@ template <typename T>
 static int pers_occ_t(bool group, int smem) {
     int n = 0;
     if (group) {
-        cudaFuncSetAttribute(k_persistent<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        raise_smem((const void*)k_persistent<T, true>, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent<T, true>, NT, smem);
     } else {
-        cudaFuncSetAttribute(k_persistent<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        raise_smem((const void*)k_persistent<T, false>, smem);
         cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_persistent<T, false>, NT, smem);
     }
     return n;
@@ -1657,6 +1938,13 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     g.smem1 = pr->ldd * (int)sizeof(double);
+    {   // K1 tiled path for short columns (DSCR_K1_TILE=0 forces the per-warp column path)
+        const int segr = 32 * (32 / dtype_size(pr->dtype)) * (pr->dtype == DSCR_F64 ? K1Cfg<double>::U : 1);
+        const int nseg = (pr->n_rows + segr - 1) / segr;
+        const char* et = getenv("DSCR_K1_TILE");
+        g.tile = (nseg >= 5 && nseg <= K1T_SEGS && max_gsize <= 64 && !(et && !strcmp(et, "0"))) ? nseg : 0;
+        if (g.tile) g.smem1 += K1T_ATOMS * g.tile * (int)sizeof(double);
+    }
     // resident K1 CTAs per SM (registers + theta staging buffer): one full wave
     // one full wave; also co-resident for the persistent kernel (grid barriers)
     const int per_sm = std::max(1, std::min(k1_occupancy(pr->dtype, pr->n_groups > 0, g.smem1),
@@ -1732,10 +2020,22 @@ struct dscr_solver {
     cudaGraphExec_t e_setup = nullptr, e_loop = nullptr;
     int world = 1, rank = 0;
     void* comm = nullptr;
+    bool pdl = false;   // chain kernels launched with programmatic dependent launch
 };
 
 extern "C" const char* dscr_last_error(void) { return err_store().c_str(); }
 extern "C" int dscr_abi_version(void) { return DSCR_ABI_VERSION; }
+
+// largest group size (1 for the Lasso); reads the device group pointer
+static int group_max_size(const dscr_problem_desc* pr, int* out) {
+    *out = 1;
+    if (pr->n_groups <= 0) return DSCR_OK;
+    if (!pr->group_ptr) return set_inval("group problems need group_ptr");
+    std::vector<int> ptr(pr->n_groups + 1);
+    CK(cudaMemcpy(ptr.data(), pr->group_ptr, ptr.size() * sizeof(int), cudaMemcpyDeviceToHost));
+    for (int g = 0; g < pr->n_groups; ++g) *out = std::max(*out, ptr[g + 1] - ptr[g]);
+    return DSCR_OK;
+}
 
 // atoms any `cap` active units can hold: sum of the `cap` largest group sizes
 static int max_atoms_per_slot(const dscr_problem_desc* pr, int cap, int* out) {
@@ -1787,54 +2087,71 @@ static int validate(const dscr_problem_desc* pr, const dscr_config* cfg, int* n_
 extern "C" size_t dscr_solver_workspace_size(const dscr_problem_desc* pr, const dscr_config* cfg) {
     int nu, mg;
     if (validate(pr, cfg, &nu, &mg) != DSCR_OK) return 0;
-    Geometry g = make_geometry(pr, nu, 1);
+    if (group_max_size(pr, &mg) != DSCR_OK) return 0;
+    Geometry g = make_geometry(pr, nu, mg);
     if (pr->n_groups > 0 && (!pr->group_ptr || max_atoms_per_slot(pr, g.cap, &g.sup_cap) != DSCR_OK)) return 0;
     size_t total;
     make_offsets(pr, cfg, g, nu, &total);
     return total;
 }
 
+// Kernel launch with optional programmatic stream serialization (PDL edges when captured).
+template <typename... KArgs>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, size_t smem, cudaStream_t s, bool pdl,
+                              const Params& P) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
+// Off by default: measured on B200 (c1, in-graph stamps) the chain is latency-bound inside
+// the kernels, and PDL edges left the loop time unchanged (39.1 vs 38.5 us/iteration).
+static bool pdl_enabled() {
+    const char* e = getenv("DSCR_PDL");
+    return e && !strcmp(e, "1");
+}
+
 static int launch_iteration(dscr_solver* h, const Params& P, cudaStream_t s, cudaEvent_t* ev = nullptr) {
     const Geometry& g = h->geo;
     const bool group = P.n_groups > 0;
     const size_t smem1 = (size_t)g.smem1;
+    const bool pdl = h->pdl && !ev;   // timed per-kernel runs keep plain launches
+    void (*k1)(Params);
+    void (*k3a)(Params);
     switch (P.dtype) {
-        case DSCR_F64:
-            if (group) k1_corr_update<double, true><<<g.G, NT, smem1, s>>>(P);
-            else k1_corr_update<double, false><<<g.G, NT, smem1, s>>>(P);
-            break;
-        case DSCR_F32:
-            if (group) k1_corr_update<float, true><<<g.G, NT, smem1, s>>>(P);
-            else k1_corr_update<float, false><<<g.G, NT, smem1, s>>>(P);
-            break;
-        default:
-            if (group) k1_corr_update<__nv_bfloat16, true><<<g.G, NT, smem1, s>>>(P);
-            else k1_corr_update<__nv_bfloat16, false><<<g.G, NT, smem1, s>>>(P);
+        case DSCR_F64: k1 = group ? k1_corr_update<double, true> : k1_corr_update<double, false>; k3a = k3a_residual<double>; break;
+        case DSCR_F32: k1 = group ? k1_corr_update<float, true> : k1_corr_update<float, false>; k3a = k3a_residual<float>; break;
+        default: k1 = group ? k1_corr_update<__nv_bfloat16, true> : k1_corr_update<__nv_bfloat16, false>; k3a = k3a_residual<__nv_bfloat16>;
     }
-    CK(cudaGetLastError());
+    cudaError_t le = launch_pdl(k1, dim3(g.G), smem1, s, pdl, P);
+    if (le != cudaSuccess) return set_err("K1 launch", le);
     if (ev) CK(cudaEventRecord(ev[1], s));
-    if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
-    else k2_screen<false><<<g.G, NT, 0, s>>>(P);
-    CK(cudaGetLastError());
+    le = launch_pdl(group ? k2_screen<true> : k2_screen<false>, dim3(g.G), 0, s, pdl, P);
+    if (le != cudaSuccess) return set_err("K2 launch", le);
     if (ev) CK(cudaEventRecord(ev[2], s));
-    dim3 g3(g.R, g.P);
-    switch (P.dtype) {
-        case DSCR_F64: k3a_residual<double><<<g3, NT, 0, s>>>(P); break;
-        case DSCR_F32: k3a_residual<float><<<g3, NT, 0, s>>>(P); break;
-        default: k3a_residual<__nv_bfloat16><<<g3, NT, 0, s>>>(P);
-    }
-    CK(cudaGetLastError());
+    le = launch_pdl(k3a, dim3(g.R, g.P), 0, s, pdl, P);
+    if (le != cudaSuccess) return set_err("K3a launch", le);
     if (ev) CK(cudaEventRecord(ev[3], s));
-    k3b_finalize<<<g.G3b, NT, 0, s>>>(P);
-    CK(cudaGetLastError());
+    le = launch_pdl(k3b_finalize, dim3(g.G3b), 0, s, pdl, P);
+    if (le != cudaSuccess) return set_err("K3b launch", le);
     return DSCR_OK;
 }
 
 template <typename T>
-static int set_smem_attrs(size_t smem) {
-    CK(cudaFuncSetAttribute(k1_corr_update<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k1_corr_update<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    CK(cudaFuncSetAttribute(k_correlate<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+static int set_smem_attrs(size_t smem, bool k1 = true) {
+    if (k1) {
+        CK(raise_smem((const void*)k1_corr_update<T, false>, (int)smem));
+        CK(raise_smem((const void*)k1_corr_update<T, true>, (int)smem));
+    }
+    CK(raise_smem((const void*)k_correlate<T>, (int)smem));
     return DSCR_OK;
 }
 
@@ -1848,15 +2165,15 @@ static int launch_correlate(int dtype, const void* D, int ldd, int n, int k, con
     int rc;
     switch (dtype) {
         case DSCR_F64:
-            if ((rc = set_smem_attrs<double>(smem))) return rc;
+            if ((rc = set_smem_attrs<double>(smem, false))) return rc;
             k_correlate<double><<<grid, NT, smem, s>>>((const double*)D, ldd, n, k, v, out, skip, keep);
             break;
         case DSCR_F32:
-            if ((rc = set_smem_attrs<float>(smem))) return rc;
+            if ((rc = set_smem_attrs<float>(smem, false))) return rc;
             k_correlate<float><<<grid, NT, smem, s>>>((const float*)D, ldd, n, k, v, out, skip, keep);
             break;
         default:
-            if ((rc = set_smem_attrs<__nv_bfloat16>(smem))) return rc;
+            if ((rc = set_smem_attrs<__nv_bfloat16>(smem, false))) return rc;
             k_correlate<__nv_bfloat16><<<grid, NT, smem, s>>>((const __nv_bfloat16*)D, ldd, n, k, v, out, skip, keep);
     }
     CK(cudaGetLastError());
@@ -1936,12 +2253,14 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     if (!out || !workspace) return set_inval("null output or workspace");
     if (pr->n_groups > 0 && !(pr->group_ptr && pr->group_w && pr->group_snorm))
         return set_inval("group problems need group_ptr, group_w and group_snorm");
-    Geometry g = make_geometry(pr, nu, 1);
+    if ((rc = group_max_size(pr, &mg))) return rc;
+    Geometry g = make_geometry(pr, nu, mg);
     if ((rc = max_atoms_per_slot(pr, g.cap, &g.sup_cap))) return rc;
     size_t total;
     Offsets o = make_offsets(pr, cfg, g, nu, &total);
     if (workspace_bytes < total) return set_inval("workspace too small");
     dscr_solver* h = new dscr_solver();
+    h->pdl = pdl_enabled();
     h->prob = *pr;
     h->cfg = *cfg;
     h->geo = g;
@@ -1983,6 +2302,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.max_kts = kts_slots(cfg);
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
+    P.k1_tile = g.tile; P.max_gsize = g.max_gsize;
     P.col_offset = pr->col_offset;
     P.group_offset = pr->group_offset;
     P.in_graph = 1;
@@ -2000,6 +2320,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
         P.persistent = coop && occ * sms >= g.G && g.G <= PERS_MAX_G && env && strcmp(env, "persistent") == 0;
     }
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
+    if (const char* ek = getenv("DSCR_L2_KEEP")) P.l2_keep = (float)atof(ek);   // experiment knob
 
     cudaStream_t us = (cudaStream_t)stream;
     // smem attributes for the K1 instantiations
@@ -2060,7 +2381,13 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     // trips after a stop or pause return at entry.
     for (int r = 0; r < TRIPS_PER_BODY && rc == DSCR_OK; ++r) rc = launch_iteration(h, h->P, cs);
     e = cudaStreamEndCapture(cs, &tmp);
-    if (rc || e != cudaSuccess) { dscr_solver_destroy(h); return rc ? rc : set_err("end capture body", e); }
+    if (rc || e != cudaSuccess) {
+        // an invalidated capture leaves the conditional body unusable and cudaGraphDestroy on its
+        // parent crashes in the driver: leak the loop graph on this error path
+        h->g_loop = nullptr;
+        dscr_solver_destroy(h);
+        return rc ? rc : set_err("end capture body", e);
+    }
     e = cudaGraphInstantiate(&h->e_loop, gl, 0);
     if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("instantiate loop", e); }
     *out = h;
