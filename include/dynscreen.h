@@ -154,6 +154,7 @@ typedef struct dscr_scalars {
     double gap, t0_ns, gst3_coef, gst3_nsq;
     double ds_sq, fc, tw_step, spare;
     double astar_nsq, gstar_w;   /* ||a_*||^2 (norm-aware DST3); weight of the extremal group (GST3) */
+    double oc_empty, oc_spare;   /* one-collective sharding: every unit screened this trip (global); spare */
 } dscr_scalars;
 
 /* Device pointers into a solver's workspace (valid while the handle lives). */
@@ -177,7 +178,7 @@ typedef struct dscr_solver_buffers {
     int32_t max_kts;
     int32_t G;               /* CTAs of the per-unit kernels (= number of slots) */
     int32_t cap;             /* slot capacity in units */
-    int32_t comm_len;        /* doubles in `comm` */
+    int32_t comm_len;        /* doubles in `comm` (incl. 64 x 8 one-collective rank slots) */
     double* comm;            /* multi-rank exchange region: [0,8) MAX, [8,16) setup, [16,32)+[32,32+2*ldd) SUM */
     double* vec;             /* ldd: extremal atom / GST3 normal (broadcast from the owner rank) */
 } dscr_solver_buffers;
@@ -346,7 +347,21 @@ int dscr_batched_destroy(dscr_batched* h);
 #define DSCR_PH_K3A 13
 #define DSCR_PH_K3S 14
 #define DSCR_PH_K3B 15
+#define DSCR_PH_K2S 16     /* one-collective trips: support of x_t / u_t before the test */
+#define DSCR_PH_K1R1 17    /* one-collective trips: radius, dropped-nonzero and all-screened flags */
+#define DSCR_PH_K2C 18     /* one-collective trips: test and compaction after the collective */
 int dscr_solver_phase(dscr_solver* h, int phase, void* stream);
+/* One collective per trip (SURVEY §7 hard part 2).  The residual partials are taken on the
+ * unreduced iterate, and each rank's MAX quantities (max |c|, non-finite flag), the largest
+ * test value over its units with a nonzero coefficient and the smallest over its active units
+ * travel in rank-indexed slots of the SUM buffer (comm[32+2*ldd + 8*rank ..+8), zeros
+ * elsewhere, so the SUM is a gather).  After the SUM every rank knows the radius and whether
+ * any rank screens a unit carrying a nonzero coefficient; only then (rare) a FIXUP trip
+ * recomputes the residuals on the reduced iterate.  Per trip: K1; K2S; K3A; K3S;
+ * SUM comm[16..32+2*ldd+8*world); K1R1; K2C; K3B.  The dome test keeps two collectives.
+ * world <= 64.  rank/world also select the slot; one_collective = 0 restores the
+ * two-collective phase semantics. */
+int dscr_solver_set_collectives(dscr_solver* h, int rank, int world, int one_collective);
 
 /* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */
 int dscr_comm_unique_id(void* id_out_128);

@@ -24,6 +24,8 @@ TRACE_FIELDS = 10
 TR_T, TR_KEPT, TR_NNZ, TR_OBJ, TR_GAP, TR_RADIUS, TR_L, TR_NS, TR_UNITS, TR_SUPPORT = range(10)
 (PH_SETUP_LOCAL, PH_SETUP_ADOPT, PH_SETUP_VEC, PH_SETUP_FINISH, PH_STATIC_LOCAL, PH_STATIC_FINISH) = range(6)
 PH_K1, PH_K1R, PH_K2, PH_K3A, PH_K3S, PH_K3B = range(10, 16)
+PH_K2S, PH_K1R1, PH_K2C = 16, 17, 18
+OC_SLOT, OC_MAX_WORLD = 8, 64   # one-collective rank slots: 8 doubles per rank after the SUM vector
 CM_MAX, CM_SETUP, CM_SUM, CM_VEC = 0, 8, 16, 32
 
 ABI_FUNCTIONS = (
@@ -31,7 +33,7 @@ ABI_FUNCTIONS = (
     "dscr_prox_group", "dscr_test_sphere", "dscr_test_dome", "dscr_test_group",
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
-    "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_phase", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
+    "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_phase", "dscr_solver_set_collectives", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
     "dscr_batched_gemm_bf16", "dscr_batched_workspace_size", "dscr_batched_create", "dscr_batched_setup",
     "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_profile", "dscr_batched_destroy",
     "dscr_corr_exact_work_size", "dscr_corr_exact_bf16", "dscr_group_spectral_norms", "dscr_ingest_rows_f64",
@@ -64,7 +66,7 @@ _SCALAR_INTS = ("t run_limit max_iters mode stop status parity xi moved have_fpr
                 "static_done trips").split()
 _SCALAR_DBLS = ("L l_acc l_new beta tau sigma phi sigma_new theta_sq theta_y yy lmax lmax_sign shift_sq "
                 "corr_inf mu rsafe_sq radius dome_rs dome_cut dome_slope dome_flat maj_cs maj_ss pen ss_red "
-                "f_prev F gap t0_ns gst3_coef gst3_nsq ds_sq fc tw_step spare astar_nsq gstar_w").split()
+                "f_prev F gap t0_ns gst3_coef gst3_nsq ds_sq fc tw_step spare astar_nsq gstar_w oc_empty oc_spare").split()
 
 
 class Scalars(C.Structure):
@@ -128,6 +130,7 @@ def _declare(lib):
         "dscr_solver_destroy": (i32, [vp]),
         "dscr_solver_profile": (i32, [vp, i32, vp, C.POINTER(C.c_float)]),
         "dscr_solver_phase": (i32, [vp, i32, vp]),
+        "dscr_solver_set_collectives": (i32, [vp, i32, i32, i32]),
         "dscr_comm_unique_id": (i32, [vp]),
         "dscr_solver_set_comm": (i32, [vp, vp, i32, i32]),
         "dscr_batched_gemm_bf16": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]),

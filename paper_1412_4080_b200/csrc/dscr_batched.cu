@@ -204,6 +204,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
         }
     } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
+        __shared__ uint4 s_cw[EPI_WARPS][32];   // per-warp column words (mask, list, threshold)
+        const int wslot = warp - 2;
         const int q = warp & 3;
         constexpr int PARTS = EPI_WARPS / 4;
         const int half = (warp - 2) >> 2;                             // which part of the tile's columns
@@ -239,34 +241,50 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     wn_n = g.nzm[(size_t)jl * g.words + (m0 >> 5)];
                     th_n = g.thr[jl];
                 }
+                // this chunk's per-column words (lane = column) staged for broadcast reads: one
+                // LDS.128 per column instead of three shuffles
+                __syncwarp();
+                s_cw[wslot][lane] = make_uint4(wa_c, wn_c, __float_as_uint(th_c), 0u);
+                __syncwarp();
                 uint32_t r[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + cbase + k * 32, r);
                 // pass 1 (branch free): activity, hot flags, per-column max over the warp's atoms
-                // (the mask / list words arrive one per column, lane = column; shuffled per column)
+                const uint32_t lbit = 1u << lane;
                 uint32_t hotbits = 0u, mymax = 0u;
 #pragma unroll
                 for (int i = 0; i < 32; ++i) {
-                    const float thi = __shfl_sync(0xffffffffu, th_c, i);
+                    const uint4 cw = s_cw[wslot][i];
                     const uint32_t abits = r[i] & 0x7fffffffu;          // |c| (float bits, monotone)
-                    const bool act = (__shfl_sync(0xffffffffu, wa_c, i) >> lane) & 1u;
-                    const bool nz = (__shfl_sync(0xffffffffu, wn_c, i) >> lane) & 1u;
+                    const bool act = (cw.x & lbit) != 0u;
+                    const bool nz = (cw.y & lbit) != 0u;
                     const uint32_t mv = __reduce_max_sync(0xffffffffu, act ? abits : 0u);
                     mymax = (lane == i) ? mv : mymax;
-                    const bool hot = act && (__uint_as_float(abits) > thi || nz);
-                    hotbits |= (hot ? 1u : 0u) << i;
+                    const bool hot = act && (__uint_as_float(abits) > __uint_as_float(cw.z) || nz);
+                    hotbits |= hot ? (1u << i) : 0u;
                 }
                 if (mymax) atomicMax(&g.cmax[nb * BN + cbase + k * 32 + lane], mymax);   // reduction, no return
-                // pass 2 (rare): append the hot entries of this lane's atom
-                if (__any_sync(0xffffffffu, hotbits != 0u)) {
-#pragma unroll
-                    for (int i = 0; i < 32; ++i) {
-                        if ((hotbits >> i) & 1u) {
-                            const int j = nb * BN + cbase + k * 32 + i;
-                            const int e = atomicAdd(&g.hot_cnt[j], 1);
-                            if (e < g.hcap) {
-                                g.hot_idx[(size_t)j * g.hcap + e] = m;
-                                g.hot_val[(size_t)j * g.hcap + e] = __uint_as_float(r[i]);
-                            }
+                // pass 2 (rare): only the columns holding a hot entry, column index warp-uniform
+                uint32_t colbits = __reduce_or_sync(0xffffffffu, hotbits);
+                while (colbits) {
+                    const int i = __ffs(colbits) - 1;
+                    colbits &= colbits - 1u;
+                    float v;
+                    switch (i) {
+#define DSCR_RCASE(n) case n: v = __uint_as_float(r[n]); break;
+                        DSCR_RCASE(0) DSCR_RCASE(1) DSCR_RCASE(2) DSCR_RCASE(3) DSCR_RCASE(4) DSCR_RCASE(5)
+                        DSCR_RCASE(6) DSCR_RCASE(7) DSCR_RCASE(8) DSCR_RCASE(9) DSCR_RCASE(10) DSCR_RCASE(11)
+                        DSCR_RCASE(12) DSCR_RCASE(13) DSCR_RCASE(14) DSCR_RCASE(15) DSCR_RCASE(16) DSCR_RCASE(17)
+                        DSCR_RCASE(18) DSCR_RCASE(19) DSCR_RCASE(20) DSCR_RCASE(21) DSCR_RCASE(22) DSCR_RCASE(23)
+                        DSCR_RCASE(24) DSCR_RCASE(25) DSCR_RCASE(26) DSCR_RCASE(27) DSCR_RCASE(28) DSCR_RCASE(29)
+                        DSCR_RCASE(30) default: v = __uint_as_float(r[31]); break;
+#undef DSCR_RCASE
+                    }
+                    if ((hotbits >> i) & 1u) {
+                        const int j = nb * BN + cbase + k * 32 + i;
+                        const int e = atomicAdd(&g.hot_cnt[j], 1);
+                        if (e < g.hcap) {
+                            g.hot_idx[(size_t)j * g.hcap + e] = m;
+                            g.hot_val[(size_t)j * g.hcap + e] = v;
                         }
                     }
                 }

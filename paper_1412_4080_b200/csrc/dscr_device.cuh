@@ -164,6 +164,28 @@ __device__ __forceinline__ void block_sum_n(double (&v)[M], double* sh) {
     __syncthreads();
 }
 
+// Max of M values over the CTA (every thread gets the results).
+template <int M>
+__device__ __forceinline__ void block_max_n(double (&v)[M], double* sh) {
+    const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = warp_max(v[m]);
+    __syncthreads();
+    if (l == 0) {
+#pragma unroll
+        for (int m = 0; m < M; ++m) sh[m * NW + w] = v[m];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < M; ++m) {
+        double r = -INFINITY;
+#pragma unroll
+        for (int q = 0; q < NW; ++q) r = fmax(r, sh[m * NW + q]);
+        v[m] = r;
+    }
+    __syncthreads();
+}
+
 // block_sum_n for a CTA of TPB threads (TPB a multiple of 32); sh holds (TPB/32)*M doubles
 template <int M, int TPB>
 __device__ __forceinline__ void block_sum_nt(double (&v)[M], double* sh) {

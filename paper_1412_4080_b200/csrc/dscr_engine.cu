@@ -55,6 +55,8 @@ constexpr int MIN_COLS_PER_SPLIT = 16;
 // comm region (doubles): [0,8) MAX-reduced, [8,16) setup exchange, [16,32) SUM-reduced scalars,
 // [32, 32+2*ldd) SUM-reduced partial residual vectors D_S a, D_S b
 constexpr int CM_MAX = 0, CM_SETUP = 8, CM_SUM = 16, CM_VEC = 32;
+constexpr int OC_SLOT = 8, OC_MAX_WORLD = 64;   // one-collective rank slots after the SUM vector
+constexpr int NP2X = 8;  // K2 partials incl. the one-collective test extremes
 constexpr int TRIPS_PER_BODY = 4;
 constexpr int PERS_MAX_G = 2048;   // persistent engine: max CTAs (support offsets kept in smem)
 
@@ -121,6 +123,9 @@ struct Params {
     unsigned long long* kts;   // per-trip kernel timestamps [trips][8]
     int max_kts;
     int max_gsize;
+    int onecoll;       // one collective per trip (dscr_solver_set_collectives)
+    int oc_rank, oc_world;
+    int k2v;           // K2 variant: 0 classic, 1 support before the test (K2S), 2 test + compaction (K2C)
     int k1_tile;       // K1 tiled path: row segments per column (0 = per-warp column path)
     int max_iters;
     int G, cap, TR, R, P, G3b;
@@ -854,20 +859,85 @@ __global__ void __launch_bounds__(NT) k3s_pack(Params P) {
         o[0] = sc->pen; o[1] = sc->nnz; o[2] = sc->kept_atoms; o[3] = sc->ss_red;
         o[4] = sc->dropped_nz; o[5] = sc->maj_cs; o[6] = sc->maj_ss; o[7] = 0.0;
     }
+    if (P.onecoll && blockIdx.x == 0) {
+        // rank slots: zeros except this rank's (the SUM gathers them); this rank's MAX
+        // quantities from K1, its test extremes and active-unit count from K2S
+        double* slots = P.comm + CM_VEC + 2 * P.ldd;
+        const bool fresh = sc->mode != MODE_FIXUP;
+        for (int i = threadIdx.x; i < OC_SLOT * OC_MAX_WORLD; i += NT) {
+            const int r = i / OC_SLOT, k = i % OC_SLOT;
+            if (r != P.oc_rank) { slots[i] = 0.0; continue; }
+            if (k < 3) slots[i] = fresh ? P.comm[CM_MAX + k] : 0.0;
+            else if (k >= 6 || !fresh) slots[i] = 0.0;
+        }
+    }
+}
+
+// one-collective trips: MAX quantities and test extremes from the gathered rank slots, the
+// radius (as k1r_radius), then whether any rank screens a unit carrying a nonzero coefficient
+// (FIXUP) and whether every active unit is screened (the all-screened stop)
+__global__ void __launch_bounds__(NT) k1r_radius_oc(Params P) {
+    __shared__ double s_sh[64];
+    __shared__ double s_v[4];
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    const int mode = sc->mode;
+    if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
+    if (threadIdx.x == 0) {
+        const double* slots = P.comm + CM_VEC + 2 * P.ldd;
+        double m = -INFINITY, nf = 0.0, any = 0.0, tmax = -INFINITY, vmin = INFINITY, units = 0.0;
+        for (int r = 0; r < P.oc_world; ++r) {
+            const double* q = slots + OC_SLOT * r;
+            m = fmax(m, q[0]); nf = fmax(nf, q[1]); any = fmax(any, q[2]);
+            tmax = fmax(tmax, q[3]); vmin = fmin(vmin, q[4]); units += q[5];
+        }
+        if (!P.n_groups && m < 0.0) m = 0.0;   // every rank empty
+        s_v[0] = m; s_v[1] = nf; s_v[2] = any;
+        sc->oc_spare = tmax;
+        sc->oc_empty = (units == 0.0) ? 1.0 : 0.0;
+        s_v[3] = vmin;
+    }
+    __syncthreads();
+    const double m = s_v[0];
+    double bound;
+    if (P.n_groups) bound = (s_v[2] > 0.0) ? -m : INFINITY;
+    else bound = (m == 0.0) ? INFINITY : 1.0 / m;
+    if (threadIdx.x == 0) {
+        sc->corr_inf = P.n_groups ? -m : m;
+        sc->nonfinite = s_v[1] > 0.0;
+    }
+    radius_epilogue(P, bound, P.theta[sc->parity], sc->theta_sq, sc->theta_y, s_sh);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const double r = sc->radius;
+        const bool dyn = P.strategy == DSCR_DYNAMIC;
+        sc->dropped_nz = dyn && (sc->oc_spare - r > SCREEN_MARGIN);
+        if (dyn && s_v[3] - r > SCREEN_MARGIN) sc->oc_empty = 1.0;
+    }
 }
 
 // ---------------------------------------------------------------------------
 // K2: screening test + order-preserving compaction + support list
 // ---------------------------------------------------------------------------
 
+// test value of a unit for the sphere tests: screened iff value - r > SCREEN_MARGIN
+// (SAFE/DST3: screening.py:359; groups: screening.py:404).  Rounding of value - r is
+// monotone in value, so max / min over units decide "any" / "all" screened exactly.
+__device__ __forceinline__ double unit_value(const Params& P, int unit) {
+    const int test = P.test;
+    if (test == DSCR_SAFE || test == DSCR_DST3) {
+        if (P.norm_aware)   // max over the sphere of |a.theta| = |a.c| + r ||a||  (non-unit atoms)
+            return (1.0 - fabs(P.cc[unit])) / P.anorm[unit];
+        return 1.0 - fabs(P.cc[unit]);
+    }
+    return (P.gw[unit] - P.cnorm[unit]) / P.gsn[unit];
+}
+
 __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* sc, int unit) {
     const int test = P.test;
     const double r = sc->radius;
-    if (test == DSCR_SAFE || test == DSCR_DST3) {
-        if (P.norm_aware)   // max over the sphere of |a.theta| = |a.c| + r ||a||  (non-unit atoms)
-            return (1.0 - fabs(P.cc[unit])) / P.anorm[unit] - r > SCREEN_MARGIN;
-        return (1.0 - fabs(P.cc[unit])) - r > SCREEN_MARGIN;   // screening.py:359
-    }
+    if (test == DSCR_SAFE || test == DSCR_DST3 || test == DSCR_GSAFE || test == DSCR_GST3)
+        return unit_value(P, unit) - r > SCREEN_MARGIN;
     if (test == DSCR_DOME) {                                    // screening.py:374-388
         if (r >= 1.0) return false;
         const double lam = P.lam;
@@ -879,13 +949,14 @@ __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* s
         const double mg = lam * SCREEN_MARGIN;
         return (u - lower > mg) && (upper - u > mg);
     }
-    if (test == DSCR_GSAFE || test == DSCR_GST3) {              // screening.py:404
-        return (P.gw[unit] - P.cnorm[unit]) / P.gsn[unit] - r > SCREEN_MARGIN;
-    }
     return false;
 }
 
-// K2 per-CTA work: test, compaction into slot b, vectors, support list, partials
+// K2 per-CTA work: test, compaction into slot b, vectors, support list, partials.
+// Variants (P.k2v): 0 classic; 1 = K2S (one collective): no test, support list and vectors
+// over every active unit (the reduced list in a FIXUP trip), plus the largest test value over
+// units carrying a nonzero coefficient and the smallest over all units; 2 = K2C: test and
+// compaction only (after the collective), kept atoms counted.
 template <bool GROUP>
 __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     __shared__ int s_scan[2 * NW + 1];
@@ -893,14 +964,20 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     __shared__ int s_off[K3_WIN];
     __shared__ int s_s0;
     dscr_scalars* sc = P.sc;
+    const int var = P.k2v;
     const bool static_mode = (sc->mode == MODE_STATIC);
+    const bool fix_pre = (var == 1 && sc->mode == MODE_FIXUP);   // K2S of a FIXUP trip: reduced list
     const int p = sc->parity, xi = sc->xi;
-    const int nu = sc->n_units;
+    const int lp = fix_pre ? (p ^ 1) : p;                         // list read
+    const int nu = fix_pre ? sc->n_units_new : sc->n_units;
     const int lo = (int)(((long long)nu * b) / G), hi = (int)(((long long)nu * (b + 1)) / G);
-    const int* act = P.act[p];
-    const int* off = P.act_off[p];
+    const int* act = P.act[lp];
+    const int* off = P.act_off[lp];
     int* actn = P.act[p ^ 1] + (size_t)b * P.cap;
-    const bool test_on = static_mode ? true : (P.strategy == DSCR_DYNAMIC);
+    const bool test_on = (var == 1) ? false : (static_mode ? true : (P.strategy == DSCR_DYNAMIC));
+    const bool do_list = (var != 1);                 // compaction into the next list
+    const bool do_vec = !static_mode && var != 2;    // vectors, support list, sums
+    const bool want_ext = (var == 1) && P.strategy == DSCR_DYNAMIC && P.test != DSCR_DOME && !fix_pre;
     const int algo = P.algo;
     const double* xc = P.x[xi];
     const double* xn = P.x[(xi + 1) % 3];
@@ -913,6 +990,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
 
     int n_keep = 0, n_sup = 0;
     double pen = 0.0, nnz = 0.0, kept_atoms = 0.0, ssr = 0.0, dropped = 0.0;
+    double tmax = -INFINITY, vmin = INFINITY;
     int wend = INT_MIN;
     const bool ident = (nu == P.n_units);   // nothing screened yet: identity list
     for (int base = lo; base < hi; base += NT) {
@@ -929,18 +1007,22 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
             }
         }
         const bool masked = valid && test_on && unit_test(P, sc, unit);
-        if (valid && !static_mode) P.mask[f] = masked ? 1 : 0;
+        if (valid && !static_mode && do_list) P.mask[f] = masked ? 1 : 0;
         const bool keep = valid && !masked;
-        int tot;
-        const int pos = block_exscan(keep ? 1 : 0, s_scan, &tot);
-        if (keep) actn[n_keep + pos] = unit;
-        n_keep += tot;
-        if (static_mode) continue;
+        if (do_list) {
+            int tot;
+            const int pos = block_exscan(keep ? 1 : 0, s_scan, &tot);
+            if (keep) actn[n_keep + pos] = unit;
+            n_keep += tot;
+        }
+        if (var == 2 && keep) kept_atoms += (double)(unit_atom_hi(P, unit) - unit_atom_lo(P, unit));
+        if (!do_vec) continue;
 
         // per-atom vectors and support entries of this unit
         int my_sup = 0;
         if (valid) {
             const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+            bool carries = false;
             for (int j = j0; j < j1; ++j) {
                 const double cand = xn[j];
                 if (keep) {
@@ -948,7 +1030,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                     if (algo == DSCR_FISTA) { bv = cand + beta * (cand - xc[j]); un[j] = bv; }
                     else if (algo == DSCR_CP) { bv = cand + phi * (cand - xc[j]); un[j] = bv; }
                     else if (algo == DSCR_SPARSA) { bv = cand - xc[j]; ssr += bv * bv; }
-                    if (cand != 0.0 || bv != 0.0) ++my_sup;
+                    if (cand != 0.0 || bv != 0.0) { ++my_sup; carries = true; }
                     if (!GROUP) pen += fabs(cand);
                     nnz += (cand != 0.0) ? 1.0 : 0.0;
                     kept_atoms += 1.0;
@@ -960,7 +1042,13 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                 const double nx = sqrt(np_segment_sum([&](int i) { double t = xn[i]; return t * t; }, j0, j1 - j0));
                 pen += P.gw[unit] * nx;
             }
+            if (want_ext) {
+                const double v = unit_value(P, unit);
+                vmin = fmin(vmin, v);
+                if (carries) tmax = fmax(tmax, v);
+            }
         }
+        int tot;
         const int spos = block_exscan(my_sup, s_scan, &tot);
         if (my_sup) {
             int w = n_sup + spos;
@@ -981,15 +1069,18 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     }
     // per-CTA outputs
     if (threadIdx.x == 0) {
-        P.act_cnt[p ^ 1][b] = n_keep;
-        if (!static_mode) P.sup_cnt[b] = n_sup;
+        if (do_list) P.act_cnt[p ^ 1][b] = n_keep;
+        if (do_vec) P.sup_cnt[b] = n_sup;
     }
     if (!static_mode) {
         double v5[5] = {pen, nnz, kept_atoms, ssr, dropped};
         block_sum_n<5>(v5, s_sh);
+        double ext[2] = {tmax, -vmin};
+        if (want_ext) block_max_n<2>(ext, s_sh);
         if (threadIdx.x == 0) {
-            double* o = P.p2 + (size_t)b * NP2;
+            double* o = P.p2 + (size_t)b * NP2X;
             o[0] = v5[0]; o[1] = v5[1]; o[2] = v5[2]; o[3] = v5[3]; o[4] = v5[4];
+            o[5] = ext[0]; o[6] = -ext[1];
         }
     }
 }
@@ -1000,7 +1091,10 @@ __device__ void k2_final(const Params& P, int G) {
     __shared__ int s_scan[2 * NW + 1];
     __shared__ double s_sh[64];
     dscr_scalars* sc = P.sc;
+    const int var = P.k2v;
     const bool static_mode = (sc->mode == MODE_STATIC);
+    const bool do_list = (var != 1);
+    const bool do_vec = !static_mode && var != 2;
     const int p = sc->parity;
 
     // ---- last CTA: scans of the slot counts, fixed-order partial reduction
@@ -1010,12 +1104,14 @@ __device__ void k2_final(const Params& P, int G) {
         const int* cn = P.act_cnt[p ^ 1];
         for (int base = 0; base < P.G; base += NT) {
             const int i = base + threadIdx.x;
-            const int v = (i < P.G) ? cn[i] : 0;
             int tot;
-            const int e = block_exscan(v, s_scan, &tot);
-            if (i < P.G && P.writer) offn[i] = carry + e;
-            carry += tot;
-            if (!static_mode) {
+            if (do_list) {
+                const int v = (i < P.G) ? cn[i] : 0;
+                const int e = block_exscan(v, s_scan, &tot);
+                if (i < P.G && P.writer) offn[i] = carry + e;
+                carry += tot;
+            }
+            if (do_vec) {
                 const int vs = (i < P.G) ? P.sup_cnt[i] : 0;
                 const int es = block_exscan(vs, s_scan, &tot);
                 if (i < P.G) P.sup_off[i] = carry_s + es;
@@ -1023,9 +1119,11 @@ __device__ void k2_final(const Params& P, int G) {
             }
         }
         if (threadIdx.x == 0) {
-            if (P.writer) offn[P.G] = carry;
-            sc->n_units_new = carry;
-            if (!static_mode) {
+            if (do_list) {
+                if (P.writer) offn[P.G] = carry;
+                sc->n_units_new = carry;
+            }
+            if (do_vec) {
                 P.sup_off[P.G] = carry_s;
                 sc->n_support = carry_s;
                 int pe = (carry_s + MIN_COLS_PER_SPLIT - 1) / MIN_COLS_PER_SPLIT;
@@ -1043,20 +1141,33 @@ __device__ void k2_final(const Params& P, int G) {
         }
         return;
     }
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, tmax = -INFINITY, vmin = INFINITY;
     for (int i = threadIdx.x; i < G; i += NT) {
-        const double* o = P.p2 + (size_t)i * NP2;
+        const double* o = P.p2 + (size_t)i * NP2X;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3]; a4 += o[4];
+        tmax = fmax(tmax, o[5]); vmin = fmin(vmin, o[6]);
     }
     double r5[5] = {a0, a1, a2, a3, a4};
     block_sum_n<5>(r5, s_sh);
     a0 = r5[0]; a1 = r5[1]; a2 = r5[2]; a3 = r5[3]; a4 = r5[4];
+    double ext[2] = {tmax, -vmin};
+    if (var == 1) block_max_n<2>(ext, s_sh);
     if (threadIdx.x == 0) {
-        sc->pen = a0;
-        sc->nnz = (int)a1;
-        sc->kept_atoms = (int)a2;
-        sc->ss_red = a3;
-        sc->dropped_nz = (a4 > 0.0);
+        if (var == 2) {                    // K2C: local kept atoms after the test
+            sc->kept_atoms = (int)a2;
+        } else {
+            sc->pen = a0;
+            sc->nnz = (int)a1;
+            sc->kept_atoms = (int)a2;
+            sc->ss_red = a3;
+            sc->dropped_nz = (a4 > 0.0);
+        }
+        if (var == 1 && sc->mode != MODE_FIXUP) {   // this rank's slot: test extremes, active units
+            double* slot = P.comm + CM_VEC + 2 * P.ldd + OC_SLOT * P.oc_rank;
+            slot[3] = ext[0];
+            slot[4] = -ext[1];
+            slot[5] = (double)sc->n_units;
+        }
         stamp(P, 3);
     }
 }
@@ -1069,7 +1180,7 @@ __global__ void __launch_bounds__(NT) k2_screen(Params P) {
     dscr_scalars* sc = P.sc;
     if (sc->stop) return;
     const int mode = sc->mode;
-    if (mode == MODE_FIXUP) return;
+    if (mode == MODE_FIXUP && P.k2v != 1) return;
     const bool static_mode = (mode == MODE_STATIC);
     if (!static_mode && sc->t >= sc->run_limit) return;
     if (!static_mode && blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 2);
@@ -1106,7 +1217,7 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     __shared__ int s_off[K3_WIN];
     __shared__ int s_s0;
     dscr_scalars* sc = P.sc;
-    const bool fix = (sc->mode == MODE_FIXUP);
+    const bool fix = (sc->mode == MODE_FIXUP) && !P.onecoll;   // one collective: K2S rebuilt the list
     const int pe = sc->p_eff;
     if (split >= pe) return;
     const int nS = sc->n_support;
@@ -1238,7 +1349,7 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
                 set_cond(P, 1);
                 return;
             }
-            if (sc->dropped_nz) {
+            if (sc->dropped_nz && !P.onecoll) {
                 // resid must be recomputed on the reduced iterate (solvers.py:354-355)
                 sc->spare = s_tn2;
                 sc->ds_sq = s_tny;
@@ -1248,7 +1359,15 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
                 return;
             }
         }
-    } else if (algo == DSCR_FISTA) {
+        if (P.onecoll && sc->dropped_nz) {
+            // one collective: the residuals were taken on the unreduced iterate; a screened unit
+            // carried a nonzero x or u / s, so both are recomputed on the reduced iterate
+            sc->mode = MODE_FIXUP;
+            sc->trips += 1;
+            set_cond(P, 1);
+            return;
+        }
+    } else if (algo == DSCR_FISTA && !P.onecoll) {
         s_tn2 = sc->spare;   // theta_{t+1} = D u - y from the normal trip
         s_tny = sc->ds_sq;
     }
@@ -1288,7 +1407,7 @@ __device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, 
         stop = DSCR_STOP_RELTOL;
     else if (P.gap_tol > 0.0 && gap <= P.gap_tol)
         stop = DSCR_STOP_GAP;
-    else if (sc->kept_atoms == 0)
+    else if (P.onecoll ? (sc->oc_empty > 0.0) : (sc->kept_atoms == 0))
         stop = DSCR_STOP_EMPTY;
     else if (t >= P.max_iters)
         stop = DSCR_STOP_MAXITER;
@@ -1312,7 +1431,7 @@ __device__ __forceinline__ void k3b_body(const Params& P, int rb) {
     __shared__ double s_pa[K3B_GROUPS][K3B_ROWS], s_pb[K3B_GROUPS][K3B_ROWS];
     dscr_scalars* sc = P.sc;
     const int mode = sc->mode;
-    const bool fix = (mode == MODE_FIXUP);
+    const bool fix = (mode == MODE_FIXUP) && !P.onecoll;
     const int algo = P.algo;
     const int p = sc->parity;
     const int pe = sc->p_eff;
@@ -1392,8 +1511,11 @@ __device__ void k3b_final(const Params& P, int G3) {
         stamp(P, 7);
         if (P.split) {      // global sums of the per-rank K1/K2 scalars
             const double* o = P.comm + CM_SUM;
-            sc->pen = o[0]; sc->nnz = (int)llround(o[1]); sc->kept_atoms = (int)llround(o[2]);
-            sc->ss_red = o[3]; sc->dropped_nz = o[4] > 0.0; sc->maj_cs = o[5]; sc->maj_ss = o[6];
+            sc->pen = o[0]; sc->nnz = (int)llround(o[1]);
+            sc->ss_red = o[3]; sc->maj_cs = o[5]; sc->maj_ss = o[6];
+            if (!P.onecoll) { sc->kept_atoms = (int)llround(o[2]); sc->dropped_nz = o[4] > 0.0; }
+            // one collective: kept_atoms stays this rank's count (trace; summed by the host),
+            // dropped_nz comes from k1r_radius_oc
         }
         iteration_epilogue(P, a0, a1, a2, a3);
     }
@@ -1993,14 +2115,14 @@ static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg,
     o.sidx = L.add(ss * 4); o.sa = L.add(ss * 8); o.sb = L.add(ss * 8);
     o.supcnt = L.add(G * 4); o.supoff = L.add((G + 1) * 4);
     o.p1 = L.add(std::max<size_t>(G * NP1, 2 * (size_t)4096) * 8);
-    o.p2 = L.add(G * NP2 * 8);
+    o.p2 = L.add(G * NP2X * 8);
     o.p3v = L.add((size_t)g.P * 2 * ldd * 8);
     o.p3s = L.add((size_t)g.G3b * NP3 * 8);
     o.tickets = L.add(64);
     o.trace = L.add((size_t)std::max(cfg->max_iters, 1) * DSCR_TRACE_FIELDS * 8);
     o.kts = L.add((size_t)kts_slots(cfg) * 8 * 8);
     o.anorm = L.add(K * 8);
-    o.comm = L.add((CM_VEC + 2 * ldd) * 8);
+    o.comm = L.add((CM_VEC + 2 * ldd + OC_SLOT * OC_MAX_WORLD) * 8);
     *total = L.total + 256;
     return o;
 }
@@ -2535,8 +2657,16 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
             k1r_radius<<<1, NT, 0, s>>>(P);
             break;
         case DSCR_PH_K2:
+        case DSCR_PH_K2S:
+        case DSCR_PH_K2C:
+            if (phase != DSCR_PH_K2 && !P.onecoll) return set_inval("K2S/K2C need one-collective mode");
+            P.k2v = (phase == DSCR_PH_K2S) ? 1 : (phase == DSCR_PH_K2C ? 2 : 0);
             if (group) k2_screen<true><<<g.G, NT, 0, s>>>(P);
             else k2_screen<false><<<g.G, NT, 0, s>>>(P);
+            break;
+        case DSCR_PH_K1R1:
+            if (!P.onecoll) return set_inval("K1R1 needs one-collective mode");
+            k1r_radius_oc<<<1, NT, 0, s>>>(P);
             break;
         case DSCR_PH_K3A: {
             dim3 g3(g.R, g.P);
@@ -2557,6 +2687,17 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
             return set_inval("unknown phase");
     }
     CK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+int dscr_solver_set_collectives(dscr_solver* h, int rank, int world, int one_collective) {
+    if (!h) return set_inval("null handle");
+    if (world < 1 || world > OC_MAX_WORLD || rank < 0 || rank >= world) return set_inval("rank / world out of range");
+    if (one_collective && h->P.test == DSCR_DOME && h->P.strategy == DSCR_DYNAMIC)
+        return set_inval("the dome test needs the two-collective trips");
+    h->P.onecoll = one_collective ? 1 : 0;
+    h->P.oc_rank = rank;
+    h->P.oc_world = world;
     return DSCR_OK;
 }
 
@@ -2581,7 +2722,7 @@ int dscr_solver_get_buffers(dscr_solver* h, dscr_solver_buffers* b) {
     b->act_off[0] = P.act_off[0]; b->act_off[1] = P.act_off[1];
     b->mask = P.mask; b->trace = P.trace;
     b->kts = (uint64_t*)P.kts; b->max_kts = P.max_kts;
-    b->comm = P.comm; b->comm_len = CM_VEC + 2 * P.ldd;
+    b->comm = P.comm; b->comm_len = CM_VEC + 2 * P.ldd + OC_SLOT * OC_MAX_WORLD;
     b->vec = P.vec;
     b->G = P.G; b->cap = P.cap;
     return DSCR_OK;

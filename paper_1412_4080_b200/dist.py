@@ -49,14 +49,20 @@ def _allreduce(tensor, op, pg):
     dist.all_reduce(tensor, op=op, group=pg)
 
 
-def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8):
-    """Run a sharded solve: setup exchange, then trips with the two collectives."""
+def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collectives=2):
+    """Run a sharded solve: setup exchange, then trips with two collectives (MAX after K1, SUM
+    after K3A) or, with ``collectives=1``, one SUM per trip (rank-slot gather of the MAX
+    quantities and test extremes, residuals on the unreduced iterate, FIXUP trip when a rank
+    screens a unit carrying a nonzero coefficient; SURVEY §7 hard part 2).  The dome test
+    always uses two."""
     import torch
     import torch.distributed as dist
     MAX, SUM = dist.ReduceOp.MAX, dist.ReduceOp.SUM
     comm = backend.comm
     world = dist.get_world_size(pg) if pg is not None else 1
     rank = dist.get_rank(pg) if pg is not None else 0
+    one = collectives == 1 and not (cfg.strategy == "dynamic" and cfg.test == "dome")
+    backend.set_collectives(rank, world, one)
 
     backend.phase(nat.PH_SETUP_LOCAL)
     cand = comm[nat.CM_SETUP: nat.CM_SETUP + 3].clone()
@@ -89,7 +95,9 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8):
         _allreduce(comm[nat.CM_MAX: nat.CM_MAX + 8], MAX, pg)
         backend.phase(nat.PH_STATIC_FINISH)
     max_sec = comm[nat.CM_MAX: nat.CM_MAX + 8]
-    sum_sec = comm[nat.CM_SUM:]
+    vec_end = nat.CM_VEC + 2 * backend.ldd
+    # two collectives: scalars + vector; one collective: also the rank slots (gather by SUM)
+    sum_sec = comm[nat.CM_SUM: vec_end + (nat.OC_SLOT * world if one else 0)]
     trips = 0
     while True:
         sc = backend.scalars()
@@ -97,14 +105,23 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8):
             break
         for _ in range(chunk):
             backend.phase(nat.PH_K1)
-            _allreduce(max_sec, MAX, pg)
-            backend.phase(nat.PH_K1R)
-            backend.phase(nat.PH_K2)
-            backend.phase(nat.PH_K3A)
-            backend.phase(nat.PH_K3S)
-            _allreduce(sum_sec, SUM, pg)
+            if one:
+                backend.phase(nat.PH_K2S)
+                backend.phase(nat.PH_K3A)
+                backend.phase(nat.PH_K3S)
+                _allreduce(sum_sec, SUM, pg)
+                backend.phase(nat.PH_K1R1)
+                backend.phase(nat.PH_K2C)
+            else:
+                _allreduce(max_sec, MAX, pg)
+                backend.phase(nat.PH_K1R)
+                backend.phase(nat.PH_K2)
+                backend.phase(nat.PH_K3A)
+                backend.phase(nat.PH_K3S)
+                _allreduce(sum_sec, SUM, pg)
             backend.phase(nat.PH_K3B)
             trips += 1
+    backend.one_collective = one
     return backend.scalars()
 
 
@@ -123,7 +140,12 @@ class GpuShard:
         self.comm = self.eng.view(b.comm, b.comm_len, torch.float64)
         self.vec = self.eng.view(b.vec, problem_local.dictionary.ldd, torch.float64)
         self.unit_offset = group_offset if problem_local.kind == GROUP else col_offset
+        self.ldd = problem_local.dictionary.ldd
         self.phase_calls = 0          # dscr_solver_phase launches (each enqueues >= 1 kernel)
+        self.one_collective = False
+
+    def set_collectives(self, rank, world, one):
+        nat.check(self.eng.L.dscr_solver_set_collectives(self.eng.h, int(rank), int(world), 1 if one else 0))
 
     def phase(self, ph):
         nat.check(self.eng.L.dscr_solver_phase(self.eng.h, int(ph), self.eng.sptr))
@@ -177,7 +199,21 @@ def sharded_operator_norm(dictionary_local, pg=None, tol=1e-11, max_iters=20000,
     return float(np.sqrt(max(val, 0.0)))
 
 
-def run_sharded(problem, cfg, pg=None, device=None, chunk=8):
+def global_kept(rows, pg):
+    """One-collective trips leave each rank's kept-atom count in its trace rows: sum them."""
+    import torch
+    import torch.distributed as dist
+    kept = torch.tensor(np.ascontiguousarray(rows[:, nat.TR_KEPT]), dtype=torch.float64)
+    if pg is not None:
+        if dist.get_backend(pg) == "nccl":
+            kept = kept.cuda()
+        dist.all_reduce(kept, op=dist.ReduceOp.SUM, group=pg)
+    rows = rows.copy()
+    rows[:, nat.TR_KEPT] = kept.cpu().numpy()
+    return rows
+
+
+def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2):
     """Solve `problem` with its columns sharded over the ranks of `pg` (None: single rank,
     split phases without collectives).  Every rank gets the full SolveResult."""
     import torch.distributed as dist
@@ -207,11 +243,13 @@ def run_sharded(problem, cfg, pg=None, device=None, chunk=8):
         shard = GpuShard(local, cfg, c0, k, 0, 0, device)
         gw = None
     try:
-        sc = orchestrate(shard, cfg, problem.lam, pg, gw, chunk)
+        sc = orchestrate(shard, cfg, problem.lam, pg, gw, chunk, collectives)
         if sc.status != 0:
             from .solver import _raise_status
             _raise_status(None, sc)
         kept_l, x_l, rows, sc = shard.local_solution()
+        if shard.one_collective:
+            rows = global_kept(rows, pg)
     finally:
         shard.close()
     if pg is not None:

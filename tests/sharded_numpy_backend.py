@@ -2,7 +2,9 @@
 
 Mirrors, phase by phase, what the CUDA engine does on one rank's column block
 (K1 correlations/update, K1R radius from the MAX-reduced bound, K2 test and
-reduction, K3A/K3S partial residuals, K3B finalize + epilogue), so the
+reduction, K3A/K3S partial residuals, K3B finalize + epilogue; with one collective per trip K2S support
+before the test, rank-slot gather, K1R1 radius / dropped / all-screened flags,
+K2C test and compaction), so the
 multi-rank orchestration (collective sequence, lambda_* argmax, owner
 broadcast, stop/redo/fixup control) can run under gloo on CPU and be compared
 with the unsharded oracle.  Lasso problems; ISTA, FISTA, SpaRSA, CP; SAFE/DST3.
@@ -30,7 +32,10 @@ class NumpyShard:
         self.cfg = cfg
         self.unit_offset = col_offset
         self.n, self.k = self.D.shape
-        self.comm = torch.zeros(nat.CM_VEC + 2 * self.n, dtype=torch.float64)
+        self.ldd = self.n
+        self.comm = torch.zeros(nat.CM_VEC + 2 * self.n + nat.OC_SLOT * nat.OC_MAX_WORLD, dtype=torch.float64)
+        self.one = False
+        self.rank, self.world = 0, 1
         self.vec = torch.zeros(self.n, dtype=torch.float64)
         self.op_norm = op_norm
         self.sc = _Scalars()
@@ -41,6 +46,9 @@ class NumpyShard:
 
     def scalars(self):
         return self.sc
+
+    def set_collectives(self, rank, world, one):
+        self.rank, self.world, self.one = rank, world, bool(one)
 
     # ---------------------------------------------------------------- phases
     def phase(self, ph):
@@ -138,8 +146,11 @@ class NumpyShard:
         sc = self.sc
         if sc.stop or sc.mode == 2:
             return
-        m = self._c()[0]
-        sc.nonfinite = self._c()[1] > 0
+        self._radius(self._c()[0], self._c()[1] > 0)
+
+    def _radius(self, m, nonfinite):
+        sc = self.sc
+        sc.nonfinite = nonfinite
         bound = np.inf if m == 0.0 else 1.0 / m
         sq, ty = sc.theta_sq, sc.theta_y
         mu = float(np.clip(ty / (self.lam * sq), -bound, bound)) if sq != 0.0 else 0.0
@@ -184,6 +195,14 @@ class NumpyShard:
         if sc.stop:
             return
         fix = sc.mode == 2
+        if self.one:      # support built by K2S (all active units; the reduced list in a FIXUP trip)
+            U = self.sup_units
+            a = np.zeros(self.k)
+            a[U] = self.xn[U]
+            b = self.un if cfg.algorithm in ("fista", "cp") else self.s_vec
+            self.Sa = self.D @ a
+            self.Sb = self.D @ b
+            return
         keep = self.new_active
         a = np.zeros(self.k)
         b = np.zeros(self.k)
@@ -202,6 +221,14 @@ class NumpyShard:
         cm = self._c()
         cm[nat.CM_VEC:nat.CM_VEC + self.n] = self.Sa
         cm[nat.CM_VEC + self.n:nat.CM_VEC + 2 * self.n] = self.Sb
+        if self.one:
+            cm[nat.CM_SUM:nat.CM_SUM + 8] = [self.pen, self.nnz, 0.0, self.ss, 0.0, self.maj[0], self.maj[1], 0.0]
+            base = nat.CM_VEC + 2 * self.n
+            cm[base:base + nat.OC_SLOT * nat.OC_MAX_WORLD] = 0.0
+            if self.sc.mode != 2:
+                o = base + nat.OC_SLOT * self.rank
+                cm[o:o + 6] = [cm[0], cm[1], cm[2], self.tmax, self.vmin, self.units]
+            return
         cm[nat.CM_SUM:nat.CM_SUM + 8] = [self.pen, self.nnz, self.kept, self.ss, float(self.dropped),
                                          self.maj[0], self.maj[1], 0.0]
 
@@ -213,7 +240,9 @@ class NumpyShard:
         Sa = cm[nat.CM_VEC:nat.CM_VEC + self.n]
         Sb = cm[nat.CM_VEC + self.n:nat.CM_VEC + 2 * self.n]
         pen, nnz, kept, ss, dropped, mcs, mss = cm[nat.CM_SUM:nat.CM_SUM + 7]
-        fix = sc.mode == 2
+        if self.one:
+            kept, dropped = self.kept_local, float(self.dropped_oc)
+        fix = sc.mode == 2 and not self.one
         qa = Sa - self.y
         algo = cfg.algorithm
         if algo == "fista":
@@ -222,7 +251,7 @@ class NumpyShard:
             tn = None if fix else (self.theta + sc.sigma_new * (Sb - self.y)) / (1.0 + sc.sigma_new)
         else:
             tn = qa
-        if not fix:
+        if sc.mode != 2:
             if sc.nonfinite:
                 sc.status, sc.stop = -2, 6
                 return
@@ -233,11 +262,14 @@ class NumpyShard:
                     sc.L *= cfg.backtrack_factor
                     sc.mode = 1
                     return
-                if dropped > 0:
+                if dropped > 0 and not self.one:
                     self.pending = tn
                     sc.mode = 2
                     return
-        elif algo == "fista":
+            if self.one and dropped > 0:
+                sc.mode = 2       # one collective: recompute both residuals on the reduced iterate
+                return
+        elif algo == "fista" and not self.one:
             tn = self.pending
         F = 0.5 * float(qa @ qa) + self.lam * pen
         gap = F - 0.5 * sc.yy + 0.5 * self.lam ** 2 * sc.rsafe_sq
@@ -255,7 +287,7 @@ class NumpyShard:
             stop = 1
         elif cfg.gap_tol is not None and gap <= cfg.gap_tol:
             stop = 2
-        elif round(kept) == 0:
+        elif (self.empty if self.one else round(kept) == 0):
             stop = 4
         elif sc.t >= cfg.max_iters:
             stop = 3
@@ -268,6 +300,59 @@ class NumpyShard:
         self.active = self.new_active
         sc.mode, sc.stop = 0, stop
         sc.gap = gap
+
+    def _ph16(self):  # K2S: vectors and support over every active unit (reduced list in FIXUP)
+        sc, cfg = self.sc, self.cfg
+        if sc.stop:
+            return
+        fix = sc.mode == 2
+        U = self.new_active if fix else self.active
+        cand = self.xn
+        self.un = np.zeros(self.k)
+        self.s_vec = np.zeros(self.k)
+        if cfg.algorithm == "fista":
+            self.un[U] = cand[U] + sc.beta * (cand[U] - self.x[U])
+        elif cfg.algorithm == "cp":
+            self.un[U] = cand[U] + sc.phi * (cand[U] - self.x[U])
+        elif cfg.algorithm == "sparsa":
+            self.s_vec[U] = cand[U] - self.x[U]
+        self.sup_units = U
+        self.pen = float(np.sum(np.abs(cand[U])))
+        self.nnz = int(np.count_nonzero(cand[U]))
+        self.ss = float(self.s_vec[U] @ self.s_vec[U])
+        if not fix:
+            self.tmax, self.vmin, self.units = -np.inf, np.inf, float(U.size)
+            if cfg.strategy == "dynamic" and U.size:
+                v = 1.0 - np.abs(self.cc[U])
+                b = self.un if cfg.algorithm in ("fista", "cp") else self.s_vec
+                carries = (cand[U] != 0.0) | (b[U] != 0.0)
+                self.vmin = float(np.min(v))
+                if np.any(carries):
+                    self.tmax = float(np.max(v[carries]))
+
+    def _ph17(self):  # K1R1: gathered rank slots -> radius, dropped-nonzero, all-screened
+        sc = self.sc
+        if sc.stop or sc.mode == 2:
+            return
+        base = nat.CM_VEC + 2 * self.n
+        sl = self._c()[base:base + nat.OC_SLOT * self.world].reshape(self.world, nat.OC_SLOT)
+        self._radius(float(np.max(sl[:, 0])), float(np.max(sl[:, 1])) > 0)
+        dyn = self.cfg.strategy == "dynamic"
+        r = sc.radius
+        self.dropped_oc = dyn and (float(np.max(sl[:, 3])) - r > 1e-12)
+        self.empty = float(np.sum(sl[:, 5])) == 0.0 or (dyn and float(np.min(sl[:, 4])) - r > 1e-12)
+
+    def _ph18(self):  # K2C: test and compaction
+        sc, cfg = self.sc, self.cfg
+        if sc.stop or sc.mode == 2:
+            return
+        A = self.active
+        masked = np.zeros(A.size, dtype=bool)
+        if cfg.strategy == "dynamic":
+            masked = (1.0 - np.abs(self.cc[A])) - sc.radius > 1e-12
+        self.mask = masked
+        self.new_active = A[~masked]
+        self.kept_local = int(self.new_active.size)
 
     @property
     def trace(self):

@@ -47,7 +47,7 @@ def _cfg(algo, test, L0mode, gap_tol, D):
                      gap_tol=gap_tol, op_norm=float(np.linalg.norm(D, 2)))
 
 
-def _worker(rank, world, port, out_path, case):
+def _worker(rank, world, port, out_path, case, collectives=2):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -58,7 +58,7 @@ def _worker(rank, world, port, out_path, case):
         cfg = _cfg(algo, test, L0mode, gap_tol, D)
         c0, c1 = pdist.shard_ranges(D.shape[1], world)[rank]
         shard = NumpyShard(D[:, c0:c1], y, lam, cfg, c0, op_norm=cfg.op_norm)
-        sc = pdist.orchestrate(shard, cfg, lam, pg=dist.group.WORLD, chunk=3)
+        sc = pdist.orchestrate(shard, cfg, lam, pg=dist.group.WORLD, chunk=3, collectives=collectives)
         if sc.trivial:
             local = (np.empty(0, np.int64), np.empty(0))
         else:
@@ -78,17 +78,21 @@ def _free_port():
         return s.getsockname()[1]
 
 
+@pytest.mark.parametrize("collectives", [2, 1], ids=["two-collectives", "one-collective"])
 @pytest.mark.parametrize("case", CASES, ids=[f"{c[0]}-{c[1]}-{c[2]}-{c[3]}" for c in CASES])
-def test_sharded_world2_matches_oracle(case):
+def test_sharded_world2_matches_oracle(case, collectives):
     with tempfile.TemporaryDirectory() as td:
         out = os.path.join(td, "res.pkl")
-        mp.spawn(_worker, args=(2, _free_port(), out, case), nprocs=2, join=True)
+        mp.spawn(_worker, args=(2, _free_port(), out, case, collectives), nprocs=2, join=True)
         with open(out, "rb") as fh:
             got = pickle.load(fh)
     algo, test, ratio, L0mode, gap_tol = case
     D, y, lam = _data(ratio)
     ref = so.solve(so.make_problem(D, y, lam), _cfg(algo, test, L0mode, gap_tol, D))
     traces = [g[1] for g in got]
+    if collectives == 1:   # kept counts are per rank in one-collective trips (summed by the host)
+        assert [t[:1] + t[2:] for t in traces[0]] == [t[:1] + t[2:] for t in traces[1]], "ranks disagree"
+        traces = [[(a[0], a[1] + b[1]) + a[2:] for a, b in zip(traces[0], traces[1])]] * 2
     assert traces[0] == traces[1], "ranks disagree on the trace"
     its = got[0][2]
     assert its == ref.iterations

@@ -26,8 +26,9 @@ def _problem(ratio):
     return ds.Problem(ds.Dictionary(D), y, ratio * wl.lambda_star(D, y)), float(np.linalg.norm(D, 2))
 
 
+@pytest.mark.parametrize("collectives", [2, 1], ids=["two-coll", "one-coll"])
 @pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c)) for c in CASES])
-def test_split_phases_match_fused(case):
+def test_split_phases_match_fused(case, collectives):
     algo, test, ratio = case
     strategy = "static" if test.startswith("static") else "dynamic"
     test = test.split("-")[-1]
@@ -35,10 +36,11 @@ def test_split_phases_match_fused(case):
     cfg = ds.SolverConfig(algorithm=algo, strategy=strategy, test=test, max_iters=3000, rel_tol=1e-300,
                           L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9, op_norm=nrm)
     a = ds.run(p, cfg)
-    b = pdist.run_sharded(p, cfg, pg=None)
+    b = pdist.run_sharded(p, cfg, pg=None, collectives=collectives)
     assert a.iterations == b.iterations
     assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
     np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+    assert b.trace.kept == a.trace.kept
     assert np.linalg.norm(a.x_star - b.x_star) <= 1e-10 * np.linalg.norm(a.x_star)
 
 
@@ -51,10 +53,12 @@ def test_group_split_phases_match_fused():
         cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test=test, max_iters=2000,
                               rel_tol=1e-300, L0=float(np.linalg.norm(w.D, 2) ** 2 * (1 + 1e-9)), gap_tol=1e-9)
         a = ds.run(p, cfg)
-        b = pdist.run_sharded(p, cfg, pg=None)
-        assert a.iterations == b.iterations
-        assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
-        np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+        for coll in (2, 1):
+            b = pdist.run_sharded(p, cfg, pg=None, collectives=coll)
+            assert a.iterations == b.iterations
+            assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
+            np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+            assert b.trace.kept == a.trace.kept
 
 
 def test_nccl_single_rank_group():

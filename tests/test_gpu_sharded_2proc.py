@@ -15,14 +15,17 @@ import pytest
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
 
-CASES = [("fista", "dst3", 0.5, "lasso"), ("ista-bt", "dst3", 0.7, "lasso"), ("fista", "static-dst3", 0.8, "lasso"),
-         ("fista", "gst3", 0.7, "group")]
+CASES = [("fista", "dst3", 0.5, "lasso", 2), ("ista-bt", "dst3", 0.7, "lasso", 2),
+         ("fista", "static-dst3", 0.8, "lasso", 2), ("fista", "gst3", 0.7, "group", 2),
+         # one collective per trip (rank-slot gather in the SUM, FIXUP on a screened nonzero)
+         ("fista", "dst3", 0.5, "lasso", 1), ("ista-bt", "dst3", 0.7, "lasso", 1), ("fista", "gst3", 0.7, "group", 1),
+         ("sparsa", "dst3", 0.6, "lasso", 1)]
 
 
 def _build(case):
     import paper_1412_4080_b200 as ds
     from paper_1412_4080_b200 import workloads as wl
-    algo, test, ratio, kind = case
+    algo, test, ratio, kind = case[:4]
     if kind == "group":
         w = wl.config3(ratio=ratio, n=300, k=1200)
         dic = ds.Dictionary(w.D)
@@ -51,9 +54,11 @@ def _worker(rank, world, port, case, q):
         torch.cuda.set_device(0)
         dist.init_process_group("gloo", rank=rank, world_size=world)
         p, cfg = _build(case)
-        res = pdist.run_sharded(p, cfg, pg=dist.group.WORLD, device=torch.device("cuda", 0))
+        res = pdist.run_sharded(p, cfg, pg=dist.group.WORLD, device=torch.device("cuda", 0),
+                                collectives=case[4])
         if rank == 0:
-            q.put(("ok", res.iterations, res.x_star, np.asarray(res.screen_state.eliminated), res.final_objective))
+            q.put(("ok", res.iterations, res.x_star, np.asarray(res.screen_state.eliminated), res.final_objective,
+                   list(res.trace.kept)))
         dist.destroy_process_group()
     except Exception as e:  # report instead of hanging the parent
         q.put(("error", rank, repr(e)))
@@ -65,7 +70,7 @@ def _free_port():
         return s.getsockname()[1]
 
 
-@pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c[:3])) for c in CASES])
+@pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c[:3])) + f"-{c[4]}coll" for c in CASES])
 def test_two_ranks_match_unsharded(case):
     import paper_1412_4080_b200 as ds
     ctx = torch.multiprocessing.get_context("spawn")
@@ -82,10 +87,11 @@ def test_two_ranks_match_unsharded(case):
             if pr.is_alive():
                 pr.kill()
     assert msg[0] == "ok", msg
-    _, iters, x, elim, obj = msg
+    _, iters, x, elim, obj, kept = msg
     p, cfg = _build(case)
     ref = ds.run(p, cfg)
     assert iters == ref.iterations
     assert np.array_equal(elim, np.asarray(ref.screen_state.eliminated))
     np.testing.assert_allclose(x, ref.x_star, rtol=1e-9, atol=1e-12)
     assert obj == pytest.approx(ref.final_objective, rel=1e-12)
+    assert kept == list(ref.trace.kept)
