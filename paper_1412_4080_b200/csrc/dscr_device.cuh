@@ -276,29 +276,56 @@ __device__ __forceinline__ double clip(double r, double b) {
 // reduceat segment: the segment value is a[0] + pairwise(a[1..n)).  Only used
 // for group norms (dictionary.py:280-284), where n is the group size.
 template <typename F>
-__device__ double np_pairwise(F get, int lo, int n) {
-    // iterative version of numpy's pairwise_sum for n <= 128; larger n recurse
+__device__ __forceinline__ double np_pairwise_leaf(F get, int lo, int n) {   // n <= 128
     if (n < 8) {
         double r = -0.0;
         for (int i = 0; i < n; ++i) r += get(lo + i);
         return r;
     }
-    if (n <= 128) {
-        double r[8];
+    double r[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
-        int i = 8;
-        for (; i < n - (n % 8); i += 8) {
+    for (int j = 0; j < 8; ++j) r[j] = get(lo + j);
+    int i = 8;
+    for (; i < n - (n % 8); i += 8) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] += get(lo + i + j);
-        }
-        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
-        for (; i < n; ++i) res += get(lo + i);
-        return res;
+        for (int j = 0; j < 8; ++j) r[j] += get(lo + i + j);
     }
-    int n2 = n / 2;
-    n2 -= n2 % 8;
-    return np_pairwise(get, lo, n2) + np_pairwise(get, lo + n2, n - n2);
+    double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+    for (; i < n; ++i) res += get(lo + i);
+    return res;
+}
+
+// numpy's pairwise_sum: blocks of <= 128 summed 8-way, larger n split at n/2 (rounded down to a
+// multiple of 8) and the halves added.  The recursion runs on an explicit stack so the whole
+// function inlines: a recursive device function taking the accessor lambda forces the kernel
+// parameters it captures into local memory (a ~700-byte Params copy per thread per launch).
+template <typename F>
+__device__ __forceinline__ double np_pairwise(F get, int lo, int n) {
+    if (n <= 128) return np_pairwise_leaf(get, lo, n);
+    int slo[32], sn[32], sst[32];
+    double sleft[32];
+    int sp = 0;
+    slo[0] = lo; sn[0] = n; sst[0] = 0; sp = 1;
+    double ret = 0.0;
+    bool have = false;   // ret holds the value of the frame just popped
+    while (sp > 0) {
+        const int k = sp - 1;
+        const int fl = slo[k], fn = sn[k];
+        int n2 = fn / 2;
+        n2 -= n2 % 8;
+        if (!have) {
+            if (fn <= 128) { ret = np_pairwise_leaf(get, fl, fn); have = true; --sp; continue; }
+            sst[k] = 1;                                   // descend left
+            slo[sp] = fl; sn[sp] = n2; sst[sp] = 0; ++sp;
+        } else if (sst[k] == 1) {                         // left done: descend right
+            sleft[k] = ret; sst[k] = 2; have = false;
+            slo[sp] = fl + n2; sn[sp] = fn - n2; sst[sp] = 0; ++sp;
+        } else {                                          // both done
+            ret = sleft[k] + ret;
+            --sp;
+        }
+    }
+    return ret;
 }
 
 template <typename F>

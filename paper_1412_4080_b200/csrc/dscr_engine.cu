@@ -1006,6 +1006,9 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                 unit = act[s * P.cap + (f - off[s])];
             }
         }
+        // Lasso: the unit's x values are loaded with the test inputs (one round trip)
+        double cand0 = 0.0, xc0 = 0.0;
+        if (!GROUP && valid && do_vec) { cand0 = xn[unit]; xc0 = xc[unit]; }
         const bool masked = valid && test_on && unit_test(P, sc, unit);
         if (valid && !static_mode && do_list) P.mask[f] = masked ? 1 : 0;
         const bool keep = valid && !masked;
@@ -1020,16 +1023,19 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
 
         // per-atom vectors and support entries of this unit
         int my_sup = 0;
+        double bv0 = 0.0;   // Lasso: b value of the unit's atom, reused for the support entry
         if (valid) {
             const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
             bool carries = false;
             for (int j = j0; j < j1; ++j) {
-                const double cand = xn[j];
+                const double cand = GROUP ? xn[j] : cand0;
+                const double xcj = GROUP ? xc[j] : xc0;
                 if (keep) {
                     double bv = 0.0;
-                    if (algo == DSCR_FISTA) { bv = cand + beta * (cand - xc[j]); un[j] = bv; }
-                    else if (algo == DSCR_CP) { bv = cand + phi * (cand - xc[j]); un[j] = bv; }
-                    else if (algo == DSCR_SPARSA) { bv = cand - xc[j]; ssr += bv * bv; }
+                    if (algo == DSCR_FISTA) { bv = cand + beta * (cand - xcj); un[j] = bv; }
+                    else if (algo == DSCR_CP) { bv = cand + phi * (cand - xcj); un[j] = bv; }
+                    else if (algo == DSCR_SPARSA) { bv = cand - xcj; ssr += bv * bv; }
+                    bv0 = bv;
                     if (cand != 0.0 || bv != 0.0) { ++my_sup; carries = true; }
                     if (!GROUP) pen += fabs(cand);
                     nnz += (cand != 0.0) ? 1.0 : 0.0;
@@ -1050,7 +1056,11 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
         }
         int tot;
         const int spos = block_exscan(my_sup, s_scan, &tot);
-        if (my_sup) {
+        if (my_sup && !GROUP) {   // single atom: values from registers
+            const int w = n_sup + spos;
+            if (keep) { sidx[w] = unit; sa[w] = cand0; sb[w] = bv0; }
+            else { sidx[w] = ~unit; sa[w] = cand0; sb[w] = 0.0; }
+        } else if (my_sup) {
             int w = n_sup + spos;
             const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
             for (int j = j0; j < j1; ++j) {
@@ -1097,22 +1107,51 @@ __device__ void k2_final(const Params& P, int G) {
     const bool do_vec = !static_mode && var != 2;
     const int p = sc->parity;
 
-    // ---- last CTA: scans of the slot counts, fixed-order partial reduction
+    // ---- last CTA: scans of the slot counts, fixed-order partial reduction.  Every count and
+    // partial this thread needs is loaded up front (one round trip), then scanned.
+    constexpr int KPF = 5;                       // prefetched slots per thread (G <= KPF * NT)
+    const bool pf = P.G <= KPF * NT;
+    int cnv[KPF], scv[KPF];
+    double pv[KPF][7];
+    if (pf) {
+#pragma unroll
+        for (int k = 0; k < KPF; ++k) {
+            const int i = k * NT + threadIdx.x;
+            const bool in = i < P.G;
+            cnv[k] = (in && do_list) ? P.act_cnt[p ^ 1][i] : 0;
+            scv[k] = (in && do_vec) ? P.sup_cnt[i] : 0;
+            const double* o = P.p2 + (size_t)i * NP2X;
+#pragma unroll
+            for (int q = 0; q < 7; ++q) pv[k][q] = (in && !static_mode) ? o[q] : ((q == 5) ? -INFINITY : (q == 6 ? INFINITY : 0.0));
+        }
+    }
     {
         int carry = 0, carry_s = 0;
         int* offn = P.act_off[p ^ 1];
         const int* cn = P.act_cnt[p ^ 1];
-        for (int base = 0; base < P.G; base += NT) {
+        for (int base = 0, kk = 0; base < P.G; base += NT, ++kk) {
             const int i = base + threadIdx.x;
             int tot;
             if (do_list) {
-                const int v = (i < P.G) ? cn[i] : 0;
+                int v = 0;
+                if (pf) {
+#pragma unroll
+                    for (int k = 0; k < KPF; ++k) if (k == kk) v = cnv[k];
+                } else {
+                    v = (i < P.G) ? cn[i] : 0;
+                }
                 const int e = block_exscan(v, s_scan, &tot);
                 if (i < P.G && P.writer) offn[i] = carry + e;
                 carry += tot;
             }
             if (do_vec) {
-                const int vs = (i < P.G) ? P.sup_cnt[i] : 0;
+                int vs = 0;
+                if (pf) {
+#pragma unroll
+                    for (int k = 0; k < KPF; ++k) if (k == kk) vs = scv[k];
+                } else {
+                    vs = (i < P.G) ? P.sup_cnt[i] : 0;
+                }
                 const int es = block_exscan(vs, s_scan, &tot);
                 if (i < P.G) P.sup_off[i] = carry_s + es;
                 carry_s += tot;
@@ -1142,10 +1181,18 @@ __device__ void k2_final(const Params& P, int G) {
         return;
     }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, a4 = 0.0, tmax = -INFINITY, vmin = INFINITY;
-    for (int i = threadIdx.x; i < G; i += NT) {
-        const double* o = P.p2 + (size_t)i * NP2X;
-        a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3]; a4 += o[4];
-        tmax = fmax(tmax, o[5]); vmin = fmin(vmin, o[6]);
+    if (pf) {
+#pragma unroll
+        for (int k = 0; k < KPF; ++k) {
+            a0 += pv[k][0]; a1 += pv[k][1]; a2 += pv[k][2]; a3 += pv[k][3]; a4 += pv[k][4];
+            tmax = fmax(tmax, pv[k][5]); vmin = fmin(vmin, pv[k][6]);
+        }
+    } else {
+        for (int i = threadIdx.x; i < G; i += NT) {
+            const double* o = P.p2 + (size_t)i * NP2X;
+            a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3]; a4 += o[4];
+            tmax = fmax(tmax, o[5]); vmin = fmin(vmin, o[6]);
+        }
     }
     double r5[5] = {a0, a1, a2, a3, a4};
     block_sum_n<5>(r5, s_sh);
