@@ -48,6 +48,7 @@
 namespace dscr {
 
 enum { MODE_NORMAL = 0, MODE_REDO = 1, MODE_FIXUP = 2, MODE_STATIC = 3 };
+static_assert(sizeof(dscr_scalars) % 8 == 0, "scalar block copied as 8-byte words");
 constexpr int NP1 = 6;   // K1 partials
 constexpr int NP2 = 6;   // K2 partials
 constexpr int NP3 = 4;   // K3b partials
@@ -226,10 +227,23 @@ __device__ void radius_epilogue(const Params& P, double bound, const double* the
     double mu = 0.0;
     if (sq != 0.0) mu = clip(ty / (lam * sq), bound);
     double acc = 0.0;
-    for (int i = threadIdx.x; i < P.n; i += NT) {
-        double v = (sq != 0.0) ? mu * theta[i] : 0.0;
-        double d = P.y[i] / lam - v;
-        acc = fma(d, d, acc);
+    // 4 rows per thread loaded before any is used (same accumulation order as one at a time)
+    for (int i0 = threadIdx.x; i0 < P.n; i0 += 4 * NT) {
+        double th4[4], y4[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * NT;
+            th4[q] = (i < P.n) ? theta[i] : 0.0;
+            y4[q] = (i < P.n) ? P.y[i] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (i0 + q * NT < P.n) {
+                double v = (sq != 0.0) ? mu * th4[q] : 0.0;
+                double d = y4[q] / lam - v;
+                acc = fma(d, d, acc);
+            }
+        }
     }
     double rsq = block_sum(acc, sh);
     if (threadIdx.x == 0) {
@@ -743,10 +757,22 @@ __device__ void k1_final(const Params& P, int G) {
 
     // ---- last CTA: fixed-order reduction of the per-CTA partials
     double m = GROUP ? INFINITY : 0.0, cs = 0.0, ss = 0.0, nf = 0.0, any = 0.0;
-    for (int i = threadIdx.x; i < G; i += NT) {
-        const double* o = P.p1 + (size_t)i * NP1;
-        m = GROUP ? fmin(m, o[0]) : fmax(m, o[0]);
-        cs += o[1]; ss += o[2]; nf = fmax(nf, o[3]); any = fmax(any, o[4]);
+    for (int i0 = threadIdx.x; i0 < G; i0 += 4 * NT) {   // 4 partials per thread in flight
+        double o4[4][5];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * NT;
+            const double* o = P.p1 + (size_t)i * NP1;
+#pragma unroll
+            for (int k = 0; k < 5; ++k) o4[q][k] = (i < G) ? o[k] : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            if (i0 + q * NT < G) {
+                m = GROUP ? fmin(m, o4[q][0]) : fmax(m, o4[q][0]);
+                cs += o4[q][1]; ss += o4[q][2]; nf = fmax(nf, o4[q][3]); any = fmax(any, o4[q][4]);
+            }
+        }
     }
     // max/min via warp + smem
     {
@@ -1359,9 +1385,8 @@ __device__ __forceinline__ void set_cond(const Params& P, unsigned v) {
     if (P.in_graph) cudaGraphSetConditional(P.h_main, v);
 }
 
-__device__ void iteration_epilogue(const Params& P, double s_qa2, double s_tn2, double s_tny,
+__device__ void iteration_epilogue(const Params& P, dscr_scalars* sc, double s_qa2, double s_tn2, double s_tny,
                                    double s_ds2) {
-    dscr_scalars* sc = P.sc;
     const int algo = P.algo;
     const int mode = sc->mode;
     if (mode != MODE_FIXUP) {
@@ -1545,14 +1570,22 @@ __device__ __forceinline__ void k3b_body(const Params& P, int rb) {
 
 __device__ void k3b_final(const Params& P, int G3) {
     __shared__ double s_sh[64];
-    dscr_scalars* sc = P.sc;
+    // the iteration epilogue is one thread's chain of scalar reads and writes: run it on a
+    // shared-memory copy of the scalar block (one cooperative load, one write-back) instead of
+    // a global round trip per field read after a write
+    __shared__ double s_scw[sizeof(dscr_scalars) / 8];
+    dscr_scalars* sc = reinterpret_cast<dscr_scalars*>(s_scw);
+    {
+        const double* g = reinterpret_cast<const double*>(P.sc);
+        for (int i = threadIdx.x; i < (int)(sizeof(dscr_scalars) / 8); i += NT) s_scw[i] = g[i];
+    }
     double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
     for (int i = threadIdx.x; i < G3; i += NT) {
         const double* o = P.p3s + (size_t)i * NP3;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3];
     }
     double r4[4] = {a0, a1, a2, a3};
-    block_sum_n<4>(r4, s_sh);
+    block_sum_n<4>(r4, s_sh);   // (syncs: the scalar copy is complete)
     a0 = r4[0]; a1 = r4[1]; a2 = r4[2]; a3 = r4[3];
     if (threadIdx.x == 0) {
         stamp(P, 7);
@@ -1564,7 +1597,12 @@ __device__ void k3b_final(const Params& P, int G3) {
             // one collective: kept_atoms stays this rank's count (trace; summed by the host),
             // dropped_nz comes from k1r_radius_oc
         }
-        iteration_epilogue(P, a0, a1, a2, a3);
+        iteration_epilogue(P, sc, a0, a1, a2, a3);
+    }
+    __syncthreads();
+    {
+        double* g = reinterpret_cast<double*>(P.sc);
+        for (int i = threadIdx.x; i < (int)(sizeof(dscr_scalars) / 8); i += NT) g[i] = s_scw[i];
     }
 }
 
