@@ -217,6 +217,18 @@ __device__ __forceinline__ int window_slot(const int* off, int G, const int* s_o
     return s0 + a;
 }
 
+// Copy n doubles (n even, both pointers 16-byte aligned) global -> shared with cp.async:
+// every 16-byte piece is in flight at once (no register round trip per element).  The
+// caller's next cp_async_wait_all() + __syncthreads() publishes the data.
+__device__ __forceinline__ void stage_async(double* dst, const double* src, int n) {
+    for (int i = 2 * threadIdx.x; i < n; i += 2 * NT) {
+        const uint32_t d = (uint32_t)__cvta_generic_to_shared(dst + i);
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" :: "r"(d), "l"(src + i) : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // test radius from the dual-scaling bound; whole CTA participates.
 // Restates dual_scale_lasso/group + _safe_radius_sq + _shifted_radius
 // (screening.py:115-205).  bound = 1/corr_inf (Lasso) or min_g w_g/||c_g||.
@@ -296,8 +308,9 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     const bool need_dot = (mode == MODE_NORMAL);
     if (need_dot && hi > lo) {
         const double* th = P.theta[p];
-        for (int i = threadIdx.x; i < P.ldd; i += NT) s_theta[i] = th[i];
+        stage_async(s_theta, th, P.ldd);
     }
+    cp_async_wait_all();
     __syncthreads();
 
     const T* D = static_cast<const T*>(P.D);
@@ -573,7 +586,7 @@ __device__ __forceinline__ void k1_body_tile(const Params& P, int b, int G, doub
     const bool need_dot = (mode == MODE_NORMAL);
     if (need_dot && hi > lo) {
         const double* th = P.theta[p];
-        for (int i = threadIdx.x; i < P.ldd; i += NT) s_theta[i] = th[i];
+        stage_async(s_theta, th, P.ldd);
     }
     const T* D = static_cast<const T*>(P.D);
     const int* act = P.act[p];
@@ -598,7 +611,8 @@ __device__ __forceinline__ void k1_body_tile(const Params& P, int b, int G, doub
     const uint64_t pol = make_policy(P.l2_keep);
     const bool ident = (nu == P.n_units);
     int wend = 0;
-    if (ident) __syncthreads();   // theta staged
+    cp_async_wait_all();          // theta staged (published by the barrier below)
+    if (ident) __syncthreads();
     else wend = stage_window(off, P.G, lo, s_off, &s_s0);   // (syncs: theta staged)
     const int ub = GROUP ? max(1, K1T_ATOMS / max(1, P.max_gsize)) : K1T_ATOMS;
 
