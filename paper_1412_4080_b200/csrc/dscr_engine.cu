@@ -50,7 +50,6 @@ namespace dscr {
 enum { MODE_NORMAL = 0, MODE_REDO = 1, MODE_FIXUP = 2, MODE_STATIC = 3 };
 static_assert(sizeof(dscr_scalars) % 8 == 0, "scalar block copied as 8-byte words");
 constexpr int NP1 = 6;   // K1 partials
-constexpr int NP2 = 6;   // K2 partials
 constexpr int NP3 = 4;   // K3b partials
 constexpr int MIN_COLS_PER_SPLIT = 16;
 // comm region (doubles): [0,8) MAX-reduced, [8,16) setup exchange, [16,32) SUM-reduced scalars,
