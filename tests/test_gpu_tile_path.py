@@ -1,0 +1,81 @@
+"""The tiled K1 path (columns of 5..16 segments of 256 rows: atom-quad x row-segment items,
+fixed-order segment sums) against the CPU oracle: fp64 and fp32 Lasso, groups of mixed sizes
+(up to the 64-atom shared-memory limit of the tiled group update), and a partition with one
+group wider than 64 atoms (per-warp column path).  Screening fires in every case, so the
+identity-list shortcut is also left behind mid-solve."""
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1412_4080_b200 as ds  # noqa: E402
+from paper_1412_4080_b200 import workloads as wl  # noqa: E402
+from oracle import screen_oracle as so  # noqa: E402
+
+
+def _run(D, y, lam, groups=None, dtype="f64", algo="fista", test="dst3", rtol=1e-9):
+    dic = ds.Dictionary(D, check_unit_norms=(dtype == "f64"), dtype=dtype)
+    part = ds.GroupPartition.build(dic, groups) if groups is not None else None
+    D64 = dic.as_float64()
+    L = float(np.linalg.norm(D64, 2) ** 2 * (1 + 1e-9))
+    cfg = ds.SolverConfig(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300,
+                          L0=L, gap_tol=1e-7)
+    res = ds.run(ds.Problem(dic, y, lam, part), cfg)
+    op = so.make_problem(D64, y, lam, groups, None if part is None else part.weights,
+                         None if part is None else part.spectral_norms)
+    ref = so.solve(op, so.Config(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300,
+                                 L0=L, gap_tol=1e-7, norm_aware=(dtype != "f64")))
+    # gap 1e-7: reached well before the objective stalls to the last bit (rel_tol 1e-300 stops on
+    # bitwise-equal consecutive objectives, where 1-ulp summation differences decide)
+    assert res.stop_reason == "gap"
+    assert res.iterations == ref.iterations
+    assert np.array_equal(res.screen_state.eliminated, ref.eliminated)
+    assert ref.eliminated.size > 0
+    np.testing.assert_allclose(res.final_objective, ref.final_objective, rtol=rtol)
+    assert np.linalg.norm(res.x_star - ref.x_star) <= 1e-6 * max(np.linalg.norm(ref.x_star), 1e-300)
+    return res
+
+
+@pytest.mark.parametrize("n", [1300, 4000])
+def test_tiled_lasso_f64(n):
+    D = wl.correlated_dictionary(n, 3000, 11)
+    y, _ = wl.planted_observation(D, 11, nnz=12)
+    _run(D, y, 0.6 * wl.lambda_star(D, y))
+
+
+def test_tiled_lasso_f32():
+    D = wl.correlated_dictionary(1300, 3000, 12).astype(np.float32)
+    y, _ = wl.planted_observation(D.astype(np.float64), 12, nnz=12)
+    _run(D, y, 0.6 * wl.lambda_star(D.astype(np.float64), y), dtype="f32", rtol=1e-6)
+
+
+def _mixed_groups(k, seed, wide=None):
+    rng = np.random.default_rng(seed)
+    sizes = []
+    while sum(sizes) < k:
+        sizes.append(int(rng.integers(1, 41)))
+    sizes[-1] -= sum(sizes) - k
+    if sizes[-1] <= 0:
+        sizes.pop()
+        sizes[-1] += k - sum(sizes)
+    if wide:
+        sizes = [wide] + sizes
+        sizes[-1] -= wide
+        while sizes[-1] <= 0:
+            extra = sizes.pop()
+            sizes[-1] += extra
+    ptr = np.concatenate(([0], np.cumsum(sizes)))
+    return [np.arange(ptr[g], ptr[g + 1]) for g in range(len(sizes))]
+
+
+@pytest.mark.parametrize("wide", [None, 80], ids=["sizes-1-40", "one-group-of-80"])
+def test_tiled_groups(wide):
+    D = wl.correlated_dictionary(1300, 2400, 13)
+    groups = _mixed_groups(2400, 13, wide)
+    y, _ = wl.planted_observation(D, 13, nnz=15)
+    corr = D.T @ y
+    w = np.sqrt([g.size for g in groups])
+    lam = 0.7 * max(np.linalg.norm(corr[g]) / wg for g, wg in zip(groups, w))
+    _run(D, y, lam, groups=groups, test="gst3")
