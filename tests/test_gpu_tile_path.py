@@ -38,15 +38,16 @@ def _run(D, y, lam, groups=None, dtype="f64", algo="fista", test="dst3", rtol=1e
     return res
 
 
-@pytest.mark.parametrize("n", [1300, 4000])
+@pytest.mark.parametrize("n", [1300, 4000, 5000])   # 5000: > 16 segments, per-warp column path
 def test_tiled_lasso_f64(n):
     D = wl.correlated_dictionary(n, 3000, 11)
     y, _ = wl.planted_observation(D, 11, nnz=12)
     _run(D, y, 0.6 * wl.lambda_star(D, y))
 
 
-def test_tiled_lasso_f32():
-    D = wl.correlated_dictionary(1300, 3000, 12).astype(np.float32)
+@pytest.mark.parametrize("n", [1300, 8192])          # 8192 (c4 rows): per-warp column path
+def test_tiled_lasso_f32(n):
+    D = wl.correlated_dictionary(n, 3000, 12).astype(np.float32)
     y, _ = wl.planted_observation(D.astype(np.float64), 12, nnz=12)
     _run(D, y, 0.6 * wl.lambda_star(D.astype(np.float64), y), dtype="f32", rtol=1e-6)
 
