@@ -1066,9 +1066,23 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
         if (valid) {
             const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
             bool carries = false;
+            // groups: the atoms' x values are loaded 4 at a time (all in flight) before use
+            constexpr int GB = GROUP ? 4 : 1;
+            double gxn[GB], gxc[GB];
             for (int j = j0; j < j1; ++j) {
-                const double cand = GROUP ? xn[j] : cand0;
-                const double xcj = GROUP ? xc[j] : xc0;
+                const int jj = (j - j0) % GB;
+                if (GROUP && jj == 0) {
+#pragma unroll
+                    for (int q = 0; q < GB; ++q) {
+                        gxn[q] = (j + q < j1) ? xn[j + q] : 0.0;
+                        gxc[q] = (j + q < j1) ? xc[j + q] : 0.0;
+                    }
+                }
+                double cand = cand0, xcj = xc0;
+                if (GROUP) {
+#pragma unroll
+                    for (int q = 0; q < GB; ++q) if (q == jj) { cand = gxn[q]; xcj = gxc[q]; }
+                }
                 if (keep) {
                     double bv = 0.0;
                     if (algo == DSCR_FISTA) { bv = cand + beta * (cand - xcj); un[j] = bv; }
@@ -1102,12 +1116,26 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
         } else if (my_sup) {
             int w = n_sup + spos;
             const int j0 = unit_atom_lo(P, unit), j1 = unit_atom_hi(P, unit);
+            double gxn[4], gb[4];
             for (int j = j0; j < j1; ++j) {
-                const double cand = xn[j];
+                const int jj = (j - j0) % 4;
+                if (jj == 0) {   // 4 atoms' values in flight at once
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const bool in = j + q < j1;
+                        gxn[q] = in ? xn[j + q] : 0.0;
+                        gb[q] = 0.0;
+                        if (in && (algo == DSCR_FISTA || algo == DSCR_CP)) gb[q] = un[j + q];
+                        else if (in && algo == DSCR_SPARSA) gb[q] = xc[j + q];
+                    }
+                }
+                double cand = 0.0, gq = 0.0;
+#pragma unroll
+                for (int q = 0; q < 4; ++q) if (q == jj) { cand = gxn[q]; gq = gb[q]; }
                 if (keep) {
                     double bv = 0.0;
-                    if (algo == DSCR_FISTA || algo == DSCR_CP) bv = un[j];
-                    else if (algo == DSCR_SPARSA) bv = cand - xc[j];
+                    if (algo == DSCR_FISTA || algo == DSCR_CP) bv = gq;
+                    else if (algo == DSCR_SPARSA) bv = cand - gq;
                     if (cand != 0.0 || bv != 0.0) { sidx[w] = j; sa[w] = cand; sb[w] = bv; ++w; }
                 } else if (cand != 0.0) {
                     sidx[w] = ~j; sa[w] = cand; sb[w] = 0.0; ++w;
