@@ -74,7 +74,7 @@ struct GemmArgs {
 template <int MODE>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     k_gemm_dt(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmArgs g) {
-    constexpr bool CL = MODE >= 1, TWO = MODE == 2;
+    constexpr bool CL = MODE >= 1, TWO = MODE >= 2, SW = MODE == 3;
     constexpr int NSTG = TWO ? 6 : STAGES;
     constexpr int SB_BYTES = TWO ? B_BYTES / 2 : B_BYTES;   // Theta bytes per stage in this CTA
     extern __shared__ uint8_t smem_raw[];
@@ -128,8 +128,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                     if (TWO) {
                         const uint32_t lfull = mapa_rank(smem_u32(&full[stage]), 0);   // leader's barrier
                         if (crank == 0) mbar_expect_tx(&full[stage], 2 * (A_BYTES + SB_BYTES));
-                        tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, lfull, k, mb * BM);
-                        tma_load_2d_2sm(sB + stage * SB_BYTES, &tmB, lfull, k, s * g.Nb + nb * BN + (int)crank * (BN / 2));
+                        // MODE 3: A = Theta (observation rows, one block per split), B = D^T
+                        tma_load_2d_2sm(sA + stage * A_BYTES, &tmA, lfull, k, (SW ? s * g.Nb : 0) + mb * BM);
+                        tma_load_2d_2sm(sB + stage * SB_BYTES, &tmB, lfull, k,
+                                        (SW ? 0 : s * g.Nb) + nb * BN + (int)crank * (BN / 2));
                     } else {
                         mbar_expect_tx(&full[stage], STAGE_BYTES);
                         tma_load_2d(sA + stage * A_BYTES, &tmA, &full[stage], k, mb * BM);
@@ -202,6 +204,72 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             } else {
                 mbar_arrive(&tempty[ab]);
             }
+        }
+    } else if (SW) {   // ---- fused epilogue, lanes = observations (MODE 3)
+        // each thread owns one observation: its threshold and the mask / list words of the 32
+        // atoms of a chunk are plain registers, the max over active atoms is a running max (no
+        // cross-lane reductions), hot atoms are appended by the owning thread
+        const int q = warp & 3;
+        constexpr int PARTS = EPI_WARPS / 4;
+        const int part = (warp - 2) >> 2;
+        constexpr int KC = BN / (32 * PARTS);                         // 32-atom chunks per warp
+        int lt = 0;
+        for (int tt = t_first; tt < t_count; tt += t_step, ++lt) {
+            int mb, nb;
+            tile_mn(tt, mb, nb);
+            const int ab = lt & 1;
+            const uint32_t aphase = (lt >> 1) & 1;
+            const int j = mb * BM + q * 32 + lane;                    // observation
+            const int cb = part * (BN / PARTS);
+            const int a_base = nb * BN + cb;                          // first atom of the warp's columns
+            const uint32_t* mrow = g.mask + (size_t)j * g.words + (a_base >> 5);
+            const uint32_t* nrow = g.nzm + (size_t)j * g.words + (a_base >> 5);
+            uint32_t wa = mrow[0], wn = nrow[0];
+            const float th = g.thr[j];
+            mbar_wait(&tfull[ab], aphase);
+            tc_fence_after();
+            uint32_t mymax = 0u;
+#pragma unroll 1
+            for (int k = 0; k < KC; ++k) {
+                uint32_t wa_n = 0u, wn_n = 0u;
+                if (k + 1 < KC) { wa_n = mrow[k + 1]; wn_n = nrow[k + 1]; }
+                uint32_t r[32];
+                tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + ab * BN + cb + k * 32, r);
+                uint32_t hb = 0u;
+#pragma unroll
+                for (int i = 0; i < 32; ++i) {
+                    const uint32_t abits = r[i] & 0x7fffffffu;       // |c| (float bits, monotone)
+                    const bool act = (wa >> i) & 1u;
+                    if (act) mymax = max(mymax, abits);
+                    const bool hot = act && (__uint_as_float(abits) > th || ((wn >> i) & 1u));
+                    hb |= hot ? (1u << i) : 0u;
+                }
+                while (hb) {                                          // rare: this observation's hot atoms
+                    const int i = __ffs(hb) - 1;
+                    hb &= hb - 1u;
+                    float v;
+                    switch (i) {
+#define DSCR_RCASE(n) case n: v = __uint_as_float(r[n]); break;
+                        DSCR_RCASE(0) DSCR_RCASE(1) DSCR_RCASE(2) DSCR_RCASE(3) DSCR_RCASE(4) DSCR_RCASE(5)
+                        DSCR_RCASE(6) DSCR_RCASE(7) DSCR_RCASE(8) DSCR_RCASE(9) DSCR_RCASE(10) DSCR_RCASE(11)
+                        DSCR_RCASE(12) DSCR_RCASE(13) DSCR_RCASE(14) DSCR_RCASE(15) DSCR_RCASE(16) DSCR_RCASE(17)
+                        DSCR_RCASE(18) DSCR_RCASE(19) DSCR_RCASE(20) DSCR_RCASE(21) DSCR_RCASE(22) DSCR_RCASE(23)
+                        DSCR_RCASE(24) DSCR_RCASE(25) DSCR_RCASE(26) DSCR_RCASE(27) DSCR_RCASE(28) DSCR_RCASE(29)
+                        DSCR_RCASE(30) default: v = __uint_as_float(r[31]); break;
+#undef DSCR_RCASE
+                    }
+                    const int e = atomicAdd(&g.hot_cnt[j], 1);
+                    if (e < g.hcap) {
+                        g.hot_idx[(size_t)j * g.hcap + e] = a_base + k * 32 + i;
+                        g.hot_val[(size_t)j * g.hcap + e] = v;
+                    }
+                }
+                wa = wa_n; wn = wn_n;
+            }
+            if (mymax) atomicMax(&g.cmax[j], mymax);
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(mapa_rank(smem_u32(&tempty[ab]), 0));
         }
     } else {   // ---- fused screening epilogue: hot entries + per-observation max |c|
         __shared__ uint4 s_cw[EPI_WARPS][32];   // per-warp column words (mask, list, threshold)
@@ -359,17 +427,29 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
     if (ecl && !strcmp(ecl, "0")) mode = 0;
     if (ecl && !strcmp(ecl, "mc") && mode) mode = 1;
     const bool cl = mode > 0;
+    // fused CTA pair: observations on the M side (TMEM lanes), atoms on the N side (MODE 3),
+    // unless DSCR_GEMM_SWAP=0
+    const char* esw = getenv("DSCR_GEMM_SWAP");
+    const bool swap = fused && mode == 2 && (Nb / BM) % 2 == 0 && M % BN == 0 && !(esw && !strcmp(esw, "0"));
     CUtensorMap ma, mb;
-    int rc = make_map(&ma, A, K, M, lda, BK, BM);
-    if (rc) return rc;
-    rc = make_map(&mb, B, K, Nb * S, ldb, BK, cl ? BN / 2 : BN);
-    if (rc) return rc;
+    int rc;
+    if (swap) {
+        rc = make_map(&ma, B, K, Nb * S, ldb, BK, BM);
+        if (rc) return rc;
+        rc = make_map(&mb, A, K, M, lda, BK, BN / 2);
+        if (rc) return rc;
+    } else {
+        rc = make_map(&ma, A, K, M, lda, BK, BM);
+        if (rc) return rc;
+        rc = make_map(&mb, B, K, Nb * S, ldb, BK, cl ? BN / 2 : BN);
+        if (rc) return rc;
+    }
     GemmArgs g{};
     g.Nb = Nb;
     g.KB = K / BK;
     g.S = S;
-    g.num_m = M / BM;
-    g.num_n = Nb / BN;
+    g.num_m = swap ? Nb / BM : M / BM;
+    g.num_n = swap ? M / BN : Nb / BN;
     g.num_tiles = g.num_m * g.num_n;
     if (fused) {
         g.mask = fused->mask; g.nzm = fused->nzm; g.thr = fused->thr; g.cmax = fused->cmax;
@@ -383,7 +463,7 @@ int gemm_dt(const void* A, int M, int lda, const void* B, int Nb, int ldb, int K
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaError_t e;
     if (cl) {
-        auto kern = (mode == 2) ? k_gemm_dt<2> : k_gemm_dt<1>;
+        auto kern = swap ? k_gemm_dt<3> : ((mode == 2) ? k_gemm_dt<2> : k_gemm_dt<1>);
         e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GEMM_SMEM);
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
         cudaLaunchConfig_t lc = {};
