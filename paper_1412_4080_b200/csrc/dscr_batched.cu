@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint32_t* nrow = g.nzm + (size_t)j * g.words + (a_base >> 5);
             uint32_t wa = mrow[0], wn = nrow[0];
             const float th = g.thr[j];
-            mbar_wait(&tfull[ab], aphase);
+            mbar_wait_sleep(&tfull[ab], aphase);
             tc_fence_after();
             uint32_t mymax = 0u;
 #pragma unroll 1
