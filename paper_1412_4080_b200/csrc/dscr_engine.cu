@@ -2190,7 +2190,9 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
         const int segr = 32 * (32 / dtype_size(pr->dtype)) * (pr->dtype == DSCR_F64 ? K1Cfg<double>::U : 1);
         const int nseg = (pr->n_rows + segr - 1) / segr;
         const char* et = getenv("DSCR_K1_TILE");
-        g.tile = (nseg >= 5 && nseg <= K1T_SEGS && max_gsize <= 64 && !(et && !strcmp(et, "0"))) ? nseg : 0;
+        const char* em = getenv("DSCR_K1_TILE_MIN");   // experiment knob: smallest tiled segment count
+        const int tmin = em ? atoi(em) : 5;
+        g.tile = (nseg >= tmin && nseg <= K1T_SEGS && max_gsize <= 64 && !(et && !strcmp(et, "0"))) ? nseg : 0;
         if (g.tile) g.smem1 += K1T_ATOMS * g.tile * (int)sizeof(double);
     }
     // resident K1 CTAs per SM (registers + theta staging buffer): one full wave
