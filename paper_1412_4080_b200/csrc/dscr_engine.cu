@@ -57,7 +57,10 @@ constexpr int MIN_COLS_PER_SPLIT = 16;
 constexpr int CM_MAX = 0, CM_SETUP = 8, CM_SUM = 16, CM_VEC = 32;
 constexpr int OC_SLOT = 8, OC_MAX_WORLD = 64;   // one-collective rank slots after the SUM vector
 constexpr int NP2X = 8;  // K2 partials incl. the one-collective test extremes
-constexpr int TRIPS_PER_BODY = 4;
+#ifndef DSCR_TRIPS_PER_BODY
+#define DSCR_TRIPS_PER_BODY 4
+#endif
+constexpr int TRIPS_PER_BODY = DSCR_TRIPS_PER_BODY;
 constexpr int PERS_MAX_G = 2048;   // persistent engine: max CTAs (support offsets kept in smem)
 
 
@@ -2310,6 +2313,9 @@ static int validate(const dscr_problem_desc* pr, const dscr_config* cfg, int* n_
     if (pr->dtype < DSCR_F64 || pr->dtype > DSCR_BF16) return set_inval("unknown dtype");
     if (pr->n_rows < 1 || pr->n_cols < 1) return set_inval("dictionary must have at least one row and one column");
     if (pr->ldd < pr->n_rows || pr->ldd % 16) return set_inval("ldd must be >= n_rows and a multiple of 16");
+    // K1 stages theta (ldd doubles) in shared memory next to ~5 KB of static state
+    if ((size_t)pr->ldd * sizeof(double) + 8192 > 227 * 1024)
+        return set_inval("n_rows too large: theta (8 bytes per row) must fit in shared memory (n_rows <= 28000)");
     if (!(pr->lam > 0)) return set_inval("lam must be strictly positive");
     if (!pr->D || !pr->y) return set_inval("null device pointer");
     if (cfg->algorithm < DSCR_ISTA || cfg->algorithm > DSCR_CP) return set_inval("unknown algorithm");
