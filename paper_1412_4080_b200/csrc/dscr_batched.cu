@@ -1003,6 +1003,26 @@ __device__ __forceinline__ double radius_sq(const BParams& P, int j, double mu, 
     return fma(dm * dm, sq, P.rsq0[j]);
 }
 
+__device__ __forceinline__ uint64_t l2_normal_policy() {
+    uint64_t pol;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+
+// rows n..n+3 of theta_j as bf16 terms (n a multiple of 4, 8-byte aligned): one store per term
+__device__ __forceinline__ void write_theta4(const BParams& P, int j, int n, double t0, double t1, double t2,
+                                             double t3) {
+    const double t[4] = {t0, t1, t2, t3};
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+        hi[v] = __double2bfloat16(t[v]);
+        lo[v] = __double2bfloat16(t[v] - (double)__bfloat162float(hi[v]));
+    }
+    *reinterpret_cast<uint2*>(P.tb + (size_t)j * P.ldy + n) = *reinterpret_cast<const uint2*>(hi);
+    if (P.splits > 1) *reinterpret_cast<uint2*>(P.tb + ((size_t)P.B + j) * P.ldy + n) = *reinterpret_cast<const uint2*>(lo);
+}
+
 __device__ __forceinline__ void write_theta(const BParams& P, int j, int n, double t) {
     const __nv_bfloat16 hi = __double2bfloat16(t);
     P.tb[(size_t)j * P.ldy + n] = hi;
@@ -1668,10 +1688,15 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
     double rx[RPT], ru[RPT], yv[RPT];
     constexpr int nch = NCH;
 #pragma unroll
-    for (int q = 0; q < RPT; ++q) {
-        rx[q] = 0.0; ru[q] = 0.0;
-        const int n = (q >> 2) * RC + 4 * threadIdx.x + (q & 3);
-        yv[q] = (n < P.N) ? P.Y[(size_t)j * P.ldy + n] : 0.0;       // independent of the list: issue early
+    for (int c = 0; c < NCH; ++c) {   // y: one 32-byte load per thread and chunk, issued early
+        const int n0 = c * RC + 4 * threadIdx.x;
+        double y4[4] = {0.0, 0.0, 0.0, 0.0};
+        if (n0 < P.ldy) Vec<double>::load(P.Y + (size_t)j * P.ldy + n0, y4, l2_normal_policy());
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            rx[c * 4 + v] = 0.0; ru[c * 4 + v] = 0.0;
+            yv[c * 4 + v] = (n0 + v < P.N) ? y4[v] : 0.0;
+        }
     }
     const int* idx = P.si[par] + lo;
     const double* xa = P.sx[par] + lo;
@@ -1713,19 +1738,23 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
 #pragma unroll
     for (int q = 0; q < RPT; ++q) {
         const int n = (q >> 2) * RC + 4 * threadIdx.x + (q & 3);
+        double tn = 0.0;                       // padding rows of theta stay zero
         if (n < P.N) {
             const double yn = yv[q];
             const double qa = rx[q] - yn;
-            const double tn = ru[q] - yn;      // theta_{t+1} = D u - y (solvers.py:212)
-            write_theta(P, j, n, tn);
+            tn = ru[q] - yn;                   // theta_{t+1} = D u - y (solvers.py:212)
             f2 = fma(qa, qa, f2);
             sq = fma(tn, tn, sq);
             tyv = fma(tn, yn, tyv);
             rx[q] = yn;                        // keep y and theta for the r_SAFE^2 pass
-            ru[q] = tn;
         }
+        ru[q] = tn;
     }
-    for (int n = P.N + threadIdx.x; n < P.ldy; n += TPB) write_theta(P, j, n, 0.0);
+#pragma unroll
+    for (int c = 0; c < NCH; ++c) {            // theta terms: one 8-byte store per thread and chunk
+        const int n0 = c * RC + 4 * threadIdx.x;
+        if (n0 < P.ldy) write_theta4(P, j, n0, ru[c * 4 + 0], ru[c * 4 + 1], ru[c * 4 + 2], ru[c * 4 + 3]);
+    }
     double v3[3] = {f2, sq, tyv};
     block_sum_nt<3, TPB>(v3, s_sh);
     const double lam = P.lam[j];
