@@ -1701,7 +1701,11 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
     const int* idx = P.si[par] + lo;
     const double* xa = P.sx[par] + lo;
     const double* ub = P.su[par] + lo;
+#ifdef BRESID_NOGATHER
+    const int cnt = 0;
+#else
     const int cnt = P.sn[par][j];
+#endif
     for (int e0 = 0; e0 < cnt; e0 += TPB) {
         __syncthreads();
         if (e0 + threadIdx.x < cnt) {
@@ -1716,19 +1720,16 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
             const int r0 = ch * RC + 4 * threadIdx.x;
             if (r0 >= P.N) continue;
             double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
-            int e = 0;
-            constexpr int EB = BRESID_EB;    // list entries in flight
-            for (; e + EB <= m; e += EB) {
+            constexpr int EB = BRESID_EB;    // list entries in flight (the last group predicated)
+            for (int e = 0; e < m; e += EB) {
                 uint2 w[EB];
 #pragma unroll
                 for (int q = 0; q < EB; ++q)
-                    w[q] = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0));
+                    w[q] = (e + q < m) ? __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0))
+                                       : make_uint2(0u, 0u);
 #pragma unroll
-                for (int q = 0; q < EB; ++q) resid_acc(w[q], s_a[e + q], s_b[e + q], a, b);
-            }
-            for (; e < m; ++e) {
-                const uint2 w = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e] * P.ldd + r0));
-                resid_acc(w, s_a[e], s_b[e], a, b);
+                for (int q = 0; q < EB; ++q)
+                    if (e + q < m) resid_acc(w[q], s_a[e + q], s_b[e + q], a, b);
             }
 #pragma unroll
             for (int v = 0; v < 4; ++v) { rx[ch * 4 + v] += a[v]; ru[ch * 4 + v] += b[v]; }
