@@ -556,11 +556,14 @@ def run_ours(args):
         dev_s = float(t.item())
     iters, trips, streamed_cols, solve_times = 0, 0, 0, []
     kernels = 0
-    for engs in steps:
+    inloop = None
+    for si, engs in enumerate(steps):
         for e, (p, c) in zip(engs, problems):
             sc = e.scalars()
             if sc.status != 0:
                 raise RuntimeError(f"solver status {sc.status}")
+            if inloop is None and si == len(steps) - 1:
+                inloop = inloop_kernel_us(e, sc)
             iters += sc.t
             trips += sc.trips
             rows = e.trace_rows(sc.t)
@@ -651,6 +654,7 @@ def run_ours(args):
                          "kernel": "k1_corr_update", "kernel_ms": ms[0],
                          "bytes_per_launch": k1_bytes, "per_kernel_ms": list(ms)},
             "solve_hbm_gbs": solve_gbs,
+            "inloop_median_us": inloop,
             "gpu_launches": kernels,
             "clocks": clocks.summary(),
             "e2e": e2e,
@@ -659,6 +663,20 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if world > 1:
         torch.distributed.destroy_process_group()
+
+
+def inloop_kernel_us(eng, sc):
+    """Median per-kernel durations (us) of a timed solve from the engine's in-graph %globaltimer
+    stamps (K1 / K2 / K3a / K3b entry and exit per trip; gaps are the launch boundaries)."""
+    import torch
+    b = eng.bufs
+    trips = min(int(sc.trips), int(b.max_kts))
+    if trips < 3:
+        return None
+    ts = eng.view(b.kts, trips * 8, torch.int64).cpu().numpy().reshape(trips, 8).astype(np.float64)[1:]
+    cols = {"K1": ts[:, 1] - ts[:, 0], "K2": ts[:, 3] - ts[:, 2], "K3a_to_K3b": ts[:, 6] - ts[:, 4],
+            "K3b": ts[:, 7] - ts[:, 6], "trip": np.diff(ts[:, 0])}
+    return {k: round(float(np.median(v)) / 1e3, 2) for k, v in cols.items()}
 
 
 def setup_launches(cfg):
