@@ -756,6 +756,8 @@ constexpr int BT = 256;              // threads of the per-observation kernels
 constexpr int BW = BT / 32;
 
 struct BParams {
+    double* trp;               // [TR_G][4] per-CTA trace partials
+    unsigned* trt;             // trace ticket
     const __nv_bfloat16* Dt;   // [K][ldd]
     int N, K, B, ldd;
     const double* Y;           // [B][ldy]
@@ -1067,7 +1069,7 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
         P.thr[j] = (float)(P.lam[j] * (1.0 - 1e-6));
         P.cmax[j] = 0u;
         P.hot_cnt[j] = 0;
-        if (j == 0) { *P.it = 0; *P.nbig = 0; *P.big_next = 0; *P.scr_ctr = 0ull; }
+        if (j == 0) { *P.it = 0; *P.nbig = 0; *P.big_next = 0; *P.scr_ctr = 0ull; *P.trt = 0u; }
     }
 }
 
@@ -1803,19 +1805,24 @@ static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
 }
 
 // per-iteration batch aggregates (fixed order): 1024 threads, loads of 4 observations in flight
-constexpr int TR_T = 1024;
+// TR_G CTAs reduce contiguous observation ranges in fixed order; the last one (ticket)
+// combines the partials in CTA order
+constexpr int TR_T = 256, TR_G = 16;
 __global__ void __launch_bounds__(TR_T) k_btrace(BParams P, int t) {
     __shared__ double s_sh[4 * (TR_T / 32)];
-    if (threadIdx.x == 0) { *P.nbig = 0; *P.big_next = 0; *P.scr_ctr = 0ull; }   // this iteration's lists consumed
+    __shared__ int s_flag;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { *P.nbig = 0; *P.big_next = 0; *P.scr_ctr = 0ull; }   // lists consumed
+    const int per = (P.B + TR_G - 1) / TR_G;
+    const int lo = blockIdx.x * per, hi = min(P.B, lo + per);
     double a[4] = {0, 0, 0, 0};
-    for (int j0 = threadIdx.x; j0 < P.B; j0 += 4 * TR_T) {
+    for (int j0 = lo + threadIdx.x; j0 < hi; j0 += 4 * TR_T) {
         int st[4];
         double f[4], gp[4];
         int nz[4], kp[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const int j = j0 + u * TR_T;
-            const bool ok = j < P.B;
+            const bool ok = j < hi;
             st[u] = ok ? P.status[j] : 1;
             f[u] = ok ? P.F[j] : 0.0;
             gp[u] = ok ? P.gap[j] : 0.0;
@@ -1830,7 +1837,20 @@ __global__ void __launch_bounds__(TR_T) k_btrace(BParams P, int t) {
     }
     block_sum_nt<4, TR_T>(a, s_sh);
     if (threadIdx.x == 0)
-        for (int q = 0; q < 4; ++q) P.trace[(size_t)t * 4 + q] = a[q];
+        for (int q = 0; q < 4; ++q) P.trp[blockIdx.x * 4 + q] = a[q];
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_flag = (atomicAdd(P.trt, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_flag) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        *P.trt = 0u;
+        double r[4] = {0, 0, 0, 0};
+        for (int g = 0; g < (int)gridDim.x; ++g)
+            for (int q = 0; q < 4; ++q) r[q] += P.trp[g * 4 + q];
+        for (int q = 0; q < 4; ++q) P.trace[(size_t)t * 4 + q] = r[q];
+    }
 }
 
 }  // namespace batched
@@ -1864,6 +1884,8 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     p.soff = (int*)take((B + 1) * 4);
     p.sptr = (int*)take(B * 4);
     p.scr_ctr = (unsigned long long*)take(8);
+    p.trp = (double*)take(64 * 4 * 8);
+    p.trt = (unsigned*)take(64);
     p.scr_j = (int*)take(B * 4);
     p.scr_p = (int*)take(B * 4);
     p.scr_off = (int*)take(B * 4);
@@ -2021,7 +2043,7 @@ static int enqueue_iterations(dscr_batched* h, int t0, int n, cudaStream_t s) {
         if (P.fused) launch_update_hot(P, t, s);
         else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
         launch_bresid(P, t, s);
-        k_btrace<<<1, TR_T, 0, s>>>(P, t);
+        k_btrace<<<TR_G, TR_T, 0, s>>>(P, t);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     }
@@ -2068,7 +2090,7 @@ int dscr_batched_profile(dscr_batched* h, int t, void* stream, float* ms_out) {
     cudaEventRecord(ev[2], s);
     launch_bresid(P, t, s);
     cudaEventRecord(ev[3], s);
-    k_btrace<<<1, TR_T, 0, s>>>(P, t);          // resets the iteration's work lists
+    k_btrace<<<TR_G, TR_T, 0, s>>>(P, t);       // resets the iteration's work lists
     cudaEventSynchronize(ev[3]);
     for (int i = 0; i < 3; ++i) cudaEventElapsedTime(&ms_out[i], ev[i], ev[i + 1]);
     for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
