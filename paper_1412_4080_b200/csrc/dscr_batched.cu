@@ -974,7 +974,10 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
 // a word, block radix sort on the key bits (descending; stable, so ties keep the atom order and
 // padding entries stay last), order and sorted keys written once.
 constexpr int BS_T = 512, BS_I = 32;
-using BlockSort = cub::BlockRadixSort<uint32_t, BS_T, BS_I>;
+#ifndef BSORT_RADIX_BITS
+#define BSORT_RADIX_BITS 4
+#endif
+using BlockSort = cub::BlockRadixSort<uint32_t, BS_T, BS_I, cub::NullType, BSORT_RADIX_BITS>;
 __global__ void __launch_bounds__(BS_T, 1) k_bsort(BParams P) {
     extern __shared__ __align__(16) uint8_t bs_raw[];
     typename BlockSort::TempStorage& tmp = *reinterpret_cast<typename BlockSort::TempStorage*>(bs_raw);
