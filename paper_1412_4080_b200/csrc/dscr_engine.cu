@@ -126,6 +126,7 @@ struct Params {
     unsigned long long* kts;   // per-trip kernel timestamps [trips][8]
     int max_kts;
     int max_gsize;
+    int min_cols;      // support columns per K3a split at least (MIN_COLS_PER_SPLIT)
     int onecoll;       // one collective per trip (dscr_solver_set_collectives)
     int oc_rank, oc_world;
     int k2v;           // K2 variant: 0 classic, 1 support before the test (K2S), 2 test + compaction (K2C)
@@ -1235,7 +1236,7 @@ __device__ void k2_final(const Params& P, int G) {
             if (do_vec) {
                 P.sup_off[P.G] = carry_s;
                 sc->n_support = carry_s;
-                int pe = (carry_s + MIN_COLS_PER_SPLIT - 1) / MIN_COLS_PER_SPLIT;
+                int pe = (carry_s + P.min_cols - 1) / P.min_cols;
                 sc->p_eff = max(1, min(P.P, pe));
             }
         }
@@ -2559,6 +2560,8 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
     P.k1_tile = g.tile; P.max_gsize = g.max_gsize;
+    P.min_cols = MIN_COLS_PER_SPLIT;
+    if (const char* em = getenv("DSCR_K3A_MIN_COLS")) P.min_cols = std::max(1, atoi(em));   // experiment knob
     P.col_offset = pr->col_offset;
     P.group_offset = pr->group_offset;
     P.in_graph = 1;
