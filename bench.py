@@ -45,8 +45,9 @@ def parse():
     ap.add_argument("--workload", choices=("c1", "c2", "c3", "c4", "c5"), default="c4")
     ap.add_argument("--splits", type=int, default=1, help="bf16 terms of theta in the c5 GEMM")
     ap.add_argument("--sharded", action="store_true", help="column-sharded phase path even at one rank")
-    ap.add_argument("--collectives", type=int, choices=(1, 2), default=1,
-                    help="sharded c4: collectives per trip (1: rank-slot gather in the SUM; 2: MAX + SUM)")
+    ap.add_argument("--collectives", choices=("1", "2", "peer"), default="1",
+                    help="sharded c4: per trip 1 NCCL SUM (rank-slot gather), 2 (MAX + SUM), or 'peer': the "
+                         "native exchange through peer memory (device stores + arrival flags, no NCCL)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="direct-launch iterations for ncu")
@@ -366,6 +367,10 @@ def run_reference_c5(args, world):
     print(json.dumps(line), flush=True)
 
 
+def _coll(args):
+    return args.collectives if args.collectives == "peer" else int(args.collectives)
+
+
 def run_c4_sharded(args, world, rank, local):
     """c4 with its 262144 columns sharded over the ranks (strong scaling).  Default: one NCCL
     all-reduce per trip (SUM of the length-N partial residuals with the ranks' MAX quantities
@@ -400,7 +405,7 @@ def run_c4_sharded(args, world, rank, local):
     prob = ds.Problem(dic, y, lam)
     shard = pdist.GpuShard(prob, cfg, c0, k, device=dev)
     for _ in range(args.warmup):
-        pdist.orchestrate(shard, cfg, lam, dist.group.WORLD, collectives=args.collectives)
+        pdist.orchestrate(shard, cfg, lam, dist.group.WORLD, collectives=_coll(args))
     torch.cuda.synchronize()
     dist.barrier()
     stream = torch.cuda.current_stream(dev)
@@ -410,7 +415,7 @@ def run_c4_sharded(args, world, rank, local):
         ev0.record(stream)
         its = 0
         for _ in range(args.steps):
-            sc = pdist.orchestrate(shard, cfg, lam, dist.group.WORLD, collectives=args.collectives)
+            sc = pdist.orchestrate(shard, cfg, lam, dist.group.WORLD, collectives=_coll(args))
             its += sc.t
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -440,7 +445,7 @@ def run_c4_sharded(args, world, rank, local):
         for _ in range(args.steps):
             dic.drop_device()
             sh = pdist.GpuShard(prob, cfg, c0, k, device=dev)
-            sc = pdist.orchestrate(sh, cfg, lam, dist.group.WORLD, collectives=args.collectives)
+            sc = pdist.orchestrate(sh, cfg, lam, dist.group.WORLD, collectives=_coll(args))
             kept_l, x_l, rows, sc = sh.local_solution()
             sh.close()
             e_its += sc.t
@@ -459,7 +464,7 @@ def run_c4_sharded(args, world, rank, local):
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox, see DESIGN.md)",
             "config": {"workload": "c4", "n": n, "k": k, "iterations_per_step": its / args.steps,
                        "time_to_gap_s": el / args.steps, "parallelism": f"colshard{world}",
-                       "columns_per_rank": c1 - c0, "collectives_per_iteration": args.collectives,
+                       "columns_per_rank": c1 - c0, "collectives_per_iteration": _coll(args),
                        "l2": "dictionary shard larger than the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
                          "traffic": None, "peak_source": peak_src,

@@ -362,6 +362,21 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream);
  * world <= 64.  rank/world also select the slot; one_collective = 0 restores the
  * two-collective phase semantics. */
 int dscr_solver_set_collectives(dscr_solver* h, int rank, int world, int one_collective);
+/* Native exchange over peer memory (replaces the NCCL SUM of one-collective trips): each rank
+ * allocates dscr_peer_buffer_bytes(world, ldd) with dscr_peer_alloc (CUDA IPC handle out),
+ * the host all-gathers the handles, opens the peers' buffers with dscr_peer_open and passes
+ * every rank's base (its own included) to dscr_solver_set_peers.  The trip then runs
+ * K1; K2S; K3A; K3S; K3X_PUSH; K3X_REDUCE; K1R1; K2C; K3B with no host collective: PUSH stores
+ * this rank's SUM section into every peer (NVLink) and signals arrival flags (release, system
+ * scope), REDUCE waits for all flags (acquire) and sums the sections in rank order. */
+#define DSCR_PH_K3X_PUSH 19
+#define DSCR_PH_K3X_REDUCE 20
+size_t dscr_peer_buffer_bytes(int world, int ldd);
+int dscr_peer_alloc(size_t bytes, void** dptr, void* handle_out_64);
+int dscr_peer_open(const void* handle_64, void** dptr);
+int dscr_peer_close(void* dptr);
+int dscr_peer_free(void* dptr);
+int dscr_solver_set_peers(dscr_solver* h, int rank, int world, void* const* recv_bases, void* const* flag_bases);
 
 /* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */
 int dscr_comm_unique_id(void* id_out_128);

@@ -25,6 +25,7 @@ TR_T, TR_KEPT, TR_NNZ, TR_OBJ, TR_GAP, TR_RADIUS, TR_L, TR_NS, TR_UNITS, TR_SUPP
 (PH_SETUP_LOCAL, PH_SETUP_ADOPT, PH_SETUP_VEC, PH_SETUP_FINISH, PH_STATIC_LOCAL, PH_STATIC_FINISH) = range(6)
 PH_K1, PH_K1R, PH_K2, PH_K3A, PH_K3S, PH_K3B = range(10, 16)
 PH_K2S, PH_K1R1, PH_K2C = 16, 17, 18
+PH_K3X_PUSH, PH_K3X_REDUCE = 19, 20   # native exchange over peer memory
 OC_SLOT, OC_MAX_WORLD = 8, 64   # one-collective rank slots: 8 doubles per rank after the SUM vector
 CM_MAX, CM_SETUP, CM_SUM, CM_VEC = 0, 8, 16, 32
 
@@ -33,7 +34,8 @@ ABI_FUNCTIONS = (
     "dscr_prox_group", "dscr_test_sphere", "dscr_test_dome", "dscr_test_group",
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
-    "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_phase", "dscr_solver_set_collectives", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
+    "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_phase", "dscr_solver_set_collectives", "dscr_solver_set_peers", "dscr_peer_buffer_bytes",
+    "dscr_peer_alloc", "dscr_peer_open", "dscr_peer_close", "dscr_peer_free", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
     "dscr_batched_gemm_bf16", "dscr_batched_workspace_size", "dscr_batched_create", "dscr_batched_setup",
     "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_profile", "dscr_batched_destroy",
     "dscr_corr_exact_work_size", "dscr_corr_exact_bf16", "dscr_group_spectral_norms", "dscr_ingest_rows_f64",
@@ -131,6 +133,12 @@ def _declare(lib):
         "dscr_solver_profile": (i32, [vp, i32, vp, C.POINTER(C.c_float)]),
         "dscr_solver_phase": (i32, [vp, i32, vp]),
         "dscr_solver_set_collectives": (i32, [vp, i32, i32, i32]),
+        "dscr_solver_set_peers": (i32, [vp, i32, i32, vp, vp]),
+        "dscr_peer_buffer_bytes": (sz, [i32, i32]),
+        "dscr_peer_alloc": (i32, [sz, C.POINTER(vp), vp]),
+        "dscr_peer_open": (i32, [vp, C.POINTER(vp)]),
+        "dscr_peer_close": (i32, [vp]),
+        "dscr_peer_free": (i32, [vp]),
         "dscr_comm_unique_id": (i32, [vp]),
         "dscr_solver_set_comm": (i32, [vp, vp, i32, i32]),
         "dscr_batched_gemm_bf16": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]),

@@ -128,6 +128,8 @@ struct Params {
     int max_gsize;
     int min_cols;      // support columns per K3a split at least (MIN_COLS_PER_SPLIT)
     int onecoll;       // one collective per trip (dscr_solver_set_collectives)
+    void** peer_tab;   // peer exchange: [0, world) receive buffers, [64, 64 + world) flag arrays
+    int peer_len;      // doubles exchanged per rank (the one-collective SUM section)
     int oc_rank, oc_world;
     int k2v;           // K2 variant: 0 classic, 1 support before the test (K2S), 2 test + compaction (K2C)
     int k1_tile;       // K1 tiled path: row segments per column (0 = per-warp column path)
@@ -913,6 +915,72 @@ __global__ void __launch_bounds__(NT) k3s_pack(Params P) {
             if (k < 3) slots[i] = fresh ? P.comm[CM_MAX + k] : 0.0;
             else if (k >= 6 || !fresh) slots[i] = 0.0;
         }
+    }
+}
+
+// ---- native exchange over peer memory (NVLink / NVSwitch), replacing the NCCL SUM ----------
+// Every rank's buffer holds 64 uint64 arrival flags then two receive areas [2][world][len]
+// (parity of the exchange sequence number).  K3X_PUSH stores this rank's SUM section into its
+// slot of every peer's receive area (remote stores), and the last CTA publishes the sequence
+// number in every peer's flag for this rank (release, system scope).  K3X_REDUCE waits for
+// every rank's flag (acquire) and sums the received sections in rank order into `comm`, so all
+// ranks hold bit-identical sums.  A rank can be at most one exchange ahead of a peer (its next
+// REDUCE waits for the peer's next PUSH, issued after the peer's current REDUCE), so two
+// receive areas suffice.  Both kernels exit on the same stop / mode state as K3S, which every
+// rank computes identically.
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" :: "l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+
+__global__ void __launch_bounds__(NT) k3x_push(Params P, unsigned long long seq) {
+    __shared__ int s_flag;
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->mode == MODE_STATIC) return;
+    const int W = P.oc_world, len = P.peer_len;
+    const size_t off = (size_t)(seq & 1ull) * W * len + (size_t)P.oc_rank * len;
+    const double* src = P.comm + CM_SUM;
+    for (int i = blockIdx.x * NT + threadIdx.x; i < len; i += gridDim.x * NT) {
+        const double v = src[i];
+        for (int r = 0; r < W; ++r) static_cast<double*>(P.peer_tab[r])[off + i] = v;
+    }
+    __threadfence_system();
+    if (!last_block(P.tickets + 3, gridDim.x, &s_flag)) return;
+    if (threadIdx.x < W) {
+        __threadfence_system();
+        st_release_sys(static_cast<unsigned long long*>(P.peer_tab[64 + threadIdx.x]) + P.oc_rank, seq);
+    }
+}
+
+__global__ void __launch_bounds__(NT) k3x_reduce(Params P, unsigned long long seq) {
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->mode == MODE_STATIC) return;
+    const int W = P.oc_world, len = P.peer_len;
+    if (threadIdx.x < W) {   // every rank's section of this exchange has arrived
+        const unsigned long long* f = static_cast<const unsigned long long*>(P.peer_tab[64 + P.oc_rank]) + threadIdx.x;
+        const unsigned long long t0 = globaltimer();
+        while (ld_acquire_sys(f) < seq) {
+            if (globaltimer() - t0 > 30000000000ull) {   // 30 s watchdog: a peer never arrived
+                sc->status = DSCR_ENOCOMM;
+                sc->stop = DSCR_STOP_ERROR;
+                break;
+            }
+            __nanosleep(64);
+        }
+    }
+    __syncthreads();
+    const double* rb = static_cast<const double*>(P.peer_tab[P.oc_rank]) + (size_t)(seq & 1ull) * W * len;
+    double* dst = P.comm + CM_SUM;
+    for (int i = blockIdx.x * NT + threadIdx.x; i < len; i += gridDim.x * NT) {
+        double a = 0.0;
+        for (int r = 0; r < W; ++r) a += rb[(size_t)r * len + i];   // rank order: identical on every rank
+        dst[i] = a;
     }
 }
 
@@ -2275,6 +2343,8 @@ struct dscr_solver {
     int world = 1, rank = 0;
     void* comm = nullptr;
     bool pdl = false;   // chain kernels launched with programmatic dependent launch
+    void** peer_tab_dev = nullptr;   // device copy of the peer pointer table
+    unsigned long long peer_seq = 0;  // exchange sequence number (host side, one per exchange)
 };
 
 extern "C" const char* dscr_last_error(void) { return err_store().c_str(); }
@@ -2817,6 +2887,14 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
         case DSCR_PH_K3S:
             k3s_pack<<<std::max(1, std::min((P.ldd + NT - 1) / NT, 256)), NT, 0, s>>>(P);
             break;
+        case DSCR_PH_K3X_PUSH:
+        case DSCR_PH_K3X_REDUCE: {
+            if (!P.peer_tab || !P.onecoll) return set_inval("peer exchange needs dscr_solver_set_peers and one-collective mode");
+            const int grid = std::max(1, std::min((P.peer_len + NT - 1) / NT, 148));
+            if (phase == DSCR_PH_K3X_PUSH) k3x_push<<<grid, NT, 0, s>>>(P, ++h->peer_seq);
+            else k3x_reduce<<<grid, NT, 0, s>>>(P, h->peer_seq);
+            break;
+        }
         case DSCR_PH_K3B:
             k3b_finalize<<<g.G3b, NT, 0, s>>>(P);
             break;
@@ -2836,6 +2914,28 @@ int dscr_solver_set_collectives(dscr_solver* h, int rank, int world, int one_col
     h->P.oc_rank = rank;
     h->P.oc_world = world;
     return DSCR_OK;
+}
+
+int dscr_solver_set_peers(dscr_solver* h, int rank, int world, void* const* recv_bases, void* const* flag_bases) {
+    if (!h || !recv_bases || !flag_bases) return set_inval("null argument");
+    if (world < 1 || world > OC_MAX_WORLD || rank < 0 || rank >= world) return set_inval("rank / world out of range");
+    void* tab[128] = {};
+    for (int r = 0; r < world; ++r) { tab[r] = recv_bases[r]; tab[64 + r] = flag_bases[r]; }
+    if (!h->peer_tab_dev) CK(cudaMalloc(&h->peer_tab_dev, sizeof tab));
+    CK(cudaMemcpy(h->peer_tab_dev, tab, sizeof tab, cudaMemcpyHostToDevice));
+    h->P.peer_tab = h->peer_tab_dev;
+    h->P.peer_len = (CM_VEC - CM_SUM) + 2 * h->P.ldd + OC_SLOT * world;
+    h->P.onecoll = 1;
+    h->P.oc_rank = rank;
+    h->P.oc_world = world;
+    h->peer_seq = 0;
+    return DSCR_OK;
+}
+
+size_t dscr_peer_buffer_bytes(int world, int ldd) {
+    if (world < 1 || world > OC_MAX_WORLD || ldd < 1) return 0;
+    const size_t len = (size_t)(CM_VEC - CM_SUM) + 2 * (size_t)ldd + (size_t)OC_SLOT * world;
+    return 64 * 8 + 2 * (size_t)world * len * 8;
 }
 
 int dscr_solver_scalars(dscr_solver* h, void* stream, dscr_scalars* out) {
@@ -2872,6 +2972,7 @@ int dscr_solver_destroy(dscr_solver* h) {
     if (h->g_loop) cudaGraphDestroy(h->g_loop);
     if (h->g_setup) cudaGraphDestroy(h->g_setup);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    if (h->peer_tab_dev) cudaFree(h->peer_tab_dev);
     delete h;
     return DSCR_OK;
 }

@@ -51,7 +51,9 @@ def _allreduce(tensor, op, pg):
 
 def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collectives=2):
     """Run a sharded solve: setup exchange, then trips with two collectives (MAX after K1, SUM
-    after K3A) or, with ``collectives=1``, one SUM per trip (rank-slot gather of the MAX
+    after K3A), with ``collectives="peer"`` one exchange per trip through peer memory (device
+    stores into every peer's buffer + arrival flags, no host collective), or, with
+    ``collectives=1``, one SUM per trip (rank-slot gather of the MAX
     quantities and test extremes, residuals on the unreduced iterate, FIXUP trip when a rank
     screens a unit carrying a nonzero coefficient; SURVEY §7 hard part 2).  The dome test
     always uses two."""
@@ -61,8 +63,11 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collect
     comm = backend.comm
     world = dist.get_world_size(pg) if pg is not None else 1
     rank = dist.get_rank(pg) if pg is not None else 0
-    one = collectives == 1 and not (cfg.strategy == "dynamic" and cfg.test == "dome")
+    peer = collectives == "peer" and not (cfg.strategy == "dynamic" and cfg.test == "dome")
+    one = (collectives == 1 or peer) and not (cfg.strategy == "dynamic" and cfg.test == "dome")
     backend.set_collectives(rank, world, one)
+    if peer:
+        backend.setup_peers(pg, rank, world)
 
     backend.phase(nat.PH_SETUP_LOCAL)
     cand = comm[nat.CM_SETUP: nat.CM_SETUP + 3].clone()
@@ -109,7 +114,11 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collect
                 backend.phase(nat.PH_K2S)
                 backend.phase(nat.PH_K3A)
                 backend.phase(nat.PH_K3S)
-                _allreduce(sum_sec, SUM, pg)
+                if peer:   # the exchange runs on the devices: stores into peer memory, flags
+                    backend.phase(nat.PH_K3X_PUSH)
+                    backend.phase(nat.PH_K3X_REDUCE)
+                else:
+                    _allreduce(sum_sec, SUM, pg)
                 backend.phase(nat.PH_K1R1)
                 backend.phase(nat.PH_K2C)
             else:
@@ -147,6 +156,39 @@ class GpuShard:
     def set_collectives(self, rank, world, one):
         nat.check(self.eng.L.dscr_solver_set_collectives(self.eng.h, int(rank), int(world), 1 if one else 0))
 
+    def setup_peers(self, pg, rank, world):
+        """Native exchange: allocate this rank's peer buffer, all-gather the CUDA IPC handles,
+        open the peers' buffers and hand every rank's base to the solver."""
+        import torch.distributed as dist
+        if getattr(self, "peer_own", None) is not None and self.peer_key == (rank, world):
+            return                      # already connected (repeated solves on this shard)
+        L = self.eng.L
+        nbytes = int(L.dscr_peer_buffer_bytes(world, self.ldd))
+        if nbytes == 0:
+            nat.check(nat.DSCR_EINVAL, "peer buffer size")
+        own = C.c_void_p()
+        hd = (C.c_char * 64)()
+        nat.check(L.dscr_peer_alloc(nbytes, C.byref(own), hd))
+        self.peer_own = own
+        handles = [bytes(hd)]
+        if pg is not None and world > 1:
+            handles = [None] * world
+            dist.all_gather_object(handles, bytes(hd), group=pg)
+        bases, self.peer_opened = [], []
+        for r in range(world):
+            if r == rank:
+                bases.append(own.value)
+                continue
+            p = C.c_void_p()
+            nat.check(L.dscr_peer_open(C.create_string_buffer(handles[r], 64), C.byref(p)))
+            self.peer_opened.append(p)
+            bases.append(p.value)
+        recv = (C.c_void_p * world)(*[b + 512 for b in bases])
+        flags = (C.c_void_p * world)(*bases)
+        nat.check(L.dscr_solver_set_peers(self.eng.h, int(rank), int(world), recv, flags))
+        self.peer_pg = pg
+        self.peer_key = (rank, world)
+
     def phase(self, ph):
         nat.check(self.eng.L.dscr_solver_phase(self.eng.h, int(ph), self.eng.sptr))
         self.phase_calls += 1
@@ -163,6 +205,15 @@ class GpuShard:
         return eng.to_original(atoms), xs, eng.trace_rows(sc.t), sc
 
     def close(self):
+        import torch.distributed as dist
+        if getattr(self, "peer_own", None) is not None:
+            self.torch.cuda.synchronize()
+            if self.peer_pg is not None and dist.get_world_size(self.peer_pg) > 1:
+                dist.barrier(group=self.peer_pg)   # no peer still stores into this buffer
+            for p in self.peer_opened:
+                self.eng.L.dscr_peer_close(p)
+            self.eng.L.dscr_peer_free(self.peer_own)
+            self.peer_own = None
         self.eng.close()
 
 

@@ -50,6 +50,25 @@ class NumpyShard:
     def set_collectives(self, rank, world, one):
         self.rank, self.world, self.one = rank, world, bool(one)
 
+    def setup_peers(self, pg, rank, world):   # the device exchange is mirrored by a host SUM
+        self.peer_pg = pg
+
+    def _ph19(self):  # K3X_PUSH: nothing to stage on the host
+        pass
+
+    def _ph20(self):  # K3X_REDUCE: the SUM the device exchange computes (rank order)
+        if self.sc.stop:
+            return
+        import torch.distributed as dist
+        sec = self.comm[nat.CM_SUM: nat.CM_VEC + 2 * self.n + nat.OC_SLOT * self.world]
+        if self.peer_pg is not None:
+            parts = [torch.empty_like(sec) for _ in range(self.world)]
+            dist.all_gather(parts, sec.clone(), group=self.peer_pg)
+            acc = torch.zeros_like(sec)
+            for part in parts:
+                acc += part
+            sec.copy_(acc)
+
     # ---------------------------------------------------------------- phases
     def phase(self, ph):
         getattr(self, "_ph%d" % ph)()

@@ -90,7 +90,7 @@ def test_sharded_world2_matches_oracle(case, collectives):
     D, y, lam = _data(ratio)
     ref = so.solve(so.make_problem(D, y, lam), _cfg(algo, test, L0mode, gap_tol, D))
     traces = [g[1] for g in got]
-    if collectives == 1:   # kept counts are per rank in one-collective trips (summed by the host)
+    if collectives in (1, "peer"):   # kept counts are per rank in one-collective trips (summed by the host)
         assert [t[:1] + t[2:] for t in traces[0]] == [t[:1] + t[2:] for t in traces[1]], "ranks disagree"
         traces = [[(a[0], a[1] + b[1]) + a[2:] for a, b in zip(traces[0], traces[1])]] * 2
     assert traces[0] == traces[1], "ranks disagree on the trace"
@@ -108,6 +108,13 @@ def test_sharded_world2_matches_oracle(case, collectives):
     assert np.linalg.norm(x - ref.x_star) <= 1e-9 * max(1.0, np.linalg.norm(ref.x_star))
     np.testing.assert_allclose([t[3] for t in traces[0]], ref.trace["objective"], rtol=1e-10)
     assert [t[1] for t in traces[0]] == ref.trace["kept"]
+
+
+@pytest.mark.parametrize("case", [CASES[0], CASES[3], CASES[5]], ids=["fista-dst3", "ista-backtracking", "sparsa"])
+def test_sharded_world2_peer_exchange_phases(case):
+    """The peer-memory exchange phase order (K3S; K3X_PUSH; K3X_REDUCE; K1R1) with the host
+    mirror of the device exchange: same result as the oracle."""
+    test_sharded_world2_matches_oracle(case, "peer")
 
 
 def test_shard_ranges_cover_and_keep_groups_whole():

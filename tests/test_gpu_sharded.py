@@ -26,7 +26,7 @@ def _problem(ratio):
     return ds.Problem(ds.Dictionary(D), y, ratio * wl.lambda_star(D, y)), float(np.linalg.norm(D, 2))
 
 
-@pytest.mark.parametrize("collectives", [2, 1], ids=["two-coll", "one-coll"])
+@pytest.mark.parametrize("collectives", [2, 1, "peer"], ids=["two-coll", "one-coll", "peer-exchange"])
 @pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c)) for c in CASES])
 def test_split_phases_match_fused(case, collectives):
     algo, test, ratio = case
