@@ -80,3 +80,14 @@ def test_tiled_groups(wide):
     w = np.sqrt([g.size for g in groups])
     lam = 0.7 * max(np.linalg.norm(corr[g]) / wg for g, wg in zip(groups, w))
     _run(D, y, lam, groups=groups, test="gst3")
+
+
+def test_rows_beyond_shared_memory_theta_are_rejected():
+    """theta is staged in shared memory (8 bytes per row): a clear ValueError, not a launch failure."""
+    D = np.zeros((30000, 8))
+    D[np.arange(8), np.arange(8)] = 1.0
+    y = np.zeros(30000)
+    y[0] = 1.0
+    cfg = ds.SolverConfig(algorithm="ista", strategy="dynamic", test="dst3", max_iters=5, L0=1.0)
+    with pytest.raises(ValueError, match="n_rows too large"):
+        ds.run(ds.Problem(ds.Dictionary(D), y, 0.5), cfg)
