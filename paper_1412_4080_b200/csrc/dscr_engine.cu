@@ -713,7 +713,8 @@ __device__ __forceinline__ void k1_body_tile(const Params& P, int b, int G, doub
             // ---- group update: one warp per group (sizes <= GMAX), as the k1_body group path
             for (int t = warp; t < nb; t += NW) {
                 const int u = s_unit[t], a0 = s_uoff[t], g = s_uoff[t + 1] - a0;
-                const int j0 = P.gptr[u];
+                const int j0 = s_atom[a0];                 // first atom (already resolved)
+                const double gwu = P.gw[u];                // in flight with the x / u loads
                 const double* gc = s_part + a0;
                 for (int c0 = lane; c0 < g; c0 += 32) {
                     const int j = j0 + c0;
@@ -730,8 +731,8 @@ __device__ __forceinline__ void k1_body_tile(const Params& P, int b, int G, doub
                 if (lane == 0) {   // group soft threshold (dictionary.py:290-301), numpy reduceat order
                     const double nv = sqrt(np_segment_sum([&](int i) { double q = s_gv[warp][i - j0]; return q * q; }, j0, g));
                     const double nc = sqrt(np_segment_sum([&](int i) { double q = gc[i - j0]; return q * q; }, j0, g));
-                    if (nc > 0.0) { wmax = fmin(wmax, P.gw[u] / nc); wany = 1.0; }
-                    fac = (nv > 0.0) ? fmax(1.0 - thr * P.gw[u] / nv, 0.0) : 0.0;
+                    if (nc > 0.0) { wmax = fmin(wmax, gwu / nc); wany = 1.0; }
+                    fac = (nv > 0.0) ? fmax(1.0 - thr * gwu / nv, 0.0) : 0.0;
                 }
                 fac = __shfl_sync(0xffffffffu, fac, 0);
                 for (int c0 = lane; c0 < g; c0 += 32) {
