@@ -1912,7 +1912,7 @@ __global__ void __launch_bounds__(NT) k_init_scalars(Params P) {
 
 // out[j] = D[:, j] . v for all local columns (setup correlations, dictionary.py:94)
 template <typename T>
-__global__ void __launch_bounds__(NT) k_correlate(const T* __restrict__ D, int ldd, int n, int k,
+__global__ void __launch_bounds__(NT, 2) k_correlate(const T* __restrict__ D, int ldd, int n, int k,
                                                   const double* __restrict__ v, double* out,
                                                   const int* skip_flag, float l2_keep) {
     extern __shared__ double s_v[];
@@ -1923,9 +1923,19 @@ __global__ void __launch_bounds__(NT) k_correlate(const T* __restrict__ D, int l
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * NT) >> 5;
-    for (int j = gw; j < k; j += nwarps) {
-        double c = warp_dot<T, 2>(D + (size_t)j * ldd, n, s_v, lane, pol);
-        if (lane == 0) out[j] = c;
+    // 4 adjacent columns per warp (4 x U loads of 32 B in flight per lane, U as in K1)
+    for (int j0 = 4 * gw; j0 < k; j0 += 4 * nwarps) {
+        const T* cols[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) cols[c] = (j0 + c < k) ? D + (size_t)(j0 + c) * ldd : nullptr;
+        double cs[4];
+        warp_dots<T, 4, K1Cfg<T>::U>(cols, n, s_v, lane, pol, cs);
+        if (lane < 4 && j0 + lane < k) {
+            double c = cs[0];
+#pragma unroll
+            for (int q = 1; q < 4; ++q) if (lane == q) c = cs[q];
+            out[j0 + lane] = c;
+        }
     }
 }
 
@@ -2499,7 +2509,7 @@ static int launch_correlate(int dtype, const void* D, int ldd, int n, int k, con
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const size_t smem = (size_t)ldd * 8;
-    const int grid = std::max(1, std::min((k + NW - 1) / NW, sms * 4));
+    const int grid = std::max(1, std::min((k + 4 * NW - 1) / (4 * NW), sms * 2));
     int rc;
     switch (dtype) {
         case DSCR_F64:
