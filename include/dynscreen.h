@@ -380,7 +380,8 @@ int dscr_solver_set_peers(dscr_solver* h, int rank, int world, void* const* recv
 
 /* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */
 int dscr_comm_unique_id(void* id_out_128);
-/* Attach a communicator: collectives run between the per-rank kernels. */
+/* Single-rank communicator check (world 1 returns OK).  Multi-rank solves use dscr_solver_phase with
+ * host collectives or the peer-memory exchange (dscr_solver_set_peers); world > 1 returns DSCR_ENOCOMM. */
 int dscr_solver_set_comm(dscr_solver* h, const void* id_128, int rank, int world);
 
 #ifdef __cplusplus

@@ -90,6 +90,7 @@ extern "C" int dscr_solver_set_comm(dscr_solver* h, const void* id_128, int rank
     (void)id_128;
     if (!h) { dscr::err_store() = "null handle"; return DSCR_EINVAL; }
     if (world == 1 && rank == 0) return DSCR_OK;
-    dscr::err_store() = "multi-rank iteration path is driven by paper_1412_4080_b200.dist (torch.distributed NCCL)";
+    dscr::err_store() = "multi-rank trips are driven phase by phase (dscr_solver_phase): host collectives "
+                        "through paper_1412_4080_b200.dist, or the native peer-memory exchange (dscr_solver_set_peers)";
     return DSCR_ENOCOMM;
 }
