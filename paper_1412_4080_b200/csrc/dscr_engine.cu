@@ -1115,7 +1115,80 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     double tmax = -INFINITY, vmin = INFINITY;
     int wend = INT_MIN;
     const bool ident = (nu == P.n_units);   // nothing screened yet: identity list
-    for (int base = lo; base < hi; base += NT) {
+    // Lasso, identity list, more units than threads (c4: ~886 per CTA): 4 consecutive units per
+    // thread and round, so one round (two block scans) covers up to 4*NT units.  Lists and
+    // support entries come out in unit order, exactly as in the one-unit-per-thread rounds.
+    const bool wide = !GROUP && ident && !static_mode && (hi - lo) > NT;
+    for (int base = lo; wide && base < hi; base += 4 * NT) {
+        constexpr int Q = 4;
+        const int f0 = base + Q * threadIdx.x;
+        double cand[Q], xcv[Q], bvq[Q];
+        bool valid[Q], keep[Q], sup[Q];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            valid[q] = f0 + q < hi;
+            cand[q] = 0.0; xcv[q] = 0.0;
+            if (valid[q] && do_vec) { cand[q] = xn[f0 + q]; xcv[q] = xc[f0 + q]; }
+        }
+        int nk = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const bool masked = valid[q] && test_on && unit_test(P, sc, f0 + q);
+            if (valid[q] && do_list) P.mask[f0 + q] = masked ? 1 : 0;
+            keep[q] = valid[q] && !masked;
+            nk += keep[q] ? 1 : 0;
+            if (var == 2 && keep[q]) kept_atoms += 1.0;
+        }
+        if (do_list) {
+            int tot;
+            int pos = n_keep + block_exscan(nk, s_scan, &tot);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) if (keep[q]) actn[pos++] = f0 + q;
+            n_keep += tot;
+        }
+        if (!do_vec) continue;
+        int ns = 0;
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            bvq[q] = 0.0;
+            sup[q] = false;
+            if (!valid[q]) continue;
+            const int j = f0 + q;
+            const double c = cand[q];
+            if (keep[q]) {
+                double bv = 0.0;
+                if (algo == DSCR_FISTA) { bv = c + beta * (c - xcv[q]); un[j] = bv; }
+                else if (algo == DSCR_CP) { bv = c + phi * (c - xcv[q]); un[j] = bv; }
+                else if (algo == DSCR_SPARSA) { bv = c - xcv[q]; ssr += bv * bv; }
+                bvq[q] = bv;
+                sup[q] = (c != 0.0 || bv != 0.0);
+                pen += fabs(c);
+                nnz += (c != 0.0) ? 1.0 : 0.0;
+                kept_atoms += 1.0;
+            } else if (c != 0.0) {
+                dropped = 1.0;
+                sup[q] = keep_masked_a;
+            }
+            if (want_ext) {
+                const double v = unit_value(P, j);
+                vmin = fmin(vmin, v);
+                if (c != 0.0 || bvq[q] != 0.0) tmax = fmax(tmax, v);
+            }
+            ns += sup[q] ? 1 : 0;
+        }
+        int tot;
+        int w = n_sup + block_exscan(ns, s_scan, &tot);
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            if (!sup[q]) continue;
+            const int j = f0 + q;
+            if (keep[q]) { sidx[w] = j; sa[w] = cand[q]; sb[w] = bvq[q]; }
+            else { sidx[w] = ~j; sa[w] = cand[q]; sb[w] = 0.0; }
+            ++w;
+        }
+        n_sup += tot;
+    }
+    for (int base = lo; !wide && base < hi; base += NT) {
         if (!ident && base >= wend) wend = stage_window(off, P.G, base, s_off, &s_s0);   // uniform
         const int f = base + threadIdx.x;
         const bool valid = f < hi;

@@ -15,18 +15,18 @@ from paper_1412_4080_b200 import workloads as wl  # noqa: E402
 from oracle import screen_oracle as so  # noqa: E402
 
 
-def _run(D, y, lam, groups=None, dtype="f64", algo="fista", test="dst3", rtol=1e-9):
+def _run(D, y, lam, groups=None, dtype="f64", algo="fista", test="dst3", rtol=1e-9, gap_tol=1e-7):
     dic = ds.Dictionary(D, check_unit_norms=(dtype == "f64"), dtype=dtype)
     part = ds.GroupPartition.build(dic, groups) if groups is not None else None
     D64 = dic.as_float64()
     L = float(np.linalg.norm(D64, 2) ** 2 * (1 + 1e-9))
     cfg = ds.SolverConfig(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300,
-                          L0=L, gap_tol=1e-7)
+                          L0=L, gap_tol=gap_tol)
     res = ds.run(ds.Problem(dic, y, lam, part), cfg)
     op = so.make_problem(D64, y, lam, groups, None if part is None else part.weights,
                          None if part is None else part.spectral_norms)
     ref = so.solve(op, so.Config(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300,
-                                 L0=L, gap_tol=1e-7, norm_aware=(dtype != "f64")))
+                                 L0=L, gap_tol=gap_tol, norm_aware=(dtype != "f64")))
     # gap 1e-7: reached well before the objective stalls to the last bit (rel_tol 1e-300 stops on
     # bitwise-equal consecutive objectives, where 1-ulp summation differences decide)
     assert res.stop_reason == "gap"
@@ -91,3 +91,12 @@ def test_rows_beyond_shared_memory_theta_are_rejected():
     cfg = ds.SolverConfig(algorithm="ista", strategy="dynamic", test="dst3", max_iters=5, L0=1.0)
     with pytest.raises(ValueError, match="n_rows too large"):
         ds.run(ds.Problem(ds.Dictionary(D), y, 0.5), cfg)
+
+
+@pytest.mark.parametrize("algo", ["fista", "ista"])
+def test_wide_k2_rounds(algo):
+    """More than 256 active units per K2 CTA (80000 columns over 296 CTAs): the 4-units-per-
+    thread K2 rounds while the list is the identity, the classic rounds after screening."""
+    D = wl.correlated_dictionary(256, 80000, 21)
+    y, _ = wl.planted_observation(D, 21, nnz=8)
+    _run(D, y, 0.85 * wl.lambda_star(D, y), algo=algo, gap_tol=1e-6)
