@@ -298,7 +298,13 @@ __device__ void radius_epilogue(const Params& P, double bound, const double* the
 // Loads in flight per lane (U) and CTAs per SM of K1.  Measured: one CTA/SM with
 // U=4 for fp32 spills (255 regs) and halves the bandwidth; 2 CTAs/SM, C=4, U=1 is best.
 template <typename T> struct K1Cfg { static constexpr int U = 2, MINB = 2; };
-template <> struct K1Cfg<float> { static constexpr int U = 1, MINB = 2; };
+#ifndef K1_UF32
+#define K1_UF32 1
+#endif
+#ifndef K1_COLS
+#define K1_COLS 4
+#endif
+template <> struct K1Cfg<float> { static constexpr int U = K1_UF32, MINB = 2; };
 template <> struct K1Cfg<__nv_bfloat16> { static constexpr int U = 1, MINB = 2; };
 
 // K1 per-CTA work: correlations, update, per-CTA partials into P.p1[b]
@@ -348,7 +354,7 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     if (!GROUP) {
         // Lasso: each warp streams C columns at once (C*U 32-byte loads in flight per lane);
         // lane c applies the update of column c.
-        constexpr int C = 4;
+        constexpr int C = K1_COLS;
         // interleaved passes (identity list only): pass k of CTA b covers the 32 columns of
         // chunk b + k*G, so the columns streamed at any moment are adjacent in HBM
         const bool ilv = P.k1_ilv && ident;
