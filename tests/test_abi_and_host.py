@@ -197,3 +197,14 @@ def test_product_fails_loudly_without_gpu():
     p = ds.Problem(ds.Dictionary(np.eye(2)), np.array([1.0, 0.0]), 0.5)
     with pytest.raises(RuntimeError, match="CUDA device"):
         ds.run(p, ds.SolverConfig())
+
+
+def test_peer_buffer_size_is_flags_plus_two_receive_areas(lib):
+    """Host-only sizing of the native exchange buffer: 64 uint64 flags + [2][world][len] doubles,
+    len = SUM scalars + 2 * ldd residual partials + 8 slot doubles per rank."""
+    for world, ldd in ((1, 1024), (2, 8192), (8, 8192), (64, 16)):
+        length = (nat.CM_VEC - nat.CM_SUM) + 2 * ldd + nat.OC_SLOT * world
+        assert lib.dscr_peer_buffer_bytes(world, ldd) == 64 * 8 + 2 * world * length * 8
+    assert lib.dscr_peer_buffer_bytes(0, 1024) == 0
+    assert lib.dscr_peer_buffer_bytes(65, 1024) == 0
+    assert lib.dscr_peer_buffer_bytes(2, 0) == 0
