@@ -96,6 +96,7 @@ class BatchedEngine:
         self.k, self.n, self.b = dictionary.n_cols, n, b
         self.iterations, self.cap = int(iterations), int(cap)
         self.Dt = dictionary.device_data(self.device)                      # (K, ldd) bf16 bits
+        self.dic = dictionary
         ldy = (n + 63) // 64 * 64
         # upload Y as given (n x b) and transpose on the device into observation rows [b][ldy]
         self.Yd = torch.zeros((b, ldy), dtype=torch.float64, device=self.device)
@@ -130,6 +131,38 @@ class BatchedEngine:
         self.h = h
         self.bufs = nat.BatchedBuffers()
         nat.check(self.L.dscr_batched_get_buffers(self.h, C.byref(self.bufs)))
+
+    def dic_current(self):
+        """The dictionary's device copy is still the one in this engine's buffer (it is not when
+        the caller dropped the device copy, e.g. after updating the host data)."""
+        return any(t.data_ptr() == self.Dt.data_ptr() for t in self.dic._dev.values())
+
+    def load(self, Y, lam):
+        """New observations and lambdas of the same shape for another solve on this engine (the
+        workspace, the captured iteration graph and the device dictionary are reused)."""
+        torch = self.torch
+        lam = np.asarray(lam, dtype=np.float64).reshape(-1)
+        if lam.shape != (self.b,) or np.any(lam <= 0):
+            raise ValueError("need one strictly positive lam per observation")
+        n = self.n
+        if torch.is_tensor(Y):
+            if Y.dtype != torch.float64 or tuple(Y.shape) != (n, self.b) or Y.device.type != "cpu":
+                raise ValueError("observations must be a float64 host tensor of shape (n_rows, batch)")
+            rows = Y.T if Y.T.is_contiguous() else Y.T.contiguous()
+            self.Yd[:, :n].copy_(rows.to(self.device, non_blocking=rows.is_pinned()))
+            y_bytes = int(Y.numel() * 8)
+        else:
+            Y = np.asarray(Y, dtype=np.float64)
+            if Y.shape != (n, self.b):
+                raise ValueError("observations must have shape (n_rows, batch)")
+            Yh = torch.from_numpy(Y.T if Y.flags.f_contiguous else np.ascontiguousarray(Y))
+            if Y.flags.f_contiguous:
+                self.Yd[:, :n].copy_(Yh.to(self.device))
+            else:
+                self.Yd[:, :n].copy_(Yh.to(self.device).T)
+            y_bytes = int(Y.nbytes)
+        self.lamd.copy_(torch.from_numpy(lam))
+        self.h2d_bytes = int(y_bytes + lam.nbytes)
 
     def setup(self):
         nat.check(self.L.dscr_batched_setup(self.h, self.sptr))
@@ -204,3 +237,58 @@ def solve_batched(dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, 
         return eng.result(ev0.elapsed_time(ev1) / 1e3)
     finally:
         eng.close()
+
+
+class BatchedSolver:
+    """Repeated batched solves on one dictionary (the dictionary-learning inner loop): the
+    engine -- workspace, captured iteration graph, device dictionary -- is built on the first
+    solve and reused while the batch shape stays the same.
+
+        solver = BatchedSolver(dictionary, L, iterations=100, test="dst3")
+        for Y, lam in batches:
+            res = solver.solve(Y, lam)
+        solver.close()
+    """
+
+    def __init__(self, dictionary, L, iterations=100, test="dst3", splits=1, cap=1024, device=None, fused=True):
+        self.args = (dictionary, L, iterations, test, splits, cap, device, fused)
+        self.eng = None
+
+    def solve(self, Y, lam, dictionary=None):
+        """Solve one batch; `dictionary` (same shape and dtype) replaces the dictionary first,
+        e.g. after a dictionary-learning update (uploaded into the engine's buffer)."""
+        d0, L, iterations, test, splits, cap, device, fused = self.args
+        if dictionary is not None:
+            if (dictionary.n_rows, dictionary.n_cols, dictionary.dtype) != (d0.n_rows, d0.n_cols, d0.dtype):
+                raise ValueError("a replacement dictionary must keep the shape and dtype")
+            self.args = (dictionary,) + self.args[1:]
+        dictionary = self.args[0]
+        shape = tuple(Y.shape)
+        if self.eng is not None and (self.eng.n, self.eng.b) == shape:
+            if self.eng.dic is not dictionary or not self.eng.dic_current():
+                prev = self.eng.dic                                      # its cache must not alias the buffer
+                for key in [k for k, t in prev._dev.items() if t.data_ptr() == self.eng.Dt.data_ptr()]:
+                    del prev._dev[key]
+                fresh = dictionary.device_data(self.eng.device)          # upload (H2D)
+                self.eng.Dt.copy_(fresh)
+                dictionary.drop_device()
+                dictionary._dev[(str(self.eng.device), None)] = self.eng.Dt   # the engine's buffer is the copy
+                self.eng.dic = dictionary
+            self.eng.load(Y, lam)
+        else:
+            self.close()
+            self.eng = BatchedEngine(dictionary, Y, lam, L, iterations, test, splits, cap, device, fused)
+        eng = self.eng
+        torch = eng.torch
+        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ev0.record(eng.stream)
+        eng.setup()
+        eng.run()
+        ev1.record(eng.stream)
+        eng.stream.synchronize()
+        return eng.result(ev0.elapsed_time(ev1) / 1e3)
+
+    def close(self):
+        if self.eng is not None:
+            self.eng.close()
+            self.eng = None

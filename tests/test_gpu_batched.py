@@ -258,3 +258,24 @@ def test_batched_max_rows_matches_oracle():
         assert abs(res.objective[j] - ref.final_objective) <= 1e-4 * ref.final_objective
         x = res.x_dense(j, 1024)
         assert np.linalg.norm(x - ref.x_star) <= 1e-3 * max(np.linalg.norm(ref.x_star), 1e-12)
+
+
+def test_batched_solver_reuses_engine_across_batches_and_dictionaries():
+    """BatchedSolver (engine, workspace and iteration graph reused) == one-shot solve_batched, for
+    a second batch on the same dictionary and after swapping in another dictionary."""
+    from paper_1412_4080_b200.batched import BatchedSolver
+    w1, dic1, _, L1 = _batch_problem(128, 1024, 256, 0.5, seed=5)
+    w2, _, _, _ = _batch_problem(128, 1024, 256, 0.7, seed=6)
+    w3, dic3, _, _ = _batch_problem(128, 1024, 256, 0.6, seed=7)
+    solver = BatchedSolver(dic1, L1, iterations=40, test="dst3")
+    try:
+        runs = [solver.solve(w1.y, w1.lam), solver.solve(w2.y, w2.lam), solver.solve(w3.y, w3.lam, dictionary=dic3)]
+    finally:
+        solver.close()
+    refs = [solve_batched(dic1, w1.y, w1.lam, L1, iterations=40, test="dst3"),
+            solve_batched(dic1, w2.y, w2.lam, L1, iterations=40, test="dst3"),
+            solve_batched(dic3, w3.y, w3.lam, L1, iterations=40, test="dst3")]
+    for got, ref in zip(runs, refs):
+        assert np.array_equal(got.objective, ref.objective)
+        assert np.array_equal(got.kept, ref.kept) and np.array_equal(got.x_ptr, ref.x_ptr)
+        assert np.array_equal(got.x_indices, ref.x_indices) and np.array_equal(got.x_values, ref.x_values)
