@@ -74,9 +74,11 @@ def test_nccl_single_rank_group():
         cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=3000,
                               rel_tol=1e-300, L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9)
         a = ds.run(p, cfg)
-        b = pdist.run_sharded(p, cfg, pg=dist.group.WORLD)
-        assert a.iterations == b.iterations
-        np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+        for coll in (2, 1, "peer"):   # NCCL MAX + SUM, one NCCL SUM (slot gather), peer exchange
+            b = pdist.run_sharded(p, cfg, pg=dist.group.WORLD, collectives=coll)
+            assert a.iterations == b.iterations
+            np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+            assert b.trace.kept == a.trace.kept
     finally:
         dist.destroy_process_group()
 
