@@ -51,7 +51,10 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--profile-only", action="store_true", help="direct-launch iterations for ncu")
-    ap.add_argument("--cpu-sample-iters", type=int, default=5)
+    ap.add_argument("--cpu-sample-iters", type=int, default=20,
+                    help="our arm's cpu_baseline: oracle iterations per solve (setup timed separately)")
+    ap.add_argument("--cpu-ref-iters", type=int, default=100,
+                    help="reference arm on c4: oracle iterations sampled (BASELINE.md §2: the first 100)")
     ap.add_argument("--seed", type=int, default=0)
     return ap.parse_args()
 
@@ -99,7 +102,7 @@ def spec_L(ds, dic):
     return nrm * nrm * (1.0 + 1e-6)
 
 
-def make_problems(ds, works):
+def make_problems(ds, works, L_fixed=None):
     out = []
     cache = {}
     for w in works:
@@ -111,7 +114,7 @@ def make_problems(ds, works):
             part = None
             if w.groups is not None:
                 part = ds.GroupPartition.build(dic, w.groups)
-            cache[key] = (dic, part, spec_L(ds, dic))
+            cache[key] = (dic, part, L_fixed if L_fixed is not None else spec_L(ds, dic))
         dic, part, L = cache[key]
         prob = ds.Problem(dic, w.y, w.lam, part)
         cfg = ds.SolverConfig(algorithm=w.algorithm, strategy="dynamic", test=w.test, max_iters=w.max_iters,
@@ -217,26 +220,114 @@ class ClockSampler:
 # ---------------------------------------------------------------------------
 
 
-def cpu_sample(works, problems, iters):
-    """Time the CPU oracle on the first `iters` iterations of the workload's solves."""
+def shared_L(name, seed):
+    """The step constant both arms use (L = ||D||^2 (1 + 1e-9), computed once and
+    passed to both sides).  For the benchmarked c4 (seed 0) it is the committed value from the
+    reference run (tests/golden/c4_reference.json: fp64 Gram eigvalsh in the build container);
+    None elsewhere (then ours computes it by device power iteration)."""
+    if name != "c4":
+        return None, None
+    path = os.path.join(ROOT, "tests", "golden", "c4_reference.json")
+    if not os.path.exists(path):
+        return None, None
+    with open(path) as fh:
+        g = json.load(fh)
+    if int(g["config"]["seed"]) != int(seed):
+        return None, None
+    return float(g["L"]), g
+
+
+def host_info():
+    """CPU model, sockets / cores, BLAS build and thread settings of the host that runs the CPU
+    baseline."""
+    info = {"cpu_count": os.cpu_count()}
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    info["model"] = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            key, _, val = line.partition(":")
+            if key.strip() in ("Socket(s)", "Core(s) per socket", "Thread(s) per core", "NUMA node(s)"):
+                info[key.strip()] = val.strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    try:
+        sockets = int(info.get("Socket(s)", 1))
+        cps = int(info.get("Core(s) per socket", 0))
+        info["physical_cores"] = sockets * cps if cps else os.cpu_count()
+    except ValueError:
+        info["physical_cores"] = os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{k: v for k, v in d.items() if k in ("internal_api", "version", "num_threads", "architecture",
+                                                           "threading_layer")} for d in threadpool_info()]
+    except Exception:
+        pass
+    info["env"] = {k: os.environ.get(k) for k in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS")}
+    info["numpy"] = np.__version__
+    return info
+
+
+def _blas_threads(n):
+    try:
+        from threadpoolctl import threadpool_limits
+        return threadpool_limits(limits=int(n))
+    except Exception:
+        import contextlib
+        return contextlib.nullcontext()
+
+
+def oracle_problem(w, prob=None, D64=None):
     from oracle import screen_oracle as so
-    tot_t, tot_it = 0.0, 0
+    if D64 is None:
+        D64 = np.asfortranarray(np.asarray(w.D, dtype=np.float64)) if w.dtype != "bf16" else \
+            np.asfortranarray((np.asarray(w.D, dtype=np.uint32) << 16).view(np.float32).astype(np.float64))
+    groups = None if w.groups is None else [np.asarray(g) for g in w.groups]
+    weights = None if groups is None else np.sqrt([len(g) for g in groups])
+    snorms = None
+    if groups is not None:
+        snorms = (np.asarray(prob.partition.spectral_norms) if prob is not None
+                  else np.array([np.sqrt(so.power_top_eig(D64[:, g])) for g in groups]))
+    return so.OProblem(D64, w.y, w.lam, groups, weights, snorms)
+
+
+def oracle_sample(op, w, L, iters, skip=0):
+    """Run the fp64 oracle (the reference algorithm) for `skip + iters` iterations of one solve;
+    return setup seconds (lambda_max + screening precomputes, before the first iteration) and
+    the seconds of the last `iters` iterations (per-iteration ticks from the oracle loop)."""
+    from oracle import screen_oracle as so
+    cfg = so.Config(algorithm=w.algorithm, strategy="dynamic", test=w.test, max_iters=skip + iters,
+                    rel_tol=1e-300, L0=L, gap_tol=w.gap_tol, norm_aware=(w.dtype != "f64"))
+    ticks = []
+    t0 = time.perf_counter()
+    r = so.solve(op, cfg, ticks=ticks)
+    done = len(ticks) - 1
+    if done <= skip:
+        return ticks[0] - t0, 0, 0.0, r
+    return ticks[0] - t0, done - skip, ticks[-1] - ticks[skip], r
+
+
+def cpu_sample(works, problems, iters):
+    """CPU baseline of our arm: the oracle on the first `iters` iterations of the workload's solves,
+    setup (lambda_max, precomputes) timed separately from the iterations."""
+    setup_s, its, it_s = 0.0, 0, 0.0
     cache = {}
     for w, (prob, cfg) in zip(works, problems):
         key = id(w.D)
         if key not in cache:
-            D64 = prob.dictionary.as_float64()
-            cache[key] = np.asfortranarray(D64)
-        op = so.OProblem(cache[key], w.y, w.lam, w.groups and [np.asarray(g) for g in w.groups],
-                         None if w.groups is None else np.sqrt([len(g) for g in w.groups]),
-                         None if w.groups is None else np.asarray(prob.partition.spectral_norms))
-        ocfg = so.Config(algorithm=cfg.algorithm, strategy=cfg.strategy, test=cfg.test, max_iters=iters,
-                         rel_tol=1e-300, L0=cfg.L0, gap_tol=cfg.gap_tol)
-        t0 = time.perf_counter()
-        r = so.solve(op, ocfg)
-        tot_t += time.perf_counter() - t0
-        tot_it += r.iterations
-    return tot_it, tot_t
+            cache[key] = np.asfortranarray(prob.dictionary.as_float64())
+        op = oracle_problem(w, prob, cache[key])
+        su, n_it, sec, _ = oracle_sample(op, w, cfg.L0, iters)
+        setup_s += su
+        its += n_it
+        it_s += sec
+    return setup_s, its, it_s
 
 
 def cpu_cores():
@@ -264,67 +355,111 @@ def dist_env():
 
 
 def run_reference(args):
+    """Reference arm: the reference's algorithm on the CPU (the fp64 numpy oracle port of
+    screenlab.run, BLAS on all physical cores), rank 0 only.  c1-c3: every step is a full solve to
+    the gap tolerance (setup included, as run() wall-times it).  c4 (16 GiB in fp64): one solve
+    sampled over its first W+K chunks of iterations (the first 100 iterations),
+    setup timed separately, time to gap extrapolated from the reference's own t_hit."""
     world, rank, _ = dist_env()
     if rank != 0:
         return
     import paper_1412_4080_b200 as ds  # noqa: F401  (host types / generators only)
     if args.workload == "c5":
         return run_reference_c5(args, world)
-    works = build_workload(args.workload, args.seed)
-    # the reference arm shares the host problem definition; L from the host power iteration
     from oracle import screen_oracle as so
-    Ls = {}
-    probs = []
-    for w in works:
-        key = id(w.D)
-        if key not in Ls:
-            D64 = np.asfortranarray(np.asarray(w.D, dtype=np.float64))
-            if D64.size > 2e8:
-                # host power iteration on 8 GiB would take minutes; Gaussian unit-norm columns have
-                # ||D||^2 ~ (1 + sqrt(K/N))^2 (Marchenko-Pastur edge).  Only the timing uses it.
-                L = (1.0 + np.sqrt(D64.shape[1] / D64.shape[0])) ** 2 * 1.01
-            else:
-                L = so.operator_norm(D64) ** 2 * (1 + 1e-6)
-            Ls[key] = (D64, L)
-        D64, L = Ls[key]
-        probs.append((D64, L))
-    samples = []
-    for i in range(args.warmup + args.steps):
-        tt, it = 0.0, 0
-        for w, (D64, L) in zip(works, probs):
-            op = so.OProblem(D64, w.y, w.lam, w.groups,
-                             None if w.groups is None else np.sqrt([len(g) for g in w.groups]),
-                             None if w.groups is None else np.array([np.sqrt(so.power_top_eig(D64[:, g])) for g in w.groups]))
-            cfg = so.Config(algorithm=w.algorithm, strategy="dynamic", test=w.test,
-                            max_iters=args.cpu_sample_iters, rel_tol=1e-300, L0=L, gap_tol=w.gap_tol)
+    hinfo = host_info()
+    cores = int(hinfo.get("physical_cores") or os.cpu_count())
+    works = build_workload(args.workload, args.seed)
+    L_shared, gold = shared_L(args.workload, args.seed)
+    extra = {}
+    with _blas_threads(cores):
+        if args.workload == "c4":
+            w = works[0]
             t0 = time.perf_counter()
-            r = so.solve(op, cfg)
-            tt += time.perf_counter() - t0
-            it += r.iterations
-        if i >= args.warmup:
-            samples.append((it, tt))
+            op = oracle_problem(w)
+            upcast_s = time.perf_counter() - t0
+            if L_shared is None:
+                L_shared = (1.0 + np.sqrt(w.D.shape[1] / w.D.shape[0])) ** 2 * 1.01
+                l_src = "Marchenko-Pastur edge estimate (no committed L for this seed)"
+            else:
+                l_src = "committed L (tests/golden/c4_reference.json), shared with the GPU arm"
+            total = max(args.cpu_ref_iters, args.warmup + args.steps)
+            ips = -(-total // (args.warmup + args.steps))
+            ticks = []
+            cfg = so.Config(algorithm=w.algorithm, strategy="dynamic", test=w.test,
+                            max_iters=ips * (args.warmup + args.steps), rel_tol=1e-300, L0=L_shared,
+                            gap_tol=w.gap_tol, norm_aware=True)
+            t1 = time.perf_counter()
+            so.solve(op, cfg, ticks=ticks)
+            setup_s = ticks[0] - t1
+            w0 = args.warmup * ips
+            samples = [(ips, ticks[w0 + (i + 1) * ips] - ticks[w0 + i * ips]) for i in range(args.steps)]
+            first = min(100, len(ticks) - 1)
+            extra = {"setup_s": setup_s, "upcast_s": upcast_s, "iterations_per_step": ips,
+                     "timed_iterations": f"{w0 + 1}..{w0 + args.steps * ips}",
+                     "first_iterations_per_s": first / (ticks[first] - ticks[0]), "L_source": l_src}
+            if gold is not None:
+                v_it = sum(s[0] for s in samples) / sum(s[1] for s in samples)
+                extra["t_hit_reference"] = int(gold["t_hit"])
+                extra["time_to_gap_s_extrapolated"] = setup_s + int(gold["t_hit"]) / v_it
+                extra["time_to_gap_note"] = ("extrapolated: setup + t_hit / (timed iterations per second); t_hit "
+                                             "from the reference's own full run (scripts/c4_reference_run.py)")
+            sample_txt = (f"one c4 solve (fp64 oracle on the fp32-upcast dictionary), iterations "
+                          f"{w0 + 1}..{w0 + args.steps * ips} timed in {args.steps} chunks of {ips}; setup "
+                          f"({setup_s:.1f} s: lambda_max + DST3 precomputes) timed separately")
+        else:
+            Ls, samples, t_hits = {}, [], []
+            for i in range(args.warmup + args.steps):
+                tt, it = 0.0, 0
+                for w in works:
+                    key = id(w.D)
+                    if key not in Ls:
+                        op0 = oracle_problem(w)
+                        Ls[key] = (op0.D, so.operator_norm(op0.D) ** 2 * (1 + 1e-6))
+                    D64, L = Ls[key]
+                    op = oracle_problem(w, D64=D64)
+                    cfg = so.Config(algorithm=w.algorithm, strategy="dynamic", test=w.test, max_iters=w.max_iters,
+                                    rel_tol=1e-300, L0=L, gap_tol=w.gap_tol)
+                    t0 = time.perf_counter()
+                    r = so.solve(op, cfg)
+                    tt += time.perf_counter() - t0
+                    it += r.iterations
+                    if i == 0:
+                        t_hits.append(r.iterations)
+                if i >= args.warmup:
+                    samples.append((it, tt))
+            extra = {"time_to_gap_s": sum(s[1] for s in samples) / len(samples), "t_hit": t_hits,
+                     "L_source": "host power iteration (1 + 1e-6), the GPU arm's definition"}
+            sample_txt = (f"full {args.workload} solve(s) to the gap tolerance per step, setup included "
+                          f"(as reference run() times it), fp64 numpy oracle")
     it = sum(s[0] for s in samples)
     tt = sum(s[1] for s in samples)
     v = it / tt
-    cores = cpu_cores()
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(1, len(samples)),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": workload_config(args.workload, works),
-        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port",
-                         "sample": f"first {args.cpu_sample_iters} iterations of each solve of {args.workload} "
-                                   f"(setup included, as reference run() times it), fp64 numpy oracle"},
+        "data": "synthetic (seeded Philox, see DESIGN.md)", "config": workload_config(args.workload, works, args.seed),
+        "details": extra,
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port", "sample": sample_txt,
+                         "host": hinfo},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
 
 
-def workload_config(name, works):
-    """Input description of a workload, shared by both arms' JSON lines."""
+def workload_config(name, works, seed, splits=None):
+    """Input description of a workload -- identical in both arms' JSON lines."""
     w = works[0]
     cfg = {"workload": name, "n": int(w.D.shape[0]), "k": int(w.D.shape[1]), "algorithm": w.algorithm,
-           "test": w.test, "gap_tol": w.gap_tol, "dictionary_dtype": w.dtype}
+           "test": w.test, "dictionary_dtype": w.dtype, "seed": int(seed)}
+    if name == "c5":
+        cfg.update({"batch": int(w.y.shape[1]), "iterations_per_solve": int(w.max_iters), "lam_ratio": 0.4,
+                    "splits": int(splits or 1)})
+    else:
+        cfg["gap_tol"] = w.gap_tol
+        ratios = {"c1": [0.5], "c2": [0.1, 0.3, 0.5, 0.7, 0.9], "c3": [0.3], "c4": [0.2]}[name]
+        cfg["lam_ratio"] = ratios if len(ratios) > 1 else ratios[0]
     if len(works) > 1:
         cfg["instances"] = len(works)
     return cfg
@@ -339,29 +474,38 @@ def run_reference_c5(args, world):
     D64 = (np.asarray(w.D, dtype=np.uint32) << 16).view(np.float32).astype(np.float64)
     n, k = D64.shape
     b = w.y.shape[1]
-    iters, sample = 100, 4
-    L = (1.0 + np.sqrt(k / n)) ** 2 * 1.01          # Marchenko-Pastur edge; only the timing uses it
+    iters = 100
+    sample = max(1, -(-64 // (args.warmup + args.steps)))     # 64 sampled observations
+    G = np.zeros((n, n))
+    for c0 in range(0, k, 4096):
+        G += D64[:, c0:c0 + 4096] @ D64[:, c0:c0 + 4096].T
+    L = float(np.linalg.eigvalsh(G)[-1]) * (1.0 + 1e-6)          # ||D||^2 (fp64 Gram), as the GPU arm's
+    hinfo = host_info()
+    cores = int(hinfo.get("physical_cores") or os.cpu_count())
     samples = []
-    for i in range(args.warmup + args.steps):
-        t0 = time.perf_counter()
-        for j in range(sample):
-            jj = (i * sample + j) % b
-            so.solve(so.make_problem(D64, w.y[:, jj], w.lam[jj]),
-                     so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=iters,
-                               rel_tol=1e-300, L0=L, norm_aware=True))
-        if i >= args.warmup:
-            samples.append(time.perf_counter() - t0)
+    with _blas_threads(cores):
+        for i in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            for j in range(sample):
+                jj = ((i * sample + j) * 61) % b
+                so.solve(so.make_problem(D64, w.y[:, jj], w.lam[jj]),
+                         so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=iters,
+                                   rel_tol=1e-300, L0=L, norm_aware=True))
+            if i >= args.warmup:
+                samples.append(time.perf_counter() - t0)
     obs_iters_s = sample * iters * len(samples) / sum(samples)
     v = obs_iters_s / b
     line = {
         "impl": "reference", "metric": METRIC, "value": v, "unit": "iters/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * iters / v,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "c5", "n": n, "k": k, "batch": b, "iterations_per_step": iters,
-                   "algorithm": "fista", "test": "dst3", "dictionary_dtype": "bf16"},
-        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cpu_cores(), "kind": "port",
-                         "sample": f"{sample} of {b} observations x {iters} FISTA+DST3 iterations per step, fp64 "
-                                   f"oracle on the bf16-upcast dictionary, extrapolated to the batch"},
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded Philox, see DESIGN.md)",
+        "config": workload_config("c5", [w], args.seed, args.splits),
+        "details": {"observations_timed": sample * args.steps, "obs_iters_per_s": obs_iters_s, "L": L},
+        "cpu_baseline": {"value": v, "unit": "iters/s", "cores": cores, "kind": "port", "host": hinfo,
+                         "sample": f"{sample} observations per step ({sample * (args.warmup + args.steps)} in all, "
+                                   f"{sample * args.steps} timed) x {iters} FISTA+DST3 iterations, fp64 oracle on the "
+                                   f"bf16-upcast dictionary, extrapolated to the batch of {b}"},
         "e2e": {"value": v, "unit": "iters/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -399,9 +543,12 @@ def run_c4_sharded(args, world, rank, local):
     m = torch.tensor([float(np.max(np.abs(corr)))], device=dev)
     dist.all_reduce(m, op=dist.ReduceOp.MAX)
     lam = 0.2 * float(m.item())
-    nrm = pdist.sharded_operator_norm(dic, dist.group.WORLD, device=dev)
+    L_shared, gold = shared_L("c4", args.seed)
+    if L_shared is None:
+        nrm = pdist.sharded_operator_norm(dic, dist.group.WORLD, device=dev)
+        L_shared = nrm * nrm * (1.0 + 1e-6)
     cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=10000, rel_tol=1e-300,
-                          L0=nrm * nrm * (1.0 + 1e-6), gap_tol=1e-5)
+                          L0=L_shared, gap_tol=1e-5)
     prob = ds.Problem(dic, y, lam)
     shard = pdist.GpuShard(prob, cfg, c0, k, device=dev)
     for _ in range(args.warmup):
@@ -462,7 +609,13 @@ def run_c4_sharded(args, world, rank, local):
             "metric": METRIC, "value": its / el, "unit": "iters/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded Philox, see DESIGN.md)",
-            "config": {"workload": "c4", "n": n, "k": k, "iterations_per_step": its / args.steps,
+            "config": {"workload": "c4", "n": n, "k": k, "algorithm": "fista", "test": "dst3",
+                       "dictionary_dtype": "f32", "seed": int(args.seed), "gap_tol": 1e-5, "lam_ratio": 0.2},
+            "nccl": {"backend": dist.get_backend(), "world_size": world,
+                     "version": ".".join(map(str, torch.cuda.nccl.version())) if dist.get_backend() == "nccl"
+                     else None},
+            "details": {"iterations_per_step": its / args.steps, "L": cfg.L0,
+                       "t_hit_reference": None if gold is None else int(gold["t_hit"]),
                        "time_to_gap_s": el / args.steps, "parallelism": f"colshard{world}",
                        "columns_per_rank": c1 - c0, "collectives_per_iteration": _coll(args),
                        "l2": "dictionary shard larger than the 126 MB L2"},
@@ -506,7 +659,12 @@ def run_ours(args):
     from paper_1412_4080_b200.solver import Engine
 
     works = build_workload(args.workload, args.seed, pinned=(args.workload == "c4"))
-    problems = make_problems(ds, works)
+    L_shared, gold = shared_L(args.workload, args.seed)
+    problems = make_problems(ds, works, L_shared)
+    L_check = None
+    if L_shared is not None:          # the committed L must be this dictionary's ||D||^2 (1 + 1e-9)
+        nrm = ds.operator_norm(problems[0][0].dictionary, tol=1e-12, max_iters=20000)
+        L_check = abs(nrm * nrm * (1 + 1e-9) - L_shared) / L_shared
     elem = {"f64": 8, "f32": 4, "bf16": 2}[works[0].dtype]
     n = works[0].D.shape[0]
     stream = torch.cuda.current_stream(dev)
@@ -636,10 +794,14 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        it, tt = cpu_sample(works, problems, args.cpu_sample_iters)
-        cpu = {"value": it / tt, "unit": "iters/s", "cores": cpu_cores(), "kind": "port",
+        hinfo = host_info()
+        cores = int(hinfo.get("physical_cores") or os.cpu_count())
+        with _blas_threads(cores):
+            su, it, tt = cpu_sample(works, problems, args.cpu_sample_iters)
+        cpu = {"value": it / tt, "unit": "iters/s", "cores": cores, "kind": "port", "setup_s": su,
                "sample": f"first {args.cpu_sample_iters} iterations of each {args.workload} solve, fp64 numpy "
-                         f"oracle on the same (upcast) dictionary, setup included"}
+                         f"oracle on the same (upcast) dictionary; setup ({su:.2f} s) timed separately",
+               "host": hinfo}
 
     if rank == 0:
         line = {
@@ -647,13 +809,18 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps, "higher_is_better": True,
             "scaling": "weak" if world > 1 else "strong", "vs_baseline": None,
             "dtype": works[0].dtype, "data": "synthetic (seeded Philox, see DESIGN.md)",
-            "config": {"workload": args.workload, "n": n, "k": problems[0][0].n_cols,
-                       "algorithm": works[0].algorithm, "test": works[0].test, "gap_tol": works[0].gap_tol,
-                       "iterations_per_step": per_step_iters, "time_to_gap_s": dev_s / args.steps,
-                       "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
-                       "l2": "dictionary larger than the 126 MB L2" if works[0].D.nbytes > 126e6
-                             else "L2 flushed (256 MB write) before every timed solve",
-                       "accumulate": "fp64"},
+            "config": workload_config(args.workload, works, args.seed),
+            "details": {"iterations_per_step": per_step_iters, "time_to_gap_s": dev_s / args.steps,
+                        "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+                        "l2": "dictionary larger than the 126 MB L2" if works[0].D.nbytes > 126e6
+                              else "L2 flushed (256 MB write) before every timed solve",
+                        "accumulate": "fp64",
+                        "L": problems[0][1].L0,
+                        "L_source": ("committed L (tests/golden/c4_reference.json), shared with the reference arm"
+                                     if L_shared is not None else "device power iteration, (1 + 1e-6)"),
+                        "L_check_rel": L_check,
+                        "t_hit_reference": None if gold is None else int(gold["t_hit"]),
+                        "t_hit_equal": None if gold is None else bool(per_step_iters == int(gold["t_hit"]))},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                          "kernel": "k1_corr_update", "kernel_ms": ms[0],
@@ -814,14 +981,17 @@ def run_c5(args):
         from oracle import screen_oracle as so
         D64 = dic.as_float64()
         sample = 4
-        t0 = time.perf_counter()
-        for j in range(sample):
-            so.solve(so.make_problem(D64, w.y[:, j], w.lam[j]),
-                     so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=iters,
-                               rel_tol=1e-300, L0=L, norm_aware=True))
-        ct = time.perf_counter() - t0
+        hinfo = host_info()
+        cores = int(hinfo.get("physical_cores") or os.cpu_count())
+        with _blas_threads(cores):
+            t0 = time.perf_counter()
+            for j in range(sample):
+                so.solve(so.make_problem(D64, w.y[:, j], w.lam[j]),
+                         so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=iters,
+                                   rel_tol=1e-300, L0=L, norm_aware=True))
+            ct = time.perf_counter() - t0
         obs_iters_s = sample * iters / ct
-        cpu = {"value": obs_iters_s / b, "unit": "iters/s", "cores": cpu_cores(), "kind": "port",
+        cpu = {"value": obs_iters_s / b, "unit": "iters/s", "cores": cores, "kind": "port", "host": hinfo,
                "sample": f"{sample} of {b} observations x {iters} FISTA+DST3 iterations with the fp64 oracle "
                          f"on the bf16-upcast dictionary, extrapolated to the batch ({obs_iters_s:.1f} obs-iters/s)"}
     if rank == 0:
@@ -830,7 +1000,8 @@ def run_c5(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dev_s / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
             "data": "synthetic (seeded Philox, see DESIGN.md)",
-            "config": {"workload": "c5", "n": n, "k": k, "batch": b, "iterations_per_step": iters,
+            "config": workload_config("c5", [w], args.seed, args.splits),
+            "details": {"batch": b, "iterations_per_step": iters,
                        "splits": args.splits, "parallelism": f"dp{world}" if world > 1 else "single-gpu",
                        "mean_objective": float(np.mean(res.objective)), "kept_min": int(res.kept.min()),
                        "nnz_mean": float(np.mean(res.nnz)), "accumulate": "fp32 (TMEM), fp64 state",
@@ -850,8 +1021,31 @@ def run_c5(args):
         torch.distributed.destroy_process_group()
 
 
+def spawn_ranks(args):
+    """`--gpus N` without a launcher (WORLD_SIZE unset): start N ranks, one process per GPU, with
+    torch.distributed.run on 127.0.0.1 and relay rank 0's JSON line; exit with the launcher's code."""
+    import socket
+    import torch
+    have = torch.cuda.device_count() if args.impl == "ours" else args.gpus
+    if args.impl == "ours" and have < args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} requested, {have} CUDA devices visible"}))
+        sys.exit(2)
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stderr.write("bench: launching " + " ".join(cmd) + "\n")
+    sys.exit(subprocess.call(cmd))
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        spawn_ranks(args)
+    world, _, _ = dist_env()
+    if world != args.gpus and "WORLD_SIZE" in os.environ:
+        sys.stderr.write(f"bench: --gpus {args.gpus} but WORLD_SIZE={world}; timing {world} ranks\n")
     if args.workload == "c5" and args.impl == "ours":
         run_c5(args)
     elif args.impl == "reference":

@@ -20,6 +20,7 @@ bit for bit.  Each function cites the reference file:line it restates.
 
 from __future__ import annotations
 
+import time
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -414,8 +415,12 @@ def flops_iteration(kind, strategy, k, n, kept, nnz, groups=0):
     return tot
 
 
-def solve(prob, cfg, hook=None):
+def solve(prob, cfg, hook=None, ticks=None):
     """Restatement of solvers.run (solvers.py:358-511) with an optional gap stop.
+
+    ``ticks`` (a list, optional): ``time.perf_counter()`` is appended once when the iteration
+    loop starts (after lambda_max, the screening precomputes and any static screen) and once
+    at the end of every iteration -- the CPU baseline times setup and iterations separately.
 
     The duality gap is the BASELINE quantity F(x_t) - 1/2||y||^2 + lam^2/2 r_SAFE,t^2
     evaluated with the dual point the iteration produced (problems.py:143-149).
@@ -495,6 +500,8 @@ def solve(prob, cfg, hook=None):
             raise FloatingPointError("solver produced a non-finite iterate")
 
     f_prev, moved, it = None, False, 0
+    if ticks is not None:
+        ticks.append(time.perf_counter())
     for t in range(1, cfg.max_iters + 1):
         if kept.size == 0:
             break
@@ -597,6 +604,8 @@ def solve(prob, cfg, hook=None):
         for key, val in (("t", t), ("kept", kept.size), ("nnz", nnz), ("objective", f_t),
                          ("gap", gap), ("radius", radius), ("flops", flops)):
             tr[key].append(val)
+        if ticks is not None:
+            ticks.append(time.perf_counter())
         moved = moved or nnz > 0
         if moved and f_prev is not None and abs(f_prev - f_t) / max(f_t, 1e-300) < cfg.rel_tol:
             break

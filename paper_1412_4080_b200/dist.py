@@ -24,20 +24,32 @@ import numpy as np
 
 from . import _native as nat
 from .problem import GROUP, Dictionary, GroupPartition, Problem
-from .solver import ScreenState, SolveResult, SolverConfig
-from .instrument import SolveTrace, flops_iteration
+from .solver import _STOP_NAMES, ScreenState, SolveResult, SolverConfig
+from .instrument import SolveTrace, flops_iteration, flops_static_init, problem_digest
 
 NEEDS_VEC = ("dst3", "dome", "gst3")
 
 
 def shard_ranges(k, world, group_sizes=None):
-    """[start, end) column block per rank; with groups, whole groups per rank (by atom count)."""
+    """[start, end) column block per rank; with groups, whole groups per rank (balanced by atom
+    count).  Every rank gets at least one column (one group): a world larger than the column
+    (group) count is rejected, as the engine has no zero-column shard."""
+    if world < 1:
+        raise ValueError("world size must be at least 1")
     if group_sizes is None:
+        if world > k:
+            raise ValueError(f"cannot shard {k} columns over {world} ranks (need at least one column per rank)")
         bounds = [round(r * k / world) for r in range(world + 1)]
         return [(bounds[r], bounds[r + 1]) for r in range(world)]
-    ptr = np.concatenate(([0], np.cumsum(group_sizes)))
-    g_bounds = [int(np.searchsorted(ptr, r * k / world, side="left")) for r in range(world)] + [len(group_sizes)]
+    sizes = np.asarray(group_sizes, dtype=np.int64)
+    ng = int(sizes.size)
+    if world > ng:
+        raise ValueError(f"cannot shard {ng} groups over {world} ranks (need at least one group per rank)")
+    ptr = np.concatenate(([0], np.cumsum(sizes)))
+    g_bounds = [int(np.searchsorted(ptr, r * k / world, side="left")) for r in range(world)] + [ng]
     g_bounds[0] = 0
+    for r in range(1, world):             # at least one group per rank, and room for the ranks after r
+        g_bounds[r] = min(max(g_bounds[r], g_bounds[r - 1] + 1), ng - (world - r))
     return [(int(ptr[g_bounds[r]]), int(ptr[g_bounds[r + 1]])) for r in range(world)], \
            [(g_bounds[r], g_bounds[r + 1]) for r in range(world)]
 
@@ -293,8 +305,15 @@ def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2):
         local = Problem(sub, problem.y, problem.lam)
         shard = GpuShard(local, cfg, c0, k, 0, 0, device)
         gw = None
+    import torch
+    start = torch.cuda.Event(enable_timing=True)
+    stop = torch.cuda.Event(enable_timing=True)
     try:
+        start.record(shard.eng.stream)
         sc = orchestrate(shard, cfg, problem.lam, pg, gw, chunk, collectives)
+        stop.record(shard.eng.stream)
+        stop.synchronize()
+        device_s = start.elapsed_time(stop) / 1e3
         if sc.status != 0:
             from .solver import _raise_status
             _raise_status(None, sc)
@@ -317,19 +336,27 @@ def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2):
     mask = np.ones(k, dtype=bool)
     mask[kept] = False
     trace = SolveTrace(kind=problem.kind, strategy=cfg.strategy, n_rows=problem.n_rows, n_cols=k,
-                       group_count=problem.partition.n_groups if problem.kind == GROUP else 0, lam=problem.lam)
+                       group_count=problem.partition.n_groups if problem.kind == GROUP else 0, lam=problem.lam,
+                       digest=problem_digest(problem))
     cum = 0
+    if cfg.strategy == "static":                      # as run() and the reference (solvers.py:425-426)
+        trace.init_flops = flops_static_init(k, problem.n_rows)
+        cum = trace.init_flops
     for r in rows:
         cum += flops_iteration(problem.kind, cfg.strategy, k, problem.n_rows, int(r[nat.TR_KEPT]),
                                int(r[nat.TR_NNZ]), trace.group_count)
         trace.append(int(r[nat.TR_T]), int(r[nat.TR_KEPT]), int(r[nat.TR_NNZ]), float(r[nat.TR_OBJ]), cum,
                      float(r[nat.TR_NS]) * 1e-9)
         trace.gap.append(float(r[nat.TR_GAP]))
+        trace.radius.append(float(r[nat.TR_RADIUS]))
+        trace.support.append(int(r[nat.TR_SUPPORT]))
+        trace.L.append(float(r[nat.TR_L]))
     if sc.trivial:
         return SolveResult(np.zeros(k), 0, trace, 0.5 * float(problem.y @ problem.y),
                            ScreenState(np.arange(k, dtype=np.int64), np.empty(0, np.int64), cfg.test),
-                           lambda_max=float(sc.lmax), stop_reason="trivial")
+                           lambda_max=float(sc.lmax), stop_reason="trivial", device_seconds=device_s)
     final = trace.objective[-1] if trace.objective else 0.5 * float(problem.y @ problem.y)
     return SolveResult(x_star, int(sc.t), trace, final,
                        ScreenState(np.flatnonzero(mask).astype(np.int64), kept, cfg.test),
-                       lambda_max=float(sc.lmax), gap=float(sc.gap))
+                       lambda_max=float(sc.lmax), gap=float(sc.gap),
+                       stop_reason=_STOP_NAMES.get(sc.stop, "running"), device_seconds=device_s)

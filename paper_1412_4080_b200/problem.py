@@ -41,14 +41,16 @@ def _pad16(n):
 class Dictionary:
     """Dense N x K column-major dictionary (reference dictionary.py:37-117).
 
-    ``dtype`` selects the device storage: "f64" (the reference's), "f32" or
-    "bf16" (bit patterns passed as uint16).  All arithmetic accumulates in fp64.
-    The unit-norm check (tolerance 1e-9) runs on the fp64 upcast.
+    ``dtype`` selects the device storage: "f64" (the default and the reference's: any input,
+    float32 included, is upcast as ``np.array(data, dtype=np.float64)`` does in
+    dictionary.py:48), "f32" or "bf16" (bit patterns passed as uint16) on request.  All
+    arithmetic accumulates in fp64.  The unit-norm check (tolerance 1e-9) runs on the exact
+    fp64 upcast; see ``norm_aware`` for which screening formulas a solve uses.
     """
 
     def __init__(self, data, check_unit_norms=True, dtype=None):
         if dtype is None:
-            dtype = "f32" if getattr(data, "dtype", None) == np.float32 else "f64"
+            dtype = "f64"
         if dtype not in _DTYPES:
             raise ValueError(f"unknown dictionary dtype {dtype!r}")
         np_t, code = _DTYPES[dtype]
@@ -73,6 +75,16 @@ class Dictionary:
         self.col_norm_checked = bool(check_unit_norms)
         self._dev = {}
         self._op_norm = None
+
+    @property
+    def norm_aware(self):
+        """Whether the screening tests use the norm-aware generalisation ((1 - |a_i.c|)/||a_i||,
+        DST3 normal a*/||a*||) instead of the reference's unit-atom formulas.  fp64 storage always
+        follows the reference (which never looks at column norms, checked or not: an fp64
+        dictionary built with ``check_unit_norms=False`` gets exactly the reference's tests,
+        radius guard included); reduced-precision storage whose rounded columns did not pass the
+        1e-9 unit-norm check uses the generalisation, which stays safe at any column norm."""
+        return self.dtype != "f64" and not self.col_norm_checked
 
     @staticmethod
     def _upcast(a, dtype):

@@ -142,18 +142,33 @@ _STOP_NAMES = {nat.STOP_RELTOL: "rel_tol", nat.STOP_GAP: "gap", nat.STOP_MAXITER
                nat.STOP_EMPTY: "empty", nat.STOP_TRIVIAL: "trivial", nat.STOP_ERROR: "error"}
 
 
-class _DeviceProblem:
-    """Device arrays of one Problem (cached on the host objects)."""
+def _partition_key(part):
+    """Content key of a GroupPartition (group order, sizes, weights, spectral norms): device
+    arrays cached on the Dictionary are shared only by partitions with equal content, never by
+    object identity (an id() can be recycled by a new partition)."""
+    if part is None:
+        return None
+    import hashlib
+    h = hashlib.sha1()
+    for arr in (np.concatenate(part.groups).astype(np.int64), part.group_sizes(),
+                np.asarray(part.weights, dtype=np.float64), np.asarray(part.spectral_norms, dtype=np.float64)):
+        h.update(np.ascontiguousarray(arr).tobytes())
+        h.update(b"|")
+    return h.hexdigest()
 
-    def __init__(self, problem, device):
+
+class _DeviceDictionary:
+    """Device arrays that depend only on the dictionary and the partition content (cached on
+    the Dictionary, shared by every Problem / Engine on it): the padded column-major D
+    (group-permuted), the group pointer, weights and spectral norms."""
+
+    def __init__(self, dic, part, device):
         import torch
-        dic = problem.dictionary
         self.n, self.k, self.ldd = dic.n_rows, dic.n_cols, dic.ldd
         self.perm = None
         self.group_ptr = self.group_w = self.group_sn = None
         self.n_groups = 0
-        if problem.kind == GROUP:
-            part = problem.partition
+        if part is not None:
             order = np.concatenate(part.groups)
             if not np.array_equal(order, np.arange(self.k)):
                 self.perm = order.astype(np.int64)      # permuted column j -> original perm[j]
@@ -165,6 +180,28 @@ class _DeviceProblem:
             self.n_groups = part.n_groups
             self.group_ptr_host = ptr
         self.D = dic.device_data(device, self.perm)
+
+
+class _DeviceProblem:
+    """One Problem on the device: the cached dictionary arrays plus this problem's own
+    observation, uploaded into a fresh buffer for every Engine (never cached: two Problems on
+    one Dictionary carry different y)."""
+
+    def __init__(self, problem, device):
+        import torch
+        dic = problem.dictionary
+        cache = dic.__dict__.setdefault("_problem_cache", {})
+        key = (str(device), _partition_key(problem.partition))
+        dd = cache.get(key)
+        if dd is None:
+            dd = _DeviceDictionary(dic, problem.partition, device)
+            cache[key] = dd
+        self.dd = dd
+        self.n, self.k, self.ldd = dd.n, dd.k, dd.ldd
+        self.perm, self.n_groups, self.D = dd.perm, dd.n_groups, dd.D
+        self.group_ptr, self.group_w, self.group_sn = dd.group_ptr, dd.group_w, dd.group_sn
+        if dd.n_groups:
+            self.group_ptr_host = dd.group_ptr_host
         y = torch.zeros(self.ldd, dtype=torch.float64)
         y[: self.n] = torch.from_numpy(problem.y)
         self.y = y.to(device, non_blocking=True)
@@ -178,7 +215,7 @@ def _desc(problem, dp):
     d.lam = problem.lam
     d.n_groups = dp.n_groups
     dic = problem.dictionary
-    d.norm_aware = int(dic.dtype != "f64" or not dic.col_norm_checked)
+    d.norm_aware = int(dic.norm_aware)
     if dp.n_groups:
         d.group_ptr, d.group_w, d.group_snorm = dp.group_ptr.data_ptr(), dp.group_w.data_ptr(), dp.group_sn.data_ptr()
     d.col_offset, d.n_cols_total = 0, dp.k
@@ -217,12 +254,7 @@ class Engine:
         self.sptr = C.c_void_p(self.stream.cuda_stream)
         dic = problem.dictionary
         with torch.cuda.stream(self.stream):
-            cache = dic.__dict__.setdefault("_problem_cache", {})
-            key = (str(self.device), id(problem.partition) if problem.partition is not None else None)
-            dp = cache.get(key)
-            if dp is None or (problem.partition is not None and dp.n_groups != problem.partition.n_groups):
-                dp = _DeviceProblem(problem, self.device)
-                cache[key] = dp
+            dp = _DeviceProblem(problem, self.device)
             self.dp = dp
             op_norm = cfg.op_norm
             need_norm = cfg.algorithm == CP or (cfg.algorithm == TWIST and cfg.twist_step is None)

@@ -109,7 +109,8 @@ def test_problem_validation():
 
 def test_dictionary_dtypes_and_layout():
     D32 = wl.gaussian_dictionary_f32(64, 100, 1)
-    dic = ds.Dictionary(D32, check_unit_norms=False)
+    dic = ds.Dictionary(D32, check_unit_norms=False, dtype="f32")
+    assert ds.Dictionary(D32, check_unit_norms=False).dtype == "f64"   # reference upcast by default
     assert dic.dtype == "f32" and dic.data is D32 and dic.ldd == 64
     dic2 = ds.Dictionary(wl.gaussian_dictionary(1000, 3, 0))
     assert dic2.ldd == 1008

@@ -127,3 +127,89 @@ def test_shard_ranges_cover_and_keep_groups_whole():
         assert c0 == ptr[g0] and c1 == ptr[g1]
     for a, b in zip(cols, cols[1:]):
         assert a[1] == b[0]
+
+
+def test_shard_ranges_one_group_per_rank_and_limits():
+    sizes = np.array([70, 10, 10, 10])          # searchsorted by atom count would give rank 1 nothing
+    cols, grps = pdist.shard_ranges(100, 4, sizes)
+    assert grps == [(0, 1), (1, 2), (2, 3), (3, 4)]
+    assert all(c1 > c0 for c0, c1 in cols)
+    cols, grps = pdist.shard_ranges(100, 2, sizes)
+    assert grps[0][1] > grps[0][0] and grps[1][1] > grps[1][0] and grps[1][1] == 4
+    for world in (3, 5, 7, 8):
+        sizes = np.array([1] * 3 + [50] + [1] * 5)
+        cols, grps = pdist.shard_ranges(int(sizes.sum()), world, sizes)
+        assert [g[1] - g[0] >= 1 for g in grps] == [True] * world
+        assert grps[0][0] == 0 and grps[-1][1] == sizes.size
+        assert all(a[1] == b[0] for a, b in zip(grps, grps[1:]))
+    with pytest.raises(ValueError, match="groups over"):
+        pdist.shard_ranges(100, 5, np.array([70, 10, 10, 10]))
+    with pytest.raises(ValueError, match="columns over"):
+        pdist.shard_ranges(3, 4)
+
+
+def _one_rank_data(ratio=0.4):
+    """A correlated dictionary with its columns reordered so that every atom the oracle screens
+    sits in the last block: with the uneven ranges below, only rank 3 ever screens."""
+    D0 = wl.correlated_dictionary(60, 120, 5)
+    y, _ = wl.planted_observation(D0, 5, nnz=5)
+    lam = ratio * wl.lambda_star(D0, y)
+    L = float(np.linalg.norm(D0, 2) ** 2 * (1 + 1e-9))
+    r = so.solve(so.make_problem(D0, y, lam), so.Config(algorithm="fista", strategy="dynamic", test="dst3",
+                                                         max_iters=3000, rel_tol=1e-300, L0=L, gap_tol=1e-9))
+    elim = np.asarray(r.eliminated)
+    perm = np.concatenate([np.setdiff1d(np.arange(120), elim), elim])
+    return np.asfortranarray(D0[:, perm]), y, lam, 120 - elim.size
+
+
+def _uneven(n_kept):
+    """Blocks of 7 / n_kept-17 / 10 kept atoms, then every screened atom on rank 3."""
+    return [(0, 7), (7, n_kept - 10), (n_kept - 10, n_kept), (n_kept, 120)]
+
+
+def _worker_uneven(rank, world, port, out_path, algo, collectives):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.sharded_numpy_backend import NumpyShard
+        D, y, lam, n_kept = _one_rank_data()
+        cfg = _cfg(algo, "dst3", "spec", 1e-9, D)
+        c0, c1 = _uneven(n_kept)[rank]
+        shard = NumpyShard(D[:, c0:c1], y, lam, cfg, c0, op_norm=cfg.op_norm)
+        sc = pdist.orchestrate(shard, cfg, lam, pg=dist.group.WORLD, chunk=4, collectives=collectives)
+        local = (shard.active + c0, shard.x[shard.active], c1 - c0 - shard.active.size)
+        got = [None] * world
+        dist.all_gather_object(got, (local, shard.trace, int(sc.t)))
+        if rank == 0:
+            with open(out_path, "wb") as fh:
+                pickle.dump(got, fh)
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("collectives", [2, 1], ids=["two-collectives", "one-collective"])
+@pytest.mark.parametrize("algo", ["fista", "ista"])
+def test_sharded_world4_uneven_screening_on_one_rank(algo, collectives):
+    """World 4 (gloo) with uneven column blocks; screening fires on
+    rank 3 only, so the ranks' active lists shrink at different rates while the control path
+    (radius, stop, redo/fixup) stays identical on every rank."""
+    with tempfile.TemporaryDirectory() as td:
+        out = os.path.join(td, "res.pkl")
+        mp.spawn(_worker_uneven, args=(4, _free_port(), out, algo, collectives), nprocs=4, join=True)
+        with open(out, "rb") as fh:
+            got = pickle.load(fh)
+    D, y, lam, n_kept = _one_rank_data()
+    assert [c1 - c0 for c0, c1 in _uneven(n_kept)] != [D.shape[1] // 4] * 4
+    ref = so.solve(so.make_problem(D, y, lam), _cfg(algo, "dst3", "spec", 1e-9, D))
+    screened = [g[0][2] for g in got]
+    assert screened[:3] == [0, 0, 0] and screened[3] > 0, screened
+    assert len({g[2] for g in got}) == 1 and got[0][2] == ref.iterations
+    kept = np.concatenate([g[0][0] for g in got])
+    x = np.zeros(D.shape[1])
+    x[kept] = np.concatenate([g[0][1] for g in got])
+    assert np.array_equal(np.setdiff1d(np.arange(D.shape[1]), kept), ref.eliminated)
+    assert np.linalg.norm(x - ref.x_star) <= 1e-9 * max(1.0, np.linalg.norm(ref.x_star))
+    objs = [[t[3] for t in g[1]] for g in got]
+    assert all(o == objs[0] for o in objs), "ranks disagree on the objective trace"
+    np.testing.assert_allclose(objs[0], ref.trace["objective"], rtol=1e-10)

@@ -1,0 +1,198 @@
+"""The reference's hook-based acceptance checks, re-run on the GPU engine through
+``run(..., iteration_hook=...)`` (the hook receives the engine's own per-iteration snapshot:
+theta_t, the pre-screening correlations, the kept set, the mask and x_t).
+
+* C3 first-iteration equivalence (reference tests/test_acceptance.py:180-198): on 50 instances
+  the first dynamic SAFE elimination equals the static SAFE set.
+* C4 nesting (test_acceptance.py:69-103, 201-209): at every iteration's dual point the GPU test
+  kernels give SAFE subset DST3 subset Dome (Lasso) and GSAFE subset GST3 (groups), over
+  all five algorithms and the suite's ratios.
+* Reduced dual feasibility (tests/test_screening.py:346-381): the scaled point built from the
+  GPU's theta and max|corr| satisfies the surviving columns' constraints.
+* Momentum buffers track the reduction, kept counts are monotone, eliminated coordinates are
+  exact zeros, the reduced objective equals the full one (tests/test_solvers.py:266-305), and
+  concurrent runs on shared inputs reproduce the serial results (test_solvers.py:307-323).
+"""
+
+from concurrent.futures import ThreadPoolExecutor
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import paper_1412_4080_b200 as ds  # noqa: E402
+from paper_1412_4080_b200 import ops  # noqa: E402
+from paper_1412_4080_b200 import workloads as wl  # noqa: E402
+from oracle import screen_oracle as so  # noqa: E402
+
+SUITE_N, SUITE_K, SUITE_GROUP_SIZE = 30, 80, 4
+
+
+def make_problem(kind, seed, ratio, n=SUITE_N, k=SUITE_K, group_size=SUITE_GROUP_SIZE, p=0.05):
+    """tests/test_acceptance.py:30-43 (and conftest make_lasso/make_group) with the restated
+    generators (datagen.py: gaussian atoms / observation, random_partition, Bernoulli-Gaussian)."""
+    D = wl.gaussian_dictionary(n, k, seed)
+    dic = ds.Dictionary(D)
+    if kind == "lasso":
+        y = wl.gaussian_observation(n, seed)
+        part, groups = None, None
+    else:
+        groups = wl.random_groups(k, group_size, seed)
+        part = ds.GroupPartition.build(dic, groups)
+        y = wl.bernoulli_gaussian_observation(D, groups, seed, p=p)
+    lstar = wl.lambda_star(D, y, groups, None if part is None else part.weights)
+    return ds.Problem(dic, y, ratio * lstar, part), D, groups
+
+
+def test_c3_first_iteration_equivalence_50_instances():
+    ratios = (0.3, 0.45, 0.6, 0.75, 0.9)
+    nonempty = 0
+    for i in range(50):
+        p, _, _ = make_problem("lasso", 100 + i, ratios[i % len(ratios)])
+        captured = {}
+
+        def hook(info):
+            if info.t == 1:
+                captured["set"] = np.sort(info.kept[info.mask])
+
+        ds.run(p, ds.SolverConfig(algorithm="ista", strategy="dynamic", test="safe", max_iters=1),
+               iteration_hook=hook)
+        static = ds.run(p, ds.SolverConfig(algorithm="ista", strategy="static", test="safe", max_iters=1))
+        assert np.array_equal(captured["set"], static.screen_state.eliminated), i
+        nonempty += captured["set"].size > 0
+    assert nonempty > 10
+
+
+def _nesting_hook(p, D, groups, geo, sink):
+    """Evaluate every applicable test with the GPU test kernels at the engine's dual point."""
+
+    def hook(info):
+        sink["checks"] += 1
+        if p.kind == "lasso":
+            ci = float(np.max(np.abs(info.corr), initial=0.0))
+            masks = {}
+            for tk in ("safe", "dst3", "dome"):
+                r, _ = geo.radius(tk, info.theta, corr_inf=ci)
+                if tk == "dome":
+                    dp = ops.DomeParams(p.lam, geo.lmax.value, geo.star_corr, geo.y_corr, r)
+                    masks[tk] = ds.test_dome(dp, info.kept)
+                else:
+                    cc = geo.safe_cc if tk == "safe" else geo.dst3_cc
+                    masks[tk] = ds.test_sphere_lasso(ops.SphereRegion(None, r, cc), info.kept)
+            pairs = (("safe", "dst3"), ("dst3", "dome"))
+        else:
+            lay = so.Layout(geo.p, info.kept)
+            norms = lay.norms(info.corr)
+            masks = {}
+            for tk in ("gsafe", "gst3"):
+                r, _ = geo.radius(tk, info.theta, norms=norms, weights=lay.weights)
+                masks[tk] = ds.test_sphere_group(ops.SphereRegion(None, r, None), p.partition, info.kept_groups,
+                                                 geo.center_group_norms(tk))
+            pairs = (("gsafe", "gst3"),)
+        for weaker, stronger in pairs:
+            extra = int(np.sum(masks[weaker] & ~masks[stronger]))
+            if extra:
+                sink["violations"].append((info.t, weaker, stronger, extra))
+
+    return hook
+
+
+@pytest.mark.parametrize("kind", ["lasso", "group"])
+def test_c4_nesting_on_engine_dual_points(kind):
+    checks, violations = 0, []
+    tests = ("safe", "dst3", "dome") if kind == "lasso" else ("gsafe", "gst3")
+    for seed in (1, 2):
+        for ratio in (0.3, 0.5, 0.7, 0.9):
+            p, D, groups = make_problem(kind, seed, ratio)
+            op = so.make_problem(D, p.y, p.lam, groups, None if groups is None else p.partition.weights,
+                                 None if groups is None else p.partition.spectral_norms)
+            geo = so.Geometry(op, so.lambda_max(op))
+            for algo in ds.ALGORITHMS:
+                for test in tests:
+                    sink = {"checks": 0, "violations": []}
+                    ds.run(p, ds.SolverConfig(algorithm=algo, strategy="dynamic", test=test, max_iters=300,
+                                              rel_tol=1e-12), iteration_hook=_nesting_hook(p, D, groups, geo, sink))
+                    checks += sink["checks"]
+                    violations += [(seed, ratio, algo, test) + v for v in sink["violations"]]
+    assert checks > 500
+    assert not violations, violations[:5]
+
+
+def test_reduced_dual_feasibility_during_run():
+    checked = []
+
+    def make_hook(p, D):
+        def hook(info):
+            if p.kind == "lasso":
+                ci = float(np.max(np.abs(info.corr), initial=0.0))
+                _, v = so.clip_scale(so.OProblem(D, p.y, p.lam), info.theta, np.inf if ci == 0 else 1.0 / ci)
+                assert np.max(np.abs(D[:, info.kept].T @ v), initial=0.0) <= 1.0 + 1e-9
+            else:
+                op = so.OProblem(D, p.y, p.lam, [np.asarray(g) for g in p.partition.groups],
+                                 np.asarray(p.partition.weights), np.asarray(p.partition.spectral_norms))
+                lay = so.Layout(op, info.kept)
+                _, v = so.dual_scale_group(op, info.theta, lay.norms(info.corr), lay.weights)
+                vn = so.full_group_norms(op, D.T @ v)[info.kept_groups]
+                assert np.all(vn <= op.weights[info.kept_groups] * (1.0 + 1e-9))
+            checked.append(info.t)
+        return hook
+
+    p, D, _ = make_problem("lasso", 40, 0.8, n=12, k=30)
+    ds.run(p, ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=60, rel_tol=1e-10),
+           iteration_hook=make_hook(p, D))
+    g, Dg, _ = make_problem("group", 41, 0.6, n=12, k=30, group_size=3, p=0.2)
+    ds.run(g, ds.SolverConfig(algorithm="ista", strategy="dynamic", test="gst3", max_iters=60, rel_tol=1e-10),
+           iteration_hook=make_hook(g, Dg))
+    assert len(checked) > 10
+
+
+def test_momentum_buffers_and_monotone_kept():
+    p, _, _ = make_problem("lasso", 16, 0.8, n=12, k=30)
+    lens = []
+    res = ds.run(p, ds.SolverConfig(algorithm="fista", strategy="dynamic", test="safe", max_iters=100,
+                                    rel_tol=1e-9), iteration_hook=lambda info: lens.append((len(info.x),
+                                                                                             info.kept.size)))
+    assert lens and all(nx == nk for nx, nk in lens)
+    p14, _, _ = make_problem("lasso", 14, 0.8, n=12, k=30)
+    res = ds.run(p14, ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=200,
+                                      rel_tol=1e-9))
+    kept = res.trace.kept
+    assert all(b <= a for a, b in zip(kept, kept[1:])) and res.screen_state.eliminated.size > 0
+    p17, _, _ = make_problem("lasso", 17, 0.7, n=12, k=30)
+    res = ds.run(p17, ds.SolverConfig(algorithm="sparsa", strategy="dynamic", test="dst3", max_iters=500,
+                                      rel_tol=1e-10))
+    assert np.all(res.x_star[res.screen_state.eliminated] == 0.0)
+
+
+def test_reduced_objective_equals_full():
+    p, D, groups = make_problem("group", 15, 0.7, n=12, k=30, group_size=3, p=0.2)
+    op = so.make_problem(D, p.y, p.lam, groups, p.partition.weights, p.partition.spectral_norms)
+    records = []
+    res = ds.run(p, ds.SolverConfig(algorithm="fista", strategy="dynamic", test="gsafe", max_iters=300,
+                                    rel_tol=1e-10), iteration_hook=lambda info: records.append(
+                                        (info.x.copy(), info.kept.copy(), info.mask.copy())))
+    assert records
+    for (x_red, kept, mask), f_rec in zip(records, res.trace.objective):
+        x_full = np.zeros(p.n_cols)
+        x_full[kept[~mask]] = x_red[~mask]            # the recorded objective is post-reduction
+        full = so.objective(op, x_full)
+        assert f_rec == pytest.approx(full, abs=1e-10 * max(1.0, full))
+
+
+def test_concurrent_runs_share_inputs():
+    p, _, _ = make_problem("lasso", 20, 0.7, n=12, k=30)
+    cfgs = [ds.SolverConfig(algorithm=a, strategy="dynamic", test="dst3", max_iters=300, rel_tol=1e-10)
+            for a in ("ista", "fista", "sparsa")]
+    serial = [ds.run(p, c) for c in cfgs]
+
+    def in_thread(cfg):
+        torch.cuda.set_device(0)
+        return ds.run(p, cfg)
+
+    with ThreadPoolExecutor(max_workers=3) as pool:
+        threaded = list(pool.map(in_thread, cfgs))
+    for a, b in zip(serial, threaded):
+        assert np.array_equal(a.x_star, b.x_star)
+        assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)

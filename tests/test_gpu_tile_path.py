@@ -26,7 +26,7 @@ def _run(D, y, lam, groups=None, dtype="f64", algo="fista", test="dst3", rtol=1e
     op = so.make_problem(D64, y, lam, groups, None if part is None else part.weights,
                          None if part is None else part.spectral_norms)
     ref = so.solve(op, so.Config(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300,
-                                 L0=L, gap_tol=gap_tol, norm_aware=(dtype != "f64")))
+                                 L0=L, gap_tol=gap_tol, norm_aware=dic.norm_aware))
     # gap 1e-7: reached well before the objective stalls to the last bit (rel_tol 1e-300 stops on
     # bitwise-equal consecutive objectives, where 1-ulp summation differences decide)
     assert res.stop_reason == "gap"
