@@ -618,11 +618,12 @@ def run_c4_sharded(args, world, rank, local):
                        "t_hit_reference": None if gold is None else int(gold["t_hit"]),
                        "time_to_gap_s": el / args.steps, "parallelism": f"colshard{world}",
                        "columns_per_rank": c1 - c0, "collectives_per_iteration": _coll(args),
+                       "trip_graph": {"captured": shard.graph_trips > 0, "trips_per_graph": shard.graph_trips},
                        "l2": "dictionary shard larger than the 126 MB L2"},
             "roofline": {"bound": "hbm", "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
                          "traffic": None, "peak_source": peak_src,
                          "kernel": "k1 stream, whole-step average per GPU (local columns x iterations / device time)"},
-            "gpu_launches": int(launches), "gpu_launches_note": "dscr_solver_phase launches on rank 0 (>= 1 kernel each)",
+            "gpu_launches": int(launches), "gpu_launches_note": "dscr_solver_phase launches on rank 0 (>= 1 kernel each; graph replays x phases per graph)",
             "clocks": clocks.summary(), "e2e": e2e, "cpu_baseline": None,
         }
         print(json.dumps(line), flush=True)

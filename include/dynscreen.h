@@ -190,7 +190,9 @@ int dscr_abi_version(void);
 
 /* ---- kernel-level entry points (unit parity) -------------------------- */
 
-/* out[j] = D[:,j] . v  for j < k.  Replaces Dictionary.correlate (dictionary.py:89-94). */
+/* out[j] = D[:,j] . v  for j < k.  Replaces Dictionary.correlate (dictionary.py:89-94).
+ * v holds n values; when 8*ldd exceeds the shared-memory staging buffer (n_rows > ~27000)
+ * it is read through L2 and must hold ldd values with rows n..ldd-1 zero. */
 int dscr_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v,
                    double* out, void* stream);
 /* out = D x (out has ldd rows).  Replaces Dictionary.apply (dictionary.py:82-87).
@@ -377,12 +379,6 @@ int dscr_peer_open(const void* handle_64, void** dptr);
 int dscr_peer_close(void* dptr);
 int dscr_peer_free(void* dptr);
 int dscr_solver_set_peers(dscr_solver* h, int rank, int world, void* const* recv_bases, void* const* flag_bases);
-
-/* 128-byte NCCL unique id created on rank 0 (dlopens libnccl.so.2). */
-int dscr_comm_unique_id(void* id_out_128);
-/* Single-rank communicator check (world 1 returns OK).  Multi-rank solves use dscr_solver_phase with
- * host collectives or the peer-memory exchange (dscr_solver_set_peers); world > 1 returns DSCR_ENOCOMM. */
-int dscr_solver_set_comm(dscr_solver* h, const void* id_128, int rank, int world);
 
 #ifdef __cplusplus
 }

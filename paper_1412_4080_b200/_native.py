@@ -35,7 +35,7 @@ ABI_FUNCTIONS = (
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
     "dscr_solver_get_buffers", "dscr_solver_profile", "dscr_solver_phase", "dscr_solver_set_collectives", "dscr_solver_set_peers", "dscr_peer_buffer_bytes",
-    "dscr_peer_alloc", "dscr_peer_open", "dscr_peer_close", "dscr_peer_free", "dscr_solver_destroy", "dscr_comm_unique_id", "dscr_solver_set_comm",
+    "dscr_peer_alloc", "dscr_peer_open", "dscr_peer_close", "dscr_peer_free", "dscr_solver_destroy",
     "dscr_batched_gemm_bf16", "dscr_batched_workspace_size", "dscr_batched_create", "dscr_batched_setup",
     "dscr_batched_run", "dscr_batched_get_buffers", "dscr_batched_profile", "dscr_batched_destroy",
     "dscr_corr_exact_work_size", "dscr_corr_exact_bf16", "dscr_group_spectral_norms", "dscr_ingest_rows_f64",
@@ -139,8 +139,6 @@ def _declare(lib):
         "dscr_peer_open": (i32, [vp, C.POINTER(vp)]),
         "dscr_peer_close": (i32, [vp]),
         "dscr_peer_free": (i32, [vp]),
-        "dscr_comm_unique_id": (i32, [vp]),
-        "dscr_solver_set_comm": (i32, [vp, vp, i32, i32]),
         "dscr_batched_gemm_bf16": (i32, [vp, i32, i32, vp, i32, i32, i32, i32, vp, i32, vp]),
         "dscr_batched_workspace_size": (sz, [C.POINTER(BatchedDesc)]),
         "dscr_batched_create": (i32, [C.POINTER(BatchedDesc), vp, sz, vp, C.POINTER(vp)]),

@@ -50,6 +50,18 @@ class BatchedResult:
     x_values: np.ndarray
     device_seconds: float = float("nan")
     d2h_bytes: int = 0           # bytes copied device -> host by result()
+    active_words: np.ndarray | None = None   # [B][K/32] active-atom bits (result(masks=True) only)
+
+    def active_mask(self, j):
+        """Boolean active-atom mask of observation j (needs the masks read back)."""
+        if self.active_words is None:
+            raise ValueError("masks were not read back (solve_batched(..., masks=True))")
+        bits = np.unpackbits(self.active_words[j].view(np.uint8), bitorder="little")
+        return bits.astype(bool)
+
+    def eliminated(self, j):
+        """Atoms screened out of observation j (sorted)."""
+        return np.flatnonzero(~self.active_mask(j)).astype(np.int64)
 
     @property
     def x_idx(self):
@@ -176,9 +188,10 @@ class BatchedEngine:
         off = int(ptr) - self.ws.data_ptr()
         return self.ws[off: off + count * isz].view(dtype)
 
-    def result(self, device_seconds=float("nan")):
+    def result(self, device_seconds=float("nan"), masks=False):
         """Copy the solution back: device-side CSR compaction of the x lists, then a few
-        packed transfers (self.d2h_bytes counts them)."""
+        packed transfers (self.d2h_bytes counts them).  ``masks=True`` also reads the active-atom
+        bit masks (B x K/32 words) for set-level checks."""
         torch = self.torch
         b, bf, cap = self.b, self.bufs, self.cap
         par = self.iterations & 1
@@ -192,7 +205,12 @@ class BatchedEngine:
         i32 = torch.cat([self._view(p, b, torch.int32) for p in (bf.nnz, bf.kept, bf.status)] + [counts_d]
                         + [self._view(bf.iterations, 1, torch.int32)]).cpu().numpy()
         trace = self._view(bf.trace, self.iterations * 4, torch.float64).cpu().numpy().reshape(-1, 4)
-        self.d2h_bytes = int(idx.nbytes + val.nbytes + f64.nbytes + i32.nbytes + trace.nbytes)
+        words = None
+        if masks:
+            words = self._view(bf.mask, b * (self.k // 32), torch.int32).view(b, self.k // 32).cpu().numpy()
+            words = words.view(np.uint32)
+        self.d2h_bytes = int(idx.nbytes + val.nbytes + f64.nbytes + i32.nbytes + trace.nbytes
+                             + (words.nbytes if words is not None else 0))
         nnz, kept, status, counts = (i32[q * b:(q + 1) * b] for q in range(4))
         if np.any(status >= 3):
             bad = np.flatnonzero(status >= 3)
@@ -206,7 +224,7 @@ class BatchedEngine:
             objective=f64[0], gap=f64[1], nnz=nnz, kept=kept, status=status,
             lambda_max=f64[2], radius=f64[3], trace=trace,
             x_ptr=ptr, x_indices=idx.astype(np.int64), x_values=val,
-            device_seconds=device_seconds, d2h_bytes=self.d2h_bytes,
+            device_seconds=device_seconds, d2h_bytes=self.d2h_bytes, active_words=words,
         )
 
     def close(self):
@@ -223,8 +241,9 @@ class BatchedEngine:
 
 
 def solve_batched(dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, cap=1024, device=None,
-                  fused=True):
-    """FISTA (fixed step 1/L) with per-observation dynamic screening for Y[:, j], lam[j]."""
+                  fused=True, masks=False):
+    """FISTA (fixed step 1/L) with per-observation dynamic screening for Y[:, j], lam[j].
+    ``masks=True`` also returns the per-observation active-atom masks (``BatchedResult.eliminated``)."""
     eng = BatchedEngine(dictionary, Y, lam, L, iterations, test, splits, cap, device, fused)
     torch = eng.torch
     try:
@@ -234,7 +253,7 @@ def solve_batched(dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, 
         eng.run()
         ev1.record(eng.stream)
         eng.stream.synchronize()
-        return eng.result(ev0.elapsed_time(ev1) / 1e3)
+        return eng.result(ev0.elapsed_time(ev1) / 1e3, masks=masks)
     finally:
         eng.close()
 

@@ -134,6 +134,8 @@ struct Params {
     int k2v;           // K2 variant: 0 classic, 1 support before the test (K2S), 2 test + compaction (K2C)
     int k1_ilv;        // K1 interleaved column passes over the identity list
     int k1_tile;       // K1 tiled path: row segments per column (0 = per-warp column path)
+    int theta_gl;      // theta read through L2 instead of staged in shared memory (tall dictionaries)
+    int sup_keep;      // K1 reads support columns with evict_last (dictionary larger than L2)
     int max_iters;
     int G, cap, TR, R, P, G3b;
     int col_offset, group_offset;
@@ -307,8 +309,16 @@ template <typename T> struct K1Cfg { static constexpr int U = 2, MINB = 2; };
 template <> struct K1Cfg<float> { static constexpr int U = K1_UF32, MINB = 2; };
 template <> struct K1Cfg<__nv_bfloat16> { static constexpr int U = 1, MINB = 2; };
 
+// Vectors of ldd doubles up to this size are staged in shared memory by K1 and the setup
+// correlations (next to ~5 KB of static state); taller dictionaries read them through L2 (the
+// vector is 8 bytes per row against s bytes of dictionary per row and column, and stays
+// resident in the 126 MB L2).
+constexpr size_t THETA_SMEM_MAX = 227 * 1024 - 8192;
+
 // K1 per-CTA work: correlations, update, per-CTA partials into P.p1[b]
-template <typename T, bool GROUP>
+// TG: theta is read through L2 (global loads) instead of being staged in shared memory -- the
+// path for dictionaries taller than the shared-memory staging buffer (8 bytes per row).
+template <typename T, bool GROUP, bool TG = false>
 __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s_theta) {
     __shared__ double s_red[NW][NP1];
     dscr_scalars* sc = P.sc;
@@ -318,10 +328,11 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
     const int lo = (int)(((long long)nu * b) / G), hi = (int)(((long long)nu * (b + 1)) / G);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const bool need_dot = (mode == MODE_NORMAL);
-    if (need_dot && hi > lo) {
+    if (!TG && need_dot && hi > lo) {
         const double* th = P.theta[p];
         stage_async(s_theta, th, P.ldd);
     }
+    if (TG) s_theta = P.theta[p];
     cp_async_wait_all();
     __syncthreads();
 
@@ -362,9 +373,19 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
         const int f_beg = ilv ? b * NW * C : lo;
         const int f_end = ilv ? nchunk * NW * C : hi;
         const int f_step = ilv ? G * NW * C : NW * C;
+        // support residency (dictionaries larger than L2, identity list): columns whose atom
+        // carries a nonzero x or u are read with evict_last, so the residual pass (K3a) and the
+        // next K1 find them in L2; the flags of the next column group are loaded one group ahead
+        const bool skeep = P.sup_keep && ident && need_dot;
+        const uint64_t pol_keep = make_policy(1.0f);
+        const int fhi = ilv ? nu : hi;
+        double nx_pre = 0.0, nu_pre = 0.0;
+        if (skeep && lane < C && f_beg + warp * C + lane < fhi) {
+            nx_pre = xc[f_beg + warp * C + lane];
+            if (algo == DSCR_FISTA || algo == DSCR_CP) nu_pre = uc[f_beg + warp * C + lane];
+        }
         for (int fb = f_beg; fb < f_end; fb += f_step) {
             const int f0 = fb + warp * C;
-            const int fhi = ilv ? nu : hi;
             int myj = -1;
             if (lane < C && f0 + lane < fhi) {
                 if (ident) {
@@ -382,7 +403,22 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
                 const T* cols[C];
 #pragma unroll
                 for (int c = 0; c < C; ++c) cols[c] = js[c] >= 0 ? D + (size_t)js[c] * P.ldd : nullptr;
-                warp_dots<T, C, K1Cfg<T>::U>(cols, P.n, s_theta, lane, pol, cs);
+                uint64_t pols[C];
+                if (skeep) {
+                    const unsigned sm = __ballot_sync(0xffffffffu, myj >= 0 && (nx_pre != 0.0 || nu_pre != 0.0));
+                    const int fn = f0 + f_step + lane;           // next group's flags, in flight during the dots
+                    nx_pre = 0.0; nu_pre = 0.0;
+                    if (lane < C && fb + f_step < f_end && fn < fhi) {
+                        nx_pre = xc[fn];
+                        if (algo == DSCR_FISTA || algo == DSCR_CP) nu_pre = uc[fn];
+                    }
+#pragma unroll
+                    for (int c = 0; c < C; ++c) pols[c] = ((sm >> c) & 1u) ? pol_keep : pol;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < C; ++c) pols[c] = pol;
+                }
+                warp_dots<T, C, K1Cfg<T>::U>(cols, P.n, s_theta, lane, pols, cs);
             } else {
 #pragma unroll
                 for (int c = 0; c < C; ++c) cs[c] = js[c] >= 0 ? P.corr[js[c]] : 0.0;
@@ -877,6 +913,7 @@ __global__ void __launch_bounds__(NT, K1Cfg<T>::MINB) k1_corr_update(Params P) {
     if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 0);
     if (P.k1_tile) k1_body_tile<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
+    else if (P.theta_gl) k1_body<T, GROUP, true>(P, blockIdx.x, gridDim.x, s_theta);
     else k1_body<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
     if (!last_block(P.tickets + 0, gridDim.x, &s_flag)) return;
     k1_final<GROUP>(P, gridDim.x);
@@ -954,11 +991,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
     return v;
 }
 
-__global__ void __launch_bounds__(NT) k3x_push(Params P, unsigned long long seq) {
+// The exchange sequence number lives on the device (a 64-bit word after the kernel tickets),
+// so a captured trip graph replays with fresh numbers: PUSH and REDUCE use counter + 1 and
+// REDUCE's last CTA stores it.  It is never reset by a new solve on the same handle (the peers'
+// flags keep the last number they saw), only by dscr_solver_set_peers.
+__device__ __forceinline__ unsigned long long* xseq_ptr(const Params& P) {
+    return reinterpret_cast<unsigned long long*>(P.tickets + 8);
+}
+
+__global__ void __launch_bounds__(NT) k3x_push(Params P) {
     __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
     if (sc->stop || sc->t >= sc->run_limit) return;
     if (sc->mode == MODE_STATIC) return;
+    const unsigned long long seq = *reinterpret_cast<volatile unsigned long long*>(xseq_ptr(P)) + 1ull;
     const int W = P.oc_world, len = P.peer_len;
     const size_t off = (size_t)(seq & 1ull) * W * len + (size_t)P.oc_rank * len;
     const double* src = P.comm + CM_SUM;
@@ -974,10 +1020,12 @@ __global__ void __launch_bounds__(NT) k3x_push(Params P, unsigned long long seq)
     }
 }
 
-__global__ void __launch_bounds__(NT) k3x_reduce(Params P, unsigned long long seq) {
+__global__ void __launch_bounds__(NT) k3x_reduce(Params P) {
+    __shared__ int s_flag;
     dscr_scalars* sc = P.sc;
     if (sc->stop || sc->t >= sc->run_limit) return;
     if (sc->mode == MODE_STATIC) return;
+    const unsigned long long seq = *reinterpret_cast<volatile unsigned long long*>(xseq_ptr(P)) + 1ull;
     const int W = P.oc_world, len = P.peer_len;
     if (threadIdx.x < W) {   // every rank's section of this exchange has arrived
         const unsigned long long* f = static_cast<const unsigned long long*>(P.peer_tab[64 + P.oc_rank]) + threadIdx.x;
@@ -999,6 +1047,8 @@ __global__ void __launch_bounds__(NT) k3x_reduce(Params P, unsigned long long se
         for (int r = 0; r < W; ++r) a += rb[(size_t)r * len + i];   // rank order: identical on every rank
         dst[i] = a;
     }
+    if (!last_block(P.tickets + 6, gridDim.x, &s_flag)) return;   // every CTA has read seq
+    if (threadIdx.x == 0) *xseq_ptr(P) = seq;
 }
 
 // one-collective trips: MAX quantities and test extremes from the gathered rank slots, the
@@ -1502,7 +1552,7 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     const int r0 = tile * P.TR + threadIdx.x * V;
     const bool rows_ok = r0 < P.n;
     const T* D = static_cast<const T*>(P.D);
-    const uint64_t pol = make_policy(P.l2_keep);
+    const uint64_t pol = make_policy(P.sup_keep ? 1.0f : P.l2_keep);   // support columns: keep for the next K1
     double acc_a[V], acc_b[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) { acc_a[v] = 0.0; acc_b[v] = 0.0; }
@@ -1593,18 +1643,12 @@ __device__ void iteration_epilogue(const Params& P, dscr_scalars* sc, double s_q
     const int algo = P.algo;
     const int mode = sc->mode;
     if (mode != MODE_FIXUP) {
-        if (sc->nonfinite) {
-            sc->status = DSCR_ENONFINITE;
-            sc->stop = DSCR_STOP_ERROR;
-            set_cond(P, 0);
-            return;
-        }
-        if (sc->status != DSCR_OK) {   // radius guard tripped in K1
-            sc->stop = DSCR_STOP_ERROR;
-            set_cond(P, 0);
-            return;
-        }
-        if (algo == DSCR_ISTA || algo == DSCR_FISTA) {
+        // reference order: the backtracking loop first (a non-finite candidate fails the
+        // majorization test and is retried with a larger L, solvers.py:176-187), then the
+        // finiteness check of the accepted step (solvers.py:157-159, 196), then the screening
+        // radius guard (screening.py:199-205)
+        const bool bt = (algo == DSCR_ISTA || algo == DSCR_FISTA);
+        if (bt) {
             // majorization test of the backtracking step (solvers.py:176-187)
             const double f0 = 0.5 * sc->theta_sq;
             const double fc = 0.5 * s_qa2;
@@ -1624,6 +1668,19 @@ __device__ void iteration_epilogue(const Params& P, dscr_scalars* sc, double s_q
                 set_cond(P, 1);
                 return;
             }
+        }
+        if (sc->nonfinite) {
+            sc->status = DSCR_ENONFINITE;
+            sc->stop = DSCR_STOP_ERROR;
+            set_cond(P, 0);
+            return;
+        }
+        if (sc->status != DSCR_OK) {   // radius guard tripped in K1
+            sc->stop = DSCR_STOP_ERROR;
+            set_cond(P, 0);
+            return;
+        }
+        if (bt) {
             if (sc->dropped_nz && !P.onecoll) {
                 // resid must be recomputed on the reduced iterate (solvers.py:354-355)
                 sc->spare = s_tn2;
@@ -1815,7 +1872,12 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
     pdl_wait();
     pdl_trigger();
     dscr_scalars* sc = P.sc;
-    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->stop || sc->t >= sc->run_limit) {
+        // stopped earlier in this trip (K1: radius guard, non-finite iterate) or before it: end
+        // the WHILE loop here too -- the epilogue below is skipped, so nothing else would
+        if (blockIdx.x == 0 && threadIdx.x == 0) set_cond(P, 0u);
+        return;
+    }
     if (sc->mode == MODE_STATIC) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 6);
     k3b_body(P, blockIdx.x);
@@ -1989,16 +2051,9 @@ __global__ void __launch_bounds__(NT) k_init_scalars(Params P) {
     }
 }
 
-// out[j] = D[:, j] . v for all local columns (setup correlations, dictionary.py:94)
 template <typename T>
-__global__ void __launch_bounds__(NT, 2) k_correlate(const T* __restrict__ D, int ldd, int n, int k,
-                                                  const double* __restrict__ v, double* out,
-                                                  const int* skip_flag, float l2_keep) {
-    extern __shared__ double s_v[];
-    if (skip_flag && *skip_flag) return;
-    const uint64_t pol = make_policy(l2_keep);
-    for (int i = threadIdx.x; i < ldd; i += NT) s_v[i] = (i < n) ? v[i] : 0.0;
-    __syncthreads();
+__device__ __forceinline__ void k_correlate_cols(const T* __restrict__ D, int ldd, int n, int k, const double* sv,
+                                                 double* out, uint64_t pol) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * NT) >> 5;
@@ -2008,7 +2063,7 @@ __global__ void __launch_bounds__(NT, 2) k_correlate(const T* __restrict__ D, in
 #pragma unroll
         for (int c = 0; c < 4; ++c) cols[c] = (j0 + c < k) ? D + (size_t)(j0 + c) * ldd : nullptr;
         double cs[4];
-        warp_dots<T, 4, K1Cfg<T>::U>(cols, n, s_v, lane, pol, cs);
+        warp_dots<T, 4, K1Cfg<T>::U>(cols, n, sv, lane, pol, cs);
         if (lane < 4 && j0 + lane < k) {
             double c = cs[0];
 #pragma unroll
@@ -2016,6 +2071,24 @@ __global__ void __launch_bounds__(NT, 2) k_correlate(const T* __restrict__ D, in
             out[j0 + lane] = c;
         }
     }
+}
+
+// out[j] = D[:, j] . v for all local columns (setup correlations, dictionary.py:94)
+// VG: v read through L2 (dictionaries taller than the shared-memory staging buffer)
+template <typename T, bool VG = false>
+__global__ void __launch_bounds__(NT, 2) k_correlate(const T* __restrict__ D, int ldd, int n, int k,
+                                                  const double* __restrict__ v, double* out,
+                                                  const int* skip_flag, float l2_keep) {
+    extern __shared__ double s_v[];
+    if (skip_flag && *skip_flag) return;
+    const uint64_t pol = make_policy(l2_keep);
+    if (VG) {                  // tall dictionary: v read through L2 (its padding rows are zero)
+        k_correlate_cols<T>(D, ldd, n, k, v, out, pol);
+        return;
+    }
+    for (int i = threadIdx.x; i < ldd; i += NT) s_v[i] = (i < n) ? v[i] : 0.0;
+    __syncthreads();
+    k_correlate_cols<T>(D, ldd, n, k, s_v, out, pol);
 }
 
 // lambda_max with lowest-index argmax (problems.py:75-86), per-CTA partials + last CTA
@@ -2268,7 +2341,7 @@ struct Layout {
 };
 
 struct Geometry {
-    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1, tile;
+    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1, tile, theta_gl;
 };
 
 static int dtype_size(int dt) { return dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2); }
@@ -2357,7 +2430,8 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     cudaGetDevice(&dev);
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    g.smem1 = pr->ldd * (int)sizeof(double);
+    g.theta_gl = (size_t)pr->ldd * sizeof(double) > THETA_SMEM_MAX;   // tall: theta through L2
+    g.smem1 = g.theta_gl ? 16 : pr->ldd * (int)sizeof(double);
     {   // K1 tiled path for short columns (DSCR_K1_TILE=0 forces the per-warp column path)
         const int segr = 32 * (32 / dtype_size(pr->dtype)) * (pr->dtype == DSCR_F64 ? K1Cfg<double>::U : 1);
         const int nseg = (pr->n_rows + segr - 1) / segr;
@@ -2444,7 +2518,6 @@ struct dscr_solver {
     void* comm = nullptr;
     bool pdl = false;   // chain kernels launched with programmatic dependent launch
     void** peer_tab_dev = nullptr;   // device copy of the peer pointer table
-    unsigned long long peer_seq = 0;  // exchange sequence number (host side, one per exchange)
 };
 
 extern "C" const char* dscr_last_error(void) { return err_store().c_str(); }
@@ -2484,9 +2557,7 @@ static int validate(const dscr_problem_desc* pr, const dscr_config* cfg, int* n_
     if (pr->dtype < DSCR_F64 || pr->dtype > DSCR_BF16) return set_inval("unknown dtype");
     if (pr->n_rows < 1 || pr->n_cols < 1) return set_inval("dictionary must have at least one row and one column");
     if (pr->ldd < pr->n_rows || pr->ldd % 16) return set_inval("ldd must be >= n_rows and a multiple of 16");
-    // K1 stages theta (ldd doubles) in shared memory next to ~5 KB of static state
-    if ((size_t)pr->ldd * sizeof(double) + 8192 > 227 * 1024)
-        return set_inval("n_rows too large: theta (8 bytes per row) must fit in shared memory (n_rows <= 28000)");
+    if (pr->ldd > (1 << 28)) return set_inval("n_rows too large");
     if (!(pr->lam > 0)) return set_inval("lam must be strictly positive");
     if (!pr->D || !pr->y) return set_inval("null device pointer");
     if (cfg->algorithm < DSCR_ISTA || cfg->algorithm > DSCR_CP) return set_inval("unknown algorithm");
@@ -2582,27 +2653,34 @@ static int set_smem_attrs(size_t smem, bool k1 = true) {
     return DSCR_OK;
 }
 
+template <typename T>
+static int launch_correlate_t(const T* D, int ldd, int n, int k, const double* v, double* out, const int* skip,
+                              float keep, cudaStream_t s, int grid) {
+    const size_t smem = (size_t)ldd * 8;
+    if (smem > THETA_SMEM_MAX) {
+        k_correlate<T, true><<<grid, NT, 0, s>>>(D, ldd, n, k, v, out, skip, keep);
+    } else {
+        int rc;
+        if ((rc = set_smem_attrs<T>(smem, false))) return rc;
+        k_correlate<T><<<grid, NT, smem, s>>>(D, ldd, n, k, v, out, skip, keep);
+    }
+    return DSCR_OK;
+}
+
+// v: ldd doubles (rows n..ldd-1 zero)
 static int launch_correlate(int dtype, const void* D, int ldd, int n, int k, const double* v, double* out,
                             const int* skip, float keep, cudaStream_t s) {
     int dev = 0, sms = 148;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    const size_t smem = (size_t)ldd * 8;
     const int grid = std::max(1, std::min((k + 4 * NW - 1) / (4 * NW), sms * 2));
     int rc;
     switch (dtype) {
-        case DSCR_F64:
-            if ((rc = set_smem_attrs<double>(smem, false))) return rc;
-            k_correlate<double><<<grid, NT, smem, s>>>((const double*)D, ldd, n, k, v, out, skip, keep);
-            break;
-        case DSCR_F32:
-            if ((rc = set_smem_attrs<float>(smem, false))) return rc;
-            k_correlate<float><<<grid, NT, smem, s>>>((const float*)D, ldd, n, k, v, out, skip, keep);
-            break;
-        default:
-            if ((rc = set_smem_attrs<__nv_bfloat16>(smem, false))) return rc;
-            k_correlate<__nv_bfloat16><<<grid, NT, smem, s>>>((const __nv_bfloat16*)D, ldd, n, k, v, out, skip, keep);
+        case DSCR_F64: rc = launch_correlate_t((const double*)D, ldd, n, k, v, out, skip, keep, s, grid); break;
+        case DSCR_F32: rc = launch_correlate_t((const float*)D, ldd, n, k, v, out, skip, keep, s, grid); break;
+        default: rc = launch_correlate_t((const __nv_bfloat16*)D, ldd, n, k, v, out, skip, keep, s, grid);
     }
+    if (rc) return rc;
     CK(cudaGetLastError());
     return DSCR_OK;
 }
@@ -2730,6 +2808,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.max_iters = cfg->max_iters;
     P.G = g.G; P.cap = g.cap; P.TR = g.TR; P.R = g.R; P.P = g.P; P.G3b = g.G3b;
     P.k1_tile = g.tile; P.max_gsize = g.max_gsize;
+    P.theta_gl = g.theta_gl;
     P.min_cols = MIN_COLS_PER_SPLIT;
     P.k1_ilv = 1;   // measured on c4: K1 1241 -> 1222 us (DSCR_K1_INTERLEAVE=0 restores contiguous passes)
     if (const char* ei = getenv("DSCR_K1_INTERLEAVE")) P.k1_ilv = atoi(ei);
@@ -2748,10 +2827,13 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
         cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
         cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int occ = pers_occupancy(pr->dtype, pr->n_groups > 0, g.smem1);
-        P.persistent = coop && occ * sms >= g.G && g.G <= PERS_MAX_G && env && strcmp(env, "persistent") == 0;
+        P.persistent = coop && occ * sms >= g.G && g.G <= PERS_MAX_G && !g.theta_gl && env &&
+                       strcmp(env, "persistent") == 0;
     }
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
     if (const char* ek = getenv("DSCR_L2_KEEP")) P.l2_keep = (float)atof(ek);   // experiment knob
+    P.sup_keep = (P.l2_keep < 1.0f && pr->n_groups == 0) ? 1 : 0;
+    if (const char* es = getenv("DSCR_SUP_KEEP")) P.sup_keep = atoi(es);
 
     cudaStream_t us = (cudaStream_t)stream;
     // smem attributes for the K1 instantiations
@@ -2993,8 +3075,8 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
         case DSCR_PH_K3X_REDUCE: {
             if (!P.peer_tab || !P.onecoll) return set_inval("peer exchange needs dscr_solver_set_peers and one-collective mode");
             const int grid = std::max(1, std::min((P.peer_len + NT - 1) / NT, 148));
-            if (phase == DSCR_PH_K3X_PUSH) k3x_push<<<grid, NT, 0, s>>>(P, ++h->peer_seq);
-            else k3x_reduce<<<grid, NT, 0, s>>>(P, h->peer_seq);
+            if (phase == DSCR_PH_K3X_PUSH) k3x_push<<<grid, NT, 0, s>>>(P);
+            else k3x_reduce<<<grid, NT, 0, s>>>(P);
             break;
         }
         case DSCR_PH_K3B:
@@ -3030,7 +3112,7 @@ int dscr_solver_set_peers(dscr_solver* h, int rank, int world, void* const* recv
     h->P.onecoll = 1;
     h->P.oc_rank = rank;
     h->P.oc_world = world;
-    h->peer_seq = 0;
+    CK(cudaMemset(h->P.tickets + 8, 0, sizeof(unsigned long long)));   // exchange sequence number
     return DSCR_OK;
 }
 

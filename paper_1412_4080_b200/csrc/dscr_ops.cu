@@ -41,25 +41,33 @@ static int sm_count() {
     return sms;
 }
 
-template <typename T>
+// VG: the vectors are read through L2 (too tall for shared memory); they then need zero rows
+// n..roundup(n, 16)-1, as every ldd-padded vector of the library has.
+template <typename T, bool VG = false>
 __global__ void __launch_bounds__(NT) k_corr(const T* __restrict__ D, int ldd, int n, int k,
                                              const double* __restrict__ v, double* out, int nvec,
                                              int ldv, int ldo) {
     extern __shared__ double s_v[];
     const uint64_t pol = make_policy(0.5f);
-    for (int q = 0; q < nvec; ++q)
-        for (int i = threadIdx.x; i < ldd; i += NT) s_v[q * ldd + i] = (i < n) ? v[(size_t)q * ldv + i] : 0.0;
-    __syncthreads();
+    if (!VG) {
+        for (int q = 0; q < nvec; ++q)
+            for (int i = threadIdx.x; i < ldd; i += NT) s_v[q * ldd + i] = (i < n) ? v[(size_t)q * ldv + i] : 0.0;
+        __syncthreads();
+    }
+    const double* vb = VG ? v : s_v;
+    const size_t vs = VG ? (size_t)ldv : (size_t)ldd;
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * NT + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * NT) >> 5;
     for (int j = gw; j < k; j += nwarps) {
         for (int q = 0; q < nvec; ++q) {
-            double c = warp_dot<T, 2>(D + (size_t)j * ldd, n, s_v + (size_t)q * ldd, lane, pol);
+            double c = warp_dot<T, 2>(D + (size_t)j * ldd, n, vb + q * vs, lane, pol);
             if (lane == 0) out[(size_t)q * ldo + j] = c;
         }
     }
 }
+
+constexpr size_t CORR_SMEM_MAX = 227 * 1024 - 1024;   // larger vector sets are read through L2
 
 // Split-K GEMV: CTA (tile, split) accumulates rows [tile*TR, +TR) of
 // D[:, cols of split] x[cols of split, q] in fp64 and writes a partial vector;
@@ -390,9 +398,13 @@ template <typename T>
 static int corr_launch(const void* D, int ldd, int n, int k, const double* v, double* out, int nvec,
                        int ldv, int ldo, cudaStream_t s) {
     const size_t smem = (size_t)ldd * 8 * nvec;
-    OCK(cudaFuncSetAttribute(k_corr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int grid = std::max(1, std::min((k + NW - 1) / NW, sm_count() * 4));
-    k_corr<T><<<grid, NT, smem, s>>>((const T*)D, ldd, n, k, v, out, nvec, ldv, ldo);
+    if (smem > CORR_SMEM_MAX) {
+        k_corr<T, true><<<grid, NT, 0, s>>>((const T*)D, ldd, n, k, v, out, nvec, ldv, ldo);
+    } else {
+        OCK(cudaFuncSetAttribute(k_corr<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_corr<T><<<grid, NT, smem, s>>>((const T*)D, ldd, n, k, v, out, nvec, ldv, ldo);
+    }
     OCK(cudaGetLastError());
     return DSCR_OK;
 }
@@ -743,7 +755,7 @@ int dscr_operator_norm(int dtype, const void* D, int ldd, int n, int k, double t
     double* part = (double*)(base + opart);
     double* H = (double*)(base + oh);
     // function attributes before capture
-    if (!gram) {
+    if (!gram && (size_t)ldd * 8 * nvec <= CORR_SMEM_MAX) {
         const size_t smem = (size_t)ldd * 8 * nvec;
         if (dtype == DSCR_F64) OCK(cudaFuncSetAttribute(k_corr<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         else if (dtype == DSCR_F32) OCK(cudaFuncSetAttribute(k_corr<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

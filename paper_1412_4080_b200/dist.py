@@ -61,14 +61,20 @@ def _allreduce(tensor, op, pg):
     dist.all_reduce(tensor, op=op, group=pg)
 
 
-def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collectives=2):
+def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collectives=2, graph=None):
     """Run a sharded solve: setup exchange, then trips with two collectives (MAX after K1, SUM
     after K3A), with ``collectives="peer"`` one exchange per trip through peer memory (device
     stores into every peer's buffer + arrival flags, no host collective), or, with
     ``collectives=1``, one SUM per trip (rank-slot gather of the MAX
     quantities and test extremes, residuals on the unreduced iterate, FIXUP trip when a rank
     screens a unit carrying a nonzero coefficient; SURVEY §7 hard part 2).  The dome test
-    always uses two."""
+    always uses two.
+
+    ``graph`` (default: whenever the backend can, i.e. a GPU shard with NCCL or no process
+    group): the per-trip phase launches and collectives are captured once into a CUDA graph of
+    ``chunk`` trips and replayed, two replays in flight, until the device stop flag is set --
+    no per-phase host launches.  Every rank computes the same stop, so all ranks replay the
+    same number of times and their captured collectives match."""
     import torch
     import torch.distributed as dist
     MAX, SUM = dist.ReduceOp.MAX, dist.ReduceOp.SUM
@@ -115,33 +121,41 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collect
     vec_end = nat.CM_VEC + 2 * backend.ldd
     # two collectives: scalars + vector; one collective: also the rank slots (gather by SUM)
     sum_sec = comm[nat.CM_SUM: vec_end + (nat.OC_SLOT * world if one else 0)]
-    trips = 0
-    while True:
-        sc = backend.scalars()
-        if sc.stop != nat.STOP_RUNNING or sc.t >= cfg.max_iters:
-            break
-        for _ in range(chunk):
-            backend.phase(nat.PH_K1)
-            if one:
-                backend.phase(nat.PH_K2S)
-                backend.phase(nat.PH_K3A)
-                backend.phase(nat.PH_K3S)
-                if peer:   # the exchange runs on the devices: stores into peer memory, flags
-                    backend.phase(nat.PH_K3X_PUSH)
-                    backend.phase(nat.PH_K3X_REDUCE)
-                else:
-                    _allreduce(sum_sec, SUM, pg)
-                backend.phase(nat.PH_K1R1)
-                backend.phase(nat.PH_K2C)
+    def trip():
+        backend.phase(nat.PH_K1)
+        if one:
+            backend.phase(nat.PH_K2S)
+            backend.phase(nat.PH_K3A)
+            backend.phase(nat.PH_K3S)
+            if peer:   # the exchange runs on the devices: stores into peer memory, flags
+                backend.phase(nat.PH_K3X_PUSH)
+                backend.phase(nat.PH_K3X_REDUCE)
             else:
-                _allreduce(max_sec, MAX, pg)
-                backend.phase(nat.PH_K1R)
-                backend.phase(nat.PH_K2)
-                backend.phase(nat.PH_K3A)
-                backend.phase(nat.PH_K3S)
                 _allreduce(sum_sec, SUM, pg)
-            backend.phase(nat.PH_K3B)
-            trips += 1
+            backend.phase(nat.PH_K1R1)
+            backend.phase(nat.PH_K2C)
+        else:
+            _allreduce(max_sec, MAX, pg)
+            backend.phase(nat.PH_K1R)
+            backend.phase(nat.PH_K2)
+            backend.phase(nat.PH_K3A)
+            backend.phase(nat.PH_K3S)
+            _allreduce(sum_sec, SUM, pg)
+        backend.phase(nat.PH_K3B)
+
+    if graph is None:
+        graph = getattr(backend, "can_capture", lambda _pg: False)(pg)
+    if graph:
+        # `chunk` trips (phase kernels + the collectives) captured once as a CUDA graph and
+        # replayed until the device stop flag is set; trips after the stop return at entry
+        backend.run_captured(trip, chunk)
+    else:
+        while True:
+            sc = backend.scalars()
+            if sc.stop != nat.STOP_RUNNING or sc.t >= cfg.max_iters:
+                break
+            for _ in range(chunk):
+                trip()
     backend.one_collective = one
     return backend.scalars()
 
@@ -164,6 +178,9 @@ class GpuShard:
         self.ldd = problem_local.dictionary.ldd
         self.phase_calls = 0          # dscr_solver_phase launches (each enqueues >= 1 kernel)
         self.one_collective = False
+        self.launch_sptr = self.eng.sptr   # stream the phases launch on (the capture stream while capturing)
+        self.graph_trips = 0
+        self.graph_replays = 0
 
     def set_collectives(self, rank, world, one):
         nat.check(self.eng.L.dscr_solver_set_collectives(self.eng.h, int(rank), int(world), 1 if one else 0))
@@ -202,8 +219,60 @@ class GpuShard:
         self.peer_key = (rank, world)
 
     def phase(self, ph):
-        nat.check(self.eng.L.dscr_solver_phase(self.eng.h, int(ph), self.eng.sptr))
+        nat.check(self.eng.L.dscr_solver_phase(self.eng.h, int(ph), self.launch_sptr))
         self.phase_calls += 1
+
+    def can_capture(self, pg):
+        """Trips can be graph-captured with no process group or an NCCL one (gloo runs on the
+        host); DSCR_SHARDED_GRAPH=0 keeps the per-phase host loop."""
+        import os
+        import torch.distributed as dist
+        if os.environ.get("DSCR_SHARDED_GRAPH", "1") == "0":
+            return False
+        return pg is None or dist.get_backend(pg) == "nccl"
+
+    def run_captured(self, trip, chunk):
+        """Capture `chunk` trips once (on a side stream: kernels are recorded, not run), then
+        replay the graph on the engine's stream until the stop flag is set.  The stop flag and
+        iteration counter of each replay are copied to pinned memory behind it; the host waits
+        for replay i-1 while replay i runs, so the device never idles on the host."""
+        torch = self.torch
+        eng = self.eng
+        cs = torch.cuda.Stream(device=eng.device)
+        cs.wait_stream(eng.stream)
+        g = torch.cuda.CUDAGraph()
+        self.launch_sptr = C.c_void_p(cs.cuda_stream)
+        calls0 = self.phase_calls
+        try:
+            with torch.cuda.graph(g, stream=cs):
+                for _ in range(chunk):
+                    trip()
+        finally:
+            self.launch_sptr = eng.sptr
+        self.graph_trips = chunk
+        sc_dev = eng.view(eng.bufs.scalars, 8, torch.int32)        # t, run_limit, max_iters, mode, stop, ...
+        pinned = torch.zeros((2, 8), dtype=torch.int32, pin_memory=True)
+        events = [torch.cuda.Event(), torch.cuda.Event()]
+        replays = 0
+        with torch.cuda.stream(eng.stream):
+            pending = []
+            while True:
+                slot = replays & 1
+                g.replay()
+                pinned[slot].copy_(sc_dev, non_blocking=True)
+                events[slot].record(eng.stream)
+                pending.append(slot)
+                replays += 1
+                if len(pending) == 2:
+                    old = pending.pop(0)
+                    events[old].synchronize()
+                    if int(pinned[old, 4]) != nat.STOP_RUNNING:
+                        break
+            eng.stream.synchronize()
+        self.graph_replays = replays
+        per_graph = self.phase_calls - calls0      # phase launches recorded into the graph
+        self.phase_calls = calls0 + replays * per_graph
+        del g
 
     def scalars(self):
         return self.eng.scalars()
@@ -276,9 +345,10 @@ def global_kept(rows, pg):
     return rows
 
 
-def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2):
+def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2, graph=None):
     """Solve `problem` with its columns sharded over the ranks of `pg` (None: single rank,
-    split phases without collectives).  Every rank gets the full SolveResult."""
+    split phases without collectives).  Every rank gets the full SolveResult.  ``graph``: see
+    ``orchestrate`` (None: capture the trips whenever the process group allows it)."""
     import torch.distributed as dist
     cfg.validate(problem.kind)
     world = dist.get_world_size(pg) if pg is not None else 1
@@ -310,7 +380,8 @@ def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2):
     stop = torch.cuda.Event(enable_timing=True)
     try:
         start.record(shard.eng.stream)
-        sc = orchestrate(shard, cfg, problem.lam, pg, gw, chunk, collectives)
+        sc = orchestrate(shard, cfg, problem.lam, pg, gw, chunk, collectives, graph)
+        replays = shard.graph_replays
         stop.record(shard.eng.stream)
         stop.synchronize()
         device_s = start.elapsed_time(stop) / 1e3
@@ -352,11 +423,14 @@ def run_sharded(problem, cfg, pg=None, device=None, chunk=8, collectives=2):
         trace.support.append(int(r[nat.TR_SUPPORT]))
         trace.L.append(float(r[nat.TR_L]))
     if sc.trivial:
-        return SolveResult(np.zeros(k), 0, trace, 0.5 * float(problem.y @ problem.y),
-                           ScreenState(np.arange(k, dtype=np.int64), np.empty(0, np.int64), cfg.test),
-                           lambda_max=float(sc.lmax), stop_reason="trivial", device_seconds=device_s)
-    final = trace.objective[-1] if trace.objective else 0.5 * float(problem.y @ problem.y)
-    return SolveResult(x_star, int(sc.t), trace, final,
-                       ScreenState(np.flatnonzero(mask).astype(np.int64), kept, cfg.test),
-                       lambda_max=float(sc.lmax), gap=float(sc.gap),
-                       stop_reason=_STOP_NAMES.get(sc.stop, "running"), device_seconds=device_s)
+        res = SolveResult(np.zeros(k), 0, trace, 0.5 * float(problem.y @ problem.y),
+                          ScreenState(np.arange(k, dtype=np.int64), np.empty(0, np.int64), cfg.test),
+                          lambda_max=float(sc.lmax), stop_reason="trivial", device_seconds=device_s)
+    else:
+        final = trace.objective[-1] if trace.objective else 0.5 * float(problem.y @ problem.y)
+        res = SolveResult(x_star, int(sc.t), trace, final,
+                          ScreenState(np.flatnonzero(mask).astype(np.int64), kept, cfg.test),
+                          lambda_max=float(sc.lmax), gap=float(sc.gap),
+                          stop_reason=_STOP_NAMES.get(sc.stop, "running"), device_seconds=device_s)
+    res.graph_replays = replays         # trip-graph replays of this rank (0: per-phase host loop)
+    return res

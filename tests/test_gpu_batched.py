@@ -141,6 +141,7 @@ def test_corr_exact_rejects_bad_shapes():
 import paper_1412_4080_b200 as ds  # noqa: E402
 from paper_1412_4080_b200 import workloads as wl  # noqa: E402
 from paper_1412_4080_b200.batched import solve_batched  # noqa: E402
+from oracle import batched_oracle as bo  # noqa: E402
 from oracle import screen_oracle as so  # noqa: E402
 
 
@@ -152,27 +153,32 @@ def _batch_problem(n, k, b, ratio, seed=0):
     return w, dic, D64, L
 
 
-@pytest.mark.parametrize("ratio,splits,tol", [(0.4, 1, 2e-2), (0.4, 2, 1e-4), (0.85, 2, 1e-4)])
-def test_batched_fista_matches_oracle(ratio, splits, tol):
+@pytest.mark.parametrize("ratio,splits", [(0.4, 1), (0.4, 2), (0.85, 1), (0.85, 2)])
+def test_batched_fista_matches_oracle(ratio, splits):
+    """Per observation: the same screened set as the operand-precision oracle (theta rounded to
+    one / two bf16 terms, everything else fp64: oracle/batched_oracle.py), objective to 1e-7
+    and x to 2e-4 of it (fp32 accumulation in the tensor cores); against the reference's fp64
+    algorithm the objective agrees to 1e-6 and the screened set is a subset of its set (the
+    dual scaling's correlation bound carries the rigorous bf16/fp32 error term, so the device
+    never screens more)."""
     w, dic, D64, L = _batch_problem(128, 1024, 256, ratio)
-    res = solve_batched(dic, w.y, w.lam, L, iterations=100, test="dst3", splits=splits)
+    res = solve_batched(dic, w.y, w.lam, L, iterations=100, test="dst3", splits=splits, masks=True)
     assert res.iterations == 100
-    worst_f = 0.0
+    worst_f, worst_fr = 0.0, 0.0
     for j in range(0, 256, 17):
-        op = so.make_problem(D64, w.y[:, j], w.lam[j])
-        ref = so.solve(op, so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=100,
-                                     rel_tol=1e-300, L0=L, norm_aware=True))
-        f = res.objective[j]
-        worst_f = max(worst_f, abs(f - ref.final_objective) / ref.final_objective)
+        y, lam = w.y[:, j], float(w.lam[j])
+        emu = bo.solve_bf16(D64, y, lam, L, 100, splits=splits)
+        ref = so.solve(so.make_problem(D64, y, lam), so.Config(algorithm="fista", strategy="dynamic", test="dst3",
+                                                                max_iters=100, rel_tol=1e-300, L0=L, norm_aware=True))
         x = res.x_dense(j, 1024)
-        assert np.linalg.norm(x - ref.x_star) <= tol * 10 * max(np.linalg.norm(ref.x_star), 1e-12)
-        ref_kept = 1024 - ref.eliminated.size
-        if splits == 1:
-            # the bf16 error bound inflates the dual-scaling bound: the screen is more conservative
-            assert res.kept[j] >= ref_kept - 2
-        else:
-            assert abs(res.kept[j] - ref_kept) <= 2
-    assert worst_f <= tol, worst_f
+        worst_f = max(worst_f, abs(res.objective[j] - emu.objective) / emu.objective)
+        worst_fr = max(worst_fr, abs(res.objective[j] - ref.final_objective) / ref.final_objective)
+        assert np.linalg.norm(x - emu.x) <= 2e-4 * max(np.linalg.norm(emu.x), 1e-12)
+        elim = res.eliminated(j)
+        assert np.array_equal(elim, emu.eliminated), j
+        assert np.all(np.isin(elim, ref.eliminated)), j
+    assert worst_f <= 1e-7, worst_f
+    assert worst_fr <= 1e-6, worst_fr
     if ratio > 0.5:
         assert res.kept.min() < 1024      # screening fired somewhere
 
@@ -185,7 +191,7 @@ def test_batched_c5_shape_runs():
         op = so.make_problem(D64, w.y[:, j], w.lam[j])
         ref = so.solve(op, so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=100,
                                      rel_tol=1e-300, L0=L, norm_aware=True))
-        assert abs(res.objective[j] - ref.final_objective) <= 2e-2 * ref.final_objective
+        assert abs(res.objective[j] - ref.final_objective) <= 1e-6 * ref.final_objective
     print(f"\nc5-shape batch of 512: {res.device_seconds * 1e3:.1f} ms for 100 iterations")
 
 

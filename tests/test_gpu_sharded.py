@@ -3,6 +3,7 @@
 The sharded path must reproduce the fused single-GPU engine (same iterations,
 screened sets, objective to 1e-12)."""
 
+import itertools
 import os
 import socket
 
@@ -26,9 +27,10 @@ def _problem(ratio):
     return ds.Problem(ds.Dictionary(D), y, ratio * wl.lambda_star(D, y)), float(np.linalg.norm(D, 2))
 
 
+@pytest.mark.parametrize("graph", [True, False], ids=["trip-graph", "host-loop"])
 @pytest.mark.parametrize("collectives", [2, 1, "peer"], ids=["two-coll", "one-coll", "peer-exchange"])
 @pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c)) for c in CASES])
-def test_split_phases_match_fused(case, collectives):
+def test_split_phases_match_fused(case, collectives, graph):
     algo, test, ratio = case
     strategy = "static" if test.startswith("static") else "dynamic"
     test = test.split("-")[-1]
@@ -36,7 +38,8 @@ def test_split_phases_match_fused(case, collectives):
     cfg = ds.SolverConfig(algorithm=algo, strategy=strategy, test=test, max_iters=3000, rel_tol=1e-300,
                           L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9, op_norm=nrm)
     a = ds.run(p, cfg)
-    b = pdist.run_sharded(p, cfg, pg=None, collectives=collectives)
+    b = pdist.run_sharded(p, cfg, pg=None, collectives=collectives, graph=graph)
+    assert (b.graph_replays > 0) == graph
     assert a.iterations == b.iterations
     assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
     np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
@@ -74,11 +77,15 @@ def test_nccl_single_rank_group():
         cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test="dst3", max_iters=3000,
                               rel_tol=1e-300, L0=nrm * nrm * (1 + 1e-9), gap_tol=1e-9)
         a = ds.run(p, cfg)
-        for coll in (2, 1, "peer"):   # NCCL MAX + SUM, one NCCL SUM (slot gather), peer exchange
-            b = pdist.run_sharded(p, cfg, pg=dist.group.WORLD, collectives=coll)
+        # NCCL MAX + SUM, one NCCL SUM (slot gather), peer exchange; all-reduces captured in the
+        # trip graph or issued by the host loop
+        for coll, graph in itertools.product((2, 1, "peer"), (True, False)):
+            b = pdist.run_sharded(p, cfg, pg=dist.group.WORLD, collectives=coll, graph=graph)
+            assert (b.graph_replays > 0) == graph
             assert a.iterations == b.iterations
             np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
             assert b.trace.kept == a.trace.kept
+            assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
     finally:
         dist.destroy_process_group()
 
