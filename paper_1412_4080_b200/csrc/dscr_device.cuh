@@ -341,21 +341,7 @@ __device__ __forceinline__ double np_segment_sum(F get, int lo, int n) {
 // consumed, and the smem vector is read once per step for all C columns.
 template <typename T, int C, int U>
 __device__ __forceinline__ void warp_dots(const T* const (&col)[C], int n, const double* sv, int lane,
-                                          const uint64_t (&pols)[C], double (&out)[C]);
-
-template <typename T, int C, int U>
-__device__ __forceinline__ void warp_dots(const T* const (&col)[C], int n, const double* sv, int lane,
                                           uint64_t pol, double (&out)[C]) {
-    uint64_t pols[C];
-#pragma unroll
-    for (int c = 0; c < C; ++c) pols[c] = pol;
-    warp_dots<T, C, U>(col, n, sv, lane, pols, out);
-}
-
-// per-column L2 policies (e.g. keep the support columns resident for the residual pass)
-template <typename T, int C, int U>
-__device__ __forceinline__ void warp_dots(const T* const (&col)[C], int n, const double* sv, int lane,
-                                          const uint64_t (&pols)[C], double (&out)[C]) {
     constexpr int V = Vec<T>::V;
     double acc[C];
 #pragma unroll
@@ -367,7 +353,7 @@ __device__ __forceinline__ void warp_dots(const T* const (&col)[C], int n, const
             const int i = base + u * 32 * V;
 #pragma unroll
             for (int c = 0; c < C; ++c) {
-                if (i < n && col[c]) Vec<T>::load_raw(col[c] + i, d[u][c], pols[c]);
+                if (i < n && col[c]) Vec<T>::load_raw(col[c] + i, d[u][c], pol);
                 else Vec<T>::zero(d[u][c]);
             }
         }

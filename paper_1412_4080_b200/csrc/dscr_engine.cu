@@ -135,7 +135,6 @@ struct Params {
     int k1_ilv;        // K1 interleaved column passes over the identity list
     int k1_tile;       // K1 tiled path: row segments per column (0 = per-warp column path)
     int theta_gl;      // theta read through L2 instead of staged in shared memory (tall dictionaries)
-    int sup_keep;      // K1 reads support columns with evict_last (dictionary larger than L2)
     int max_iters;
     int G, cap, TR, R, P, G3b;
     int col_offset, group_offset;
@@ -373,17 +372,7 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
         const int f_beg = ilv ? b * NW * C : lo;
         const int f_end = ilv ? nchunk * NW * C : hi;
         const int f_step = ilv ? G * NW * C : NW * C;
-        // support residency (dictionaries larger than L2, identity list): columns whose atom
-        // carries a nonzero x or u are read with evict_last, so the residual pass (K3a) and the
-        // next K1 find them in L2; the flags of the next column group are loaded one group ahead
-        const bool skeep = P.sup_keep && ident && need_dot;
-        const uint64_t pol_keep = make_policy(1.0f);
         const int fhi = ilv ? nu : hi;
-        double nx_pre = 0.0, nu_pre = 0.0;
-        if (skeep && lane < C && f_beg + warp * C + lane < fhi) {
-            nx_pre = xc[f_beg + warp * C + lane];
-            if (algo == DSCR_FISTA || algo == DSCR_CP) nu_pre = uc[f_beg + warp * C + lane];
-        }
         for (int fb = f_beg; fb < f_end; fb += f_step) {
             const int f0 = fb + warp * C;
             int myj = -1;
@@ -403,22 +392,7 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
                 const T* cols[C];
 #pragma unroll
                 for (int c = 0; c < C; ++c) cols[c] = js[c] >= 0 ? D + (size_t)js[c] * P.ldd : nullptr;
-                uint64_t pols[C];
-                if (skeep) {
-                    const unsigned sm = __ballot_sync(0xffffffffu, myj >= 0 && (nx_pre != 0.0 || nu_pre != 0.0));
-                    const int fn = f0 + f_step + lane;           // next group's flags, in flight during the dots
-                    nx_pre = 0.0; nu_pre = 0.0;
-                    if (lane < C && fb + f_step < f_end && fn < fhi) {
-                        nx_pre = xc[fn];
-                        if (algo == DSCR_FISTA || algo == DSCR_CP) nu_pre = uc[fn];
-                    }
-#pragma unroll
-                    for (int c = 0; c < C; ++c) pols[c] = ((sm >> c) & 1u) ? pol_keep : pol;
-                } else {
-#pragma unroll
-                    for (int c = 0; c < C; ++c) pols[c] = pol;
-                }
-                warp_dots<T, C, K1Cfg<T>::U>(cols, P.n, s_theta, lane, pols, cs);
+                warp_dots<T, C, K1Cfg<T>::U>(cols, P.n, s_theta, lane, pol, cs);
             } else {
 #pragma unroll
                 for (int c = 0; c < C; ++c) cs[c] = js[c] >= 0 ? P.corr[js[c]] : 0.0;
@@ -1552,7 +1526,7 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     const int r0 = tile * P.TR + threadIdx.x * V;
     const bool rows_ok = r0 < P.n;
     const T* D = static_cast<const T*>(P.D);
-    const uint64_t pol = make_policy(P.sup_keep ? 1.0f : P.l2_keep);   // support columns: keep for the next K1
+    const uint64_t pol = make_policy(P.l2_keep);
     double acc_a[V], acc_b[V];
 #pragma unroll
     for (int v = 0; v < V; ++v) { acc_a[v] = 0.0; acc_b[v] = 0.0; }
@@ -2832,8 +2806,6 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     }
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
     if (const char* ek = getenv("DSCR_L2_KEEP")) P.l2_keep = (float)atof(ek);   // experiment knob
-    P.sup_keep = (P.l2_keep < 1.0f && pr->n_groups == 0) ? 1 : 0;
-    if (const char* es = getenv("DSCR_SUP_KEEP")) P.sup_keep = atoi(es);
 
     cudaStream_t us = (cudaStream_t)stream;
     // smem attributes for the K1 instantiations

@@ -54,7 +54,7 @@ def test_tall_solve_matches_oracle(algo, test, ratio):
 def test_tall_fp32_group_solve_matches_oracle():
     n, k, gs = 36000, 800, 8
     D, _ = _tall(n, k, 7)
-    groups = [list(range(g, g + gs)) for g in range(0, k, gs)]
+    groups = [np.arange(g, g + gs) for g in range(0, k, gs)]
     dic = ds.Dictionary(D.astype(np.float32), check_unit_norms=False, dtype="f32")
     D64 = dic.as_float64()
     part = ds.GroupPartition.build(dic, groups)
