@@ -113,6 +113,9 @@ typedef struct dscr_problem_desc {
     int32_t n_cols_total;
     int32_t group_offset;
     int32_t n_groups_total;
+    const double* col_norms;    /* n_cols (device), ||d_j||_2 of the stored columns for the norm-aware
+                                   tests, e.g. cached per dictionary from dscr_column_norms; null: the
+                                   solver's setup computes them (a full pass over D per solve) */
 } dscr_problem_desc;
 
 /* SolverConfig (solvers.py:44-63) plus the BASELINE duality-gap stop. */
@@ -190,6 +193,9 @@ int dscr_abi_version(void);
 
 /* ---- kernel-level entry points (unit parity) -------------------------- */
 
+/* out[j] = ||D[:,j]||_2 in fp64 for j < k (the norms the norm-aware tests use; a property of D
+ * alone, so callers cache it per dictionary and pass it as dscr_problem_desc.col_norms). */
+int dscr_column_norms(int dtype, const void* D, int ldd, int n, int k, double* out, void* stream);
 /* out[j] = D[:,j] . v  for j < k.  Replaces Dictionary.correlate (dictionary.py:89-94).
  * v holds n values; when 8*ldd exceeds the shared-memory staging buffer (n_rows > ~27000)
  * it is read through L2 and must hold ldd values with rows n..ldd-1 zero. */

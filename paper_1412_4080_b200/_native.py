@@ -13,6 +13,7 @@ import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_lib", "libdynscreen.so")
+CHECKED_PATH = os.path.join(HERE, "_lib", "libdynscreen_checked.so")   # DSCR_LIB=checked: bounds-checked build
 
 DSCR_OK, DSCR_EINVAL, DSCR_ENONFINITE, DSCR_ERADIUS, DSCR_ECUDA, DSCR_ENOCOMM = 0, -1, -2, -3, -4, -5
 F64, F32, BF16 = 0, 1, 2
@@ -30,7 +31,7 @@ OC_SLOT, OC_MAX_WORLD = 8, 64   # one-collective rank slots: 8 doubles per rank 
 CM_MAX, CM_SETUP, CM_SUM, CM_VEC = 0, 8, 16, 32
 
 ABI_FUNCTIONS = (
-    "dscr_last_error", "dscr_abi_version", "dscr_correlate", "dscr_apply_work_size", "dscr_apply", "dscr_prox_l1",
+    "dscr_last_error", "dscr_abi_version", "dscr_correlate", "dscr_column_norms", "dscr_apply_work_size", "dscr_apply", "dscr_prox_l1",
     "dscr_prox_group", "dscr_test_sphere", "dscr_test_dome", "dscr_test_group",
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
@@ -50,6 +51,7 @@ class ProblemDesc(C.Structure):
         ("group_ptr", C.c_void_p), ("group_w", C.c_void_p), ("group_snorm", C.c_void_p),
         ("col_offset", C.c_int32), ("n_cols_total", C.c_int32),
         ("group_offset", C.c_int32), ("n_groups_total", C.c_int32),
+        ("col_norms", C.c_void_p),
     ]
 
 
@@ -114,6 +116,7 @@ def _declare(lib):
         "dscr_last_error": (C.c_char_p, []),
         "dscr_abi_version": (i32, []),
         "dscr_correlate": (i32, [i32, vp, i32, i32, i32, vp, vp, vp]),
+        "dscr_column_norms": (i32, [i32, vp, i32, i32, i32, vp, vp]),
         "dscr_apply_work_size": (sz, [i32, i32, i32]),
         "dscr_apply": (i32, [i32, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
         "dscr_prox_l1": (i32, [vp, i64, dbl, vp, vp]),
@@ -172,13 +175,15 @@ def lib():
         return _lib
     with _lock:
         if _lib is None:
-            if not os.path.exists(LIB_PATH):
+            sel = os.environ.get("DSCR_LIB", "")
+            path = CHECKED_PATH if sel == "checked" else (sel if sel.endswith(".so") else LIB_PATH)
+            if not os.path.exists(path):
                 raise RuntimeError(
-                    f"libdynscreen.so not built ({LIB_PATH}); run `python -m paper_1412_4080_b200.build`")
+                    f"{os.path.basename(path)} not built ({path}); run `python -m paper_1412_4080_b200.build`")
             import torch
             if not torch.cuda.is_available():
                 raise RuntimeError("paper_1412_4080_b200 needs a CUDA device (sm_100a); none is available")
-            _lib = load_library()
+            _lib = load_library(path)
     return _lib
 
 

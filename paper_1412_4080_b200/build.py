@@ -18,6 +18,10 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_DIR = os.path.join(HERE, "_lib")
 LIB_PATH = os.path.join(LIB_DIR, "libdynscreen.so")
+# bounds-checked variant (device asserts on list / slot / support indices, -DDSCR_CHECKS); loaded
+# instead of the default library when DSCR_LIB=checked -- the substitute for compute-sanitizer,
+# which this GPU pool does not allow
+CHECKED_PATH = os.path.join(LIB_DIR, "libdynscreen_checked.so")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -32,17 +36,18 @@ def sources():
     return sorted(glob.glob(os.path.join(HERE, "csrc", "*.cu")))
 
 
-def needs_build():
-    if not os.path.exists(LIB_PATH):
+def needs_build(path=LIB_PATH):
+    if not os.path.exists(path):
         return True
-    t = os.path.getmtime(LIB_PATH)
+    t = os.path.getmtime(path)
     deps = sources() + glob.glob(os.path.join(HERE, "csrc", "*.cuh")) + [os.path.join(ROOT, "include", "dynscreen.h")]
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force=False, verbose=False):
-    if not force and not needs_build():
-        return LIB_PATH
+def build(force=False, verbose=False, checked=False):
+    out_path = CHECKED_PATH if checked else LIB_PATH
+    if not force and not needs_build(out_path):
+        return out_path
     os.makedirs(LIB_DIR, exist_ok=True)
     objs = []
     cmd_base = [nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
@@ -51,7 +56,9 @@ def build(force=False, verbose=False):
     if verbose:
         cmd_base += ["-Xptxas", "-v"]
     cmd_base += os.environ.get("DSCR_NVCC_EXTRA", "").split()   # experiment knobs (-D...), empty by default
-    build_dir = os.path.join(LIB_DIR, "obj")
+    if checked:
+        cmd_base += ["-DDSCR_CHECKS"]
+    build_dir = os.path.join(LIB_DIR, "obj_checked" if checked else "obj")
     os.makedirs(build_dir, exist_ok=True)
     procs = []
     for src in sources():
@@ -66,15 +73,15 @@ def build(force=False, verbose=False):
             raise RuntimeError(f"nvcc failed on {src}")
         if verbose and out:
             sys.stderr.write(out.decode())
-    tmp = LIB_PATH + ".tmp"
+    tmp = out_path + ".tmp"
     link = [nvcc_path(), *ARCH, "-shared", "-o", tmp, *objs, "-ldl"]
     p = subprocess.run(link, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)
     if p.returncode != 0:
         sys.stderr.write(p.stdout.decode())
         raise RuntimeError("nvcc link failed")
-    os.replace(tmp, LIB_PATH)
-    return LIB_PATH
+    os.replace(tmp, out_path)
+    return out_path
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv, checked="--checked" in sys.argv))

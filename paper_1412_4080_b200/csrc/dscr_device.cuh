@@ -7,6 +7,14 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <string>
+#ifdef DSCR_CHECKS
+#include <assert.h>
+// bounds checks of the checked build (libdynscreen_checked.so, DSCR_LIB=checked): a failed check
+// traps the kernel (cudaErrorAssert) with the file and line; compiled out of the default build
+#define DSCR_CHECK(cond) assert(cond)
+#else
+#define DSCR_CHECK(cond) ((void)0)
+#endif
 
 namespace dscr {
 

@@ -381,7 +381,9 @@ __device__ __forceinline__ void k1_body(const Params& P, int b, int G, double* s
                     myj = f0 + lane;
                 } else {
                     const int s = window_slot(off, P.G, s_off, s_s0, wend, f0 + lane);
+                    DSCR_CHECK(s >= 0 && s < P.G && f0 + lane - off[s] < P.cap);
                     myj = act[s * P.cap + (f0 + lane - off[s])];
+                    DSCR_CHECK(myj >= 0 && myj < P.kcols);
                 }
             }
             int js[C];
@@ -875,7 +877,10 @@ __device__ void k1_final(const Params& P, int G) {
 }
 
 
-template <typename T, bool GROUP>
+// TG (tall dictionaries, theta through L2) is a separate instantiation so the common kernel
+// keeps its code size (one k1_body copy: a second one in the same kernel measured +6% on c1 /
+// +18% on c2's K1)
+template <typename T, bool GROUP, bool TG = false>
 __global__ void __launch_bounds__(NT, K1Cfg<T>::MINB) k1_corr_update(Params P) {
     extern __shared__ double s_theta[];
     __shared__ int s_flag;
@@ -886,8 +891,8 @@ __global__ void __launch_bounds__(NT, K1Cfg<T>::MINB) k1_corr_update(Params P) {
     const int mode = sc->mode;
     if (mode == MODE_FIXUP || mode == MODE_STATIC) return;
     if (blockIdx.x == 0 && threadIdx.x == 0) stamp(P, 0);
-    if (P.k1_tile) k1_body_tile<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
-    else if (P.theta_gl) k1_body<T, GROUP, true>(P, blockIdx.x, gridDim.x, s_theta);
+    if (TG) k1_body<T, GROUP, true>(P, blockIdx.x, gridDim.x, s_theta);
+    else if (P.k1_tile) k1_body_tile<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
     else k1_body<T, GROUP>(P, blockIdx.x, gridDim.x, s_theta);
     if (!last_block(P.tickets + 0, gridDim.x, &s_flag)) return;
     k1_final<GROUP>(P, gridDim.x);
@@ -1173,7 +1178,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
             int tot;
             int pos = n_keep + block_exscan(nk, s_scan, &tot);
 #pragma unroll
-            for (int q = 0; q < Q; ++q) if (keep[q]) actn[pos++] = f0 + q;
+            for (int q = 0; q < Q; ++q) if (keep[q]) { DSCR_CHECK(pos < P.cap); actn[pos++] = f0 + q; }
             n_keep += tot;
         }
         if (!do_vec) continue;
@@ -1212,6 +1217,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
         for (int q = 0; q < Q; ++q) {
             if (!sup[q]) continue;
             const int j = f0 + q;
+            DSCR_CHECK(w < P.sup_cap && j >= 0 && j < P.kcols);
             if (keep[q]) { sidx[w] = j; sa[w] = cand[q]; sb[w] = bvq[q]; }
             else { sidx[w] = ~j; sa[w] = cand[q]; sb[w] = 0.0; }
             ++w;
@@ -1240,7 +1246,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
         if (do_list) {
             int tot;
             const int pos = block_exscan(keep ? 1 : 0, s_scan, &tot);
-            if (keep) actn[n_keep + pos] = unit;
+            if (keep) { DSCR_CHECK(n_keep + pos < P.cap && unit >= 0 && unit < P.n_units); actn[n_keep + pos] = unit; }
             n_keep += tot;
         }
         if (var == 2 && keep) kept_atoms += (double)(unit_atom_hi(P, unit) - unit_atom_lo(P, unit));
@@ -1297,6 +1303,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
         const int spos = block_exscan(my_sup, s_scan, &tot);
         if (my_sup && !GROUP) {   // single atom: values from registers
             const int w = n_sup + spos;
+            DSCR_CHECK(w < P.sup_cap);
             if (keep) { sidx[w] = unit; sa[w] = cand0; sb[w] = bv0; }
             else { sidx[w] = ~unit; sa[w] = cand0; sb[w] = 0.0; }
         } else if (my_sup) {
@@ -1322,8 +1329,9 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                     double bv = 0.0;
                     if (algo == DSCR_FISTA || algo == DSCR_CP) bv = gq;
                     else if (algo == DSCR_SPARSA) bv = cand - gq;
-                    if (cand != 0.0 || bv != 0.0) { sidx[w] = j; sa[w] = cand; sb[w] = bv; ++w; }
+                    if (cand != 0.0 || bv != 0.0) { DSCR_CHECK(w < P.sup_cap); sidx[w] = j; sa[w] = cand; sb[w] = bv; ++w; }
                 } else if (cand != 0.0) {
+                    DSCR_CHECK(w < P.sup_cap);
                     sidx[w] = ~j; sa[w] = cand; sb[w] = 0.0; ++w;
                 }
             }
@@ -1538,7 +1546,9 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
             const int f = c0 + i;
             const int s = window_slot(off, P.G, s_off, s_s0, wend, f);
             const size_t e = (size_t)s * P.sup_cap + (f - off[s]);
+            DSCR_CHECK(s >= 0 && s < P.G && f - off[s] >= 0 && f - off[s] < P.sup_cap);
             int idx = P.sidx[e];
+            DSCR_CHECK((idx < 0 ? ~idx : idx) < P.kcols);
             double a = P.sa[e], bb = P.sb[e];
             if (fix) {
                 if (idx < 0) a = 0.0;   // masked entry: excluded from the reduced iterate
@@ -2177,20 +2187,29 @@ __global__ void __launch_bounds__(NT) k_gst3_scalars(Params P) {
 
 // ||d_j||_2 in fp64 for the norm-aware tests (reduced-precision dictionaries)
 template <typename T>
-__global__ void __launch_bounds__(NT) k_colnorms(Params P) {
-    if (P.sc->stop) return;
-    const T* D = static_cast<const T*>(P.D);
+__device__ __forceinline__ void colnorms_body(const T* D, int ldd, int n, int k, double* out) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * NT + threadIdx.x) >> 5, nw = (gridDim.x * NT) >> 5;
-    for (int j = gw; j < P.kcols; j += nw) {
+    for (int j = gw; j < k; j += nw) {
         double acc = 0.0;
-        for (int i = lane; i < P.n; i += 32) {
-            const double d = elem<T>(D + (size_t)j * P.ldd + i);
+        for (int i = lane; i < n; i += 32) {
+            const double d = elem<T>(D + (size_t)j * ldd + i);
             acc = fma(d, d, acc);
         }
         acc = warp_sum(acc);
-        if (lane == 0) P.anorm[j] = sqrt(acc);
+        if (lane == 0) out[j] = sqrt(acc);
     }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_colnorms(Params P) {
+    if (P.sc->stop) return;
+    colnorms_body<T>(static_cast<const T*>(P.D), P.ldd, P.n, P.kcols, P.anorm);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(NT) k_colnorms_op(const T* D, int ldd, int n, int k, double* out) {
+    colnorms_body<T>(D, ldd, n, k, out);
 }
 
 // ||vec||^2 of the broadcast extremal atom (norm-aware DST3)
@@ -2567,6 +2586,18 @@ extern "C" size_t dscr_solver_workspace_size(const dscr_problem_desc* pr, const 
     return total;
 }
 
+// K1 kernel of a problem: dtype x (Lasso | groups) x (theta in shared memory | through L2)
+static void (*k1_kernel(int dtype, bool group, bool tall))(Params) {
+#define DSCR_K1_SEL(T) (group ? (tall ? k1_corr_update<T, true, true> : k1_corr_update<T, true>) \
+                              : (tall ? k1_corr_update<T, false, true> : k1_corr_update<T, false>))
+    switch (dtype) {
+        case DSCR_F64: return DSCR_K1_SEL(double);
+        case DSCR_F32: return DSCR_K1_SEL(float);
+        default: return DSCR_K1_SEL(__nv_bfloat16);
+    }
+#undef DSCR_K1_SEL
+}
+
 // Kernel launch with optional programmatic stream serialization (PDL edges when captured).
 template <typename... KArgs>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, size_t smem, cudaStream_t s, bool pdl,
@@ -2598,10 +2629,11 @@ static int launch_iteration(dscr_solver* h, const Params& P, cudaStream_t s, cud
     const bool pdl = h->pdl && !ev;   // timed per-kernel runs keep plain launches
     void (*k1)(Params);
     void (*k3a)(Params);
+    k1 = k1_kernel(P.dtype, group, P.theta_gl != 0);
     switch (P.dtype) {
-        case DSCR_F64: k1 = group ? k1_corr_update<double, true> : k1_corr_update<double, false>; k3a = k3a_residual<double>; break;
-        case DSCR_F32: k1 = group ? k1_corr_update<float, true> : k1_corr_update<float, false>; k3a = k3a_residual<float>; break;
-        default: k1 = group ? k1_corr_update<__nv_bfloat16, true> : k1_corr_update<__nv_bfloat16, false>; k3a = k3a_residual<__nv_bfloat16>;
+        case DSCR_F64: k3a = k3a_residual<double>; break;
+        case DSCR_F32: k3a = k3a_residual<float>; break;
+        default: k3a = k3a_residual<__nv_bfloat16>;
     }
     cudaError_t le = launch_pdl(k1, dim3(g.G), smem1, s, pdl, P);
     if (le != cudaSuccess) return set_err("K1 launch", le);
@@ -2695,7 +2727,7 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
             CK(cudaGetLastError());
             if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, P.l2_keep, s))) return rc;
         }
-        if (P.norm_aware) {
+        if (P.norm_aware && !h->prob.col_norms) {   // not cached by the caller: one pass over D
             const int cg = std::max(1, std::min((P.kcols + NW - 1) / NW, 2048));
             switch (P.dtype) {
                 case DSCR_F64: k_colnorms<double><<<cg, NT, 0, s>>>(P); break;
@@ -2721,6 +2753,25 @@ static int enqueue_setup(dscr_solver* h, cudaStream_t s) {
         }
     }
     return DSCR_OK;
+}
+
+template <typename T>
+static int launch_colnorms(const void* D, int ldd, int n, int k, double* out, cudaStream_t s) {
+    const int cg = std::max(1, std::min((k + NW - 1) / NW, 2048));
+    k_colnorms_op<T><<<cg, NT, 0, s>>>(static_cast<const T*>(D), ldd, n, k, out);
+    CK(cudaGetLastError());
+    return DSCR_OK;
+}
+
+extern "C" int dscr_column_norms(int dtype, const void* D, int ldd, int n, int k, double* out, void* stream) {
+    if (!D || !out || n < 1 || k < 1 || ldd < n) return set_inval("bad column-norm arguments");
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (dtype) {
+        case DSCR_F64: return launch_colnorms<double>(D, ldd, n, k, out, s);
+        case DSCR_F32: return launch_colnorms<float>(D, ldd, n, k, out, s);
+        case DSCR_BF16: return launch_colnorms<__nv_bfloat16>(D, ldd, n, k, out, s);
+        default: return set_inval("unknown dtype");
+    }
 }
 
 extern "C" {
@@ -2775,7 +2826,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.p3s = (double*)(base + o.p3s); P.tickets = (unsigned*)(base + o.tickets);
     P.trace = (double*)(base + o.trace);
     P.kts = (unsigned long long*)(base + o.kts);
-    P.anorm = (double*)(base + o.anorm);
+    P.anorm = pr->col_norms ? const_cast<double*>(pr->col_norms) : (double*)(base + o.anorm);
     P.comm = (double*)(base + o.comm);
     P.norm_aware = pr->norm_aware;
     P.max_kts = kts_slots(cfg);
@@ -2978,7 +3029,7 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
                 k_gst3_scalars<<<1, NT, 0, s>>>(P);
                 if ((rc = launch_correlate(P.dtype, P.D, P.ldd, P.n, P.kcols, P.vec, P.dn, stop_flag, P.l2_keep, s))) return rc;
             }
-            if (P.norm_aware) {
+            if (P.norm_aware && !h->prob.col_norms) {
                 const int cg = std::max(1, std::min((P.kcols + NW - 1) / NW, 2048));
                 switch (P.dtype) {
                     case DSCR_F64: k_colnorms<double><<<cg, NT, 0, s>>>(P); break;
@@ -3001,19 +3052,7 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
             break;
         case DSCR_PH_K1: {
             const size_t smem1 = (size_t)g.smem1;
-            switch (P.dtype) {
-                case DSCR_F64:
-                    if (group) k1_corr_update<double, true><<<g.G, NT, smem1, s>>>(P);
-                    else k1_corr_update<double, false><<<g.G, NT, smem1, s>>>(P);
-                    break;
-                case DSCR_F32:
-                    if (group) k1_corr_update<float, true><<<g.G, NT, smem1, s>>>(P);
-                    else k1_corr_update<float, false><<<g.G, NT, smem1, s>>>(P);
-                    break;
-                default:
-                    if (group) k1_corr_update<__nv_bfloat16, true><<<g.G, NT, smem1, s>>>(P);
-                    else k1_corr_update<__nv_bfloat16, false><<<g.G, NT, smem1, s>>>(P);
-            }
+            k1_kernel(P.dtype, group, P.theta_gl != 0)<<<g.G, NT, smem1, s>>>(P);
             break;
         }
         case DSCR_PH_K1R:

@@ -134,7 +134,10 @@ class Dictionary:
         return dev
 
     def drop_device(self):
+        """Forget every device copy (the dictionary, the per-partition arrays and column norms
+        the solver caches on it): the next solve uploads again."""
         self._dev.clear()
+        self.__dict__.pop("_problem_cache", None)
 
     # -- GPU-backed operators --------------------------------------------
     def apply(self, x):

@@ -180,6 +180,14 @@ class _DeviceDictionary:
             self.n_groups = part.n_groups
             self.group_ptr_host = ptr
         self.D = dic.device_data(device, self.perm)
+        self.col_norms = None
+        if dic.norm_aware:
+            # ||d_j|| of the stored (rounded) columns, a property of D alone: computed once per
+            # dictionary upload instead of in every solve's setup (8.6 GB pass on c4)
+            self.col_norms = torch.empty(self.k, dtype=torch.float64, device=device)
+            L = nat.lib()
+            nat.check(L.dscr_column_norms(dic.dtype_code, self.D.data_ptr(), self.ldd, self.n, self.k,
+                                          self.col_norms.data_ptr(), nat.stream_ptr()))
 
 
 class _DeviceProblem:
@@ -200,6 +208,7 @@ class _DeviceProblem:
         self.n, self.k, self.ldd = dd.n, dd.k, dd.ldd
         self.perm, self.n_groups, self.D = dd.perm, dd.n_groups, dd.D
         self.group_ptr, self.group_w, self.group_sn = dd.group_ptr, dd.group_w, dd.group_sn
+        self.col_norms = dd.col_norms
         if dd.n_groups:
             self.group_ptr_host = dd.group_ptr_host
         y = torch.zeros(self.ldd, dtype=torch.float64)
@@ -220,6 +229,7 @@ def _desc(problem, dp):
         d.group_ptr, d.group_w, d.group_snorm = dp.group_ptr.data_ptr(), dp.group_w.data_ptr(), dp.group_sn.data_ptr()
     d.col_offset, d.n_cols_total = 0, dp.k
     d.group_offset, d.n_groups_total = 0, dp.n_groups
+    d.col_norms = dp.col_norms.data_ptr() if dp.col_norms is not None else None
     return d
 
 
