@@ -147,9 +147,15 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collect
         graph = getattr(backend, "can_capture", lambda _pg: False)(pg)
     if graph:
         # `chunk` trips (phase kernels + the collectives) captured once as a CUDA graph and
-        # replayed until the device stop flag is set; trips after the stop return at entry
-        backend.run_captured(trip, chunk)
-    else:
+        # replayed until the device stop flag is set; trips after the stop return at entry.
+        # A capture that fails (before anything was replayed) falls back to the host loop.
+        try:
+            backend.run_captured(trip, chunk)
+        except _CaptureFailed as exc:
+            import sys
+            sys.stderr.write(f"dist: trip-graph capture failed ({exc.__cause__!r}); per-phase host loop\n")
+            graph = False
+    if not graph:
         while True:
             sc = backend.scalars()
             if sc.stop != nat.STOP_RUNNING or sc.t >= cfg.max_iters:
@@ -158,6 +164,10 @@ def orchestrate(backend, cfg, lam, pg=None, group_weights=None, chunk=8, collect
                 trip()
     backend.one_collective = one
     return backend.scalars()
+
+
+class _CaptureFailed(RuntimeError):
+    """The trip graph could not be captured (e.g. a collective backend without capture support)."""
 
 
 class GpuShard:
@@ -247,6 +257,9 @@ class GpuShard:
             with torch.cuda.graph(g, stream=cs):
                 for _ in range(chunk):
                     trip()
+        except Exception as exc:            # nothing was enqueued for execution: host loop instead
+            self.phase_calls = calls0
+            raise _CaptureFailed() from exc
         finally:
             self.launch_sptr = eng.sptr
         self.graph_trips = chunk
