@@ -223,6 +223,45 @@ int dscr_test_dome(const double* star_corr, const double* y_corr, const int32_t*
 int dscr_test_group(const double* w, const double* cnorm, const double* snorm,
                     const int32_t* kept_groups, int n_kept, double radius, uint8_t* mask,
                     void* stream);
+/* ---- inner seams of the iteration (SURVEY §8(b) kernel-level entry points) ----------------
+ * Values are indexed by atom (K-length arrays); `active` lists the atoms (or groups) to touch.
+ * The engine fuses the same arithmetic into its per-iteration kernels (K1: corr + prox,
+ * K2: test + compaction, K3: residual). */
+
+/* One proximal gradient step over the active atoms: corr_out[j] = D[:,j] . theta,
+ * x_out[j] = soft(v, thr) with v = point[j] - corr[j] / step (mult = 0: ISTA / FISTA / SpaRSA,
+ * solvers.py:178, 276) or v = point[j] - step * corr[j] (mult = 1: CP / TwIST, solvers.py:302,
+ * 242); u_out[j] = x_out + beta (x_out - x_prev[j]) if u_out (FISTA momentum, solvers.py:216-218).
+ * red_out[3] = max |corr|, corr . (x_out - point), ||x_out - point||^2 over the active atoms
+ * (dual-scaling bound screening.py:126-140; majorization terms of _backtrack solvers.py:176-183).
+ * theta: ldd doubles, rows n..ldd-1 zero.  Replaces update_ista / update_fista's step. */
+int dscr_corr_prox(int dtype, const void* D, int ldd, int n, const int32_t* active, int n_active,
+                   const double* theta, const double* point, const double* x_prev, double step, int mult, double thr,
+                   double beta, double* x_out, double* u_out, double* corr_out, double* red_out, void* stream);
+/* The group-Lasso step: correlations of `active_atoms`, then per active group g (contiguous atoms
+ * group_ptr[g]..group_ptr[g+1]) the block soft threshold x_g = v_g max(1 - thr w_g / ||v_g||, 0)
+ * with numpy's pairwise sum for the norm (GroupLayout.prox, dictionary.py:290-301);
+ * group_cnorm[i] = ||corr_g|| of active_groups[i]; red_out[0] = min w_g / ||corr_g|| over the
+ * active groups with ||corr_g|| > 0 (screening.py:143-165), red_out[1..2] as dscr_corr_prox. */
+int dscr_group_corr_prox(int dtype, const void* D, int ldd, int n, const int32_t* group_ptr,
+                         const int32_t* active_groups, int n_active, const int32_t* active_atoms, int n_atoms,
+                         const double* group_w, const double* theta, const double* point, const double* x_prev,
+                         double step, int mult, double thr, double beta, double* x_out, double* u_out,
+                         double* corr_out, double* group_cnorm, double* red_out, void* stream);
+/* Residuals over a compact support list (idx[e], x[e], u[e]): r_x = D_S x - y, r_u = D_S u - y
+ * (r_u / u optional), entries accumulated in list order per row; red_out[3] = ||r_x||^2,
+ * ||r_u||^2, r_u . y.  Replaces _residual / Dictionary.apply(x) - y (solvers.py:160-165,
+ * dictionary.py:82-87). */
+int dscr_residual(int dtype, const void* D, int ldd, int n, const int32_t* idx, int nnz, const double* x,
+                  const double* u, const double* y, double* r_x, double* r_u, double* red_out, void* stream);
+/* Order-preserving compaction of a kept list by a test mask (mask[i] = 1: screened):
+ * active_out = active[~mask], *n_out (device int) = its length.  Replaces screen_update's kept
+ * set (screening.py:104-112) and Dictionary.reduce's column selection (dictionary.py:99-117).
+ * `work`: dscr_compact_work_size(n) bytes of device memory. */
+size_t dscr_compact_work_size(int n);
+int dscr_compact(const int32_t* active, int n, const uint8_t* mask, int32_t* active_out, int32_t* n_out, void* work,
+                 size_t work_bytes, void* stream);
+
 /* Largest singular value of D by 2-vector block power iteration (dictionary.py:120-171);
  * blocking; `work` must hold dscr_operator_norm_work_size() bytes of device memory. */
 /* DSMX ingestion (dictionary.py:304-335: row-major little-endian fp64 payload): `nr` file rows

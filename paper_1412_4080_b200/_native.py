@@ -31,7 +31,8 @@ OC_SLOT, OC_MAX_WORLD = 8, 64   # one-collective rank slots: 8 doubles per rank 
 CM_MAX, CM_SETUP, CM_SUM, CM_VEC = 0, 8, 16, 32
 
 ABI_FUNCTIONS = (
-    "dscr_last_error", "dscr_abi_version", "dscr_correlate", "dscr_column_norms", "dscr_apply_work_size", "dscr_apply", "dscr_prox_l1",
+    "dscr_last_error", "dscr_abi_version", "dscr_correlate", "dscr_column_norms", "dscr_corr_prox",
+    "dscr_group_corr_prox", "dscr_residual", "dscr_compact_work_size", "dscr_compact", "dscr_apply_work_size", "dscr_apply", "dscr_prox_l1",
     "dscr_prox_group", "dscr_test_sphere", "dscr_test_dome", "dscr_test_group",
     "dscr_operator_norm_work_size", "dscr_operator_norm", "dscr_solver_workspace_size",
     "dscr_solver_create", "dscr_solver_setup", "dscr_solver_run", "dscr_solver_scalars",
@@ -117,6 +118,12 @@ def _declare(lib):
         "dscr_abi_version": (i32, []),
         "dscr_correlate": (i32, [i32, vp, i32, i32, i32, vp, vp, vp]),
         "dscr_column_norms": (i32, [i32, vp, i32, i32, i32, vp, vp]),
+        "dscr_corr_prox": (i32, [i32, vp, i32, i32, vp, i32, vp, vp, vp, dbl, i32, dbl, dbl, vp, vp, vp, vp, vp]),
+        "dscr_group_corr_prox": (i32, [i32, vp, i32, i32, vp, vp, i32, vp, i32, vp, vp, vp, vp, dbl, i32, dbl, dbl,
+                                       vp, vp, vp, vp, vp, vp]),
+        "dscr_residual": (i32, [i32, vp, i32, i32, vp, i32, vp, vp, vp, vp, vp, vp, vp]),
+        "dscr_compact_work_size": (sz, [i32]),
+        "dscr_compact": (i32, [vp, i32, vp, vp, vp, vp, sz, vp]),
         "dscr_apply_work_size": (sz, [i32, i32, i32]),
         "dscr_apply": (i32, [i32, vp, i32, i32, i32, vp, vp, vp, sz, vp]),
         "dscr_prox_l1": (i32, [vp, i64, dbl, vp, vp]),
