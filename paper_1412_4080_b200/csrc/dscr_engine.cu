@@ -135,6 +135,9 @@ struct Params {
     int k1_ilv;        // K1 interleaved column passes over the identity list
     int k1_tile;       // K1 tiled path: row segments per column (0 = per-warp column path)
     int theta_gl;      // theta read through L2 instead of staged in shared memory (tall dictionaries)
+    int f23;           // fused graph: K2 (test / compaction) and K3a-scan (residual) run concurrently
+    int P23;           // K3a-scan splits
+    int* p3c;          // [P23] support entries per K3a-scan split
     int max_iters;
     int G, cap, TR, R, P, G3b;
     int col_offset, group_offset;
@@ -1109,11 +1112,23 @@ __device__ __forceinline__ bool unit_test(const Params& P, const dscr_scalars* s
     return false;
 }
 
+// b value of an atom for the residual pass (D b - y is theta_{t+1} or, for SpaRSA, D s): FISTA
+// u = c + beta (c - x) (solvers.py:216-218), CP u = c + phi (c - x) (solvers.py:305-307),
+// SpaRSA s = c - x (solvers.py:272), none for ISTA / TwIST
+__device__ __forceinline__ double b_value(int algo, double c, double xc, double beta, double phi) {
+    if (algo == DSCR_FISTA) return c + beta * (c - xc);
+    if (algo == DSCR_CP) return c + phi * (c - xc);
+    if (algo == DSCR_SPARSA) return c - xc;
+    return 0.0;
+}
+
 // K2 per-CTA work: test, compaction into slot b, vectors, support list, partials.
 // Variants (P.k2v): 0 classic; 1 = K2S (one collective): no test, support list and vectors
 // over every active unit (the reduced list in a FIXUP trip), plus the largest test value over
 // units carrying a nonzero coefficient and the smallest over all units; 2 = K2C: test and
-// compaction only (after the collective), kept atoms counted.
+// compaction only (after the collective), kept atoms counted; 3 = K2F (single GPU, residual
+// pass running concurrently over the unreduced iterate): test, compaction, vectors and sums,
+// no support list; dropped = a screened unit carries a nonzero x or b (FIXUP trip).
 template <bool GROUP>
 __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     __shared__ int s_scan[2 * NW + 1];
@@ -1134,6 +1149,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     const bool test_on = (var == 1) ? false : (static_mode ? true : (P.strategy == DSCR_DYNAMIC));
     const bool do_list = (var != 1);                 // compaction into the next list
     const bool do_vec = !static_mode && var != 2;    // vectors, support list, sums
+    const bool do_sup = do_vec && var != 3;           // support list for K3a
     const bool want_ext = (var == 1) && P.strategy == DSCR_DYNAMIC && P.test != DSCR_DOME && !fix_pre;
     const int algo = P.algo;
     const double* xc = P.x[xi];
@@ -1200,6 +1216,8 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                 pen += fabs(c);
                 nnz += (c != 0.0) ? 1.0 : 0.0;
                 kept_atoms += 1.0;
+            } else if (var == 3) {
+                if (c != 0.0 || b_value(algo, c, xcv[q], beta, phi) != 0.0) dropped = 1.0;
             } else if (c != 0.0) {
                 dropped = 1.0;
                 sup[q] = keep_masked_a;
@@ -1211,6 +1229,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
             }
             ns += sup[q] ? 1 : 0;
         }
+        if (!do_sup) continue;
         int tot;
         int w = n_sup + block_exscan(ns, s_scan, &tot);
 #pragma unroll
@@ -1285,6 +1304,8 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                     if (!GROUP) pen += fabs(cand);
                     nnz += (cand != 0.0) ? 1.0 : 0.0;
                     kept_atoms += 1.0;
+                } else if (var == 3) {
+                    if (cand != 0.0 || b_value(algo, cand, xcj, beta, phi) != 0.0) dropped = 1.0;
                 } else {
                     if (cand != 0.0) { dropped = 1.0; if (keep_masked_a) ++my_sup; }
                 }
@@ -1299,6 +1320,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
                 if (carries) tmax = fmax(tmax, v);
             }
         }
+        if (!do_sup) continue;
         int tot;
         const int spos = block_exscan(my_sup, s_scan, &tot);
         if (my_sup && !GROUP) {   // single atom: values from registers
@@ -1341,7 +1363,7 @@ __device__ __forceinline__ void k2_body(const Params& P, int b, int G) {
     // per-CTA outputs
     if (threadIdx.x == 0) {
         if (do_list) P.act_cnt[p ^ 1][b] = n_keep;
-        if (do_vec) P.sup_cnt[b] = n_sup;
+        if (do_sup) P.sup_cnt[b] = n_sup;
     }
     if (!static_mode) {
         double v5[5] = {pen, nnz, kept_atoms, ssr, dropped};
@@ -1365,7 +1387,7 @@ __device__ void k2_final(const Params& P, int G) {
     const int var = P.k2v;
     const bool static_mode = (sc->mode == MODE_STATIC);
     const bool do_list = (var != 1);
-    const bool do_vec = !static_mode && var != 2;
+    const bool do_vec = !static_mode && var != 2 && var != 3;   // support-list offsets (K3a)
     const int p = sc->parity;
 
     // ---- last CTA: scans of the slot counts, fixed-order partial reduction.  Every count and
@@ -1518,6 +1540,44 @@ __device__ __forceinline__ void k3a_acc(const typename Vec<T>::Raw (&d)[4], cons
     }
 }
 
+// rows r0..r0+V-1 of D_S [a b] for the cn staged entries (column s_idx[i], coefficients s_a[i],
+// s_b[i]), accumulated in entry order; groups of 4 columns, the next group's loads in flight
+// while this group accumulates
+template <typename T>
+__device__ __forceinline__ void k3a_stream(const T* D, int ldd, int r0, const int* s_idx, const double* s_a,
+                                           const double* s_b, int cn, uint64_t pol, double* acc_a, double* acc_b) {
+    constexpr int V = Vec<T>::V;
+    const int ng = cn / 4;
+    typename Vec<T>::Raw d0[4], d1[4];
+    if (ng > 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[q] * ldd + r0, d0[q], pol);
+    }
+    int g = 0;
+    for (; g + 2 <= ng; g += 2) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[4 * g + 4 + q] * ldd + r0, d1[q], pol);
+        k3a_acc<T>(d0, s_a + 4 * g, s_b + 4 * g, acc_a, acc_b);
+        if (g + 2 < ng) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[4 * g + 8 + q] * ldd + r0, d0[q], pol);
+        }
+        k3a_acc<T>(d1, s_a + 4 * g + 4, s_b + 4 * g + 4, acc_a, acc_b);
+    }
+    if (g < ng) k3a_acc<T>(d0, s_a + 4 * g, s_b + 4 * g, acc_a, acc_b);   // odd group count
+    for (int i = 4 * ng; i < cn; ++i) {
+        typename Vec<T>::Raw d;
+        Vec<T>::load_raw(D + (size_t)s_idx[i] * ldd + r0, d, pol);
+        const double a = s_a[i], bb = s_b[i];
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            const double x = Vec<T>::get(d, v);
+            acc_a[v] = fma(a, x, acc_a[v]);
+            acc_b[v] = fma(bb, x, acc_b[v]);
+        }
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
     __shared__ int s_idx[K3_CHUNK];
@@ -1559,39 +1619,7 @@ __device__ __forceinline__ void k3a_body(const Params& P, int tile, int split) {
             s_b[i] = bb;
         }
         __syncthreads();
-        if (rows_ok) {
-            // groups of 4 columns, next group's loads in flight while this group accumulates
-            const int ng = cn / 4;
-            typename Vec<T>::Raw d0[4], d1[4];
-            if (ng > 0) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[q] * P.ldd + r0, d0[q], pol);
-            }
-            int g = 0;
-            for (; g + 2 <= ng; g += 2) {
-#pragma unroll
-                for (int q = 0; q < 4; ++q) Vec<T>::load_raw(D + (size_t)s_idx[4 * g + 4 + q] * P.ldd + r0, d1[q], pol);
-                k3a_acc<T>(d0, s_a + 4 * g, s_b + 4 * g, acc_a, acc_b);
-                if (g + 2 < ng) {
-#pragma unroll
-                    for (int q = 0; q < 4; ++q)
-                        Vec<T>::load_raw(D + (size_t)s_idx[4 * g + 8 + q] * P.ldd + r0, d0[q], pol);
-                }
-                k3a_acc<T>(d1, s_a + 4 * g + 4, s_b + 4 * g + 4, acc_a, acc_b);
-            }
-            if (g < ng) k3a_acc<T>(d0, s_a + 4 * g, s_b + 4 * g, acc_a, acc_b);   // odd group count
-            for (int i = 4 * ng; i < cn; ++i) {
-                typename Vec<T>::Raw d;
-                Vec<T>::load_raw(D + (size_t)s_idx[i] * P.ldd + r0, d, pol);
-                const double a = s_a[i], bb = s_b[i];
-#pragma unroll
-                for (int v = 0; v < V; ++v) {
-                    const double x = Vec<T>::get(d, v);
-                    acc_a[v] = fma(a, x, acc_a[v]);
-                    acc_b[v] = fma(bb, x, acc_b[v]);
-                }
-            }
-        }
+        if (rows_ok) k3a_stream<T>(D, P.ldd, r0, s_idx, s_a, s_b, cn, pol, acc_a, acc_b);
     }
     if (rows_ok) {
         double* pa = P.p3v + ((size_t)split * 2) * P.ldd + r0;
@@ -1612,6 +1640,139 @@ __global__ void __launch_bounds__(NT) k3a_residual(Params P) {
     if (sc->mode == MODE_STATIC) return;
     if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stamp(P, 4);
     k3a_body<T>(P, blockIdx.x, blockIdx.y);
+}
+
+// K3a-scan (single GPU, with K2 running concurrently): the residual partials over the
+// *unreduced* iterate, read straight from x_{t+1} (written by K1) and the current active list
+// -- no support list from K2, so K2's test / compaction and this pass overlap.  Split `split`
+// of P23 scans the active units [nu*split/P23, nu*(split+1)/P23) in rounds of K3S_UNITS
+// (4 consecutive units per thread on the identity list), stages the atoms with a nonzero
+// a = x_{t+1} or b (b_value) in shared memory in unit order and streams their columns.  A
+// FIXUP trip (K2 found a screened unit carrying a nonzero a or b) rescans the compacted list.
+constexpr int K3S_UNITS = 4 * NT;
+
+template <typename T, bool GROUP>
+__device__ __forceinline__ void k3a_scan_body(const Params& P, int tile, int split) {
+    __shared__ int s_idx[K3S_UNITS];
+    __shared__ double s_a[K3S_UNITS], s_b[K3S_UNITS];
+    __shared__ int s_scan[2 * NW + 1];
+    __shared__ int s_off[K3_WIN];
+    __shared__ int s_s0;
+    dscr_scalars* sc = P.sc;
+    const bool fixup = (sc->mode == MODE_FIXUP);
+    const int p = sc->parity, xi = sc->xi;
+    const int lp = fixup ? (p ^ 1) : p;
+    const int nu = fixup ? sc->n_units_new : sc->n_units;
+    const int* act = P.act[lp];
+    const int* off = P.act_off[lp];
+    const bool ident = !fixup && (nu == P.n_units);
+    const int S = P.P23;
+    const int lo = (int)(((long long)nu * split) / S), hi = (int)(((long long)nu * (split + 1)) / S);
+    const double* xn = P.x[(xi + 1) % 3];
+    const double* xc = P.x[xi];
+    const int algo = P.algo;
+    const double beta = sc->beta, phi = sc->phi;
+    constexpr int V = Vec<T>::V;
+    const int r0 = tile * P.TR + threadIdx.x * V;
+    const bool rows_ok = r0 < P.n;
+    const T* D = static_cast<const T*>(P.D);
+    const uint64_t pol = make_policy(P.l2_keep);
+    double acc_a[V], acc_b[V];
+#pragma unroll
+    for (int v = 0; v < V; ++v) { acc_a[v] = 0.0; acc_b[v] = 0.0; }
+    int count = 0;
+    const int upr = GROUP ? max(1, min(NT, K3S_UNITS / max(1, P.max_gsize))) : K3S_UNITS;   // units per round
+    int wend = INT_MIN;
+    for (int u0 = lo; u0 < hi; u0 += upr) {
+        const int cu = min(upr, hi - u0);
+        if (!ident && u0 + cu > wend) wend = stage_window(off, P.G, u0, s_off, &s_s0);   // uniform
+        // this thread's units: 4 consecutive flat positions (Lasso) or one group
+        constexpr int Q = GROUP ? 1 : 4;
+        int units[Q];
+        int my = 0;
+        double av[GROUP ? 1 : 4], bv[GROUP ? 1 : 4];
+#pragma unroll
+        for (int q = 0; q < Q; ++q) {
+            const int f = u0 + Q * threadIdx.x + q;
+            units[q] = -1;
+            if (f < u0 + cu) {
+                if (ident) units[q] = f;
+                else {
+                    const int sl = window_slot(off, P.G, s_off, s_s0, wend, f);
+                    units[q] = act[sl * P.cap + (f - off[sl])];
+                }
+            }
+        }
+        if (!GROUP) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                av[q] = 0.0; bv[q] = 0.0;
+                if (units[q] >= 0) {
+                    av[q] = xn[units[q]];
+                    bv[q] = b_value(algo, av[q], xc[units[q]], beta, phi);
+                }
+                my += (av[q] != 0.0 || bv[q] != 0.0) ? 1 : 0;
+            }
+        } else if (units[0] >= 0) {
+            // 8 atoms' x values in flight at a time
+            const int j0 = unit_atom_lo(P, units[0]), j1 = unit_atom_hi(P, units[0]);
+            for (int jb = j0; jb < j1; jb += 8) {
+                double xa[8], xb[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    xa[q] = (jb + q < j1) ? xn[jb + q] : 0.0;
+                    xb[q] = (jb + q < j1) ? xc[jb + q] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    my += (jb + q < j1 && (xa[q] != 0.0 || b_value(algo, xa[q], xb[q], beta, phi) != 0.0)) ? 1 : 0;
+            }
+        }
+        int tot;
+        int w = block_exscan(my, s_scan, &tot);
+        if (!GROUP) {
+#pragma unroll
+            for (int q = 0; q < Q; ++q)
+                if (av[q] != 0.0 || bv[q] != 0.0) { s_idx[w] = units[q]; s_a[w] = av[q]; s_b[w] = bv[q]; ++w; }
+        } else if (my) {
+            const int j0 = unit_atom_lo(P, units[0]), j1 = unit_atom_hi(P, units[0]);
+            for (int jb = j0; jb < j1; jb += 8) {
+                double xa[8], xb[8];
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    xa[q] = (jb + q < j1) ? xn[jb + q] : 0.0;
+                    xb[q] = (jb + q < j1) ? xc[jb + q] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const double b = b_value(algo, xa[q], xb[q], beta, phi);
+                    if (jb + q < j1 && (xa[q] != 0.0 || b != 0.0)) { s_idx[w] = jb + q; s_a[w] = xa[q]; s_b[w] = b; ++w; }
+                }
+            }
+        }
+        __syncthreads();
+        if (rows_ok && tot) k3a_stream<T>(D, P.ldd, r0, s_idx, s_a, s_b, tot, pol, acc_a, acc_b);
+        count += tot;
+        __syncthreads();
+    }
+    if (rows_ok) {
+        double* pa = P.p3v + ((size_t)split * 2) * P.ldd + r0;
+        double* pb = P.p3v + ((size_t)split * 2 + 1) * P.ldd + r0;
+#pragma unroll
+        for (int v = 0; v < V; ++v) {
+            if (r0 + v < P.ldd) { pa[v] = acc_a[v]; pb[v] = acc_b[v]; }
+        }
+    }
+    if (tile == 0 && threadIdx.x == 0) P.p3c[split] = count;
+}
+
+template <typename T, bool GROUP>
+__global__ void __launch_bounds__(NT) k3a_scan(Params P) {
+    dscr_scalars* sc = P.sc;
+    if (sc->stop || sc->t >= sc->run_limit) return;
+    if (sc->mode == MODE_STATIC) return;
+    if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) stamp(P, 4);
+    k3a_scan_body<T, GROUP>(P, blockIdx.x, blockIdx.y);
 }
 
 // ---------------------------------------------------------------------------
@@ -1663,7 +1824,7 @@ __device__ void iteration_epilogue(const Params& P, dscr_scalars* sc, double s_q
             set_cond(P, 0);
             return;
         }
-        if (bt) {
+        if (bt && !P.f23) {
             if (sc->dropped_nz && !P.onecoll) {
                 // resid must be recomputed on the reduced iterate (solvers.py:354-355)
                 sc->spare = s_tn2;
@@ -1673,14 +1834,15 @@ __device__ void iteration_epilogue(const Params& P, dscr_scalars* sc, double s_q
                 return;
             }
         }
-        if (P.onecoll && sc->dropped_nz) {
-            // one collective: the residuals were taken on the unreduced iterate; a screened unit
-            // carried a nonzero x or u / s, so both are recomputed on the reduced iterate
+        if ((P.onecoll || P.f23) && sc->dropped_nz) {
+            // one collective / concurrent K2 + K3a-scan: the residuals were taken on the unreduced
+            // iterate; a screened unit carried a nonzero x or u / s, so both are recomputed on the
+            // reduced iterate
             sc->mode = MODE_FIXUP;
             sc->trips += 1;
             return;
         }
-    } else if (algo == DSCR_FISTA && !P.onecoll) {
+    } else if (algo == DSCR_FISTA && !P.onecoll && !P.f23) {
         s_tn2 = sc->spare;   // theta_{t+1} = D u - y from the normal trip
         s_tny = sc->ds_sq;
     }
@@ -1746,10 +1908,10 @@ __device__ __forceinline__ void k3b_body(const Params& P, int rb) {
     __shared__ double s_pa[K3B_GROUPS][K3B_ROWS], s_pb[K3B_GROUPS][K3B_ROWS];
     dscr_scalars* sc = P.sc;
     const int mode = sc->mode;
-    const bool fix = (mode == MODE_FIXUP) && !P.onecoll;
+    const bool fix = (mode == MODE_FIXUP) && !P.onecoll && !P.f23;   // FIXUP re-derives a only
     const int algo = P.algo;
     const int p = sc->parity;
-    const int pe = sc->p_eff;
+    const int pe = P.f23 ? P.P23 : sc->p_eff;
     // split reduction: group g sums splits g, g+8, ... ; groups combined in order (deterministic)
     {
         const int rr = threadIdx.x % K3B_ROWS, g = threadIdx.x / K3B_ROWS;
@@ -1822,14 +1984,17 @@ __device__ void k3b_final(const Params& P, int G3) {
         const double* g = reinterpret_cast<const double*>(P.sc);
         for (int i = threadIdx.x; i < (int)(sizeof(dscr_scalars) / 8); i += NT) s_scw[i] = g[i];
     }
-    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+    double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0, ns = 0.0;
     for (int i = threadIdx.x; i < G3; i += NT) {
         const double* o = P.p3s + (size_t)i * NP3;
         a0 += o[0]; a1 += o[1]; a2 += o[2]; a3 += o[3];
     }
-    double r4[4] = {a0, a1, a2, a3};
-    block_sum_n<4>(r4, s_sh);   // (syncs: the scalar copy is complete)
-    a0 = r4[0]; a1 = r4[1]; a2 = r4[2]; a3 = r4[3];
+    if (P.f23)                  // columns streamed by K3a-scan this trip (trace)
+        for (int i = threadIdx.x; i < P.P23; i += NT) ns += (double)P.p3c[i];
+    double r5[5] = {a0, a1, a2, a3, ns};
+    block_sum_n<5>(r5, s_sh);   // (syncs: the scalar copy is complete)
+    a0 = r5[0]; a1 = r5[1]; a2 = r5[2]; a3 = r5[3];
+    if (P.f23 && threadIdx.x == 0) sc->n_support = (int)r5[4];
     if (threadIdx.x == 0) {
         stamp(P, 7);
         if (P.split) {      // global sums of the per-rank K1/K2 scalars
@@ -2333,7 +2498,7 @@ struct Layout {
 };
 
 struct Geometry {
-    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1, tile, theta_gl;
+    int G, cap, sup_cap, TR, R, P, G3b, max_gsize, smem1, tile, theta_gl, P23;
 };
 
 static int dtype_size(int dt) { return dt == DSCR_F64 ? 8 : (dt == DSCR_F32 ? 4 : 2); }
@@ -2448,6 +2613,10 @@ static Geometry make_geometry(const dscr_problem_desc* pr, int n_units, int max_
     g.R = (pr->n_rows + g.TR - 1) / g.TR;
     g.P = std::max(1, (sms * k3a_occupancy(pr->dtype)) / g.R);   // (row tile x split) CTAs: one wave
     g.G3b = (pr->n_rows + K3B_ROWS - 1) / K3B_ROWS;
+    // K3a-scan splits (fused graph): ~512 atoms scanned per split (measured on c1-c3: more splits
+    // cost more in K3b's reduction and in slots taken from K2 than they save), one wave at most
+    g.P23 = std::max(1, std::min(g.P, pr->n_cols / 512));
+    if (const char* e = getenv("DSCR_P23")) g.P23 = std::max(1, std::min(g.P, atoi(e)));
     return g;
 }
 
@@ -2456,7 +2625,7 @@ static int kts_slots(const dscr_config* cfg) { return std::min(std::max(cfg->max
 struct Offsets {
     size_t sc, theta0, theta1, resid, corr, x0, x1, x2, u0, u1, ycorr, star, cc, cnorm, vec, dn;
     size_t act0, act1, cnt0, cnt1, off0, off1, mask, sidx, sa, sb, supcnt, supoff;
-    size_t p1, p2, p3v, p3s, tickets, trace, kts, anorm, comm;
+    size_t p1, p2, p3v, p3s, p3c, tickets, trace, kts, anorm, comm;
 };
 
 static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg, const Geometry& g,
@@ -2484,6 +2653,7 @@ static Offsets make_offsets(const dscr_problem_desc* pr, const dscr_config* cfg,
     o.p2 = L.add(G * NP2X * 8);
     o.p3v = L.add((size_t)g.P * 2 * ldd * 8);
     o.p3s = L.add((size_t)g.G3b * NP3 * 8);
+    o.p3c = L.add((size_t)g.P * 4);
     o.tickets = L.add(64);
     o.trace = L.add((size_t)std::max(cfg->max_iters, 1) * DSCR_TRACE_FIELDS * 8);
     o.kts = L.add((size_t)kts_slots(cfg) * 8 * 8);
@@ -2510,6 +2680,8 @@ struct dscr_solver {
     void* comm = nullptr;
     bool pdl = false;   // chain kernels launched with programmatic dependent launch
     void** peer_tab_dev = nullptr;   // device copy of the peer pointer table
+    cudaStream_t fork_stream = nullptr;          // K3a-scan branch of the captured trip (f23)
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
 };
 
 extern "C" const char* dscr_last_error(void) { return err_store().c_str(); }
@@ -2600,18 +2772,35 @@ static void (*k1_kernel(int dtype, bool group, bool tall))(Params) {
 // Kernel launch with optional programmatic stream serialization (PDL edges when captured).
 template <typename... KArgs>
 static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, size_t smem, cudaStream_t s, bool pdl,
-                              const Params& P) {
+                              const Params& P, int priority = INT_MIN) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = dim3(NT);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (priority != INT_MIN) {   // graph node priority (the loop graph is instantiated with node priorities)
+        at[na].id = cudaLaunchAttributePriority;
+        at[na].val.priority = priority;
+        ++na;
+    }
     cfg.attrs = at;
-    cfg.numAttrs = pdl ? 1 : 0;
+    cfg.numAttrs = na;
     return cudaLaunchKernelEx(&cfg, kern, P);
+}
+
+// greatest / least stream priority of the device (numerically lowest = greatest)
+static void priority_range(int* greatest, int* least) {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);   // (least, greatest)
+    *least = lo;
+    *greatest = hi;
 }
 
 // Off by default: measured on B200 (c1, in-graph stamps) the chain is latency-bound inside
@@ -2637,6 +2826,43 @@ static int launch_iteration(dscr_solver* h, const Params& P, cudaStream_t s, cud
     cudaError_t le = launch_pdl(k1, dim3(g.G), smem1, s, pdl, P);
     if (le != cudaSuccess) return set_err("K1 launch", le);
     if (ev) CK(cudaEventRecord(ev[1], s));
+    if (P.f23) {
+        // K2 (test, compaction, vectors) and K3a-scan (residual partials of the unreduced
+        // iterate) have no dependency on each other: two branches of the trip graph, joined
+        // before K3b (timed runs launch them one after the other)
+        void (*k3s)(Params);
+        switch (P.dtype) {
+            case DSCR_F64: k3s = group ? k3a_scan<double, true> : k3a_scan<double, false>; break;
+            case DSCR_F32: k3s = group ? k3a_scan<float, true> : k3a_scan<float, false>; break;
+            default: k3s = group ? k3a_scan<__nv_bfloat16, true> : k3a_scan<__nv_bfloat16, false>;
+        }
+        Params P2 = P;
+        P2.k2v = 3;
+        if (ev) {      // timed: K2, then K3a-scan, each between events
+            le = launch_pdl(group ? k2_screen<true> : k2_screen<false>, dim3(g.G), 0, s, false, P2);
+            if (le != cudaSuccess) return set_err("K2 launch", le);
+            CK(cudaEventRecord(ev[2], s));
+            k3s<<<dim3(g.R, g.P23), NT, 0, s>>>(P);
+            CK(cudaGetLastError());
+            CK(cudaEventRecord(ev[3], s));
+        } else {
+            // K2 at the greatest priority, so its CTAs are dispatched first and K3a-scan fills the
+            // slots they free (a K3a-scan CTA holding a slot first delayed K2 by 2-6 us)
+            int hi_pr = 0, lo_pr = 0;
+            priority_range(&hi_pr, &lo_pr);
+            CK(cudaEventRecord(h->ev_fork, s));
+            CK(cudaStreamWaitEvent(h->fork_stream, h->ev_fork, 0));
+            le = launch_pdl(k3s, dim3(g.R, g.P23), 0, h->fork_stream, false, P, lo_pr);
+            if (le != cudaSuccess) return set_err("K3a-scan launch", le);
+            le = launch_pdl(group ? k2_screen<true> : k2_screen<false>, dim3(g.G), 0, s, false, P2, hi_pr);
+            if (le != cudaSuccess) return set_err("K2 launch", le);
+            CK(cudaEventRecord(h->ev_join, h->fork_stream));
+            CK(cudaStreamWaitEvent(s, h->ev_join, 0));
+        }
+        le = launch_pdl(k3b_finalize, dim3(g.G3b), 0, s, false, P);
+        if (le != cudaSuccess) return set_err("K3b launch", le);
+        return DSCR_OK;
+    }
     le = launch_pdl(group ? k2_screen<true> : k2_screen<false>, dim3(g.G), 0, s, pdl, P);
     if (le != cudaSuccess) return set_err("K2 launch", le);
     if (ev) CK(cudaEventRecord(ev[2], s));
@@ -2823,6 +3049,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.sup_cnt = (int*)(base + o.supcnt); P.sup_off = (int*)(base + o.supoff); P.sup_cap = g.sup_cap;
     P.p1 = (double*)(base + o.p1); P.p2 = (double*)(base + o.p2); P.p3v = (double*)(base + o.p3v);
     P.p3s = (double*)(base + o.p3s); P.tickets = (unsigned*)(base + o.tickets);
+    P.p3c = (int*)(base + o.p3c);
     P.trace = (double*)(base + o.trace);
     P.kts = (unsigned long long*)(base + o.kts);
     P.anorm = pr->col_norms ? const_cast<double*>(pr->col_norms) : (double*)(base + o.anorm);
@@ -2854,6 +3081,14 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
         P.persistent = coop && occ * sms >= g.G && g.G <= PERS_MAX_G && !g.theta_gl && env &&
                        strcmp(env, "persistent") == 0;
     }
+    P.P23 = g.P23;
+    // K2 concurrent with the K3a-scan residual: measured c1 37.0 -> 32.2, c2 58.0 -> 52.4,
+    // c3 67.8 -> 64.8, c4 proxy (128 MB) 61.4 -> 57.7 us per iteration; neutral on c4 (8.6 GB,
+    // K3a streams ~160 MB per trip and waits for K2's slots anyway), so the bandwidth-bound
+    // sizes keep the support-list K3a.  DSCR_F23=0/1 overrides.
+    const size_t dict_bytes = (size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype);
+    P.f23 = (!P.persistent && dict_bytes <= ((size_t)1 << 30)) ? 1 : 0;
+    if (const char* ef = getenv("DSCR_F23")) P.f23 = P.persistent ? 0 : atoi(ef);
     P.l2_keep = l2_keep_fraction((size_t)pr->ldd * pr->n_cols * dtype_size(pr->dtype));
     if (const char* ek = getenv("DSCR_L2_KEEP")) P.l2_keep = (float)atof(ek);   // experiment knob
 
@@ -2867,6 +3102,12 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     if (rc) { delete h; return rc; }
     cudaError_t e = cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete h; return set_err("cudaStreamCreate", e); }
+    if (P.f23) {
+        e = cudaStreamCreateWithFlags(&h->fork_stream, cudaStreamNonBlocking);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming);
+        if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming);
+        if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("fork stream / events", e); }
+    }
     // tickets must start at zero before any kernel runs
     e = cudaMemsetAsync(P.tickets, 0, 64, us);
     if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("cudaMemsetAsync", e); }
@@ -2923,7 +3164,7 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
         dscr_solver_destroy(h);
         return rc ? rc : set_err("end capture body", e);
     }
-    e = cudaGraphInstantiate(&h->e_loop, gl, 0);
+    e = cudaGraphInstantiate(&h->e_loop, gl, cudaGraphInstantiateFlagUseNodePriority);
     if (e != cudaSuccess) { dscr_solver_destroy(h); return set_err("instantiate loop", e); }
     *out = h;
     return DSCR_OK;
@@ -2996,6 +3237,7 @@ int dscr_solver_phase(dscr_solver* h, int phase, void* stream) {
     Params P = h->P;
     P.in_graph = 0;
     P.split = 1;
+    P.f23 = 0;   // split mode: K2S / K2 build the support list, K3A reads it
     const Geometry& g = h->geo;
     const bool group = P.n_groups > 0;
     const int test = P.test;
@@ -3166,6 +3408,9 @@ int dscr_solver_destroy(dscr_solver* h) {
     if (h->g_loop) cudaGraphDestroy(h->g_loop);
     if (h->g_setup) cudaGraphDestroy(h->g_setup);
     if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
+    if (h->fork_stream) cudaStreamDestroy(h->fork_stream);
+    if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+    if (h->ev_join) cudaEventDestroy(h->ev_join);
     if (h->peer_tab_dev) cudaFree(h->peer_tab_dev);
     delete h;
     return DSCR_OK;

@@ -17,6 +17,15 @@ import paper_1412_4080_b200 as ds  # noqa: E402
 from paper_1412_4080_b200 import dist as pdist  # noqa: E402
 from paper_1412_4080_b200 import workloads as wl  # noqa: E402
 
+@pytest.fixture(autouse=True)
+def _support_list_engine(monkeypatch):
+    """The fused engine compared against is the one whose K2 builds the support list for K3a
+    (DSCR_F23=0): the split phases read the same list in the same order, so the comparison is
+    bit for bit.  The default fused graph (K2 and K3a-scan concurrently) sums the residual in a
+    different order; test_concurrent_residual_matches_support_list_engine covers it."""
+    monkeypatch.setenv("DSCR_F23", "0")
+
+
 CASES = [("fista", "dst3", 0.5), ("fista", "safe", 0.9), ("ista", "dst3", 0.7), ("sparsa", "dst3", 0.7),
          ("cp", "safe", 0.8), ("fista", "static-dst3", 0.8)]
 
@@ -109,10 +118,38 @@ def test_persistent_engine_matches_graph_engine():
     import pickle
     res = {}
     for mode in ("graph", "persistent"):
-        env = dict(os.environ, DSCR_ENGINE=mode)
+        env = dict(os.environ, DSCR_ENGINE=mode, DSCR_F23="0")
         proc = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, check=True,
                               cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         res[mode] = pickle.loads(proc.stdout)
     for a, b in zip(res["graph"], res["persistent"]):
         assert a[0] == b[0] and a[1] == b[1]
         np.testing.assert_allclose(b[2], a[2], rtol=1e-13)
+
+
+ALGOS = [("ista", "dst3", 0.7), ("fista", "dst3", 0.5), ("fista", "safe", 0.85), ("sparsa", "dst3", 0.7),
+         ("cp", "safe", 0.8), ("twist", "dst3", 0.7), ("fista", "dome", 0.7), ("ista", "dst3", 0.6, 1.0)]
+
+
+@pytest.mark.parametrize("case", ALGOS, ids=["-".join(map(str, c)) for c in ALGOS])
+def test_concurrent_residual_matches_support_list_engine(case, monkeypatch):
+    """Default fused graph (K2 test / compaction concurrent with the K3a-scan residual of the
+    unreduced iterate, FIXUP trip when a screened unit carried a nonzero x or b) vs the engine
+    whose K2 builds the support list first: same iterations to the gap, screened sets, and
+    objective / x to rounding (the residual's summation order differs)."""
+    algo, test, ratio = case[:3]
+    p, nrm = _problem(ratio)
+    L0 = case[3] if len(case) > 3 else nrm * nrm * (1 + 1e-9)     # L0 = 1: backtracking REDO trips
+    cfg = ds.SolverConfig(algorithm=algo, strategy="dynamic", test=test, max_iters=3000, rel_tol=1e-300,
+                          L0=L0, gap_tol=1e-8, op_norm=nrm)
+    res = {}
+    for f23 in ("0", "1"):
+        monkeypatch.setenv("DSCR_F23", f23)
+        res[f23] = ds.run(p, cfg)
+    a, b = res["0"], res["1"]
+    assert a.stop_reason == b.stop_reason == "gap"
+    assert a.iterations == b.iterations
+    assert np.array_equal(a.screen_state.eliminated, b.screen_state.eliminated)
+    assert a.trace.kept == b.trace.kept
+    np.testing.assert_allclose(b.trace.objective, a.trace.objective, rtol=1e-12)
+    assert np.linalg.norm(a.x_star - b.x_star) <= 1e-9 * np.linalg.norm(a.x_star)

@@ -71,8 +71,9 @@ def _free_port():
 
 
 @pytest.mark.parametrize("case", CASES, ids=["-".join(map(str, c[:3])) + f"-{c[4]}coll" for c in CASES])
-def test_two_ranks_match_unsharded(case):
+def test_two_ranks_match_unsharded(case, monkeypatch):
     import paper_1412_4080_b200 as ds
+    monkeypatch.setenv("DSCR_F23", "0")   # unsharded reference: K2 builds the support list (same order)
     ctx = torch.multiprocessing.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
