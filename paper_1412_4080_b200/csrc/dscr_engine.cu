@@ -2230,13 +2230,13 @@ __global__ void __launch_bounds__(NT, 2) k_correlate(const T* __restrict__ D, in
     extern __shared__ double s_v[];
     if (skip_flag && *skip_flag) return;
     const uint64_t pol = make_policy(l2_keep);
-    if (VG) {                  // tall dictionary: v read through L2 (its padding rows are zero)
+    if constexpr (VG) {        // tall dictionary: v read through L2 (its padding rows are zero)
         k_correlate_cols<T>(D, ldd, n, k, v, out, pol);
-        return;
+    } else {
+        for (int i = threadIdx.x; i < ldd; i += NT) s_v[i] = (i < n) ? v[i] : 0.0;
+        __syncthreads();
+        k_correlate_cols<T>(D, ldd, n, k, s_v, out, pol);
     }
-    for (int i = threadIdx.x; i < ldd; i += NT) s_v[i] = (i < n) ? v[i] : 0.0;
-    __syncthreads();
-    k_correlate_cols<T>(D, ldd, n, k, s_v, out, pol);
 }
 
 // lambda_max with lowest-index argmax (problems.py:75-86), per-CTA partials + last CTA
