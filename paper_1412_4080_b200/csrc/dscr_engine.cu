@@ -1754,7 +1754,10 @@ __device__ __forceinline__ void k3a_scan_body(const Params& P, int tile, int spl
         if (!GROUP) {
 #pragma unroll
             for (int q = 0; q < Q; ++q)
-                if (av[q] != 0.0 || bv[q] != 0.0) { s_idx[w] = units[q]; s_a[w] = av[q]; s_b[w] = bv[q]; ++w; }
+                if (av[q] != 0.0 || bv[q] != 0.0) {
+                    DSCR_CHECK(w < K3S_UNITS && units[q] < P.kcols);
+                    s_idx[w] = units[q]; s_a[w] = av[q]; s_b[w] = bv[q]; ++w;
+                }
         } else if (my) {
             const int j0 = unit_atom_lo(P, units[0]), j1 = unit_atom_hi(P, units[0]);
             for (int jb = j0; jb < j1; jb += 8) {
@@ -1767,7 +1770,10 @@ __device__ __forceinline__ void k3a_scan_body(const Params& P, int tile, int spl
 #pragma unroll
                 for (int q = 0; q < 8; ++q) {
                     const double b = b_value(algo, xa[q], xb[q], beta, phi);
-                    if (jb + q < j1 && (xa[q] != 0.0 || b != 0.0)) { s_idx[w] = jb + q; s_a[w] = xa[q]; s_b[w] = b; ++w; }
+                    if (jb + q < j1 && (xa[q] != 0.0 || b != 0.0)) {
+                        DSCR_CHECK(w < K3S_UNITS && jb + q < P.kcols);
+                        s_idx[w] = jb + q; s_a[w] = xa[q]; s_b[w] = b; ++w;
+                    }
                 }
             }
         }
