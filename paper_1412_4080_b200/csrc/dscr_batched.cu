@@ -1525,6 +1525,11 @@ __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
 // barriers.  Same arithmetic per entry as update_hot_cta.
 constexpr int WU = 64;
 constexpr int UW = 8;            // observations (warps) per CTA
+// 4 CTAs per SM (<= 64 registers): a 4096-observation batch is 512 CTAs = one wave of 148 x 4
+// (at 74 registers, 3 CTAs per SM, it was 1.15 waves)
+#ifndef BUPD_MINB
+#define BUPD_MINB 4
+#endif
 
 __device__ __forceinline__ void warp_cas(int& k, float& v, int partner_lane_mask, bool take_min) {
     const int ok = __shfl_xor_sync(0xffffffffu, k, partner_lane_mask);
@@ -1533,7 +1538,7 @@ __device__ __forceinline__ void warp_cas(int& k, float& v, int partner_lane_mask
     if (swap) { k = ok; v = ov; }
 }
 
-__global__ void __launch_bounds__(UW * 32) k_bupdate_warp(BParams P, int t) {
+__global__ void __launch_bounds__(UW * 32, BUPD_MINB) k_bupdate_warp(BParams P, int t) {
     __shared__ int s_si[UW][WU];
     __shared__ double s_sx[UW][WU], s_su[UW][WU];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1791,13 +1796,234 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_bresid_w: the same residual pass with TPO threads per observation and 256 / TPO
+// observations per CTA.  Each thread owns NCHK chunks of 8 consecutive rows (one 16-byte column
+// load per entry and chunk), so the per-thread fixed work of an observation (scalar loads, list
+// staging, reductions, theta conversion) is spread over 8 * NCHK rows instead of 4, the
+// reductions of an observation are warp shuffles plus one exchange between its TPO / 32 warps
+// on a named barrier, and several observations are resident per CTA.  r_SAFE^2 at mu0 is summed
+// as ||y * (1/lam) - mu0 theta||^2 (one reciprocal per thread instead of a division per row).
+// ---------------------------------------------------------------------------
+#ifndef BRESID_W_NCHK
+#define BRESID_W_NCHK 2
+#endif
+#ifndef BRESID_W_EB
+#define BRESID_W_EB 4
+#endif
+#ifndef BRESID_W_MINB
+#define BRESID_W_MINB 2
+#endif
+#ifndef BRESID_W_SPEC
+#define BRESID_W_SPEC 0      // 1: first list window loaded together with the count (measured neutral)
+#endif
+
+template <int TPO>
+__device__ __forceinline__ void obs_sync(int o) {
+    if (TPO == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" :: "r"(o + 1), "n"(TPO) : "memory");
+}
+
+// sums of M values over the TPO threads of observation slot o (fixed order)
+template <int M, int TPO>
+__device__ __forceinline__ void obs_sum(double (&v)[M], double* sred, int o, int lt) {
+    constexpr int W = TPO / 32;
+#pragma unroll
+    for (int m = 0; m < M; ++m) v[m] = warp_sum(v[m]);
+    if (W > 1) {
+        obs_sync<TPO>(o);
+        if ((lt & 31) == 0) {
+#pragma unroll
+            for (int m = 0; m < M; ++m) sred[m * W + (lt >> 5)] = v[m];
+        }
+        obs_sync<TPO>(o);
+#pragma unroll
+        for (int m = 0; m < M; ++m) {
+            double r = 0.0;
+#pragma unroll
+            for (int q = 0; q < W; ++q) r += sred[m * W + q];
+            v[m] = r;
+        }
+    }
+}
+
+// 8 consecutive bf16 rows of one column (w) times the entry's x and u values
+__device__ __forceinline__ void resid_acc8(const uint4& w, double va, double vb, double* a, double* b) {
+    const uint32_t ww[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+        const double d0 = (double)__uint_as_float(ww[h] << 16), d1 = (double)__uint_as_float(ww[h] & 0xffff0000u);
+        a[2 * h] = fma(va, d0, a[2 * h]);         b[2 * h] = fma(vb, d0, b[2 * h]);
+        a[2 * h + 1] = fma(va, d1, a[2 * h + 1]); b[2 * h + 1] = fma(vb, d1, b[2 * h + 1]);
+    }
+}
+
+// rows n..n+7 of theta_j as bf16 terms (n a multiple of 8): one 16-byte store per term
+__device__ __forceinline__ void write_theta8(const BParams& P, int j, int n, const double* t) {
+    __align__(16) __nv_bfloat16 hi[8];
+    __align__(16) __nv_bfloat16 lo[8];
+#pragma unroll
+    for (int v = 0; v < 8; ++v) {
+        hi[v] = __double2bfloat16(t[v]);
+        lo[v] = __double2bfloat16(t[v] - (double)__bfloat162float(hi[v]));
+    }
+    *reinterpret_cast<uint4*>(P.tb + (size_t)j * P.ldy + n) = *reinterpret_cast<const uint4*>(hi);
+    if (P.splits > 1) *reinterpret_cast<uint4*>(P.tb + ((size_t)P.B + j) * P.ldy + n) = *reinterpret_cast<const uint4*>(lo);
+}
+
+template <int TPO, int NCHK>
+__global__ void __launch_bounds__(256, BRESID_W_MINB) k_bresid_w(BParams P, int t) {
+    constexpr int OPC = 256 / TPO, W = TPO / 32, RPT = 8 * NCHK, CR = 8 * TPO;   // CR: rows per chunk
+    constexpr int EB = BRESID_W_EB;
+    __shared__ int s_idx[OPC][TPO];
+    __shared__ double s_a[OPC][TPO], s_b[OPC][TPO];
+    __shared__ double s_red[OPC][3 * W];
+    const int nblk = P.B / OPC;           // B % 256 == 0
+    if ((int)blockIdx.x >= nblk) {        // appended blocks: this iteration's screening (k_bscreen)
+        bscreen_body(P, blockIdx.x - nblk, gridDim.x - nblk);
+        return;
+    }
+    const int o = threadIdx.x / TPO, lt = threadIdx.x % TPO;
+    const int j = blockIdx.x * OPC + o;
+    const int par = (t + 1) & 1;          // list written by this iteration's update
+    const size_t lo = (size_t)j * P.cap;
+    const int* idx = P.si[par] + lo;
+    const double* xa = P.sx[par] + lo;
+    const double* ub = P.su[par] + lo;
+    // status and list count in one round trip, then the first list window (BRESID_W_SPEC=1
+    // loads it speculatively with the count)
+    const int status = P.status[j];
+    const int cnt = P.sn[par][j];
+    int i_first = 0;
+    double a_first = 0.0, b_first = 0.0;
+    if (BRESID_W_SPEC ? (lt < P.cap) : (lt < cnt)) { i_first = idx[lt]; a_first = xa[lt]; b_first = ub[lt]; }
+    if (status != 0) {                    // (uniform over the observation's threads)
+        if (lt == 0 && j == 0) *P.it = t + 1;
+        return;
+    }
+    double rx[RPT], ru[RPT];
+#pragma unroll
+    for (int q = 0; q < RPT; ++q) { rx[q] = 0.0; ru[q] = 0.0; }
+    const __nv_bfloat16* dbase = P.Dt;
+    bool rows_ok[NCHK];
+    int coff[NCHK];             // row offset of the thread's chunk (0: no rows, loads row 0 and discards)
+#pragma unroll
+    for (int c = 0; c < NCHK; ++c) { rows_ok[c] = c * CR + 8 * lt < P.N; coff[c] = rows_ok[c] ? c * CR + 8 * lt : 0; }
+    for (int e0 = 0; e0 < cnt; e0 += TPO) {
+        if (e0) obs_sync<TPO>(o);
+        if (e0 == 0) {
+            s_idx[o][lt] = i_first; s_a[o][lt] = a_first; s_b[o][lt] = b_first;
+        } else if (e0 + lt < cnt) {
+            s_idx[o][lt] = idx[e0 + lt];
+            s_a[o][lt] = xa[e0 + lt];
+            s_b[o][lt] = ub[e0 + lt];
+        }
+        obs_sync<TPO>(o);
+        const int m = min(TPO, cnt - e0);
+        for (int e = 0; e < m; e += EB) {
+            uint4 w[NCHK][EB];
+#pragma unroll
+            for (int q = 0; q < EB; ++q) {
+                const __nv_bfloat16* col = dbase + (size_t)s_idx[o][min(e + q, m - 1)] * P.ldd;
+                // entries past the end reload the last one (an L1 hit) and are not accumulated;
+                // chunks past the last row load the column's first rows and stay zero (no predicated zero fills)
+#pragma unroll
+                for (int c = 0; c < NCHK; ++c) w[c][q] = __ldg(reinterpret_cast<const uint4*>(col + coff[c]));
+            }
+#pragma unroll
+            for (int q = 0; q < EB; ++q) {
+                if (e + q < m) {
+                    const double va = s_a[o][e + q], vb = s_b[o][e + q];
+#pragma unroll
+                    for (int c = 0; c < NCHK; ++c)
+                        if (rows_ok[c]) resid_acc8(w[c][q], va, vb, rx + 8 * c, ru + 8 * c);
+                }
+            }
+        }
+    }
+    // y (L2-resident across iterations; staging it in shared memory with cp.async at entry
+    // measured 4 us slower), residuals, next theta
+    double f2 = 0.0, sq = 0.0, tyv = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCHK; ++c) {
+        const int n0 = c * CR + 8 * lt;
+        if (n0 < P.N) {                    // N % 64 == 0: a chunk of 8 rows is inside or outside
+            double y8[8];
+            {
+                double y4[4];
+                Vec<double>::load(P.Y + (size_t)j * P.ldy + n0, y4, l2_normal_policy());
+#pragma unroll
+                for (int v = 0; v < 4; ++v) y8[v] = y4[v];
+                Vec<double>::load(P.Y + (size_t)j * P.ldy + n0 + 4, y4, l2_normal_policy());
+#pragma unroll
+                for (int v = 0; v < 4; ++v) y8[4 + v] = y4[v];
+            }
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const double yn = y8[v];
+                const double qa = rx[c * 8 + v] - yn;
+                const double tn = ru[c * 8 + v] - yn;      // theta_{t+1} = D u - y (solvers.py:212)
+                f2 = fma(qa, qa, f2);
+                sq = fma(tn, tn, sq);
+                tyv = fma(tn, yn, tyv);
+                rx[c * 8 + v] = yn;                        // keep y and theta for the r_SAFE^2 pass
+                ru[c * 8 + v] = tn;
+            }
+            write_theta8(P, j, n0, ru + 8 * c);
+        }
+    }
+    double v3[3] = {f2, sq, tyv};
+    obs_sum<3, TPO>(v3, s_red[o], o, lt);
+    const double lam = P.lam[j];
+    const double mu0 = (v3[1] != 0.0) ? v3[2] / (lam * v3[1]) : 0.0;
+    const double ilam = 1.0 / lam;
+    double d2 = 0.0;
+#pragma unroll
+    for (int c = 0; c < NCHK; ++c) {
+        if (c * CR + 8 * lt < P.N) {
+#pragma unroll
+            for (int v = 0; v < 8; ++v) {
+                const double d = fma(rx[c * 8 + v], ilam, -(mu0 * ru[c * 8 + v]));
+                d2 = fma(d, d, d2);
+            }
+        }
+    }
+    double d1[1] = {d2};
+    obs_sum<1, TPO>(d1, s_red[o], o, lt);
+    if (lt == 0) {
+        P.mu0[j] = mu0;
+        P.rsq0[j] = d1[0];
+        const double F = 0.5 * v3[0] + lam * P.pen[j];
+        P.F[j] = F;
+        P.gap[j] = F - 0.5 * P.yy[j] + 0.5 * lam * lam * P.rsq[j];
+        P.sq[j] = v3[1];
+        P.ty[j] = v3[2];
+        if (j == 0) *P.it = t + 1;
+    }
+}
+
+static bool bresid_cta_variant() {      // DSCR_BATCHED_RESID=cta: one CTA per observation (round-1 kernel)
+    const char* e = getenv("DSCR_BATCHED_RESID");
+    return e && !strcmp(e, "cta");
+}
+
 static void launch_update_hot(const BParams& P, int t, cudaStream_t s) {
     k_bupdate_warp<<<(P.B + UW - 1) / UW, UW * 32, 0, s>>>(P, t);
     k_bupdate_hot<<<std::min(P.B, 5 * 148), BT, 0, s>>>(P, t);   // resident grid, dynamic work list
-    if (BRESID_TPB != 256) k_bscreen<<<NSCR, 256, 0, s>>>(P);   // else: blocks of the residual launch
+    if (BRESID_TPB != 256 && bresid_cta_variant()) k_bscreen<<<NSCR, 256, 0, s>>>(P);   // else: blocks of the residual launch
 }
 
 static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
+    if (!bresid_cta_variant()) {
+        // rows per observation thread group: NCHK chunks of 8 * TPO rows
+        constexpr int C = BRESID_W_NCHK;
+        const int need = (P.N + 8 * C - 1) / (8 * C);            // threads an observation needs
+        if (need <= 32) k_bresid_w<32, C><<<P.B / 8 + NSCR, 256, 0, s>>>(P, t);
+        else if (need <= 64) k_bresid_w<64, C><<<P.B / 4 + NSCR, 256, 0, s>>>(P, t);
+        else if (need <= 128) k_bresid_w<128, C><<<P.B / 2 + NSCR, 256, 0, s>>>(P, t);
+        else k_bresid_w<256, C><<<P.B + NSCR, 256, 0, s>>>(P, t);
+        return;
+    }
     constexpr int TPB = BRESID_TPB;
     constexpr int RC = 4 * TPB;
     const int grid = P.B + (TPB == 256 ? NSCR : 0);
@@ -1868,6 +2094,8 @@ struct dscr_batched {
     cudaGraph_t g = nullptr;
     cudaGraphExec_t ge = nullptr;
     cudaStream_t cs = nullptr;
+    cudaStream_t fs = nullptr;                   // side branch of the captured iterations (k_btrace)
+    cudaEvent_t ev_a = nullptr, ev_b = nullptr;
     int max_iters;
 };
 
@@ -1978,6 +2206,15 @@ int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void
     if (e != cudaSuccess) { delete h; err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     e = cudaStreamCreateWithFlags(&h->cs, cudaStreamNonBlocking);
     if (e != cudaSuccess) { delete h; err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+    {
+        const char* eb = getenv("DSCR_BATCHED_TRACE_BRANCH");      // "0": k_btrace in line
+        if (!(eb && !strcmp(eb, "0"))) {
+            e = cudaStreamCreateWithFlags(&h->fs, cudaStreamNonBlocking);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_a, cudaEventDisableTiming);
+            if (e == cudaSuccess) e = cudaEventCreateWithFlags(&h->ev_b, cudaEventDisableTiming);
+            if (e != cudaSuccess) { dscr_batched_destroy(h); err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+        }
+    }
     *out = h;
     return DSCR_OK;
 }
@@ -2040,16 +2277,33 @@ static int enqueue_iterations(dscr_batched* h, int t0, int n, cudaStream_t s) {
     GemmArgs fz{};
     fz.mask = P.mask; fz.nzm = P.nzm; fz.thr = P.thr; fz.cmax = P.cmax;
     fz.hot_cnt = P.hot_cnt; fz.hot_idx = P.hot_idx; fz.hot_val = P.hot_val; fz.hcap = P.hcap;
+    // The batch aggregates of iteration t (k_btrace) only feed the trace and reset the work
+    // lists the next *update* uses, so they run on a side branch of the captured graph, next to
+    // the GEMM of iteration t + 1, and join before that iteration's update.
+    const bool side = h->fs && h->ev_a && h->ev_b;
+    bool pending = false;
     for (int t = t0; t < t0 + n; ++t) {
         int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, P.splits, P.C, P.K, s, P.fused ? &fz : nullptr);
         if (rc) return rc;
+        if (pending) { if (cudaStreamWaitEvent(s, h->ev_b, 0) != cudaSuccess) return DSCR_ECUDA; pending = false; }
         if (P.fused) launch_update_hot(P, t, s);
         else k_bupdate<<<P.B, BT, 0, s>>>(P, t);
         launch_bresid(P, t, s);
-        k_btrace<<<TR_G, TR_T, 0, s>>>(P, t);
+        if (side) {
+            cudaError_t e = cudaEventRecord(h->ev_a, s);
+            if (e == cudaSuccess) e = cudaStreamWaitEvent(h->fs, h->ev_a, 0);
+            if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+            k_btrace<<<TR_G, TR_T, 0, h->fs>>>(P, t);
+            e = cudaEventRecord(h->ev_b, h->fs);
+            if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
+            pending = true;
+        } else {
+            k_btrace<<<TR_G, TR_T, 0, s>>>(P, t);
+        }
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { err_store() = cudaGetErrorString(e); return DSCR_ECUDA; }
     }
+    if (pending && cudaStreamWaitEvent(s, h->ev_b, 0) != cudaSuccess) return DSCR_ECUDA;
     return DSCR_OK;
 }
 
@@ -2119,6 +2373,9 @@ int dscr_batched_destroy(dscr_batched* h) {
     if (h->ge) cudaGraphExecDestroy(h->ge);
     if (h->g) cudaGraphDestroy(h->g);
     if (h->cs) cudaStreamDestroy(h->cs);
+    if (h->fs) cudaStreamDestroy(h->fs);
+    if (h->ev_a) cudaEventDestroy(h->ev_a);
+    if (h->ev_b) cudaEventDestroy(h->ev_b);
     delete h;
     return DSCR_OK;
 }

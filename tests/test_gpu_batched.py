@@ -267,6 +267,29 @@ def test_batched_max_rows_matches_oracle():
         assert np.linalg.norm(x - ref.x_star) <= 1e-3 * max(np.linalg.norm(ref.x_star), 1e-12)
 
 
+@pytest.mark.parametrize("n,k,b", [(64, 1024, 256), (320, 1024, 256), (640, 2048, 256), (1024, 2048, 256),
+                                   (1088, 1024, 256)])
+def test_group_residual_matches_cta_residual(n, k, b, monkeypatch):
+    """Residual pass with 32 / 64 / 128 threads per observation (several observations per CTA, 8-row
+    chunks; row counts that leave the second chunk partly or wholly empty) vs the one-CTA-per-
+    observation kernel: same lists and screening, objective / gap equal up to the reduction order."""
+    w, dic, D64, L = _batch_problem(n, k, b, 0.6, seed=21)
+    a = solve_batched(dic, w.y, w.lam, L, iterations=50, test="dst3", splits=2)
+    monkeypatch.setenv("DSCR_BATCHED_RESID", "cta")
+    c = solve_batched(dic, w.y, w.lam, L, iterations=50, test="dst3", splits=2)
+    assert np.all(a.status == 0) and np.all(c.status == 0)
+    assert np.array_equal(a.kept, c.kept) and np.array_equal(a.nnz, c.nnz)
+    np.testing.assert_allclose(a.objective, c.objective, rtol=1e-12)
+    np.testing.assert_allclose(a.gap, c.gap, rtol=1e-8, atol=1e-11)
+    for j in range(0, b, 19):
+        assert np.array_equal(a.x_idx[j], c.x_idx[j])
+        np.testing.assert_allclose(a.x_val[j], c.x_val[j], rtol=1e-11, atol=1e-14)
+    ref = so.solve(so.make_problem(D64, w.y[:, 3], w.lam[3]),
+                   so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=50, rel_tol=1e-300,
+                             L0=L, norm_aware=True))
+    assert abs(a.objective[3] - ref.final_objective) <= 1e-4 * ref.final_objective
+
+
 def test_batched_solver_reuses_engine_across_batches_and_dictionaries():
     """BatchedSolver (engine, workspace and iteration graph reused) == one-shot solve_batched, for
     a second batch on the same dictionary and after swapping in another dictionary."""
