@@ -1805,14 +1805,16 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
 // on a named barrier, and several observations are resident per CTA.  r_SAFE^2 at mu0 is summed
 // as ||y * (1/lam) - mu0 theta||^2 (one reciprocal per thread instead of a division per row).
 // ---------------------------------------------------------------------------
+// measured on c5 (B200, batch-it/s): NCHK 2 / EB 4 / 2 CTAs per SM 4888; NCHK 1 / EB 8 / 3 CTAs 4782-4951;
+// NCHK 1 / EB 6 / 3 CTAs 4929-4957 (default)
 #ifndef BRESID_W_NCHK
-#define BRESID_W_NCHK 2
+#define BRESID_W_NCHK 1
 #endif
 #ifndef BRESID_W_EB
-#define BRESID_W_EB 4
+#define BRESID_W_EB 6
 #endif
 #ifndef BRESID_W_MINB
-#define BRESID_W_MINB 2
+#define BRESID_W_MINB 3
 #endif
 #ifndef BRESID_W_SPEC
 #define BRESID_W_SPEC 0      // 1: first list window loaded together with the count (measured neutral)

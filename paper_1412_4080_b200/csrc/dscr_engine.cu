@@ -2070,22 +2070,22 @@ __global__ void __launch_bounds__(NT) k3b_finalize(Params P) {
 // state.  The tails are deterministic, so all copies stay identical and no CTA
 // waits on another's tail.  Four grid barriers per iteration, no launches.
 
-// sense-counting grid barrier; the gpu-scope fences also invalidate this SM's
-// L1, so data written by other CTAs before the barrier is re-read from L2.
-__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* gen, unsigned n) {
+// Grid barrier on a monotonic arrival counter (zeroed by the host before each launch): thread 0
+// arrives with a fire-and-forget red.release and polls with ld.acquire until the count reaches
+// epoch * n -- one L2 round trip to detect completion, no generation word, no fences around an
+// atomic with a return value (that version measured ~3 us per barrier).  The acquire by thread 0
+// followed by the CTA barrier orders every thread's later loads after all arrivals' earlier
+// writes (and invalidates this SM's L1).
+__device__ __forceinline__ void grid_sync(unsigned* count, unsigned* /*gen*/, unsigned n, unsigned& epoch) {
     __syncthreads();
     if (threadIdx.x == 0) {
-        volatile unsigned* vgen = gen;
-        const unsigned g = *vgen;
-        __threadfence();
-        if (atomicAdd(count, 1u) == n - 1) {
-            atomicExch(count, 0u);
-            __threadfence();
-            atomicAdd(gen, 1u);
-        } else {
-            while (*vgen == g) __nanosleep(20);
-        }
-        __threadfence();
+        epoch += 1u;
+        const unsigned target = epoch * n;
+        asm volatile("red.release.gpu.global.add.u32 [%0], 1;" :: "l"(count) : "memory");
+        unsigned v;
+        do {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(count) : "memory");
+        } while ((int)(v - target) < 0);
     }
     __syncthreads();
 }
@@ -2103,6 +2103,7 @@ __global__ void __launch_bounds__(NT, 2) k_persistent(Params P0) {
     const int G = gridDim.x;
     unsigned* bc = P0.tickets + 4;
     unsigned* bg = P0.tickets + 5;
+    unsigned epoch = 0u;
     if (threadIdx.x == 0) {
         s_sc = *P0.sc;
         if (s_sc.stop == DSCR_RUNNING && s_sc.n_units == 0) s_sc.stop = DSCR_STOP_EMPTY;   // solvers.py:435
@@ -2114,12 +2115,12 @@ __global__ void __launch_bounds__(NT, 2) k_persistent(Params P0) {
         if (mode == MODE_NORMAL || mode == MODE_REDO) {
             if (threadIdx.x == 0) stamp(P, 0);
             k1_body<T, GROUP>(P, blockIdx.x, G, s_theta);
-            grid_sync(bc, bg, G);
+            grid_sync(bc, bg, G, epoch);
             k1_final<GROUP>(P, G);
             __syncthreads();
             if (threadIdx.x == 0) stamp(P, 2);
             k2_body<GROUP>(P, blockIdx.x, G);
-            grid_sync(bc, bg, G);
+            grid_sync(bc, bg, G, epoch);
             k2_final<GROUP>(P, G);
             __syncthreads();
         }
@@ -2129,13 +2130,13 @@ __global__ void __launch_bounds__(NT, 2) k_persistent(Params P0) {
             k3a_body<T>(P, v % P.R, v / P.R);
             __syncthreads();
         }
-        grid_sync(bc, bg, G);
+        grid_sync(bc, bg, G, epoch);
         if (threadIdx.x == 0) stamp(P, 6);
         for (int v = blockIdx.x; v < P.G3b; v += G) {
             k3b_body(P, v);
             __syncthreads();
         }
-        grid_sync(bc, bg, G);
+        grid_sync(bc, bg, G, epoch);
         k3b_final(P, P.G3b);
         __syncthreads();
     }
@@ -3097,8 +3098,9 @@ int dscr_solver_create(const dscr_problem_desc* pr, const dscr_config* cfg, void
     P.writer = 1;
     {
         // engine mode: the conditional-graph chain (default) or, with DSCR_ENGINE=persistent, one
-        // cooperative launch with grid barriers (measured slower on B200: ~3 us per grid barrier plus
-        // the redundant tails exceed the ~1.5 us launch gaps it removes; kept as an alternative)
+        // cooperative launch with grid barriers (measured slower on B200 -- c1 70 vs 32 us per
+        // iteration even with the ~1 us arrival-counter barrier: K1 inside the all-in-one kernel runs
+        // at half speed and the redundant tails exceed the launch gaps it removes; an alternative)
         const char* env = getenv("DSCR_ENGINE");
         int dev = 0, coop = 0, sms = 148;
         cudaGetDevice(&dev);
@@ -3214,6 +3216,7 @@ static int launch_persistent(dscr_solver* h, cudaStream_t s) {
         case DSCR_F32: fn = group ? (const void*)k_persistent<float, true> : (const void*)k_persistent<float, false>; break;
         default: fn = group ? (const void*)k_persistent<__nv_bfloat16, true> : (const void*)k_persistent<__nv_bfloat16, false>;
     }
+    CK(cudaMemsetAsync(P.tickets + 4, 0, 8, s));     // grid-barrier arrival counter
     CK(cudaLaunchCooperativeKernel(fn, dim3(h->geo.G), dim3(NT), args, (size_t)h->geo.smem1, s));
     return DSCR_OK;
 }
