@@ -517,7 +517,8 @@ struct OzArgs {
     int num_m, num_tiles;
     const int* eA;             // [K] row exponents of the A slices
     const int* eB;             // [B] row exponents of the B slices
-    int mode;                  // 0: out[j][i] fp64 ; 1: DST3 centre correlation cc (fp32)
+    int mode;                  // 0: out[j][i] fp64 ; 1: DST3 centre correlation cc (fp32) from ycorr and
+                               // D^T a_* ; 2: cc[j][i] = (float) product (the B rows are the centres)
     double* out; int ldo;
     const double *ycorr, *lam, *lmax, *anorm, *sgn;
     const int* istar;
@@ -631,6 +632,10 @@ __global__ void __launch_bounds__(OZ_THREADS, 1)
                 double* o = g.out + (size_t)j0 * g.ldo + i;
 #pragma unroll
                 for (int c = 0; c < 64; ++c) o[(size_t)c * g.ldo] = ldexp((double)acc[c], ei + g.eB[j0 + c]);
+            } else if (g.mode == 2) {
+#pragma unroll
+                for (int c = 0; c < 64; ++c)
+                    g.cc[(size_t)(j0 + c) * g.K + i] = (float)ldexp((double)acc[c], ei + g.eB[j0 + c]);
             } else {
 #pragma unroll
                 for (int c = 0; c < 64; ++c) {
@@ -778,7 +783,7 @@ struct BParams {
     int* eD;                   // [K]
     int8_t* Vs;                // [OZ_SV][B][N] int8 slices of y / of the DST3 atoms
     int* eV;                   // [B]
-    int oz;                    // setup correlations on the integer tensor cores
+    int oz;                    // setup correlations on the integer tensor cores (2: single product D^T Z)
     uint32_t* mask;            // [B][K/32]
     // support lists by parity: sorted atoms with x or u nonzero, their x and u values, count
     int* si[2]; double* sx[2]; double* su[2]; int* sn[2];
@@ -939,6 +944,110 @@ __global__ void __launch_bounds__(BT) k_blmax(BParams P) {
         P.astar[(size_t)j * P.ldy + n] = (n < P.N) ? (double)__bfloat162float(P.Dt[(size_t)ist * P.ldd + n]) : 0.0;
 }
 
+// ---- single-product setup (round 2): the test centre of observation j is one vector,
+// z_j = y_j/lam_j - coef_j a_* (DST3; y_j/lam_j for SAFE), so the centre correlations are ONE
+// exact integer-slice product D^T Z instead of D^T Y followed by D^T A_*.  lambda_* and a_* come
+// first from an approximate bf16 tensor-core product c~ = D^T (y_hi + y_lo) (fp32 accumulation):
+// |c~_i - c_i| <= e_i = eps ||d_i|| ||y_j|| with eps = 2^-16 (two bf16 terms) + 4 N 2^-24
+// (accumulation), so every atom with |c~_i| + e_i >= max_k (|c~_k| - e_k) is a candidate for the
+// argmax and is recomputed by an exact fp64 dot; lowest index wins ties (problems.py:79).
+
+// y_j as two bf16 terms in the theta buffer (rows of the setup GEMM), padding zero
+__global__ void __launch_bounds__(BT) k_ysplit(BParams P) {
+    const int j = blockIdx.x;
+    for (int n = threadIdx.x; n < P.ldy; n += BT) {
+        const double yn = (n < P.N) ? P.Y[(size_t)j * P.ldy + n] : 0.0;
+        const __nv_bfloat16 hi = __double2bfloat16(yn);
+        P.tb[(size_t)j * P.ldy + n] = hi;
+        P.tb[((size_t)P.B + j) * P.ldy + n] = __double2bfloat16(yn - (double)__bfloat162float(hi));
+    }
+}
+
+// lambda_*, a_*, sign, shift^2, trivial flag from the approximate correlations in P.C
+__global__ void __launch_bounds__(BT) k_blmax_approx(BParams P) {
+    __shared__ double s_sh[64];
+    __shared__ double s_m[BW];
+    __shared__ double s_bv[BW];
+    __shared__ int s_bi[BW];
+    const int j = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const float* row = P.C + (size_t)j * P.K;
+    const double* y = P.Y + (size_t)j * P.ldy;
+    double yy = 0.0;
+    for (int n = threadIdx.x; n < P.N; n += BT) yy = fma(y[n], y[n], yy);
+    yy = block_sum(yy, s_sh);
+    // |c~_i - c_i| <= e_i = eps ||d_i|| ||y||: eps = 2^-16 for the two bf16 terms of y plus
+    // 4 N 2^-24 for the fp32 accumulation of the 2 N products (as err_rel of the iterations)
+    const double eps = (1.6e-5 + 4.0 * (double)P.N * 5.96e-8) * sqrt(yy) * 1.001;
+    double m = -1.0;                       // lower bound of max |c|: max_i (|c~_i| - e_i)
+    for (int i = threadIdx.x; i < P.K; i += BT) m = fmax(m, (double)fabsf(row[i]) - eps * P.anorm[i]);
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_m[warp] = m;
+    __syncthreads();
+    m = s_m[0];
+    for (int w = 1; w < BW; ++w) m = fmax(m, s_m[w]);
+    // each warp scans a contiguous range of atoms in index order; candidates get an exact dot
+    double best = -1.0;
+    int bi = 0x7fffffff;
+    double bdot = 0.0;
+    const int per = (P.K + BW - 1) / BW;
+    const int i_lo = warp * per, i_hi = min(P.K, i_lo + per);
+    for (int i0 = i_lo; i0 < i_hi; i0 += 32) {
+        const int i = i0 + lane;
+        const bool cand = i < i_hi && (double)fabsf(row[i]) + eps * P.anorm[i] >= m;   // could be the maximum
+        unsigned bal = __ballot_sync(0xffffffffu, cand);
+        while (bal) {
+            const int q = __ffs(bal) - 1;
+            bal &= bal - 1u;
+            const int ia = i0 + q;
+            const __nv_bfloat16* d = P.Dt + (size_t)ia * P.ldd;
+            double dot = 0.0;
+            for (int n = lane; n < P.N; n += 32) dot = fma((double)__bfloat162float(d[n]), y[n], dot);
+            dot = warp_sum(dot);
+            if (fabs(dot) > best) { best = fabs(dot); bi = ia; bdot = dot; }   // index order: lowest index keeps ties
+        }
+    }
+    if (lane == 0) { s_bv[warp] = best; s_bi[warp] = bi; s_sh[warp] = bdot; }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double bv = s_bv[0], bd = s_sh[0];
+        int bidx = s_bi[0];
+        for (int w = 1; w < BW; ++w)
+            if (s_bv[w] > bv || (s_bv[w] == bv && s_bi[w] < bidx)) { bv = s_bv[w]; bidx = s_bi[w]; bd = s_sh[w]; }
+        const double lm = bv;
+        P.lmax[j] = lm;
+        P.istar[j] = bidx;
+        P.sgn[j] = (bd >= 0.0) ? 1.0 : -1.0;
+        const double shift = lm / P.lam[j] - 1.0;
+        const double an = P.anorm[bidx];
+        P.shift_sq[j] = (P.test == DSCR_DST3) ? shift * shift / (an * an) : 0.0;   // normal a_*/||a_*||
+        P.status[j] = (P.lam[j] > lm) ? 1 : 0;     // 1 = trivial (solvers.py:384-397)
+    }
+}
+
+// test centre z_j = y_j/lam_j - coef_j d_{i*} (DST3, screening.py:221-231 with the norm-aware
+// normal) or y_j/lam_j (SAFE), fp64, into the astar buffer
+__global__ void __launch_bounds__(BT) k_bcentre(BParams P) {
+    const int j = blockIdx.x;
+    const double lam = P.lam[j];
+    double coef = 0.0;
+    const __nv_bfloat16* d = P.Dt;
+    if (P.test == DSCR_DST3) {
+        const int i = P.istar[j];
+        const double a = P.anorm[i];
+        coef = (P.lmax[j] / lam - 1.0) / (a * a) * P.sgn[j];
+        d = P.Dt + (size_t)i * P.ldd;
+    }
+    for (int n = threadIdx.x; n < P.ldy; n += BT) {
+        double z = 0.0;
+        if (n < P.N) {
+            z = P.Y[(size_t)j * P.ldy + n] / lam;
+            if (P.test == DSCR_DST3) z -= coef * (double)__bfloat162float(d[n]);
+        }
+        P.astar[(size_t)j * P.ldy + n] = z;
+    }
+}
+
 // 16-bit order-preserving image of an fp32 value (unsigned order = float order, top 16 bits of
 // the radix image), monotone non-decreasing: v > t implies okey16(v) >= okey16(t).
 __device__ __forceinline__ uint16_t okey16(float v) {
@@ -953,7 +1062,8 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
     const int j = blockIdx.x;
     float m = -INFINITY;   // best (1 - |cc_i|)/||a_i|| of the column
     for (int i = threadIdx.x; i < P.K; i += BT) {
-        if (P.test == DSCR_SAFE) P.cc[(size_t)j * P.K + i] = (float)(P.ycorr[(size_t)j * P.K + i] / P.lam[j]);
+        if (P.test == DSCR_SAFE && P.oz != 2)
+            P.cc[(size_t)j * P.K + i] = (float)(P.ycorr[(size_t)j * P.K + i] / P.lam[j]);
         const float v = (float)((1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / P.anorm[i]);
         m = fmaxf(m, v);
         P.skey_in[(size_t)j * P.K + i] = okey16(v);   // sort key of the screening order
@@ -2108,7 +2218,7 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     auto take = [&](size_t bytes) { size_t o = off; off = bw_align(off + bytes); return base ? base + o : nullptr; };
     const size_t B = d->n_obs, K = d->n_atoms, ly = d->ldy, cap = d->cap;
     BParams p{};
-    p.tb = (__nv_bfloat16*)take((size_t)d->splits * B * ly * 2);
+    p.tb = (__nv_bfloat16*)take((size_t)std::max(d->splits, 2) * B * ly * 2);   // (two terms of y at setup)
     p.C = (float*)take(B * K * 4);
     p.skey_in = reinterpret_cast<uint16_t*>(p.C);
     p.skey = (uint16_t*)take(B * K * 2);
@@ -2197,6 +2307,9 @@ int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void
         const bool fp64 = ev && !strcmp(ev, "fp64");
         P.oz = (!fp64 && d->n_rows % OZ_BK == 0 && d->n_rows <= 2048 && d->n_obs % OZ_BN == 0 &&
                 d->n_atoms % OZ_BM == 0) ? 1 : 0;
+        // default: one exact product D^T Z (centres) after an approximate argmax; "oz2" keeps the
+        // two exact products D^T Y, D^T A_*
+        if (P.oz && !(ev && !strcmp(ev, "oz2"))) P.oz = 2;
         const char* eu = getenv("DSCR_BATCHED_UPDATE");   // "cta": every observation on the CTA update
         P.wu_max = (eu && !strcmp(eu, "cta")) ? 0 : WU;
     }
@@ -2227,7 +2340,24 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
     BParams& P = h->P;
     dim3 g(P.K / DG_T, P.B / DG_T);
     k_bnorms<<<std::max(1, P.K / BW / 4), BT, 0, s>>>(P);
-    if (P.oz) {   // exact slice products on the integer tensor cores
+    if (P.oz == 2) {
+        k_slice_rows<<<P.K / 8, 256, 0, s>>>(P.Dt, P.K, P.N, P.ldd, OZ_SD, P.Ds, P.eD);
+        k_ysplit<<<P.B, BT, 0, s>>>(P);
+        int rc = gemm_dt(P.Dt, P.K, P.ldd, P.tb, P.B, P.ldy, P.N, 2, P.C, P.K, s, nullptr);   // c~ = D^T (y_hi + y_lo)
+        if (rc) return rc;
+        k_blmax_approx<<<P.B, BT, 0, s>>>(P);
+        if (P.test != DSCR_TEST_OFF) {
+            k_bcentre<<<P.B, BT, 0, s>>>(P);
+            // centres keep 28 bits below their row maximum (T = 4) and pairs with s + t <= 4, as the
+            // observations did in the two-product setup: errors ~1e-9 of |z| ||d||_1, far inside the
+            // fp32 storage of cc and the 1e-6 test slack
+            k_slice_rows<<<P.B / 8, 256, 0, s>>>(P.astar, P.B, P.N, P.ldy, 4, P.Vs, P.eV);
+            OzArgs oc{};
+            oc.eA = P.eD; oc.eB = P.eV; oc.mode = 2; oc.cc = P.cc;
+            rc = ozaki_launch(P.Ds, P.K, OZ_SD, P.Vs, P.B, 4, P.N, oc, s, 4);
+            if (rc) return rc;
+        }
+    } else if (P.oz) {   // exact slice products on the integer tensor cores
         k_slice_rows<<<P.K / 8, 256, 0, s>>>(P.Dt, P.K, P.N, P.ldd, OZ_SD, P.Ds, P.eD);
         // The centre correlations are stored in fp32 and tested with a 1e-6 slack, and lambda_* is
         // recomputed in fp64: y keeps 28 bits (T = 4) and pairs with s + t <= 4 (13 pairs), the

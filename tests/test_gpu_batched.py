@@ -212,13 +212,19 @@ def test_fused_epilogue_matches_dense_update(ratio):
 
 
 @pytest.mark.parametrize("ratio", [0.4, 0.85])
-def test_integer_slice_setup_matches_fp64_setup(ratio, monkeypatch):
-    """Setup correlations on the integer tensor cores (default) vs the fp64 FMA path: same
-    screening decisions, support and trace (centres differ by < 2^-30, far inside the test slack)."""
+@pytest.mark.parametrize("setup,test", [("", "dst3"), ("oz2", "dst3"), ("", "safe"), ("oz2", "safe")])
+def test_integer_slice_setup_matches_fp64_setup(ratio, setup, test, monkeypatch):
+    """Setup correlations on the integer tensor cores -- the default single exact product D^T Z of
+    the test centres after an approximate argmax, and the two exact products D^T Y, D^T A_*
+    (DSCR_BATCHED_SETUP=oz2) -- vs the fp64 FMA path: same lambda_*, screening decisions, support
+    and trace (centres differ by < 2^-28 of their scale, far inside the test slack)."""
     w, dic, D64, L = _batch_problem(256, 2048, 512, ratio, seed=5)
-    a = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    if setup:
+        monkeypatch.setenv("DSCR_BATCHED_SETUP", setup)
+    a = solve_batched(dic, w.y, w.lam, L, iterations=60, test=test, splits=2)
     monkeypatch.setenv("DSCR_BATCHED_SETUP", "fp64")
-    b = solve_batched(dic, w.y, w.lam, L, iterations=60, test="dst3", splits=2)
+    b = solve_batched(dic, w.y, w.lam, L, iterations=60, test=test, splits=2)
+    np.testing.assert_allclose(a.lambda_max, b.lambda_max, rtol=1e-12)
     assert np.array_equal(a.kept, b.kept) and np.array_equal(a.nnz, b.nnz)
     np.testing.assert_allclose(a.objective, b.objective, rtol=1e-12)
     np.testing.assert_allclose(a.gap, b.gap, rtol=1e-9, atol=1e-12)
