@@ -259,6 +259,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #undef DSCR_RCASE
                     }
                     const int e = atomicAdd(&g.hot_cnt[j], 1);
+                    DSCR_CHECK(e >= 0 && a_base + k * 32 + i < g.words * 32);
                     if (e < g.hcap) {
                         g.hot_idx[(size_t)j * g.hcap + e] = a_base + k * 32 + i;
                         g.hot_val[(size_t)j * g.hcap + e] = v;
@@ -1000,6 +1001,7 @@ __global__ void __launch_bounds__(BT) k_blmax_approx(BParams P) {
             const int q = __ffs(bal) - 1;
             bal &= bal - 1u;
             const int ia = i0 + q;
+            DSCR_CHECK(ia >= 0 && ia < P.K);
             const __nv_bfloat16* d = P.Dt + (size_t)ia * P.ldd;
             double dot = 0.0;
             for (int n = lane; n < P.N; n += 32) dot = fma((double)__bfloat162float(d[n]), y[n], dot);
@@ -1448,6 +1450,7 @@ __device__ __forceinline__ void screen_enqueue(const BParams& P, int j, const Sc
     if (lane != 0 || r.end <= r.p) return;
     const unsigned long long old = atomicAdd(P.scr_ctr, (1ull << 32) | (unsigned long long)(r.end - r.p));
     const int item = (int)(old >> 32);
+    DSCR_CHECK(item >= 0 && item < P.B && r.p >= 0 && r.end <= P.K);   // at most one item per observation
     P.scr_j[item] = j;
     P.scr_p[item] = r.p;
     P.scr_off[item] = (int)(old & 0xffffffffull);
@@ -1477,8 +1480,10 @@ __device__ __forceinline__ void bscreen_body(const BParams& P, int bid, int nblk
             while (b - a > 1) { const int m = (a + b) >> 1; if (P.scr_off[m] <= g) a = m; else b = m; }
             j = P.scr_j[a];
             const int q = P.scr_p[a] + (g - P.scr_off[a]);
+            DSCR_CHECK(a >= 0 && a < items && j >= 0 && j < P.B && q >= 0 && q < P.K);
             const double rho = P.radius[j];
             const int i = P.sorder[(size_t)j * P.K + q];
+            DSCR_CHECK(i >= 0 && i < P.K);
             if (screened_now(P, j, i, rho, margin)) {
                 const uint32_t bit = 1u << (i & 31);
                 const uint32_t old = atomicAnd(&P.mask[(size_t)j * (P.K / 32) + (i >> 5)], ~bit);
@@ -1663,6 +1668,7 @@ __global__ void __launch_bounds__(UW * 32, BUPD_MINB) k_bupdate_warp(BParams P, 
         return;
     }
     const int cnt = min(hc, P.hcap);
+    DSCR_CHECK(hc >= 0 && scnt >= 0 && scnt <= P.cap);
     if (cnt > P.wu_max || scnt > P.wu_max) {     // the CTA kernel takes it
         if (lane == 0) P.big[atomicAdd(P.nbig, 1)] = j;
         return;
@@ -1680,6 +1686,7 @@ __global__ void __launch_bounds__(UW * 32, BUPD_MINB) k_bupdate_warp(BParams P, 
     const int* si = P.si[par] + lo;
     for (int e = lane; e < scnt; e += 32) {
         const int a = si[e];
+        DSCR_CHECK(a >= 0 && a < P.K && e < WU);
         s_si[warp][e] = a;
         s_sx[warp][e] = P.sx[par][lo + e];
         s_su[warp][e] = P.su[par][lo + e];
@@ -1741,6 +1748,7 @@ __global__ void __launch_bounds__(UW * 32, BUPD_MINB) k_bupdate_warp(BParams P, 
     const unsigned ltm = (1u << lane) - 1u;
     const int p0 = __popc(b0 & ltm), p1 = __popc(b0) + __popc(b1 & ltm);
     const int total = __popc(b0) + __popc(b1);
+    DSCR_CHECK((!keep0 || (k0 >= 0 && k0 < P.K)) && (!keep1 || (k1 >= 0 && k1 < P.K)));
     if (keep0 && p0 < P.cap) {
         P.si[par ^ 1][lo + p0] = k0; P.sx[par ^ 1][lo + p0] = c0; P.su[par ^ 1][lo + p0] = u0;
         atomicOr(&nrow[k0 >> 5], 1u << (k0 & 31));
@@ -1845,7 +1853,8 @@ __global__ void __launch_bounds__(TPB, TPB == 256 ? (NCH == 1 ? BRESID_MINB : 2)
                 uint2 w[EB];
 #pragma unroll
                 for (int q = 0; q < EB; ++q)
-                    w[q] = (e + q < m) ? __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0))
+                    w[q] = (e + q < m) ? (DSCR_CHECK(s_idx[e + q] >= 0 && s_idx[e + q] < P.K),
+                                          __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)s_idx[e + q] * P.ldd + r0)))
                                        : make_uint2(0u, 0u);
 #pragma unroll
                 for (int q = 0; q < EB; ++q)
@@ -1997,6 +2006,7 @@ __global__ void __launch_bounds__(256, BRESID_W_MINB) k_bresid_w(BParams P, int 
     }
     const int o = threadIdx.x / TPO, lt = threadIdx.x % TPO;
     const int j = blockIdx.x * OPC + o;
+    DSCR_CHECK(j >= 0 && j < P.B && 8 * TPO * NCHK >= P.N);
     const int par = (t + 1) & 1;          // list written by this iteration's update
     const size_t lo = (size_t)j * P.cap;
     const int* idx = P.si[par] + lo;
@@ -2032,10 +2042,12 @@ __global__ void __launch_bounds__(256, BRESID_W_MINB) k_bresid_w(BParams P, int 
         }
         obs_sync<TPO>(o);
         const int m = min(TPO, cnt - e0);
+        DSCR_CHECK(cnt >= 0 && cnt <= P.cap);
         for (int e = 0; e < m; e += EB) {
             uint4 w[NCHK][EB];
 #pragma unroll
             for (int q = 0; q < EB; ++q) {
+                DSCR_CHECK(s_idx[o][min(e + q, m - 1)] >= 0 && s_idx[o][min(e + q, m - 1)] < P.K);
                 const __nv_bfloat16* col = dbase + (size_t)s_idx[o][min(e + q, m - 1)] * P.ldd;
                 // entries past the end reload the last one (an L1 hit) and are not accumulated;
                 // chunks past the last row load the column's first rows and stay zero (no predicated zero fills)
