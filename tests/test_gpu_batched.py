@@ -296,6 +296,44 @@ def test_group_residual_matches_cta_residual(n, k, b, monkeypatch):
     assert abs(a.objective[3] - ref.final_objective) <= 1e-4 * ref.final_objective
 
 
+@pytest.mark.parametrize("setup", ["", "oz2", "fp64"])
+def test_setup_trivial_regime_ties_and_lambda_max(setup, monkeypatch):
+    """Setup edge cases on every setup path (single exact product after the approximate argmax,
+    two exact products, fp64): lambda_* equals max|D^T y_j| of the stored bf16 atoms (reference
+    problems.py:75-86); observations with lam_j > lambda_* are trivial (status 1, x = 0, nothing
+    kept -- solvers.py:384-397); a duplicated extremal atom (an exact tie of the two largest
+    correlations) changes nothing in the outcome; the other observations match the oracle."""
+    w, dic, D64, L = _batch_problem(128, 1024, 256, 0.6, seed=33)
+    lmax_ref = np.max(np.abs(D64.T @ w.y), axis=0)
+    lam = w.lam.copy()
+    triv = np.arange(0, 256, 9)
+    lam[triv] = 1.05 * lmax_ref[triv]
+    # duplicate the extremal atom of observation 5 at a later index (same bf16 bits)
+    Dq = np.array(dic.data, copy=True)
+    i_star = int(np.argmax(np.abs(D64.T @ w.y[:, 5])))
+    dup = 1000 if i_star != 1000 else 999
+    Dq[:, dup] = Dq[:, i_star]
+    dic2 = ds.Dictionary(Dq, check_unit_norms=False, dtype="bf16")
+    D2 = dic2.as_float64()
+    L2 = float(np.linalg.norm(D2, 2) ** 2 * (1 + 1e-6))
+    lmax2 = np.max(np.abs(D2.T @ w.y), axis=0)
+    if setup:
+        monkeypatch.setenv("DSCR_BATCHED_SETUP", setup)
+    res = solve_batched(dic2, w.y, lam, L2, iterations=50, test="dst3", splits=2, masks=True)
+    np.testing.assert_allclose(res.lambda_max, lmax2, rtol=1e-12)
+    assert np.all(res.status[triv] == 1) and np.all(res.nnz[triv] == 0) and np.all(res.kept[triv] == 0)
+    ok = np.setdiff1d(np.arange(256), triv)
+    assert np.all(res.status[ok] == 0)
+    for j in (5, 6, 100):
+        if j in triv:
+            continue
+        ref = so.solve(so.make_problem(D2, w.y[:, j], lam[j]),
+                       so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=50, rel_tol=1e-300,
+                                 L0=L2, norm_aware=True))
+        assert abs(res.objective[j] - ref.final_objective) <= 1e-6 * ref.final_objective
+        assert np.all(np.isin(res.eliminated(j), ref.eliminated)), j
+
+
 def test_batched_solver_reuses_engine_across_batches_and_dictionaries():
     """BatchedSolver (engine, workspace and iteration graph reused) == one-shot solve_batched, for
     a second batch on the same dictionary and after swapping in another dictionary."""
