@@ -2126,6 +2126,107 @@ __global__ void __launch_bounds__(256, BRESID_W_MINB) k_bresid_w(BParams P, int 
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_bresid_tall: the residual pass for dictionaries taller than 2048 rows (up to BTALL_MAX_ROWS).
+// One CTA per observation walks the rows in chunks of 1024 (4 per thread), re-reading the support
+// list per chunk; theta_{t+1} (fp64) stays in dynamic shared memory for the r_SAFE^2 pass, which
+// needs mu0 from the sums over all rows.  Same arithmetic per row as the kernels above.
+// ---------------------------------------------------------------------------
+constexpr int BTALL_MAX_ROWS = 16384;     // N * 8 bytes of theta in shared memory (128 KB)
+
+__global__ void __launch_bounds__(256) k_bresid_tall(BParams P, int t) {
+    extern __shared__ double s_th[];       // [N] theta_{t+1} of this observation
+    __shared__ double s_sh[64];
+    __shared__ int s_idx[256];
+    __shared__ double s_a[256], s_b[256];
+    if ((int)blockIdx.x >= P.B) {           // appended blocks: this iteration's screening (k_bscreen)
+        bscreen_body(P, blockIdx.x - P.B, gridDim.x - P.B);
+        return;
+    }
+    const int j = blockIdx.x;
+    const int par = (t + 1) & 1;
+    if (P.status[j] != 0) {
+        if (threadIdx.x == 0 && j == 0) *P.it = t + 1;
+        return;
+    }
+    const size_t lo = (size_t)j * P.cap;
+    const int* idx = P.si[par] + lo;
+    const double* xa = P.sx[par] + lo;
+    const double* ub = P.su[par] + lo;
+    const int cnt = P.sn[par][j];
+    DSCR_CHECK(cnt >= 0 && cnt <= P.cap && P.N <= BTALL_MAX_ROWS);
+    const double* y = P.Y + (size_t)j * P.ldy;
+    double f2 = 0.0, sq = 0.0, tyv = 0.0;
+    for (int base = 0; base < P.N; base += 1024) {            // (uniform: barriers inside)
+        const int r0 = base + 4 * threadIdx.x;
+        const bool ok = r0 < P.N;                               // N % 64 == 0: 4 rows in or out together
+        double a[4] = {0.0, 0.0, 0.0, 0.0}, b[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int e0 = 0; e0 < cnt; e0 += 256) {
+            __syncthreads();
+            if (e0 + (int)threadIdx.x < cnt) {
+                s_idx[threadIdx.x] = idx[e0 + threadIdx.x];
+                s_a[threadIdx.x] = xa[e0 + threadIdx.x];
+                s_b[threadIdx.x] = ub[e0 + threadIdx.x];
+            }
+            __syncthreads();
+            const int m = min(256, cnt - e0);
+            for (int e = 0; e < m && ok; e += 4) {
+                uint2 w[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int ia = s_idx[min(e + q, m - 1)];
+                    DSCR_CHECK(ia >= 0 && ia < P.K);
+                    w[q] = __ldg(reinterpret_cast<const uint2*>(P.Dt + (size_t)ia * P.ldd + r0));
+                }
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (e + q < m) resid_acc(w[q], s_a[e + q], s_b[e + q], a, b);
+            }
+        }
+        if (ok) {
+            double y4[4], tn[4];
+            Vec<double>::load(y + r0, y4, l2_normal_policy());
+#pragma unroll
+            for (int v = 0; v < 4; ++v) {
+                const double qa = a[v] - y4[v];
+                tn[v] = b[v] - y4[v];                           // theta_{t+1} = D u - y (solvers.py:212)
+                f2 = fma(qa, qa, f2);
+                sq = fma(tn[v], tn[v], sq);
+                tyv = fma(tn[v], y4[v], tyv);
+                s_th[r0 + v] = tn[v];
+            }
+            write_theta4(P, j, r0, tn[0], tn[1], tn[2], tn[3]);
+        }
+    }
+    double v3[3] = {f2, sq, tyv};
+    block_sum_nt<3, 256>(v3, s_sh);
+    const double lam = P.lam[j];
+    const double mu0 = (v3[1] != 0.0) ? v3[2] / (lam * v3[1]) : 0.0;
+    const double ilam = 1.0 / lam;
+    double d2 = 0.0;
+    for (int r0 = 4 * threadIdx.x; r0 < P.N; r0 += 1024) {     // own rows: no barrier needed for s_th
+        double y4[4];
+        Vec<double>::load(y + r0, y4, l2_normal_policy());
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+            const double d = fma(y4[v], ilam, -(mu0 * s_th[r0 + v]));
+            d2 = fma(d, d, d2);
+        }
+    }
+    double d1[1] = {d2};
+    block_sum_nt<1, 256>(d1, s_sh);
+    if (threadIdx.x == 0) {
+        P.mu0[j] = mu0;
+        P.rsq0[j] = d1[0];
+        const double F = 0.5 * v3[0] + lam * P.pen[j];
+        P.F[j] = F;
+        P.gap[j] = F - 0.5 * P.yy[j] + 0.5 * lam * lam * P.rsq[j];
+        P.sq[j] = v3[1];
+        P.ty[j] = v3[2];
+        if (j == 0) *P.it = t + 1;
+    }
+}
+
 static bool bresid_cta_variant() {      // DSCR_BATCHED_RESID=cta: one CTA per observation (round-1 kernel)
     const char* e = getenv("DSCR_BATCHED_RESID");
     return e && !strcmp(e, "cta");
@@ -2138,6 +2239,10 @@ static void launch_update_hot(const BParams& P, int t, cudaStream_t s) {
 }
 
 static void launch_bresid(const BParams& P, int t, cudaStream_t s) {
+    if (P.N > 2048) {      // tall dictionaries: rows in chunks, theta in shared memory
+        k_bresid_tall<<<P.B + NSCR, 256, (size_t)P.N * sizeof(double), s>>>(P, t);
+        return;
+    }
     if (!bresid_cta_variant()) {
         // rows per observation thread group: NCHK chunks of 8 * TPO rows
         constexpr int C = BRESID_W_NCHK;
@@ -2295,10 +2400,16 @@ size_t dscr_batched_workspace_size(const dscr_batched_desc* d) {
 
 int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void* stream, dscr_batched** out) {
     if (!d || !ws || !out) { err_store() = "null argument"; return DSCR_EINVAL; }
-    if (d->n_atoms % BM || d->n_obs % BN || d->n_rows % BK || d->n_rows > 2048 || d->ldd % 8 || d->ldy < d->n_rows ||
-        d->ldy % 64 || d->splits < 1 || d->splits > 2 || d->cap < 32 || d->max_iters < 1 || !(d->L > 0)) {
-        err_store() = "batched: need K%128==0, B%256==0, N%64==0 (N<=2048), ldy%64==0, splits in {1,2}";
+    if (d->n_atoms % BM || d->n_obs % BN || d->n_rows % BK || d->n_rows > BTALL_MAX_ROWS || d->ldd % 8 ||
+        d->ldy < d->n_rows || d->ldy % 64 || d->splits < 1 || d->splits > 2 || d->cap < 32 || d->max_iters < 1 ||
+        !(d->L > 0)) {
+        err_store() = "batched: need K%128==0, B%256==0, N%64==0 (N<=16384), ldy%64==0, splits in {1,2}";
         return DSCR_EINVAL;
+    }
+    if (d->n_rows > 2048) {   // the tall residual kernel keeps theta (8 N bytes) in shared memory
+        cudaError_t ae = cudaFuncSetAttribute(k_bresid_tall, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)(d->n_rows * sizeof(double)));
+        if (ae != cudaSuccess) { err_store() = cudaGetErrorString(ae); return DSCR_ECUDA; }
     }
     if (d->test != DSCR_TEST_OFF && d->test != DSCR_SAFE && d->test != DSCR_DST3) {
         err_store() = "batched path supports the SAFE and DST3 tests";

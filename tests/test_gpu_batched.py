@@ -261,7 +261,8 @@ def test_block_sort_matches_device_sort(monkeypatch):
 
 
 def test_batched_max_rows_matches_oracle():
-    """N = 2048 (the batched path's maximum): two-chunk residual, integer-slice setup at its limit."""
+    """N = 2048 (the largest row count of the register-resident residual kernels and of the
+    integer-slice setup)."""
     w, dic, D64, L = _batch_problem(2048, 1024, 256, 0.5, seed=17)
     res = solve_batched(dic, w.y, w.lam, L, iterations=40, test="dst3", splits=2)
     for j in (0, 77, 255):
@@ -271,6 +272,36 @@ def test_batched_max_rows_matches_oracle():
         assert abs(res.objective[j] - ref.final_objective) <= 1e-4 * ref.final_objective
         x = res.x_dense(j, 1024)
         assert np.linalg.norm(x - ref.x_star) <= 1e-3 * max(np.linalg.norm(ref.x_star), 1e-12)
+
+
+@pytest.mark.parametrize("n,splits", [(2112, 2), (4160, 1), (8192, 2)])
+def test_batched_tall_dictionaries_match_oracle(n, splits):
+    """Dictionaries taller than 2048 rows (the register-resident residual kernels' limit): fp64
+    setup correlations and the chunked residual pass with theta in shared memory, against the
+    oracle (objective, x, screened set a subset of the reference's) and the operand-precision
+    oracle (identical screened set)."""
+    w, dic, D64, L = _batch_problem(n, 1024, 256, 0.6, seed=41)
+    res = solve_batched(dic, w.y, w.lam, L, iterations=40, test="dst3", splits=splits, masks=True)
+    assert res.iterations == 40 and np.all(res.status == 0)
+    for j in (0, 131, 255):
+        y, lam = w.y[:, j], float(w.lam[j])
+        ref = so.solve(so.make_problem(D64, y, lam),
+                       so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=40, rel_tol=1e-300,
+                                 L0=L, norm_aware=True))
+        emu = bo.solve_bf16(D64, y, lam, L, 40, splits=splits)
+        assert abs(res.objective[j] - ref.final_objective) <= 1e-5 * ref.final_objective
+        assert abs(res.objective[j] - emu.objective) <= 1e-6 * emu.objective
+        x = res.x_dense(j, 1024)
+        assert np.linalg.norm(x - emu.x) <= 1e-3 * max(np.linalg.norm(emu.x), 0.1)
+        elim = res.eliminated(j)
+        assert np.array_equal(elim, emu.eliminated), j
+        assert np.all(np.isin(elim, ref.eliminated)), j
+
+
+def test_batched_rejects_more_than_16384_rows():
+    with pytest.raises((ValueError, RuntimeError)):
+        w, dic, D64, L = _batch_problem(16448, 128, 256, 0.6, seed=43)
+        solve_batched(dic, w.y, w.lam, L, iterations=5, test="dst3", splits=1)
 
 
 @pytest.mark.parametrize("n,k,b", [(64, 1024, 256), (320, 1024, 256), (640, 2048, 256), (1024, 2048, 256),
