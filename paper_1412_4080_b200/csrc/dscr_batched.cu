@@ -717,8 +717,13 @@ static void oz_pairs(OzArgs& g, int S, int T, int dmax) {
 // A slices [S][K][N], B slices [T][B][N]; K, B, N multiples of 128
 static int ozaki_launch(const int8_t* As, int K, int S, const int8_t* Bs, int B, int T, int N, OzArgs& g, cudaStream_t s,
                         int dmax = OZ_DMAX) {
-    if (K % OZ_BM || B % OZ_BN || N % OZ_BK || N > 2048) {
-        err_store() = "exact correlation: need atoms, observations, rows multiples of 128 and rows <= 2048";
+    // int32 diagonals hold <= 4 pairs x N x 127^2 < 2^31 up to N = 16384; the int64 combination
+    // sum_d C_d 2^(7(D-d)) stays below 2^63 for D = dmax <= 4 there (2^30 x 2^28) and needs
+    // N <= 2048 (2^27 x 2^35) with the sixth diagonal
+    const int n_max = std::min(dmax, OZ_DMAX) >= 5 ? 2048 : 16384;
+    if (K % OZ_BM || B % OZ_BN || N % OZ_BK || N > n_max) {
+        err_store() = "exact correlation: need atoms, observations, rows multiples of 128 and rows <= 2048 "
+                      "(<= 16384 with at most five slice diagonals)";
         return DSCR_EINVAL;
     }
     CUtensorMap ma, mb;
@@ -2428,7 +2433,7 @@ int dscr_batched_create(const dscr_batched_desc* d, void* ws, size_t bytes, void
     {   // setup correlations: integer-slice tensor-core products unless DSCR_BATCHED_SETUP=fp64
         const char* ev = getenv("DSCR_BATCHED_SETUP");
         const bool fp64 = ev && !strcmp(ev, "fp64");
-        P.oz = (!fp64 && d->n_rows % OZ_BK == 0 && d->n_rows <= 2048 && d->n_obs % OZ_BN == 0 &&
+        P.oz = (!fp64 && d->n_rows % OZ_BK == 0 && d->n_rows <= BTALL_MAX_ROWS && d->n_obs % OZ_BN == 0 &&
                 d->n_atoms % OZ_BM == 0) ? 1 : 0;
         // default: one exact product D^T Z (centres) after an approximate argmax; "oz2" keeps the
         // two exact products D^T Y, D^T A_*

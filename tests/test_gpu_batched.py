@@ -274,10 +274,11 @@ def test_batched_max_rows_matches_oracle():
         assert np.linalg.norm(x - ref.x_star) <= 1e-3 * max(np.linalg.norm(ref.x_star), 1e-12)
 
 
-@pytest.mark.parametrize("n,splits", [(2112, 2), (4160, 1), (8192, 2)])
+@pytest.mark.parametrize("n,splits", [(2112, 2), (2176, 1), (4160, 1), (8192, 2)])
 def test_batched_tall_dictionaries_match_oracle(n, splits):
-    """Dictionaries taller than 2048 rows (the register-resident residual kernels' limit): fp64
-    setup correlations and the chunked residual pass with theta in shared memory, against the
+    """Dictionaries taller than 2048 rows (the register-resident residual kernels' limit): the
+    chunked residual pass with theta in shared memory, setup on the integer tensor cores when the
+    row count is a multiple of 128 (2176, 8192) and on the fp64 path otherwise, against the
     oracle (objective, x, screened set a subset of the reference's) and the operand-precision
     oracle (identical screened set)."""
     w, dic, D64, L = _batch_problem(n, 1024, 256, 0.6, seed=41)
