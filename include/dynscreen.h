@@ -330,8 +330,8 @@ int dscr_corr_exact_bf16(const void* Dt, int n_atoms, int n_rows, int ldd, const
  * the fp64 setup computes lambda_*, a_* and the test centres. */
 typedef struct dscr_batched_desc {
     int32_t n_rows;          /* N features, multiple of 64, <= 16384 (above 2048: fp64 setup correlations, chunked residual pass) */
-    int32_t n_atoms;         /* K, multiple of 128 */
-    int32_t n_obs;           /* B, multiple of 256 */
+    int32_t n_atoms;         /* K, multiple of 128 (all-zero columns are allowed as padding: never active, not counted as kept) */
+    int32_t n_obs;           /* B, multiple of 256 (pad with observations whose lam exceeds lambda_*: status 1, skipped) */
     int32_t ldd;             /* row stride of D^T (elements), multiple of 8 */
     const void* Dt;          /* bf16 [K][ldd] */
     const double* Y;         /* fp64 [B][ldy], unit-norm observations */

@@ -23,6 +23,9 @@ import numpy as np
 from . import _native as nat
 
 
+_PAD_LAM = 1e30      # lam of the padding observations: above any lambda_*, so they are trivial (status 1)
+
+
 def fista_betas(iters):
     """Momentum coefficients (l_t - 1)/l_{t+1} of solvers.py:216-218, same fp64 ops."""
     out = np.empty(iters)
@@ -51,13 +54,14 @@ class BatchedResult:
     device_seconds: float = float("nan")
     d2h_bytes: int = 0           # bytes copied device -> host by result()
     active_words: np.ndarray | None = None   # [B][K/32] active-atom bits (result(masks=True) only)
+    n_atoms: int | None = None               # the caller's atom count (the device pads it to a multiple of 128)
 
     def active_mask(self, j):
         """Boolean active-atom mask of observation j (needs the masks read back)."""
         if self.active_words is None:
             raise ValueError("masks were not read back (solve_batched(..., masks=True))")
         bits = np.unpackbits(self.active_words[j].view(np.uint8), bitorder="little")
-        return bits.astype(bool)
+        return bits.astype(bool)[:self.n_atoms]
 
     def eliminated(self, j):
         """Atoms screened out of observation j (sorted)."""
@@ -105,29 +109,45 @@ class BatchedEngine:
         self.torch = torch
         self.L = nat.lib()
         self.device = device if device is not None else torch.device("cuda", torch.cuda.current_device())
-        self.k, self.n, self.b = dictionary.n_cols, n, b
+        # The kernels take N % 64 == 0, K % 128 == 0, B % 256 == 0 (tile shapes).  Other shapes are
+        # padded here: zero rows (no contribution to any product), all-zero atoms (never active:
+        # the kernels drop them from the masks and the kept counts) and trivial observations
+        # (a copy of observation 0 with lam > lambda_*: status 1, skipped by every kernel and by
+        # the batch aggregates); results are cut back to the caller's shapes.
+        self.k_user, self.n_user, self.b_user = dictionary.n_cols, n, b
+        kp, np_, bp = (dictionary.n_cols + 127) // 128 * 128, (n + 63) // 64 * 64, (b + 255) // 256 * 256
+        self.k, self.n, self.b = kp, np_, bp
         self.iterations, self.cap = int(iterations), int(cap)
-        self.Dt = dictionary.device_data(self.device)                      # (K, ldd) bf16 bits
+        self.Dt_src = dictionary.device_data(self.device)                  # (K, ldd) bf16 bits
         self.dic = dictionary
-        ldy = (n + 63) // 64 * 64
+        if kp != dictionary.n_cols or np_ > dictionary.ldd:
+            self.Dt = torch.zeros((kp, np_), dtype=self.Dt_src.dtype, device=self.device)
+            self.Dt[:dictionary.n_cols, :min(dictionary.ldd, np_)].copy_(self.Dt_src[:, :min(dictionary.ldd, np_)])
+            ldd = np_
+        else:
+            self.Dt, ldd = self.Dt_src, dictionary.ldd
+        ldy = np_
         # upload Y as given (n x b) and transpose on the device into observation rows [b][ldy]
-        self.Yd = torch.zeros((b, ldy), dtype=torch.float64, device=self.device)
+        self.Yd = torch.zeros((bp, ldy), dtype=torch.float64, device=self.device)
         if y_torch:
             rows = Y.T if Y.T.is_contiguous() else Y.T.contiguous()              # (b, n)
-            self.Yd[:, :n].copy_(rows.to(self.device, non_blocking=rows.is_pinned()))
+            self.Yd[:b, :n].copy_(rows.to(self.device, non_blocking=rows.is_pinned()))
             y_bytes = int(Y.numel() * 8)
         else:
             Yh = torch.from_numpy(Y.T if Y.flags.f_contiguous else np.ascontiguousarray(Y))
             if Y.flags.f_contiguous:
-                self.Yd[:, :n].copy_(Yh.to(self.device))
+                self.Yd[:b, :n].copy_(Yh.to(self.device))
             else:
-                self.Yd[:, :n].copy_(Yh.to(self.device).T)
+                self.Yd[:b, :n].copy_(Yh.to(self.device).T)
             y_bytes = int(Y.nbytes)
-        self.lamd = torch.from_numpy(lam.copy()).to(self.device)
+        self.lamd = torch.full((bp,), _PAD_LAM, dtype=torch.float64, device=self.device)
+        self.lamd[:b].copy_(torch.from_numpy(lam.copy()))
+        if bp != b:
+            self.Yd[b:].copy_(self.Yd[0:1].expand(bp - b, ldy))
         self.h2d_bytes = int(y_bytes + lam.nbytes)
         self.betas = fista_betas(self.iterations)
         d = nat.BatchedDesc()
-        d.n_rows, d.n_atoms, d.n_obs, d.ldd = n, self.k, b, dictionary.ldd
+        d.n_rows, d.n_atoms, d.n_obs, d.ldd = np_, kp, bp, ldd
         d.Dt, d.Y, d.ldy, d.splits = self.Dt.data_ptr(), self.Yd.data_ptr(), ldy, int(splits)
         d.lam, d.L, d.test, d.cap = self.lamd.data_ptr(), float(L), nat.TEST_CODES[test], self.cap
         d.max_iters = self.iterations
@@ -147,33 +167,36 @@ class BatchedEngine:
     def dic_current(self):
         """The dictionary's device copy is still the one in this engine's buffer (it is not when
         the caller dropped the device copy, e.g. after updating the host data)."""
-        return any(t.data_ptr() == self.Dt.data_ptr() for t in self.dic._dev.values())
+        return any(t.data_ptr() == self.Dt_src.data_ptr() for t in self.dic._dev.values())
 
     def load(self, Y, lam):
         """New observations and lambdas of the same shape for another solve on this engine (the
         workspace, the captured iteration graph and the device dictionary are reused)."""
         torch = self.torch
         lam = np.asarray(lam, dtype=np.float64).reshape(-1)
-        if lam.shape != (self.b,) or np.any(lam <= 0):
+        b = self.b_user
+        if lam.shape != (b,) or np.any(lam <= 0):
             raise ValueError("need one strictly positive lam per observation")
-        n = self.n
+        n = self.n_user
         if torch.is_tensor(Y):
-            if Y.dtype != torch.float64 or tuple(Y.shape) != (n, self.b) or Y.device.type != "cpu":
+            if Y.dtype != torch.float64 or tuple(Y.shape) != (n, b) or Y.device.type != "cpu":
                 raise ValueError("observations must be a float64 host tensor of shape (n_rows, batch)")
             rows = Y.T if Y.T.is_contiguous() else Y.T.contiguous()
-            self.Yd[:, :n].copy_(rows.to(self.device, non_blocking=rows.is_pinned()))
+            self.Yd[:b, :n].copy_(rows.to(self.device, non_blocking=rows.is_pinned()))
             y_bytes = int(Y.numel() * 8)
         else:
             Y = np.asarray(Y, dtype=np.float64)
-            if Y.shape != (n, self.b):
+            if Y.shape != (n, b):
                 raise ValueError("observations must have shape (n_rows, batch)")
             Yh = torch.from_numpy(Y.T if Y.flags.f_contiguous else np.ascontiguousarray(Y))
             if Y.flags.f_contiguous:
-                self.Yd[:, :n].copy_(Yh.to(self.device))
+                self.Yd[:b, :n].copy_(Yh.to(self.device))
             else:
-                self.Yd[:, :n].copy_(Yh.to(self.device).T)
+                self.Yd[:b, :n].copy_(Yh.to(self.device).T)
             y_bytes = int(Y.nbytes)
-        self.lamd.copy_(torch.from_numpy(lam))
+        if self.b != b:
+            self.Yd[b:].copy_(self.Yd[0:1].expand(self.b - b, self.Yd.shape[1]))
+        self.lamd[:b].copy_(torch.from_numpy(lam))
         self.h2d_bytes = int(y_bytes + lam.nbytes)
 
     def setup(self):
@@ -193,21 +216,21 @@ class BatchedEngine:
         packed transfers (self.d2h_bytes counts them).  ``masks=True`` also reads the active-atom
         bit masks (B x K/32 words) for set-level checks."""
         torch = self.torch
-        b, bf, cap = self.b, self.bufs, self.cap
+        bp, b, bf, cap = self.b, self.b_user, self.bufs, self.cap      # padded / caller's batch size
         par = self.iterations & 1
-        cnt = self._view(bf.s_cnt[par], b, torch.int32)
-        xs = self._view(bf.s_x[par], b * cap, torch.float64).view(b, cap)
+        cnt = self._view(bf.s_cnt[par], bp, torch.int32)[:b]
+        xs = self._view(bf.s_x[par], bp * cap, torch.float64).view(bp, cap)[:b]
         live = (torch.arange(cap, device=self.device, dtype=torch.int32)[None, :] < cnt[:, None]) & (xs != 0.0)
         counts_d = live.sum(dim=1, dtype=torch.int32)
-        idx = self._view(bf.s_idx[par], b * cap, torch.int32).view(b, cap)[live].cpu().numpy()
+        idx = self._view(bf.s_idx[par], bp * cap, torch.int32).view(bp, cap)[:b][live].cpu().numpy()
         val = xs[live].cpu().numpy()
-        f64 = torch.stack([self._view(p, b, torch.float64) for p in (bf.F, bf.gap, bf.lmax, bf.radius)]).cpu().numpy()
-        i32 = torch.cat([self._view(p, b, torch.int32) for p in (bf.nnz, bf.kept, bf.status)] + [counts_d]
+        f64 = torch.stack([self._view(p, bp, torch.float64)[:b] for p in (bf.F, bf.gap, bf.lmax, bf.radius)]).cpu().numpy()
+        i32 = torch.cat([self._view(p, bp, torch.int32)[:b] for p in (bf.nnz, bf.kept, bf.status)] + [counts_d]
                         + [self._view(bf.iterations, 1, torch.int32)]).cpu().numpy()
         trace = self._view(bf.trace, self.iterations * 4, torch.float64).cpu().numpy().reshape(-1, 4)
         words = None
         if masks:
-            words = self._view(bf.mask, b * (self.k // 32), torch.int32).view(b, self.k // 32).cpu().numpy()
+            words = self._view(bf.mask, bp * (self.k // 32), torch.int32).view(bp, self.k // 32)[:b].cpu().numpy()
             words = words.view(np.uint32)
         self.d2h_bytes = int(idx.nbytes + val.nbytes + f64.nbytes + i32.nbytes + trace.nbytes
                              + (words.nbytes if words is not None else 0))
@@ -224,7 +247,7 @@ class BatchedEngine:
             objective=f64[0], gap=f64[1], nnz=nnz, kept=kept, status=status,
             lambda_max=f64[2], radius=f64[3], trace=trace,
             x_ptr=ptr, x_indices=idx.astype(np.int64), x_values=val,
-            device_seconds=device_seconds, d2h_bytes=self.d2h_bytes, active_words=words,
+            device_seconds=device_seconds, d2h_bytes=self.d2h_bytes, active_words=words, n_atoms=self.k_user,
         )
 
     def close(self):
@@ -283,8 +306,16 @@ class BatchedSolver:
             self.args = (dictionary,) + self.args[1:]
         dictionary = self.args[0]
         shape = tuple(Y.shape)
-        if self.eng is not None and (self.eng.n, self.eng.b) == shape:
-            if self.eng.dic is not dictionary or not self.eng.dic_current():
+        if self.eng is not None and (self.eng.n_user, self.eng.b_user) == shape:
+            if (self.eng.dic is not dictionary or not self.eng.dic_current()) and self.eng.Dt is not self.eng.Dt_src:
+                # padded engine buffer: the dictionary keeps its own device copy, the engine's
+                # padded buffer is refreshed from it
+                fresh = dictionary.device_data(self.eng.device)          # upload (H2D) if not cached
+                ld = min(dictionary.ldd, self.eng.Dt.shape[1])
+                self.eng.Dt[:dictionary.n_cols, :ld].copy_(fresh[:, :ld])
+                self.eng.Dt_src = fresh
+                self.eng.dic = dictionary
+            elif self.eng.dic is not dictionary or not self.eng.dic_current():
                 prev = self.eng.dic                                      # its cache must not alias the buffer
                 for key in [k for k, t in prev._dev.items() if t.data_ptr() == self.eng.Dt.data_ptr()]:
                     del prev._dev[key]
@@ -292,6 +323,7 @@ class BatchedSolver:
                 self.eng.Dt.copy_(fresh)
                 dictionary.drop_device()
                 dictionary._dev[(str(self.eng.device), None)] = self.eng.Dt   # the engine's buffer is the copy
+                self.eng.Dt_src = self.eng.Dt
                 self.eng.dic = dictionary
             self.eng.load(Y, lam)
         else:

@@ -795,6 +795,8 @@ struct BParams {
     int* si[2]; double* sx[2]; double* su[2]; int* sn[2];
     double *sq, *ty, *mu0, *rsq0, *yy, *lmax, *sgn, *shift_sq, *rsq, *radius, *F, *gap, *pen, *ccmin;
     double* anorm;             // [K] column norms of the bf16 dictionary (fp64)
+    uint32_t* vmask;           // [K/32] atoms with a nonzero column (all-zero padding columns are never active)
+    int* nvalid;               // number of such atoms
     int *istar, *nnz, *kept, *status;
     const double* beta;        // [iters]
     int fused;                 // GEMM epilogue emits hot entries (no dense C round trip)
@@ -896,6 +898,27 @@ __global__ void __launch_bounds__(BT) k_bnorms(BParams P) {
         }
         acc = warp_sum(acc);
         if (lane == 0) P.anorm[i] = sqrt(acc);
+    }
+}
+
+// atoms with a nonzero column: an all-zero column (the host pads the atom count to a multiple of
+// 128 with them) has no correlation with anything and is never active
+__global__ void __launch_bounds__(BT) k_bvalid(BParams P) {
+    __shared__ int s_cnt[BW];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    int cnt = 0;
+    for (int w = warp; w < P.K / 32; w += BW) {          // one CTA: K / 32 words
+        const bool ok = P.anorm[w * 32 + lane] > 0.0;
+        const unsigned bal = __ballot_sync(0xffffffffu, ok);
+        if (lane == 0) P.vmask[w] = bal;
+        cnt += __popc(bal);
+    }
+    if (lane == 0) s_cnt[warp] = cnt;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int tot = 0;
+        for (int w = 0; w < BW; ++w) tot += s_cnt[w];
+        *P.nvalid = tot;
     }
 }
 
@@ -1071,7 +1094,9 @@ __global__ void __launch_bounds__(BT) k_bcc(BParams P) {
     for (int i = threadIdx.x; i < P.K; i += BT) {
         if (P.test == DSCR_SAFE && P.oz != 2)
             P.cc[(size_t)j * P.K + i] = (float)(P.ycorr[(size_t)j * P.K + i] / P.lam[j]);
-        const float v = (float)((1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / P.anorm[i]);
+        const double an = P.anorm[i];
+        // (an all-zero column is inactive from the start: it sorts last and never enters a range)
+        const float v = an > 0.0 ? (float)((1.0 - fabs((double)P.cc[(size_t)j * P.K + i])) / an) : -INFINITY;
         m = fmaxf(m, v);
         P.skey_in[(size_t)j * P.K + i] = okey16(v);   // sort key of the screening order
         P.sval_in[(size_t)j * P.K + i] = i;
@@ -1178,13 +1203,13 @@ __global__ void __launch_bounds__(BT) k_binit(BParams P) {
     d2 = block_sum(d2, s_sh);
     const bool trivial = P.status[j] == 1;
     for (int w = threadIdx.x; w < P.K / 32; w += BT) {
-        P.mask[(size_t)j * (P.K / 32) + w] = trivial ? 0u : 0xffffffffu;
+        P.mask[(size_t)j * (P.K / 32) + w] = trivial ? 0u : P.vmask[w];
         P.nzm[(size_t)j * (P.K / 32) + w] = 0u;
     }
     if (threadIdx.x == 0) {
         P.yy[j] = v3[0]; P.sq[j] = v3[1]; P.ty[j] = v3[2]; P.mu0[j] = mu0; P.rsq0[j] = d2;
         P.sn[0][j] = 0; P.sn[1][j] = 0;
-        P.F[j] = 0.5 * v3[0]; P.gap[j] = NAN; P.nnz[j] = 0; P.kept[j] = trivial ? 0 : P.K;
+        P.F[j] = 0.5 * v3[0]; P.gap[j] = NAN; P.nnz[j] = 0; P.kept[j] = trivial ? 0 : *P.nvalid;
         P.radius[j] = NAN;
         P.thr[j] = (float)(P.lam[j] * (1.0 - 1e-6));
         P.cmax[j] = 0u;
@@ -2377,6 +2402,8 @@ static size_t batched_layout(const dscr_batched_desc* d, BParams* P, char* base)
     double** dv[] = {&p.sq, &p.ty, &p.mu0, &p.rsq0, &p.yy, &p.lmax, &p.sgn, &p.shift_sq, &p.rsq, &p.radius, &p.F, &p.gap, &p.pen, &p.ccmin};
     for (double** q : dv) *q = (double*)take(B * 8);
     p.anorm = (double*)take(K * 8);
+    p.vmask = (uint32_t*)take(K / 8);
+    p.nvalid = (int*)take(64);
     int** iv[] = {&p.istar, &p.nnz, &p.kept, &p.status};
     for (int** q : iv) *q = (int*)take(B * 4);
     p.nzm = (uint32_t*)take(B * K / 8);
@@ -2468,6 +2495,7 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
     BParams& P = h->P;
     dim3 g(P.K / DG_T, P.B / DG_T);
     k_bnorms<<<std::max(1, P.K / BW / 4), BT, 0, s>>>(P);
+    k_bvalid<<<1, BT, 0, s>>>(P);
     if (P.oz == 2) {
         k_slice_rows<<<P.K / 8, 256, 0, s>>>(P.Dt, P.K, P.N, P.ldd, OZ_SD, P.Ds, P.eD);
         k_ysplit<<<P.B, BT, 0, s>>>(P);

@@ -299,6 +299,55 @@ def test_batched_tall_dictionaries_match_oracle(n, splits):
         assert np.all(np.isin(elim, ref.eliminated)), j
 
 
+@pytest.mark.parametrize("n,k,b,splits", [(1000, 5000, 300, 2), (200, 1000, 37, 1), (1024, 2048, 256, 1)])
+def test_batched_any_shape_matches_oracle(n, k, b, splits):
+    """Row, atom and batch counts that are not multiples of the kernels' tiles (64 / 128 / 256):
+    the host pads with zero rows, all-zero atoms (inactive from the start, not counted as kept)
+    and trivial observations, and cuts the results back.  Per observation the result equals the
+    oracle's on the unpadded problem; the batch aggregates count only the caller's observations."""
+    w, dic, D64, L = _batch_problem(n, k, b, 0.6, seed=51)
+    res = solve_batched(dic, w.y, w.lam, L, iterations=50, test="dst3", splits=splits, masks=True)
+    assert res.objective.shape == (b,) and res.kept.shape == (b,) and res.status.shape == (b,)
+    assert np.all(res.status == 0) and res.kept.max() <= k and len(res.x_idx) == b
+    np.testing.assert_allclose(res.trace[-1, 0], res.objective.sum(), rtol=1e-12)
+    np.testing.assert_allclose(res.trace[-1, 3], res.kept.sum(), rtol=0, atol=0.5)
+    for j in sorted({0, b // 2, b - 1}):
+        y, lam = w.y[:, j], float(w.lam[j])
+        emu = bo.solve_bf16(D64, y, lam, L, 50, splits=splits)
+        ref = so.solve(so.make_problem(D64, y, lam),
+                       so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=50, rel_tol=1e-300,
+                                 L0=L, norm_aware=True))
+        assert abs(res.objective[j] - emu.objective) <= 1e-7 * emu.objective
+        assert abs(res.objective[j] - ref.final_objective) <= 1e-6 * ref.final_objective
+        x = res.x_dense(j, k)
+        assert np.linalg.norm(x - emu.x) <= 1e-3 * max(np.linalg.norm(emu.x), 0.1)
+        elim = res.eliminated(j)
+        assert res.active_mask(j).shape == (k,)
+        assert np.array_equal(elim, emu.eliminated), j
+        assert np.all(np.isin(elim, ref.eliminated)), j
+        assert res.kept[j] == k - elim.size
+
+
+def test_batched_solver_any_shape_reuse_and_dictionary_swap():
+    """BatchedSolver on a padded shape: a second batch and a swapped dictionary reuse the engine
+    and equal one-shot solves."""
+    from paper_1412_4080_b200.batched import BatchedSolver
+    w1, dic1, _, L1 = _batch_problem(200, 1000, 37, 0.5, seed=61)
+    w2, dic2, _, L2 = _batch_problem(200, 1000, 37, 0.5, seed=62)
+    L = max(L1, L2)
+    solver = BatchedSolver(dic1, L, iterations=40, test="dst3", splits=2)
+    a1 = solver.solve(w1.y, w1.lam)
+    eng = solver.eng
+    a2 = solver.solve(w2.y, w2.lam, dictionary=dic2)
+    assert solver.eng is eng
+    solver.close()
+    b1 = solve_batched(dic1, w1.y, w1.lam, L, iterations=40, test="dst3", splits=2)
+    b2 = solve_batched(dic2, w2.y, w2.lam, L, iterations=40, test="dst3", splits=2)
+    for a, c in ((a1, b1), (a2, b2)):
+        assert np.array_equal(a.objective, c.objective) and np.array_equal(a.kept, c.kept)
+        assert np.array_equal(a.x_indices, c.x_indices) and np.array_equal(a.x_values, c.x_values)
+
+
 def test_batched_rejects_more_than_16384_rows():
     with pytest.raises((ValueError, RuntimeError)):
         w, dic, D64, L = _batch_problem(16448, 128, 256, 0.6, seed=43)
