@@ -23,6 +23,12 @@ import numpy as np
 from . import _native as nat
 
 
+class BatchedCapacityError(RuntimeError):
+    """An observation had more hot correlations than the fused epilogue's per-observation list
+    (2048) or more nonzeros than ``cap``; solve_batched / BatchedSolver retry once on the dense
+    path with ``cap`` = the atom count."""
+
+
 _PAD_LAM = 1e30      # lam of the padding observations: above any lambda_*, so they are trivial (status 1)
 
 
@@ -238,8 +244,9 @@ class BatchedEngine:
         if np.any(status >= 3):
             bad = np.flatnonzero(status >= 3)
             code = int(status[bad[0]])
-            raise RuntimeError(f"batched solve failed on {bad.size} observations (status {code}: "
-                               f"{'radius guard' if code == 3 else 'nonzero capacity exceeded'})")
+            exc = BatchedCapacityError if np.all(status[bad] == 4) else RuntimeError
+            raise exc(f"batched solve failed on {bad.size} observations (status {code}: "
+                      f"{'radius guard' if code == 3 else 'nonzero capacity exceeded'})")
         ptr = np.zeros(b + 1, dtype=np.int64)
         np.cumsum(counts, out=ptr[1:])
         return BatchedResult(
@@ -267,18 +274,25 @@ def solve_batched(dictionary, Y, lam, L, iterations=100, test="dst3", splits=1, 
                   fused=True, masks=False):
     """FISTA (fixed step 1/L) with per-observation dynamic screening for Y[:, j], lam[j].
     ``masks=True`` also returns the per-observation active-atom masks (``BatchedResult.eliminated``)."""
-    eng = BatchedEngine(dictionary, Y, lam, L, iterations, test, splits, cap, device, fused)
-    torch = eng.torch
+    def once(cap_, fused_):
+        eng = BatchedEngine(dictionary, Y, lam, L, iterations, test, splits, cap_, device, fused_)
+        torch = eng.torch
+        try:
+            ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ev0.record(eng.stream)
+            eng.setup()
+            eng.run()
+            ev1.record(eng.stream)
+            eng.stream.synchronize()
+            return eng.result(ev0.elapsed_time(ev1) / 1e3, masks=masks)
+        finally:
+            eng.close()
+
     try:
-        ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ev0.record(eng.stream)
-        eng.setup()
-        eng.run()
-        ev1.record(eng.stream)
-        eng.stream.synchronize()
-        return eng.result(ev0.elapsed_time(ev1) / 1e3, masks=masks)
-    finally:
-        eng.close()
+        return once(cap, fused)
+    except BatchedCapacityError:
+        # the reference has no support-size limit: rerun with room for every atom, dense update
+        return once((dictionary.n_cols + 127) // 128 * 128, False)
 
 
 class BatchedSolver:
@@ -337,7 +351,13 @@ class BatchedSolver:
         eng.run()
         ev1.record(eng.stream)
         eng.stream.synchronize()
-        return eng.result(ev0.elapsed_time(ev1) / 1e3)
+        try:
+            return eng.result(ev0.elapsed_time(ev1) / 1e3)
+        except BatchedCapacityError:
+            # rebuild the engine with room for every atom and the dense update, and keep it
+            self.close()
+            self.args = (dictionary, L, iterations, test, splits, (dictionary.n_cols + 127) // 128 * 128, device, False)
+            return self.solve(Y, lam)
 
     def close(self):
         if self.eng is not None:

@@ -348,6 +348,29 @@ def test_batched_solver_any_shape_reuse_and_dictionary_swap():
         assert np.array_equal(a.x_indices, c.x_indices) and np.array_equal(a.x_values, c.x_values)
 
 
+def test_batched_capacity_overflow_falls_back_to_dense_path():
+    """A small lam makes supports larger than the per-observation list capacity: the solve reruns
+    on the dense-update path with room for every atom (the reference has no support limit) and
+    matches the oracle."""
+    from paper_1412_4080_b200.batched import BatchedCapacityError, BatchedEngine
+    w, dic, D64, L = _batch_problem(128, 1024, 256, 0.02, seed=71)
+    eng = BatchedEngine(dic, w.y, w.lam, L, iterations=30, test="dst3", splits=2, cap=32)
+    eng.setup()
+    eng.run()
+    eng.stream.synchronize()
+    with pytest.raises(BatchedCapacityError):
+        eng.result()
+    eng.close()
+    res = solve_batched(dic, w.y, w.lam, L, iterations=30, test="dst3", splits=2, cap=32)
+    assert np.all(res.status == 0) and res.nnz.max() > 32
+    for j in (0, 200):
+        ref = so.solve(so.make_problem(D64, w.y[:, j], w.lam[j]),
+                       so.Config(algorithm="fista", strategy="dynamic", test="dst3", max_iters=30, rel_tol=1e-300,
+                                 L0=L, norm_aware=True))
+        assert abs(res.objective[j] - ref.final_objective) <= 1e-6 * ref.final_objective
+        assert res.nnz[j] == np.count_nonzero(ref.x_star)
+
+
 def test_batched_rejects_more_than_16384_rows():
     with pytest.raises((ValueError, RuntimeError)):
         w, dic, D64, L = _batch_problem(16448, 128, 256, 0.6, seed=43)
