@@ -1654,6 +1654,7 @@ __device__ void update_hot_cta(const BParams& P, int t, int j) {
 __global__ void __launch_bounds__(BT) k_bupdate_hot(BParams P, int t) {
     __shared__ int s_b;
     const int nb = *P.nbig;                      // final: the warp kernel ran before this launch
+    if (nb == 0) return;                         // the common case: no work-counter atomics at all
     for (;;) {                                   // a resident-sized grid pulls observations off the list
         __syncthreads();
         if (threadIdx.x == 0) s_b = atomicAdd(P.big_next, 1);
