@@ -903,22 +903,15 @@ __global__ void __launch_bounds__(BT) k_bnorms(BParams P) {
 
 // atoms with a nonzero column: an all-zero column (the host pads the atom count to a multiple of
 // 128 with them) has no correlation with anything and is never active
-__global__ void __launch_bounds__(BT) k_bvalid(BParams P) {
-    __shared__ int s_cnt[BW];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    int cnt = 0;
-    for (int w = warp; w < P.K / 32; w += BW) {          // one CTA: K / 32 words
-        const bool ok = P.anorm[w * 32 + lane] > 0.0;
-        const unsigned bal = __ballot_sync(0xffffffffu, ok);
-        if (lane == 0) P.vmask[w] = bal;
-        cnt += __popc(bal);
-    }
-    if (lane == 0) s_cnt[warp] = cnt;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int tot = 0;
-        for (int w = 0; w < BW; ++w) tot += s_cnt[w];
-        *P.nvalid = tot;
+__global__ void __launch_bounds__(BT) k_bvalid(BParams P) {      // one warp per 32-atom word; *nvalid zeroed before
+    const int lane = threadIdx.x & 31;
+    const int w = (blockIdx.x * BT + threadIdx.x) >> 5;
+    if (w >= P.K / 32) return;
+    const bool ok = P.anorm[w * 32 + lane] > 0.0;
+    const unsigned bal = __ballot_sync(0xffffffffu, ok);
+    if (lane == 0) {
+        P.vmask[w] = bal;
+        atomicAdd(P.nvalid, __popc(bal));
     }
 }
 
@@ -2496,7 +2489,8 @@ int dscr_batched_setup(dscr_batched* h, void* stream) {
     BParams& P = h->P;
     dim3 g(P.K / DG_T, P.B / DG_T);
     k_bnorms<<<std::max(1, P.K / BW / 4), BT, 0, s>>>(P);
-    k_bvalid<<<1, BT, 0, s>>>(P);
+    cudaMemsetAsync(P.nvalid, 0, sizeof(int), s);
+    k_bvalid<<<(P.K / 32 + BW - 1) / BW, BT, 0, s>>>(P);
     if (P.oz == 2) {
         k_slice_rows<<<P.K / 8, 256, 0, s>>>(P.Dt, P.K, P.N, P.ldd, OZ_SD, P.Ds, P.eD);
         k_ysplit<<<P.B, BT, 0, s>>>(P);
