@@ -38,6 +38,8 @@ constexpr int TMEM_COLS = 2 * BN;
 #define GEMM_EPI_WARPS 16
 #endif
 constexpr int EPI_WARPS = GEMM_EPI_WARPS;   // epilogue warps: EPI_WARPS / 4 per TMEM lane quarter
+static_assert(EPI_WARPS % 4 == 0 && EPI_WARPS >= 4 && (256 % (32 * (EPI_WARPS / 4))) == 0 && 64 + 32 * EPI_WARPS <= 1024,
+              "GEMM_EPI_WARPS: 4, 8 or 16 (each lane quarter's warps split the 256 tile columns into 32-column chunks)");
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;   // warp 0 TMA, warp 1 MMA, then the epilogue warps
 constexpr int EPI_THREADS = GEMM_THREADS - 64;
 constexpr size_t GEMM_SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256 + 64;
