@@ -38,7 +38,7 @@ def _connect(shards):
     return bases
 
 
-def _lockstep(shards, cfg, lam, vec_tests=("dst3",)):
+def _lockstep(shards, cfg, lam, vec_tests=("dst3", "gst3"), group_weights=None):
     world = len(shards)
     for r, sh in enumerate(shards):
         sh.set_collectives(r, world, True)
@@ -52,10 +52,11 @@ def _lockstep(shards, cfg, lam, vec_tests=("dst3",)):
             best = r
     lmax, gidx, sign = float(allc[best, 0]), int(allc[best, 1]), float(allc[best, 2])
     assert lam <= lmax
+    w_star = float(group_weights[gidx]) if group_weights is not None else 0.0
     for r, sh in enumerate(shards):
         local_unit = gidx - sh.unit_offset if r == best else -1
         sh.comm[nat.CM_SETUP: nat.CM_SETUP + 7] = torch.tensor(
-            [lmax, gidx, sign, 0.0, 1.0 if r == best else 0.0, 0.0, local_unit], dtype=sh.comm.dtype).to(sh.comm.device)
+            [lmax, gidx, sign, 0.0, 1.0 if r == best else 0.0, w_star, local_unit], dtype=sh.comm.dtype).to(sh.comm.device)
         sh.phase(nat.PH_SETUP_ADOPT)
     if cfg.test in vec_tests:
         shards[best].phase(nat.PH_SETUP_VEC)
@@ -113,6 +114,55 @@ def test_peer_exchange_lockstep_matches_unsharded(algo, ratio, cuts):
         assert np.linalg.norm(x - ref.x_star) <= 1e-9 * max(np.linalg.norm(ref.x_star), 1e-12)
         assert abs(float(sc.F) - ref.final_objective) <= 1e-12 * abs(ref.final_objective)
         # every rank reduced the same bits
+        assert len({(float(s[3].F), float(s[3].gap)) for s in sols}) == 1
+    finally:
+        for sh in shards:
+            sh.close()
+        for b in bases:
+            shards[0].eng.L.dscr_peer_free(b)
+
+
+def test_group_peer_exchange_lockstep_matches_unsharded():
+    """Group-Lasso, FISTA + dynamic GST3, two ranks holding whole groups (48 + 80 groups of 8)."""
+    n, k, gs = 200, 1024, 8
+    D = wl.correlated_dictionary(n, k, 1)
+    groups = [np.arange(g, g + gs) for g in range(0, k, gs)]
+    dic = ds.Dictionary(D)
+    part = ds.GroupPartition.build(dic, groups)
+    rng = np.random.default_rng(5)
+    x0 = np.zeros(k)
+    for g in rng.choice(len(groups), 4, replace=False):
+        x0[groups[g]] = rng.standard_normal(gs)
+    y = D @ x0 + 0.01 * rng.standard_normal(n)
+    y /= np.linalg.norm(y)
+    lmax = max(np.linalg.norm(D[:, g].T @ y) / part.weights[i] for i, g in enumerate(groups))
+    lam = 0.7 * lmax
+    L = float(np.linalg.norm(D, 2) ** 2 * (1 + 1e-9))
+    cfg = ds.SolverConfig(algorithm="fista", strategy="dynamic", test="gst3", max_iters=400, rel_tol=1e-300, L0=L,
+                          gap_tol=1e-7)
+    ref = ds.run(ds.Problem(dic, y, lam, part), cfg)
+    assert ref.screen_state.eliminated.size > 0
+    gcuts = [(0, 48), (48, len(groups))]
+    shards = []
+    for g0, g1 in gcuts:
+        c0, c1 = g0 * gs, g1 * gs
+        sub = ds.Dictionary(np.asfortranarray(D[:, c0:c1]))
+        lp = ds.GroupPartition.build(sub, [g - c0 for g in groups[g0:g1]], weights=part.weights[g0:g1],
+                                     spectral_norms=part.spectral_norms[g0:g1])
+        shards.append(pdist.GpuShard(ds.Problem(sub, y, lam, lp), cfg, c0, k, g0, len(groups)))
+    bases = []
+    try:
+        bases, trips = _lockstep(shards, cfg, lam, group_weights=np.asarray(part.weights))
+        sols = [sh.local_solution() for sh in shards]
+        sc = sols[0][3]
+        assert sc.t == ref.iterations
+        kept = np.concatenate([s[0] + g0 * gs for s, (g0, _) in zip(sols, gcuts)])
+        xs = np.concatenate([s[1] for s in sols])
+        x = np.zeros(k)
+        x[kept] = xs
+        assert np.array_equal(np.setdiff1d(np.arange(k), kept), ref.screen_state.eliminated)
+        assert np.linalg.norm(x - ref.x_star) <= 1e-9 * max(np.linalg.norm(ref.x_star), 1e-12)
+        assert abs(float(sc.F) - ref.final_objective) <= 1e-12 * abs(ref.final_objective)
         assert len({(float(s[3].F), float(s[3].gap)) for s in sols}) == 1
     finally:
         for sh in shards:
